@@ -1,0 +1,163 @@
+"""Pins for the full oracle randUTV (O1-O11), against things other than itself:
+the explicit-matrix mini-oracle (paper Sec. 3.1 equations taken literally),
+LAPACK's SVD in the cases where randUTV reduces to it, closed forms of the c1
+spectrum, exact invariants (orthogonality, triangularity, norms), and the
+identity rho = ||A - A_k||_F of the truncated variant.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle.bruteforce import randutv_bruteforce
+from oracle.randutv import orthogonality_error, randutv, reconstruction_error
+from paper_2002_06960_b200.inputs import make_numpy, sigma_powspec
+
+U = 2.0 ** -53
+
+
+@pytest.fixture(scope="module")
+def c1():
+    A = make_numpy("powspec", 512, 512, cfg_index=1)
+    out = randutv(A, 64, 2, 2001)
+    return A, out
+
+
+@pytest.mark.parametrize("m,n,b,q", [(12, 12, 4, 1), (14, 10, 3, 2), (9, 9, 2, 0), (10, 7, 7, 1),
+                                     (8, 8, 8, 0), (11, 11, 1, 1), (16, 13, 5, 2), (13, 13, 20, 1)])
+def test_matches_explicit_matrix_bruteforce(m, n, b, q):
+    rng = np.random.default_rng(m * 100 + n * 10 + b)
+    A = rng.standard_normal((m, n))
+    o = randutv(A, b, q, 77)
+    bf = randutv_bruteforce(A, b, q, 77)
+    # singular-vector signs may differ (LAPACK vs Jacobi); magnitudes are invariant
+    for key in ("T", "U", "V"):
+        assert np.max(np.abs(np.abs(o[key]) - np.abs(bf[key]))) <= 1e-13, key
+
+
+def test_c1_exact_invariants(c1):
+    A, o = c1
+    Uo, T, V = o["U"], o["T"], o["V"]
+    assert reconstruction_error(A, Uo, T, V) <= 1e-13
+    assert orthogonality_error(Uo) <= 1e-13
+    assert orthogonality_error(V) <= 1e-13
+    assert np.all(np.tril(T, -1) == 0.0)                 # exactly triangular (A15)
+    assert abs(np.linalg.norm(T) / np.linalg.norm(A) - 1) <= 1e-14
+    assert np.all(np.diag(T) >= 0)                       # A14
+
+
+def test_c1_log_det_closed_form(c1):
+    # tests/golden/small_cases.txt: c1_logdet = -2048
+    _, o = c1
+    s = np.sum(np.log10(np.abs(np.diag(o["T"]))))
+    assert abs(s - (-2048.0)) <= 1e-6
+
+
+def test_c1_weyl_log_majorisation(c1):
+    # diag(T) are T's eigenvalues; |lambda| are log-majorised by the singular values
+    _, o = c1
+    t = np.sort(np.abs(np.diag(o["T"])))[::-1]
+    sig = sigma_powspec(512)
+    assert np.all(np.cumsum(np.log(t)) <= np.cumsum(np.log(sig)) + 1e-9)
+
+
+def test_c1_diag_tracks_singular_values(c1):
+    # calibrated (not from the paper): P:227-236 says q = 1, 2 get "within striking
+    # distance" of the SVD and diag(T) approximates the singular values.
+    _, o = c1
+    rel = np.abs(np.abs(np.diag(o["T"])) / sigma_powspec(512) - 1)
+    assert np.median(rel) <= 1e-2 and np.max(rel) <= 0.3
+
+
+@pytest.mark.parametrize("k", [64, 128])
+def test_c1_rank_k_error_near_optimal_and_truncated_agrees(c1, k):
+    A, o = c1
+    sig = sigma_powspec(512)
+    Ak = o["U"][:, :k] @ o["T"][:k, :] @ o["V"].T
+    e2 = np.linalg.norm(A - Ak, 2)
+    ratio = e2 / sig[k]
+    assert 1.0 - 1e-9 <= ratio <= 1.5                    # Eckart-Young and the calibrated bound
+    rho_full = np.linalg.norm(o["T"][k:, k:])
+    assert abs(np.linalg.norm(A - Ak) - rho_full) <= 1e-12 * np.linalg.norm(A)
+    tr = randutv(A, 64, 2, 2001, k=k)
+    Ak_t = tr["Uk"] @ tr["Tk"] @ tr["V"].T
+    assert np.linalg.norm(Ak_t - Ak) <= 1e-12 * np.linalg.norm(A)
+    assert abs(tr["rho"] - rho_full) <= 1e-12 * np.linalg.norm(A)
+    assert abs(tr["rho"] - np.linalg.norm(A - Ak_t)) <= 1e-12 * np.linalg.norm(A)
+
+
+def test_b_at_least_n_reduces_to_svd():
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((40, 30))
+    o = randutv(A, 30, 1, 5)
+    s = np.linalg.svd(A, compute_uv=False)
+    assert np.max(np.abs(np.abs(np.diag(o["T"])) - s)) <= 1e-13 * s[0]
+    assert reconstruction_error(A, o["U"], o["T"], o["V"]) <= 1e-13
+
+
+def test_exact_low_rank_within_first_block():
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((96, 5))
+    Y = rng.standard_normal((96, 5))
+    A = X @ Y.T
+    o = randutv(A, 16, 1, 9)
+    s = np.linalg.svd(A, compute_uv=False)
+    d = np.abs(np.diag(o["T"]))
+    assert np.max(np.abs(d[:5] - s[:5]) / s[:5]) <= 1e-12
+    assert np.max(d[5:]) <= 1e-13 * s[0]
+    assert np.linalg.norm(o["T"][16:, 16:]) <= 1e-13 * s[0]
+
+
+def test_tall_and_ragged_and_thin_u():
+    rng = np.random.default_rng(6)
+    A = rng.standard_normal((150, 70))
+    o = randutv(A, 16, 1, 11)
+    assert reconstruction_error(A, o["U"], o["T"], o["V"]) <= 1e-13
+    assert np.all(np.tril(o["T"], -1) == 0.0)
+    assert np.all(o["T"][70:, :] == 0.0)
+    th = randutv(A, 16, 1, 11, thin_u=True)
+    assert np.max(np.abs(th["U"] - o["U"][:, :70])) <= 1e-13
+    assert np.array_equal(th["T"], o["T"])
+    tr = randutv(A, 16, 1, 11, k=40, thin_u=True)
+    Ak = tr["Uk"] @ tr["Tk"] @ tr["V"].T
+    assert abs(np.linalg.norm(A - Ak) - tr["rho"]) <= 1e-12 * np.linalg.norm(A)
+    assert orthogonality_error(tr["Uk"]) <= 1e-13
+
+
+def test_q_improves_rank_revealing():
+    A = make_numpy("powspec", 256, 256, cfg_index=1)
+    sig = sigma_powspec(256)
+    errs = {}
+    for q in (0, 2):
+        o = randutv(A, 32, q, 3)
+        errs[q] = np.mean(np.abs(np.abs(np.diag(o["T"])) / sig - 1))
+    assert errs[2] < errs[0]
+
+
+def test_zero_matrix_and_b1():
+    Z = np.zeros((10, 6))
+    o = randutv(Z, 4, 1, 1)
+    assert np.all(o["T"] == 0.0)
+    assert orthogonality_error(o["U"]) <= 1e-15 and orthogonality_error(o["V"]) <= 1e-15
+    rng = np.random.default_rng(8)
+    A = rng.standard_normal((9, 9))
+    o = randutv(A, 1, 1, 2)
+    assert reconstruction_error(A, o["U"], o["T"], o["V"]) <= 1e-13
+    assert abs(np.prod(np.abs(np.diag(o["T"]))) / abs(np.linalg.det(A)) - 1) <= 1e-12
+
+
+def test_seed_determinism():
+    rng = np.random.default_rng(10)
+    A = rng.standard_normal((40, 40))
+    o1 = randutv(A, 8, 1, 123)
+    o2 = randutv(A, 8, 1, 123)
+    o3 = randutv(A, 8, 1, 124)
+    assert np.array_equal(o1["T"], o2["T"])
+    assert not np.array_equal(o1["T"], o3["T"])
+
+
+def test_invalid_arguments():
+    with pytest.raises(ValueError):
+        randutv(np.zeros((3, 5)), 2, 1, 0)
+    with pytest.raises(ValueError):
+        randutv(np.zeros((5, 5)), 0, 1, 0)
