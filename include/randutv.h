@@ -1,0 +1,166 @@
+/*
+ * randutv.h -- C ABI of the B200-native randUTV library (librandutv.so).
+ *
+ * randUTV is the blocked randomized UTV factorization with power iteration of
+ * Heavner, Martinsson, Quintana-Orti, "Computing rank-revealing factorizations
+ * of matrices stored out-of-core" (arXiv:2002.06960), Sec. 3.1 (PAPER.md
+ * P:529-688):
+ *
+ *     A = U T V^T,   A: m x n (m >= n),  U: m x m and V: n x n orthogonal,
+ *                    T: m x n upper triangular
+ *
+ * built b columns at a time: per block a Gaussian G^(i), the
+ * sample Y = (A_t^T A_t)^q A_t^T G, a Householder QR of Y applied
+ * from the right, a Householder QR of the leading column block
+ * applied from the left and an SVD of the b x b diagonal block
+ * folded into U, T, V.  Conventions the paper leaves
+ * open are fixed in DESIGN.md ("Readings"): Philox4x32-10 G (A7), LAPACK dlarfg
+ * reflectors (A9), one-sided Jacobi SVD with tol sqrt(b)*2^-53 (A10), the final
+ * block (n - k <= b) is not sampled (A5), the right transform touches all m rows
+ * (A2).
+ *
+ * Common conventions
+ *   - Every matrix is column-major FP64 (IEEE binary64) with a leading dimension
+ *     ld >= rows.  Pointers are DEVICE pointers unless the function says host.
+ *   - The caller owns every buffer.  The library owns only its workspace, kept
+ *     in a randutv_ctx and grown on demand (one cudaMalloc per growth, never
+ *     inside the factorisation loop).
+ *   - All work is ordered on the ctx stream; every call synchronises that stream
+ *     before returning its status.
+ *   - Status codes (LAPACK "info" style):
+ *        0            success
+ *       -i            argument i (1-based, in the C signature) is invalid
+ *       +j            the Jacobi SVD of diagonal block j (1-based) did not
+ *                     converge in 30 sweeps; outputs are undefined
+ *       RANDUTV_ERR_* >= 1000: CUDA / allocation / non-finite-input failures
+ *   - No CPU fallback exists: without a CUDA device every compute entry point
+ *     returns RANDUTV_ERR_CUDA.
+ */
+#ifndef RANDUTV_H
+#define RANDUTV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RANDUTV_API __attribute__((visibility("default")))
+
+/* status codes >= 1000 */
+#define RANDUTV_ERR_CUDA      1000  /* a CUDA runtime call failed (message: randutv_last_error) */
+#define RANDUTV_ERR_ALLOC     1001  /* device workspace allocation failed                      */
+#define RANDUTV_ERR_NONFINITE 1002  /* A holds a NaN/Inf (only with RANDUTV_CHECK_FINITE)       */
+#define RANDUTV_ERR_CTX       1003  /* NULL or destroyed context                                */
+
+/* flags */
+#define RANDUTV_NO_UV         1u    /* do not build U and V ("no orthonormal matrices") */
+#define RANDUTV_CHECK_FINITE  2u    /* pre-scan A for NaN/Inf and fail with RANDUTV_ERR_NONFINITE    */
+
+typedef struct randutv_ctx randutv_ctx;
+
+/* Per-context counters, reset by randutv_reset_stats. */
+typedef struct randutv_stats {
+  int64_t kernel_launches;   /* kernels launched by the library on the ctx stream */
+  int64_t factorizations;    /* completed randutv_factor* calls                   */
+  int64_t workspace_bytes;   /* current device workspace size                     */
+  int64_t h2d_bytes;         /* host->device bytes copied (host-pointer entries)  */
+  int64_t d2h_bytes;         /* device->host bytes copied                          */
+} randutv_stats;
+
+/* Create a context on CUDA device `device`; `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  Returns 0 or RANDUTV_ERR_*.  *ctx owns device
+ * workspace only; destroy it with randutv_destroy. */
+RANDUTV_API int randutv_create(randutv_ctx** ctx, int device, void* stream);
+RANDUTV_API int randutv_destroy(randutv_ctx* ctx);
+/* Re-bind the ctx to another stream of the same device. */
+RANDUTV_API int randutv_set_stream(randutv_ctx* ctx, void* stream);
+
+/* Device workspace (bytes) the ctx grows to for an m x n problem with block b and
+ * power steps q.  Pure host arithmetic; 0 or -i. */
+RANDUTV_API int randutv_workspace_bytes(int64_t m, int64_t n, int64_t b, int q, unsigned flags,
+                                        size_t* bytes);
+
+/* Literal north-star form (BASELINE.json): factor the m x n matrix A (lda >= m).
+ *   U: m x m (ld m), T: m x n (ld m), V: n x n (ld n); all written.
+ *   A, U, T, V are either ALL device pointers or ALL host pointers; with host
+ *   pointers the call stages through device memory (whole-matrix copies on the
+ *   internal stream; counted in randutv_stats.h2d/d2h_bytes).  A is read only.
+ * Uses an internal context on the current CUDA device.
+ * Arguments: 1 m, 2 n, 3 A, 4 lda, 5 b (block size, >= 1), 6 q (power steps,
+ * >= 0), 7 seed (64-bit seed of G), 8 U, 9 T, 10 V. */
+RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int q,
+                               uint64_t seed, double* U, double* T, double* V);
+
+/* Full form on device pointers.
+ *   T: m x n (ldt >= m) receives the triangular factor; T may alias A exactly
+ *   (T == A and ldt == lda): A is then overwritten; any other overlap is -12.
+ *   U: m x m (ldu >= m) and V: n x n (ldv >= n); ignored (may be NULL) with
+ *   RANDUTV_NO_UV.
+ * Arguments: 1 ctx, 2 m, 3 n, 4 A, 5 lda, 6 b, 7 q, 8 seed, 9 flags, 10 U, 11 ldu,
+ * 12 T, 13 ldt, 14 V, 15 ldv. */
+RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda,
+                                  int64_t b, int q, uint64_t seed, unsigned flags,
+                                  double* U, int64_t ldu, double* T, int64_t ldt, double* V, int64_t ldv);
+
+/* Truncated rank-k variant: K = ceil(k/b) sampled steps, no final
+ * step (if K*b >= n - b + 1 the full factorisation runs and is truncated).
+ *   Uk: m x k (ldu >= m) = U(:, 0:k), formed by backward accumulation of the
+ *       left transforms (reading A12), never an m x m matrix
+ *   Tk: k x n (ldt >= k) = T(0:k, :)
+ *   V : n x n (ldv >= n)
+ *   *resid_fro (host) = ||T(k:m, k:n)||_F = ||A - Uk Tk V^T||_F
+ * Uk and V may be NULL with RANDUTV_NO_UV.  A is read only.
+ * Arguments: 1 ctx, 2 m, 3 n, 4 A, 5 lda, 6 k, 7 b, 8 q, 9 seed, 10 flags, 11 Uk,
+ * 12 ldu, 13 Tk, 14 ldt, 15 V, 16 ldv, 17 resid_fro. */
+RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda,
+                                    int64_t k, int64_t b, int q, uint64_t seed, unsigned flags,
+                                    double* Uk, int64_t ldu, double* Tk, int64_t ldt, double* V, int64_t ldv,
+                                    double* resid_fro);
+
+RANDUTV_API const char* randutv_status_string(int status);
+/* Last CUDA error message seen by any call of this thread ("" if none). */
+RANDUTV_API const char* randutv_last_error(void);
+RANDUTV_API int randutv_get_stats(randutv_ctx* ctx, randutv_stats* out);
+RANDUTV_API int randutv_reset_stats(randutv_ctx* ctx);
+
+/* ---------------------------------------------------------------------------
+ * Step-level entry points (the steps S1, S2/S3, S4/S6, S8 of SURVEY.md §8(a)),
+ * exported so each kernel can be parity-checked against the oracle on its own.
+ * Device pointers, ctx stream, synchronous like the rest.
+ * ------------------------------------------------------------------------- */
+
+/* S1: G(0:rows, 0:cols) of iteration `it` (reading A7: Philox4x32-10,
+ * counter (row>>1, col, it, 0), key (seed lo, seed hi), Box-Muller).
+ * Arguments: 1 ctx, 2 seed, 3 it, 4 rows, 5 cols, 6 G, 7 ldg. */
+RANDUTV_API int randutv_gaussian(randutv_ctx* ctx, uint64_t seed, int64_t it, int64_t rows, int64_t cols,
+                                 double* G, int64_t ldg);
+
+/* S2/S3/S5/S7: C := alpha op(A) op(B) + beta C with the library's FP64 DMMA
+ * GEMM (op(X) = X if trans == 0, X^T if trans == 1); C is M x N.  beta == 0
+ * never reads C.  Arguments: 1 ctx, 2 transa, 3 transb, 4 M, 5 N, 6 K, 7 alpha,
+ * 8 A, 9 lda, 10 B, 11 ldb, 12 beta, 13 C, 14 ldc. */
+RANDUTV_API int randutv_dgemm(randutv_ctx* ctx, int transa, int transb, int64_t M, int64_t N, int64_t K,
+                              double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                              double beta, double* C, int64_t ldc);
+
+/* S4/S6: Householder QR of the h x w panel P (h >= w, ldp >= h) in place, LAPACK
+ * dgeqrf layout (R on/above the diagonal, reflector tails below), tau (w),
+ * and the compact-WY factor Tf (w x w, ldtf >= w, upper triangular, forward
+ * columnwise: H_1...H_w = I - W Tf W^T).  Arguments: 1 ctx, 2 h, 3 w, 4 P, 5 ldp,
+ * 6 tau, 7 Tf, 8 ldtf. */
+RANDUTV_API int randutv_panel_qr(randutv_ctx* ctx, int64_t h, int64_t w, double* P, int64_t ldp,
+                                 double* tau, double* Tf, int64_t ldtf);
+
+/* S8: SVD of the w x w block B (ldb >= w, read only): B = Us diag(d) Vs^T, d >= 0
+ * descending, by one-sided Jacobi (reading A10).  Us, Vs: w x w (ld w).
+ * Returns +1 on non-convergence.  Arguments: 1 ctx, 2 w, 3 B, 4 ldb, 5 Us,
+ * 6 d, 7 Vs. */
+RANDUTV_API int randutv_small_svd(randutv_ctx* ctx, int64_t w, const double* B, int64_t ldb,
+                                  double* Us, double* d, double* Vs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RANDUTV_H */

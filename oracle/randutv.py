@@ -20,7 +20,7 @@ Follows Sec. 3.1 of the paper step by step, in the order of the FLAME loop
                                                                  Set_to_zero P:1577-1582)
    O7  T[k:m, k+b:n] -= W_U T_U^T (W_U^T T[k:m, k+b:n])  (A3)
        U[0:m, k:m]   -= (U[0:m,k:m] W_U) T_U W_U^T
-   O8  R = U_s diag(d) V_s^T (oracle.jacobi)
+   O8  R = U_s diag(d) V_s^T (oracle.jacobi.svd_block)
    O9  T[k:k+b,k:k+b] := diag(d); T[0:k, k:k+b] := T[0:k,k:k+b] V_s;
        T[k:k+b, k+b:n] := U_s^T T[k:k+b, k+b:n]; U[:,k:k+b] := U[:,k:k+b] U_s;
        V[:,k:k+b] := V[:,k:k+b] V_s                             (P:1359-1362)
@@ -40,7 +40,7 @@ import math
 import numpy as np
 
 from .householder import householder_qr, larft, unit_lower, upper_r
-from .jacobi import one_sided_jacobi
+from .jacobi import svd_block
 from .philox import gaussian_block
 
 
@@ -155,7 +155,7 @@ def _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin, record):
         XU = U[:, kk:]
         U[:, kk:] = XU - ((XU @ WU) @ TU) @ WU.T
     # O8, O9
-    Us, d, Vs, sweeps = one_sided_jacobi(R)
+    Us, d, Vs, sweeps = svd_block(R)
     _fold(T, U, V, kk, b, Us, d, Vs)
     if thin:
         lefts.append((kk, WU, TU, Us))
@@ -182,7 +182,7 @@ def _final_step(T, U, V, lefts, kk, thin, record):
         B = R
     else:
         B = np.array(T[kk:, kk:], order="F", copy=True)   # dense final block (O10)
-    Us, d, Vs, sweeps = one_sided_jacobi(B)
+    Us, d, Vs, sweeps = svd_block(B)
     _fold(T, U, V, kk, s, Us, d, Vs)
     if thin:
         lefts.append((kk, WU, TU, Us))

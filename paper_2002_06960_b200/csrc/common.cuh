@@ -1,0 +1,100 @@
+// Internal declarations shared by the librandutv.so translation units.
+// All matrices are column-major FP64; i64 sizes; device pointers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+
+#include "../../include/randutv.h"
+
+namespace rutv {
+
+typedef int64_t i64;
+
+constexpr int kNumSMs = 148;  // B200; launch heuristics only (never correctness)
+
+// Error plumbing: kernels are launched through these so the ctx can count them
+// and the first CUDA error is remembered for randutv_last_error().
+void set_last_error(const char* where, cudaError_t e);
+const char* last_error();
+
+struct Launch {
+  cudaStream_t stream;
+  int64_t* counter;  // incremented per kernel launch
+  int device_sms;
+  void count(int n = 1) const {
+    if (counter) *counter += n;
+  }
+};
+
+#define RUTV_CUDA(call)                                         \
+  do {                                                          \
+    cudaError_t e__ = (call);                                   \
+    if (e__ != cudaSuccess) {                                   \
+      ::rutv::set_last_error(#call, e__);                       \
+      return RANDUTV_ERR_CUDA;                                  \
+    }                                                           \
+  } while (0)
+
+#define RUTV_CHECK_LAUNCH(where)                                \
+  do {                                                          \
+    cudaError_t e__ = cudaGetLastError();                       \
+    if (e__ != cudaSuccess) {                                   \
+      ::rutv::set_last_error(where, e__);                       \
+      return RANDUTV_ERR_CUDA;                                  \
+    }                                                           \
+  } while (0)
+
+#define RUTV_TRY(expr)                                          \
+  do {                                                          \
+    int s__ = (expr);                                           \
+    if (s__ != 0) return s__;                                   \
+  } while (0)
+
+// ---------------------------------------------------------------- launchers
+// K1: G(rows x cols, ldg) of iteration `it` (philox.cu)
+int launch_gaussian(const Launch& L, uint64_t seed, i64 it, i64 rows, i64 cols, double* G, i64 ldg);
+
+// K2: C = alpha op(A) op(B) + beta C (dgemm.cu).  `ws`/`ws_elems`: split-K
+// partial buffer (may be null -> no split).
+int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha,
+                 const double* A, i64 lda, const double* B, i64 ldb, double beta, double* C, i64 ldc,
+                 double* ws, i64 ws_elems);
+
+// K3/K4: panel Householder QR (qr.cu).  P (h x w, ldp) factored in place; tau (w);
+// Wx: explicit unit-lower-trapezoidal W (h x w, ldw); Tf: compact-WY factor (w x w, ldtf).
+struct QrWork {
+  double* S;        // w x w  (W^T W)
+  double* tmp1;     // w x w
+  double* tmp2;     // h x w or w x (w)  trailing-update temporaries, >= h*nb and nb*w
+  double* tmp3;     // nb x w
+  double* partials; // leaf-kernel cross-CTA partial sums
+  i64 partials_elems;
+  double* gemm_ws;  // split-K buffer
+  i64 gemm_ws_elems;
+};
+int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, double* Wx, i64 ldw,
+             double* Tf, i64 ldtf, const QrWork& qw);
+i64 panel_qr_partials_elems(i64 h, i64 w);
+
+// K7: one-sided Jacobi SVD of the w x w block B (jacobi.cu).  `status`: device
+// int, set (atomicMin) to `block_id` (1-based) on non-convergence.
+int launch_jacobi_svd(const Launch& L, i64 w, const double* B, i64 ldb, double* Us, double* d, double* Vs,
+                      int* status, int block_id, double* scratch, i64 scratch_elems);
+i64 jacobi_scratch_elems(i64 w);
+
+// misc.cu
+int launch_set_identity(const Launch& L, i64 rows, i64 cols, double* X, i64 ldx);
+int launch_copy(const Launch& L, i64 rows, i64 cols, const double* S, i64 lds, double* D, i64 ldd);
+int launch_fill(const Launch& L, i64 rows, i64 cols, double v, double* X, i64 ldx);
+// zero the strictly lower part of the rows x cols block X (X = triu(X))
+int launch_triu(const Launch& L, i64 rows, i64 cols, double* X, i64 ldx);
+// X (w x w) := diag(d)
+int launch_set_diag(const Launch& L, i64 w, const double* d, double* X, i64 ldx);
+// partial sums of squares of a rows x cols block -> out[0] = ||X||_F^2 (deterministic)
+int launch_sumsq(const Launch& L, i64 rows, i64 cols, const double* X, i64 ldx, double* partial, double* out);
+// nonfinite scan: *flag = 1 if any NaN/Inf
+int launch_nonfinite(const Launch& L, i64 rows, i64 cols, const double* X, i64 ldx, int* flag);
+
+}  // namespace rutv

@@ -1,0 +1,259 @@
+// K2 -- the FP64 dense contractions of randUTV on the B200 tensor cores.
+//
+// Every flop-heavy step of the loop is a product of column blocks:
+//   S2/S3  Y = A_t^T G,  Z = A_t Y,  Y = A_t^T Z
+//   S5     Z = X W_V,  X -= (Z T_V) W_V^T  for X = T, V
+//   S7     Z = W_U^T X,  X -= W_U (T_U^T Z);  U likewise
+//   S9     the SVD folds A01 V_SVD, U_SVD^T A12, U1 U_SVD, V1 V_SVD
+// so one GEMM kernel C = alpha op(A) op(B) + beta C serves them all.
+//
+// sm_100a has no FP64 kind of tcgen05.mma (ptxas rejects .kind::f64), so FP64
+// tensor work is the warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4); the
+// measured chip peak is 37.0 TFLOP/s (profiles/fp64_peak_r01.json), equal to
+// the DFMA peak, and DMMA needs 8x fewer issue slots.  Design:
+//   * CTA tile 128 x 128, BK = 16, 256 threads = 8 warps (2 x 4), warp tile
+//     64 x 32 = 8 x 4 DMMA tiles, 64 FP64 accumulators per thread in registers.
+//   * Operands staged global -> shared with cp.async (16 B when the operand is
+//     16 B aligned with an even leading dimension, else 8 B), 4-stage ring.
+//     The shared layout follows the global contiguous dimension (m- or k-major)
+//     with a row pad of 4 doubles, which makes every fragment load conflict-free
+//     (the 16 lanes of each half-warp hit 16 distinct 8-byte bank pairs).
+//   * Skinny outputs with long K (A_t^T G, W^T X: K up to 262144) use split-K;
+//     partial tiles go to a workspace and a second kernel sums them in a fixed
+//     order, so results are bitwise deterministic run to run.
+#include "common.cuh"
+
+namespace rutv {
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
+constexpr int PAD = 4;
+constexpr int A_ELEMS = (BK * (BM + PAD) > BM * (BK + PAD)) ? BK * (BM + PAD) : BM * (BK + PAD);
+constexpr int B_ELEMS = (BK * (BN + PAD) > BN * (BK + PAD)) ? BK * (BN + PAD) : BN * (BK + PAD);
+constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+template <int VEC>
+__device__ __forceinline__ void cp_async(uint32_t dst, const double* src, int src_bytes) {
+  if constexpr (VEC == 2) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// Copy one Lc x Lo tile (Lc along the global contiguous dimension) into shared
+// memory rows of length Lc + PAD.  lim_c / lim_o: first invalid global index.
+template <int Lc, int Lo, int VEC>
+__device__ __forceinline__ void load_tile(double* sm, const double* __restrict__ g, i64 ld, i64 c0, i64 o0,
+                                          i64 lim_c, i64 lim_o, int tid) {
+  constexpr int CPR = Lc / VEC;           // chunks per row
+  constexpr int NCH = CPR * Lo;           // chunks per tile
+  static_assert(NCH % THREADS == 0, "tile/threads mismatch");
+#pragma unroll
+  for (int it = 0; it < NCH / THREADS; ++it) {
+    const int ch = tid + it * THREADS;
+    const int o = ch / CPR;
+    const int ci = (ch % CPR) * VEC;
+    const i64 gc = c0 + ci, go = o0 + o;
+    i64 nvalid = lim_c - gc;
+    nvalid = nvalid < 0 ? 0 : (nvalid > VEC ? VEC : nvalid);
+    if (go >= lim_o) nvalid = 0;
+    const double* src = nvalid > 0 ? g + gc + go * ld : g;
+    cp_async<VEC>(smem_u32(sm + o * (Lc + PAD) + ci), src, (int)(nvalid * 8));
+  }
+}
+
+template <bool TA, bool TB, int VA, int VB>
+__global__ void __launch_bounds__(THREADS, 1)
+    dgemm_kernel(i64 M, i64 N, i64 K, double alpha, const double* __restrict__ A, i64 lda,
+                 const double* __restrict__ B, i64 ldb, double beta, double* __restrict__ C, i64 ldc,
+                 i64 kchunk, double* __restrict__ part) {
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const i64 m0 = (i64)blockIdx.x * BM, n0 = (i64)blockIdx.y * BN;
+  const i64 kb = (i64)blockIdx.z * kchunk;
+  const i64 ke = (kb + kchunk < K) ? kb + kchunk : K;
+  const int ktiles = ke > kb ? (int)((ke - kb + BK - 1) / BK) : 0;
+
+  auto load_stage = [&](int stage, int kt) {
+    double* As = smem + stage * STAGE_ELEMS;
+    double* Bs = As + A_ELEMS;
+    const i64 k0 = kb + (i64)kt * BK;
+    if constexpr (!TA) load_tile<BM, BK, VA>(As, A, lda, m0, k0, M, ke, tid);   // rows: k, contiguous m
+    else load_tile<BK, BM, VA>(As, A, lda, k0, m0, ke, M, tid);                 // rows: m, contiguous k
+    if constexpr (!TB) load_tile<BK, BN, VB>(Bs, B, ldb, k0, n0, ke, N, tid);   // rows: n, contiguous k
+    else load_tile<BN, BK, VB>(Bs, B, ldb, n0, k0, N, ke, tid);                 // rows: k, contiguous n
+  };
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < ktiles) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double* As = smem + (kt % STAGES) * STAGE_ELEMS;
+    const double* Bs = As + A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const int k = kk * 4 + t;
+      double a[8], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) {
+        const int row = wm * 64 + mi * 8 + g;
+        a[mi] = TA ? As[row * (BK + PAD) + k] : As[k * (BM + PAD) + row];
+      }
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int col = wn * 32 + ni * 8 + g;
+        b[ni] = TB ? Bs[k * (BN + PAD) + col] : Bs[col * (BK + PAD) + k];
+      }
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni], a[mi], b[ni]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: lane holds C[row g][cols 2t, 2t+1] of each 8x8 tile
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi) {
+    const i64 row = m0 + wm * 64 + mi * 8 + g;
+    if (row >= M) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const i64 col = n0 + wn * 32 + ni * 8 + 2 * t + e;
+        if (col >= N) continue;
+        if (part) {
+          part[(i64)blockIdx.z * M * N + row + col * M] = acc[mi][ni][e];
+        } else {
+          double* cp = C + row + col * ldc;
+          const double v = alpha * acc[mi][ni][e];
+          *cp = (beta == 0.0) ? v : v + beta * (*cp);
+        }
+      }
+    }
+  }
+}
+
+__global__ void splitk_reduce_kernel(i64 M, i64 N, int splits, double alpha, const double* __restrict__ part,
+                                     double beta, double* __restrict__ C, i64 ldc) {
+  const i64 total = M * N;
+  for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += part[(i64)z * total + idx];
+    const i64 row = idx % M, col = idx / M;
+    double* cp = C + row + col * ldc;
+    const double v = alpha * s;
+    *cp = (beta == 0.0) ? v : v + beta * (*cp);
+  }
+}
+
+template <bool TA, bool TB, int VA, int VB>
+int launch_t(const Launch& L, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+             i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
+  static bool attr_set = false;  // per instantiation; first call from any ctx
+  if (!attr_set) {
+    RUTV_CUDA(cudaFuncSetAttribute(dgemm_kernel<TA, TB, VA, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)SMEM_BYTES));
+    attr_set = true;
+  }
+  dgemm_kernel<TA, TB, VA, VB><<<grid, THREADS, SMEM_BYTES, L.stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C,
+                                                                       ldc, kchunk, part);
+  L.count();
+  RUTV_CHECK_LAUNCH("dgemm_kernel");
+  return 0;
+}
+
+template <bool TA, bool TB>
+int launch_v(const Launch& L, int va, int vb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+             const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
+  if (va == 2 && vb == 2) return launch_t<TA, TB, 2, 2>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (va == 2) return launch_t<TA, TB, 2, 1>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (vb == 2) return launch_t<TA, TB, 1, 2>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  return launch_t<TA, TB, 1, 1>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+}
+
+inline int vec_of(const double* p, i64 ld) {
+  return (((uintptr_t)p & 15) == 0 && (ld % 2) == 0) ? 2 : 1;
+}
+
+}  // namespace
+
+int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                 const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
+  if (M <= 0 || N <= 0) return 0;
+  const i64 gm = (M + BM - 1) / BM, gn = (N + BN - 1) / BN;
+  if (gn > 65535) return -5;
+  const i64 tiles = gm * gn;
+  i64 splits = 1;
+  const i64 target = 2 * (i64)L.device_sms;
+  if (ws && K > 0 && tiles < target) {
+    splits = (target + tiles - 1) / tiles;
+    const i64 maxk = K / (8 * BK);  // at least 128 of K per split
+    if (splits > maxk) splits = maxk;
+    const i64 maxws = ws_elems / (M * N);
+    if (splits > maxws) splits = maxws;
+    if (splits > 64) splits = 64;
+    if (splits < 1) splits = 1;
+  }
+  i64 kchunk = K;
+  if (splits > 1) {
+    kchunk = ((K + splits - 1) / splits + BK - 1) / BK * BK;
+    splits = (K + kchunk - 1) / kchunk;
+  }
+  if (kchunk <= 0) kchunk = 1;
+  const int va = vec_of(A, lda), vb = vec_of(B, ldb);
+  dim3 grid((unsigned)gm, (unsigned)gn, (unsigned)splits);
+  double* part = splits > 1 ? ws : nullptr;
+  int st;
+  if (!ta && !tb) st = launch_v<false, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  else if (ta && !tb) st = launch_v<true, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  else if (!ta && tb) st = launch_v<false, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  else st = launch_v<true, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (st) return st;
+  if (splits > 1) {
+    const i64 total = M * N;
+    i64 blocks = (total + 255) / 256;
+    if (blocks > (i64)L.device_sms * 8) blocks = (i64)L.device_sms * 8;
+    splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, L.stream>>>(M, N, (int)splits, alpha, ws, beta, C, ldc);
+    L.count();
+    RUTV_CHECK_LAUNCH("splitk_reduce_kernel");
+  }
+  return 0;
+}
+
+}  // namespace rutv

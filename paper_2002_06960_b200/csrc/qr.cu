@@ -1,0 +1,300 @@
+// K3/K4 -- S4 and S6 of SURVEY.md §8(a): unpivoted Householder QR of a tall
+// panel and its compact-WY factor.
+//
+// Paper: "[Y, T_V] := unpivoted_QR(Y)" and "[[A11; A21], T_U] := unpivoted_QR(...)"
+// (Fig. fig:FLArandutv), with W_V / W_U "the unit
+// lower trapezoidal matrices stored below the diagonal" and the
+// transforms applied as X - X W T W^T.  Sec. 3.1 steps 1-2
+// (P:570-582).  Conventions (reading A9): LAPACK dlarfg
+// reflectors -- xi = ||x'||; xi == 0 -> tau = 0; else beta = -sign(alpha)
+// hypot(alpha, xi), tau = (beta - alpha)/beta, v = (1, x'/(alpha - beta)) -- and
+// the dlarft forward/columnwise factor, Q = H_1...H_w = I - W T W^T.
+//
+// Structure (right-looking blocked QR with leaf width NB = 32):
+//   for each leaf L of NB columns:
+//     qr_leaf_kernel   cooperative grid over the panel rows.  Per column: ONE
+//                      grid-wide barrier.  Each CTA forms, over its rows, the
+//                      partial ||x'||^2 and the partial dots x'.P(:,l) of the
+//                      *unscaled* column with the later leaf columns; after the
+//                      barrier every CTA reduces the partials in the same fixed
+//                      order (bitwise identical beta, tau, w in every CTA) and
+//                      updates its own rows, so no second barrier is needed.
+//                      The NB x NB top block is replicated in every CTA's
+//                      shared memory and updated identically by all of them.
+//     extract_w        explicit W columns (unit diagonal, zeros above)
+//     S = W^T W_L      DMMA GEMM (K = h - c0, split-K)
+//     larft_leaf       T_L from S_LL and tau (one warp, NB^3/6 flops)
+//     T merge          T(0:c0, L) = -T(0:c0,0:c0) S(0:c0, L) T_L   (2 GEMMs)
+//     trailing update  P(c0:h, L+:) -= W_L T_L^T (W_L^T P(c0:h, L+:))  (3 GEMMs)
+// The leaf kernel is bound by L2 latency and the per-column barrier; the
+// GEMMs carry the O(h w^2) flops.  All reductions are fixed-order, so the
+// factorisation is bitwise deterministic (required for the redundant QR(Y) on
+// every rank of the multi-GPU layout).
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rutv {
+
+namespace {
+
+constexpr int NB = 32;
+constexpr int LEAF_THREADS = 256;
+constexpr int LEAF_MAX_CTAS = 128;
+constexpr int PSTRIDE = NB + 1;  // partial record: [0] = ||x'||^2, [1+l] = x'.P(:,l)
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// P points at the panel's top-left element (row 0, col 0); the leaf is columns
+// [c0, c0+nb), rows [c0, h).  Rows [c0, c0+nb) form the replicated top block;
+// rows [c0+nb, h) are split into contiguous slabs, one per CTA.
+__global__ void __launch_bounds__(LEAF_THREADS)
+    qr_leaf_kernel(double* __restrict__ P, i64 h, i64 ldp, i64 c0, int nb, double* __restrict__ tau,
+                   double* __restrict__ partials) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double TB[NB][NB + 1];  // TB[r][c]: top-block row r, leaf column c
+  __shared__ double wred[LEAF_THREADS / 32][PSTRIDE];
+  __shared__ double tot[PSTRIDE];
+  __shared__ double wv[NB];
+  __shared__ double sc[4];  // tau, scal, beta, flag
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, cta = blockIdx.x;
+  double* L0 = P + c0 + c0 * ldp;  // leaf top-left
+  const i64 slab_rows = h - c0 - nb;
+  const i64 per = (slab_rows + G - 1) / G;
+  const i64 rb = nb + (i64)cta * per;
+  i64 re = rb + per;
+  if (re > nb + slab_rows) re = nb + slab_rows;
+
+  for (int e = tid; e < NB * NB; e += LEAF_THREADS) {
+    const int r = e % NB, c = e / NB;
+    TB[r][c] = (r < nb && c < nb) ? L0[r + (i64)c * ldp] : 0.0;
+  }
+  __syncthreads();
+
+  for (int j = 0; j < nb; ++j) {
+    // ---------------- phase A: partial sums over this CTA's rows
+    double acc[PSTRIDE];
+#pragma unroll
+    for (int l = 0; l < PSTRIDE; ++l) acc[l] = 0.0;
+    const double* xcol = L0 + (i64)j * ldp;
+    for (i64 r = rb + tid; r < re; r += LEAF_THREADS) {
+      const double x = xcol[r];
+      acc[0] += x * x;
+#pragma unroll
+      for (int l = 0; l < NB; ++l)
+        if (l > j && l < nb) acc[1 + l] += x * L0[r + (i64)l * ldp];
+    }
+    if (cta == 0) {  // the top-block rows below the diagonal count once (CTA 0)
+      for (int r = j + 1 + tid; r < nb; r += LEAF_THREADS) {
+        const double x = TB[r][j];
+        acc[0] += x * x;
+#pragma unroll
+        for (int l = 0; l < NB; ++l)
+          if (l > j && l < nb) acc[1 + l] += x * TB[r][l];
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < PSTRIDE; ++l) {
+      const double s = warp_sum(acc[l]);
+      if (lane == 0) wred[warp][l] = s;
+    }
+    __syncthreads();
+    double* pj = partials + (size_t)(j & 1) * G * PSTRIDE;
+    if (tid < PSTRIDE) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < LEAF_THREADS / 32; ++w) s += wred[w][tid];
+      pj[(size_t)cta * PSTRIDE + tid] = s;
+    }
+    grid.sync();
+    // ---------------- phase B: every CTA reduces the partials in CTA order
+    if (tid < PSTRIDE) {
+      double s = 0.0;
+      for (int c = 0; c < G; ++c) s += pj[(size_t)c * PSTRIDE + tid];
+      tot[tid] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double alpha = TB[j][j];
+      const double xi = sqrt(tot[0]);
+      if (xi == 0.0) {
+        sc[0] = 0.0;
+        sc[1] = 0.0;
+        sc[2] = alpha;
+        sc[3] = 0.0;
+      } else {
+        const double beta = -copysign(hypot(alpha, xi), alpha);
+        sc[0] = (beta - alpha) / beta;
+        sc[1] = 1.0 / (alpha - beta);
+        sc[2] = beta;
+        sc[3] = 1.0;
+      }
+    }
+    __syncthreads();
+    const double t = sc[0], scal = sc[1];
+    const bool active = sc[3] != 0.0;
+    if (tid < NB) wv[tid] = (active && tid > j && tid < nb) ? TB[j][tid] + scal * tot[1 + tid] : 0.0;
+    __syncthreads();
+    if (active) {
+      // own slab rows
+      double* xw = L0 + (i64)j * ldp;
+      for (i64 r = rb + tid; r < re; r += LEAF_THREADS) {
+        const double v = xw[r] * scal;
+        xw[r] = v;
+        const double tv = t * v;
+#pragma unroll
+        for (int l = 0; l < NB; ++l)
+          if (l > j && l < nb) L0[r + (i64)l * ldp] -= tv * wv[l];
+      }
+      // replicated top block: rows > j, then the pivot row j
+      for (int r = j + 1 + tid; r < nb; r += LEAF_THREADS) {
+        const double v = TB[r][j] * scal;
+        TB[r][j] = v;
+        const double tv = t * v;
+        for (int l = j + 1; l < nb; ++l) TB[r][l] -= tv * wv[l];
+      }
+      if (tid > j && tid < nb) TB[j][tid] -= t * wv[tid];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      TB[j][j] = sc[2];
+      if (cta == 0) tau[c0 + j] = t;
+    }
+    __syncthreads();
+  }
+  if (cta == 0) {
+    for (int e = tid; e < nb * nb; e += LEAF_THREADS) {
+      const int r = e % nb, c = e / nb;
+      L0[r + (i64)c * ldp] = TB[r][c];
+    }
+  }
+}
+
+// Wx(0:h, c0:c0+w) := explicit reflectors of the factored columns (unit diag, 0 above).
+__global__ void extract_w_kernel(const double* __restrict__ P, i64 ldp, i64 h, i64 c0, i64 w,
+                                 double* __restrict__ Wx, i64 ldw) {
+  const i64 total = h * w;
+  for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
+    const i64 r = idx % h, cl = idx / h, c = c0 + cl;
+    double v;
+    if (r > c) v = P[r + c * ldp];
+    else v = (r == c) ? 1.0 : 0.0;
+    Wx[r + c * ldw] = v;
+  }
+}
+
+// T(c0:c0+w, c0:c0+w) from S = W^T W (same block) and tau: T_jj = tau_j,
+// T(0:j, j) = -tau_j T(0:j,0:j) S(0:j, j)   (dlarft, forward, columnwise).  One warp.
+__global__ void larft_leaf_kernel(const double* __restrict__ S, i64 lds, const double* __restrict__ tau, int w,
+                                  double* __restrict__ T, i64 ldt) {
+  __shared__ double Ts[NB][NB + 1];
+  __shared__ double Ss[NB][NB + 1];
+  const int lane = threadIdx.x;
+  for (int e = lane; e < w * w; e += 32) {
+    const int r = e % w, c = e / w;
+    Ss[r][c] = S[r + (i64)c * lds];
+    Ts[r][c] = 0.0;
+  }
+  __syncwarp();
+  for (int j = 0; j < w; ++j) {
+    const double tj = tau[j];
+    double v = 0.0;
+    if (lane < j && tj != 0.0) {
+      double s = 0.0;
+      for (int l = lane; l < j; ++l) s += Ts[lane][l] * Ss[l][j];
+      v = -tj * s;
+    }
+    __syncwarp();
+    if (lane < j) Ts[lane][j] = v;
+    if (lane == j) Ts[j][j] = tj;
+    __syncwarp();
+  }
+  for (int e = lane; e < w * w; e += 32) {
+    const int r = e % w, c = e / w;
+    T[r + (i64)c * ldt] = Ts[r][c];
+  }
+}
+
+int leaf_ctas(i64 slab_rows) {
+  i64 g = (slab_rows + LEAF_THREADS - 1) / LEAF_THREADS;
+  if (g < 1) g = 1;
+  if (g > LEAF_MAX_CTAS) g = LEAF_MAX_CTAS;
+  return (int)g;
+}
+
+}  // namespace
+
+i64 panel_qr_partials_elems(i64 h, i64 w) {
+  (void)h;
+  (void)w;
+  return 2 * (i64)LEAF_MAX_CTAS * PSTRIDE;
+}
+
+int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, double* Wx, i64 ldw, double* Tf,
+             i64 ldtf, const QrWork& qw) {
+  if (w <= 0) return 0;
+  if (h < w) return -2;
+  for (i64 c0 = 0; c0 < w; c0 += NB) {
+    const int wl = (int)((w - c0) < NB ? (w - c0) : NB);
+    // ---- leaf factorisation (cooperative grid)
+    {
+      const int G = leaf_ctas(h - c0 - wl);
+      double* Pp = P;
+      i64 hh = h, ld = ldp, cc = c0;
+      int nbv = wl;
+      double* taup = tau;
+      double* part = qw.partials;
+      void* args[] = {&Pp, &hh, &ld, &cc, &nbv, &taup, &part};
+      RUTV_CUDA(cudaLaunchCooperativeKernel((void*)qr_leaf_kernel, dim3(G), dim3(LEAF_THREADS), args, 0, L.stream));
+      L.count();
+    }
+    // ---- explicit W for this leaf
+    {
+      const i64 total = h * wl;
+      i64 blocks = (total + 255) / 256;
+      if (blocks > (i64)L.device_sms * 8) blocks = (i64)L.device_sms * 8;
+      extract_w_kernel<<<(unsigned)blocks, 256, 0, L.stream>>>(P, ldp, h, c0, wl, Wx, ldw);
+      L.count();
+      RUTV_CHECK_LAUNCH("extract_w_kernel");
+    }
+    // ---- S(0:c0+wl, L) = W(c0:h, 0:c0+wl)^T W(c0:h, L)
+    double* SL = qw.S + c0 * w;  // S stored w x w, ld w
+    RUTV_TRY(launch_dgemm(L, true, false, c0 + wl, wl, h - c0, 1.0, Wx + c0, ldw, Wx + c0 + c0 * ldw, ldw, 0.0,
+                          SL, w, qw.gemm_ws, qw.gemm_ws_elems));
+    // ---- T_LL
+    larft_leaf_kernel<<<1, 32, 0, L.stream>>>(SL + c0, w, tau + c0, wl, Tf + c0 + c0 * ldtf, ldtf);
+    L.count();
+    RUTV_CHECK_LAUNCH("larft_leaf_kernel");
+    // ---- T(0:c0, L) = -T(0:c0,0:c0) S(0:c0,L) T_LL
+    if (c0 > 0) {
+      RUTV_TRY(launch_dgemm(L, false, false, c0, wl, c0, 1.0, Tf, ldtf, SL, w, 0.0, qw.tmp1, c0, nullptr, 0));
+      RUTV_TRY(launch_dgemm(L, false, false, c0, wl, wl, -1.0, qw.tmp1, c0, Tf + c0 + c0 * ldtf, ldtf, 0.0,
+                            Tf + c0 * ldtf, ldtf, nullptr, 0));
+    }
+    // ---- zero T(L, 0:c0) (strictly lower part of the w x w factor)
+    if (c0 > 0) RUTV_TRY(launch_fill(L, wl, c0, 0.0, Tf + c0, ldtf));
+    // ---- trailing panel update C -= W_L T_LL^T (W_L^T C), C = P(c0:h, c0+wl:w)
+    const i64 nrest = w - c0 - wl;
+    if (nrest > 0) {
+      double* Cp = P + c0 + (c0 + wl) * ldp;
+      const double* WL = Wx + c0 + c0 * ldw;
+      RUTV_TRY(launch_dgemm(L, true, false, wl, nrest, h - c0, 1.0, WL, ldw, Cp, ldp, 0.0, qw.tmp3, wl,
+                            qw.gemm_ws, qw.gemm_ws_elems));
+      RUTV_TRY(launch_dgemm(L, true, false, wl, nrest, wl, 1.0, Tf + c0 + c0 * ldtf, ldtf, qw.tmp3, wl, 0.0,
+                            qw.tmp2, wl, nullptr, 0));
+      RUTV_TRY(launch_dgemm(L, false, false, h - c0, nrest, wl, -1.0, WL, ldw, qw.tmp2, wl, 1.0, Cp, ldp, nullptr,
+                            0));
+    }
+  }
+  return 0;
+}
+
+}  // namespace rutv

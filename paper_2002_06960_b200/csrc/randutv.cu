@@ -1,0 +1,677 @@
+// randUTV driver and C ABI (include/randutv.h).
+//
+// The host side of the hot path: one right-looking loop over column blocks of
+// width b (FLAME Fig. fig:FLArandutv P:1311-1363), every
+// step a handful of kernels on the ctx stream, all data resident in HBM:
+//
+//   sampled step i (s = n - k > b), k = i b, r = m - k, A_t = T(k:m, k:n):
+//     S1  G = gaussian(seed, i)                      r x b
+//     S2  Y = A_t^T G                                 s x b
+//     S3  q x { Z = A_t Y ; Y = A_t^T Z }                          (A8)
+//     S4  [W_V, tau_V, T_V] = QR(Y)
+//     S5  T(:, k:n) -= (T(:,k:n) W_V) T_V W_V^T   (all m rows, A2)
+//         V(:, k:n) -= (V(:,k:n) W_V) T_V W_V^T
+//     S6  [W_U, tau_U, T_U] = QR(T(k:m, k:k+b)); keep R, zero below
+//     S7  T(k:m, k+b:n) -= W_U T_U^T (W_U^T T(k:m, k+b:n))   (A3)
+//         U(:, k:m) -= (U(:,k:m) W_U) T_U W_U^T
+//     S8  R = U_s diag(d) V_s^T  (Jacobi)
+//     S9  T11 = diag(d); T01 V_s; U_s^T T12; U1 U_s; V1 V_s
+//   final step (s <= b): QR if tall, SVD of R or of the dense block, fold (A5, O10)
+//   truncated: K = ceil(k/b) sampled steps, rho = ||T(k:m,k:n)||_F, U_k by
+//   backward accumulation of (W_U, T_U, U_s) (A12)
+//
+// Workspace is carved from one cudaMalloc per ctx (grown on demand, never in
+// the loop).  No CPU fallback: every arithmetic step is a kernel in this .so.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include "common.cuh"
+
+using rutv::i64;
+
+namespace rutv {
+
+static thread_local char g_last_error[512] = "";
+
+void set_last_error(const char* where, cudaError_t e) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+const char* last_error() { return g_last_error; }
+
+}  // namespace rutv
+
+struct randutv_ctx {
+  int magic;
+  int device;
+  cudaStream_t stream;
+  int sms;
+  void* ws;
+  size_t ws_bytes;
+  randutv_stats stats;
+  // host-staging buffers of the literal (host pointer) entry
+  double* stage;
+  size_t stage_bytes;
+};
+
+static const int kMagic = 0x52555456;  // "RUTV"
+
+namespace {
+
+using namespace rutv;
+
+constexpr i64 kAlign = 256;
+
+struct Carver {
+  char* base;
+  size_t off;
+  size_t cap;
+  bool dry;
+  template <typename Tp>
+  Tp* take(i64 elems) {
+    size_t bytes = ((size_t)(elems > 0 ? elems : 1) * sizeof(Tp) + kAlign - 1) / kAlign * kAlign;
+    Tp* p = dry ? nullptr : reinterpret_cast<Tp*>(base + off);
+    off += bytes;
+    return p;
+  }
+};
+
+// All per-call device buffers.
+struct Work {
+  double *G, *Y, *Z, *Z2, *Wv, *Wu, *TV, *TU, *tauV, *tauU;
+  double *Us, *Vs, *d;
+  double *jac, *gemm_ws, *red, *scal;
+  i64 jac_elems, gemm_ws_elems;
+  int *status, *flag;
+  QrWork qw;
+  double* lefts;  // truncated-U records
+  i64 lefts_elems;
+  double* Twork;  // m x n working T for the truncated variant
+};
+
+i64 gemm_ws_elems_for(i64 m, i64 n, i64 b) {
+  const i64 mx = m > n ? m : n;
+  i64 e = 4 * mx * b;
+  if (e < (1 << 20)) e = 1 << 20;
+  return e;
+}
+
+// lefts record per step: W_U (m x b) + T_U (b x b) + U_s (b x b)
+i64 lefts_elems_for(i64 m, i64 b, i64 K) { return K * (m * b + 2 * b * b); }
+
+size_t carve(Carver& c, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork) {
+  const i64 mx = m > n ? m : n;
+  w.G = c.take<double>(m * b);
+  w.Y = c.take<double>(n * b);
+  w.Z = c.take<double>(mx * b);
+  w.Z2 = c.take<double>(mx * b);
+  w.Wv = c.take<double>(n * b);
+  w.Wu = c.take<double>(m * b);
+  w.TV = c.take<double>(b * b);
+  w.TU = c.take<double>(b * b);
+  w.tauV = c.take<double>(b);
+  w.tauU = c.take<double>(b);
+  w.Us = c.take<double>(b * b);
+  w.Vs = c.take<double>(b * b);
+  w.d = c.take<double>(b);
+  w.jac_elems = jacobi_scratch_elems(b);
+  w.jac = c.take<double>(w.jac_elems);
+  w.gemm_ws_elems = gemm_ws_elems_for(m, n, b);
+  w.gemm_ws = c.take<double>(w.gemm_ws_elems);
+  w.red = c.take<double>(1024);
+  w.scal = c.take<double>(16);
+  w.status = c.take<int>(16);
+  w.flag = w.status + 4;
+  w.qw.S = c.take<double>(b * b);
+  w.qw.tmp1 = c.take<double>(b * 32);
+  w.qw.tmp2 = c.take<double>(32 * b);
+  w.qw.tmp3 = c.take<double>(32 * b);
+  w.qw.partials_elems = panel_qr_partials_elems(mx, b);
+  w.qw.partials = c.take<double>(w.qw.partials_elems);
+  w.qw.gemm_ws = w.gemm_ws;
+  w.qw.gemm_ws_elems = w.gemm_ws_elems;
+  w.lefts_elems = lefts_K > 0 ? lefts_elems_for(m, b, lefts_K) : 0;
+  w.lefts = lefts_K > 0 ? c.take<double>(w.lefts_elems) : nullptr;
+  w.Twork = twork ? c.take<double>(m * n) : nullptr;
+  return c.off;
+}
+
+int ensure_ws(randutv_ctx* ctx, size_t bytes) {
+  if (ctx->ws_bytes >= bytes) return 0;
+  if (ctx->ws) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_bytes = 0;
+  }
+  cudaError_t e = cudaMalloc(&ctx->ws, bytes);
+  if (e != cudaSuccess) {
+    set_last_error("cudaMalloc(workspace)", e);
+    cudaGetLastError();
+    return RANDUTV_ERR_ALLOC;
+  }
+  ctx->ws_bytes = bytes;
+  ctx->stats.workspace_bytes = (int64_t)bytes;
+  return 0;
+}
+
+int prepare(randutv_ctx* ctx, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork) {
+  Carver dry{nullptr, 0, 0, true};
+  const size_t need = carve(dry, w, m, n, b, lefts_K, twork);
+  RUTV_TRY(ensure_ws(ctx, need));
+  Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
+  carve(real, w, m, n, b, lefts_K, twork);
+  return 0;
+}
+
+struct Problem {
+  i64 m, n, b;
+  int q;
+  uint64_t seed;
+  double* T;
+  i64 ldt;
+  double* U;  // forward m x m accumulation (may be null)
+  i64 ldu;
+  double* V;  // n x n (may be null)
+  i64 ldv;
+  bool record_lefts;
+};
+
+i64 sampled_steps(i64 n, i64 b) { return n > b ? (n - b + b - 1) / b : 0; }
+
+// X(rows x s, ldx) -= ((X W) Tf) W^T : the right application of Q = I - W Tf W^T
+int apply_right(const Launch& L, Work& w, i64 rows, i64 s, i64 bw, double* X, i64 ldx, const double* W, i64 ldw,
+                const double* Tf, i64 ldtf) {
+  RUTV_TRY(launch_dgemm(L, false, false, rows, bw, s, 1.0, X, ldx, W, ldw, 0.0, w.Z, rows, w.gemm_ws,
+                        w.gemm_ws_elems));
+  RUTV_TRY(launch_dgemm(L, false, false, rows, bw, bw, 1.0, w.Z, rows, Tf, ldtf, 0.0, w.Z2, rows, nullptr, 0));
+  RUTV_TRY(launch_dgemm(L, false, true, rows, s, bw, -1.0, w.Z2, rows, W, ldw, 1.0, X, ldx, nullptr, 0));
+  return 0;
+}
+
+// X(r x c) -= W Tf^T (W^T X): the left application of Q^T
+int apply_left_t(const Launch& L, Work& w, i64 r, i64 c, i64 bw, double* X, i64 ldx, const double* W, i64 ldw,
+                 const double* Tf, i64 ldtf) {
+  if (c <= 0) return 0;
+  RUTV_TRY(launch_dgemm(L, true, false, bw, c, r, 1.0, W, ldw, X, ldx, 0.0, w.Z, bw, w.gemm_ws, w.gemm_ws_elems));
+  RUTV_TRY(launch_dgemm(L, true, false, bw, c, bw, 1.0, Tf, ldtf, w.Z, bw, 0.0, w.Z2, bw, nullptr, 0));
+  RUTV_TRY(launch_dgemm(L, false, false, r, c, bw, -1.0, W, ldw, w.Z2, bw, 1.0, X, ldx, nullptr, 0));
+  return 0;
+}
+
+// X(rows x bw) := X M  (M bw x bw), via Z
+int right_mult_inplace(const Launch& L, Work& w, i64 rows, i64 bw, double* X, i64 ldx, const double* M, i64 ldm) {
+  if (rows <= 0) return 0;
+  RUTV_TRY(launch_dgemm(L, false, false, rows, bw, bw, 1.0, X, ldx, M, ldm, 0.0, w.Z, rows, nullptr, 0));
+  return launch_copy(L, rows, bw, w.Z, rows, X, ldx);
+}
+
+// X(bw x cols) := M^T X
+int left_mult_t_inplace(const Launch& L, Work& w, i64 bw, i64 cols, double* X, i64 ldx, const double* M, i64 ldm) {
+  if (cols <= 0) return 0;
+  RUTV_TRY(launch_dgemm(L, true, false, bw, cols, bw, 1.0, M, ldm, X, ldx, 0.0, w.Z, bw, w.gemm_ws,
+                        w.gemm_ws_elems));
+  return launch_copy(L, bw, cols, w.Z, bw, X, ldx);
+}
+
+// S8 + S9 for a bw x bw diagonal block at (kk, kk).  `B` is the block to
+// decompose (T11 itself).
+int svd_and_fold(const Launch& L, Work& w, const Problem& P, i64 kk, i64 bw, int block_id) {
+  double* T11 = P.T + kk + kk * P.ldt;
+  RUTV_TRY(launch_jacobi_svd(L, bw, T11, P.ldt, w.Us, w.d, w.Vs, w.status, block_id, w.jac, w.jac_elems));
+  RUTV_TRY(launch_set_diag(L, bw, w.d, T11, P.ldt));
+  RUTV_TRY(right_mult_inplace(L, w, kk, bw, P.T + kk * P.ldt, P.ldt, w.Vs, bw));                 // A01 V_s
+  RUTV_TRY(left_mult_t_inplace(L, w, bw, P.n - kk - bw, P.T + kk + (kk + bw) * P.ldt, P.ldt, w.Us, bw));  // U_s^T A12
+  if (P.U) RUTV_TRY(right_mult_inplace(L, w, P.m, bw, P.U + kk * P.ldu, P.ldu, w.Us, bw));         // U1 U_s
+  if (P.V) RUTV_TRY(right_mult_inplace(L, w, P.n, bw, P.V + kk * P.ldv, P.ldv, w.Vs, bw));         // V1 V_s
+  return 0;
+}
+
+int record_left(const Launch& L, Work& w, const Problem& P, int step, i64 r, i64 bw, bool has_w) {
+  const i64 b = P.b;
+  double* rec = w.lefts + (i64)step * (P.m * b + 2 * b * b);
+  if (has_w) {
+    RUTV_TRY(launch_copy(L, r, bw, w.Wu, r, rec, r));
+    RUTV_TRY(launch_copy(L, bw, bw, w.TU, b, rec + P.m * b, bw));
+  }
+  RUTV_TRY(launch_copy(L, bw, bw, w.Us, bw, rec + P.m * b + b * b, bw));
+  return 0;
+}
+
+int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
+  const i64 m = P.m, n = P.n, b = P.b, kk = i * b, r = m - kk, s = n - kk;
+  double* At = P.T + kk + kk * P.ldt;
+  // S1, S2, S3
+  RUTV_TRY(launch_gaussian(L, P.seed, i, r, b, w.G, r));
+  RUTV_TRY(launch_dgemm(L, true, false, s, b, r, 1.0, At, P.ldt, w.G, r, 0.0, w.Y, s, w.gemm_ws, w.gemm_ws_elems));
+  for (int qq = 0; qq < P.q; ++qq) {
+    RUTV_TRY(launch_dgemm(L, false, false, r, b, s, 1.0, At, P.ldt, w.Y, s, 0.0, w.Z, r, w.gemm_ws,
+                          w.gemm_ws_elems));
+    RUTV_TRY(launch_dgemm(L, true, false, s, b, r, 1.0, At, P.ldt, w.Z, r, 0.0, w.Y, s, w.gemm_ws,
+                          w.gemm_ws_elems));
+  }
+  // S4
+  RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
+  // S5: all m rows of T(:, k:n); V(:, k:n)
+  RUTV_TRY(apply_right(L, w, m, s, b, P.T + kk * P.ldt, P.ldt, w.Wv, s, w.TV, b));
+  if (P.V) RUTV_TRY(apply_right(L, w, n, s, b, P.V + kk * P.ldv, P.ldv, w.Wv, s, w.TV, b));
+  // S6: QR of the column block in place; keep R, zero below
+  RUTV_TRY(panel_qr(L, r, b, At, P.ldt, w.tauU, w.Wu, r, w.TU, b, w.qw));
+  RUTV_TRY(launch_triu(L, b, b, At, P.ldt));
+  RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, P.ldt));
+  // S7
+  RUTV_TRY(apply_left_t(L, w, r, s - b, b, At + b * P.ldt, P.ldt, w.Wu, r, w.TU, b));
+  if (P.U) RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
+  // S8, S9
+  RUTV_TRY(svd_and_fold(L, w, P, kk, b, (int)(i + 1)));
+  if (P.record_lefts) RUTV_TRY(record_left(L, w, P, (int)i, r, b, true));
+  return 0;
+}
+
+int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
+  const i64 m = P.m, n = P.n, kk = i * P.b, r = m - kk, s = n - kk;
+  if (s <= 0) return 0;
+  double* At = P.T + kk + kk * P.ldt;
+  const bool tall = r > s;
+  if (tall) {
+    RUTV_TRY(panel_qr(L, r, s, At, P.ldt, w.tauU, w.Wu, r, w.TU, P.b, w.qw));
+    RUTV_TRY(launch_triu(L, s, s, At, P.ldt));
+    RUTV_TRY(launch_fill(L, r - s, s, 0.0, At + s, P.ldt));
+    if (P.U) RUTV_TRY(apply_right(L, w, m, r, s, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, P.b));
+  }
+  RUTV_TRY(svd_and_fold(L, w, P, kk, s, (int)(i + 1)));
+  if (P.record_lefts) {
+    // T_U of the final step has leading dimension b in w.TU; record_left copies with ld b
+    RUTV_TRY(record_left(L, w, P, (int)i, r, s, tall));
+  }
+  return 0;
+}
+
+// Runs steps [0, nsteps) (sampled) and the final step if `with_final`.
+int run_loop(const Launch& L, Work& w, const Problem& P, i64 nsteps, bool with_final) {
+  for (i64 i = 0; i < nsteps; ++i) RUTV_TRY(sampled_step(L, w, P, i));
+  if (with_final) RUTV_TRY(final_step(L, w, P, nsteps));
+  return 0;
+}
+
+int begin_call(randutv_ctx* ctx) {
+  if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
+  RUTV_CUDA(cudaSetDevice(ctx->device));
+  return 0;
+}
+
+int finish(randutv_ctx* ctx, const Work& w) {
+  int status = 0x7f7f7f7f;
+  RUTV_CUDA(cudaMemcpyAsync(&status, w.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+  RUTV_CUDA(cudaGetLastError());
+  if (status != 0x7f7f7f7f) return status;  // 1-based block of a non-converged SVD
+  return 0;
+}
+
+int start_status(randutv_ctx* ctx, const Work& w) {
+  RUTV_CUDA(cudaMemsetAsync(w.status, 0x7f, sizeof(int), ctx->stream));  // 0x7f7f7f7f
+  return 0;
+}
+
+int check_finite(randutv_ctx* ctx, const Launch& L, const Work& w, i64 m, i64 n, const double* A, i64 lda) {
+  RUTV_CUDA(cudaMemsetAsync(w.flag, 0, sizeof(int), ctx->stream));
+  RUTV_TRY(launch_nonfinite(L, m, n, A, lda, w.flag));
+  int flag = 0;
+  RUTV_CUDA(cudaMemcpyAsync(&flag, w.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+  return flag ? RANDUTV_ERR_NONFINITE : 0;
+}
+
+bool overlaps(const double* a, size_t abytes, const double* b, size_t bbytes) {
+  const char *pa = (const char*)a, *pb = (const char*)b;
+  return pa < pb + bbytes && pb < pa + abytes;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+RANDUTV_API int randutv_create(randutv_ctx** out, int device, void* stream) {
+  if (!out) return -1;
+  *out = nullptr;
+  int ndev = 0;
+  RUTV_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return -2;
+  RUTV_CUDA(cudaSetDevice(device));
+  int sms = 0;
+  RUTV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  randutv_ctx* c = new (std::nothrow) randutv_ctx();
+  if (!c) return RANDUTV_ERR_ALLOC;
+  c->magic = kMagic;
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  c->sms = sms;
+  *out = c;
+  return 0;
+}
+
+RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
+  if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->stage) cudaFree(ctx->stage);
+  ctx->magic = 0;
+  delete ctx;
+  return 0;
+}
+
+RANDUTV_API int randutv_set_stream(randutv_ctx* ctx, void* stream) {
+  if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
+  ctx->stream = (cudaStream_t)stream;
+  return 0;
+}
+
+RANDUTV_API int randutv_get_stats(randutv_ctx* ctx, randutv_stats* out) {
+  if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
+  if (!out) return -2;
+  *out = ctx->stats;
+  return 0;
+}
+
+RANDUTV_API int randutv_reset_stats(randutv_ctx* ctx) {
+  if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
+  const int64_t ws = ctx->stats.workspace_bytes;
+  memset(&ctx->stats, 0, sizeof(ctx->stats));
+  ctx->stats.workspace_bytes = ws;
+  return 0;
+}
+
+RANDUTV_API const char* randutv_last_error(void) { return rutv::last_error(); }
+
+RANDUTV_API const char* randutv_status_string(int s) {
+  if (s == 0) return "success";
+  if (s < 0) return "invalid argument (see the 1-based index in the status)";
+  if (s == RANDUTV_ERR_CUDA) return "CUDA runtime error (randutv_last_error has the message)";
+  if (s == RANDUTV_ERR_ALLOC) return "device workspace allocation failed";
+  if (s == RANDUTV_ERR_NONFINITE) return "input matrix holds NaN or Inf";
+  if (s == RANDUTV_ERR_CTX) return "invalid or destroyed context";
+  return "Jacobi SVD of a diagonal block did not converge (status = 1-based block index)";
+}
+
+RANDUTV_API int randutv_workspace_bytes(int64_t m, int64_t n, int64_t b, int q, unsigned flags, size_t* bytes) {
+  if (m < n) return -1;
+  if (n < 1) return -2;
+  if (b < 1) return -3;
+  if (q < 0) return -4;
+  if (!bytes) return -6;
+  (void)flags;
+  const i64 bb = b < n ? b : n;
+  Work w;
+  Carver dry{nullptr, 0, 0, true};
+  *bytes = carve(dry, w, m, n, bb, 0, false);
+  return 0;
+}
+
+RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b,
+                                  int q, uint64_t seed, unsigned flags, double* U, int64_t ldu, double* T,
+                                  int64_t ldt, double* V, int64_t ldv) {
+  RUTV_TRY(begin_call(ctx));
+  const bool uv = !(flags & RANDUTV_NO_UV);
+  if (n < 1) return -3;
+  if (m < n) return -2;
+  if (!A) return -4;
+  if (lda < m) return -5;
+  if (b < 1) return -6;
+  if (q < 0) return -7;
+  if (uv && !U) return -10;
+  if (uv && ldu < m) return -11;
+  if (!T) return -12;
+  if (ldt < m) return -13;
+  if (uv && !V) return -14;
+  if (uv && ldv < n) return -15;
+  const bool alias = (T == A);
+  if (alias && ldt != lda) return -13;
+  if (!alias && overlaps(A, (size_t)lda * n * 8, T, (size_t)ldt * n * 8)) return -12;
+  const i64 bb = b < n ? b : n;
+  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Work w;
+  RUTV_TRY(prepare(ctx, w, m, n, bb, 0, false));
+  if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
+  RUTV_TRY(start_status(ctx, w));
+  if (!alias) RUTV_CUDA(cudaMemcpy2DAsync(T, ldt * 8, A, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (uv) {
+    RUTV_TRY(launch_set_identity(L, m, m, U, ldu));
+    RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
+  }
+  Problem P{m, n, bb, q, seed, T, ldt, uv ? U : nullptr, ldu, uv ? V : nullptr, ldv, false};
+  const i64 nsamp = sampled_steps(n, bb);
+  RUTV_TRY(run_loop(L, w, P, nsamp, true));
+  const int st = finish(ctx, w);
+  if (st == 0) ctx->stats.factorizations++;
+  return st;
+}
+
+RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t k,
+                                    int64_t b, int q, uint64_t seed, unsigned flags, double* Uk, int64_t ldu,
+                                    double* Tk, int64_t ldt, double* V, int64_t ldv, double* resid_fro) {
+  RUTV_TRY(begin_call(ctx));
+  const bool uv = !(flags & RANDUTV_NO_UV);
+  if (n < 1) return -3;
+  if (m < n) return -2;
+  if (!A) return -4;
+  if (lda < m) return -5;
+  if (k < 1 || k > n) return -6;
+  if (b < 1) return -7;
+  if (q < 0) return -8;
+  if (uv && !Uk) return -11;
+  if (uv && ldu < m) return -12;
+  if (!Tk) return -13;
+  if (ldt < k) return -14;
+  if (uv && !V) return -15;
+  if (uv && ldv < n) return -16;
+  if (!resid_fro) return -17;
+  const i64 bb = b < n ? b : n;
+  const i64 nsamp = sampled_steps(n, bb);
+  i64 K = (k + bb - 1) / bb;
+  bool with_final = false;
+  if (K > nsamp) {
+    K = nsamp;
+    with_final = true;
+  }
+  const i64 nrec = uv ? K + (with_final ? 1 : 0) : 0;
+  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Work w;
+  RUTV_TRY(prepare(ctx, w, m, n, bb, nrec, true));
+  if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
+  RUTV_TRY(start_status(ctx, w));
+  RUTV_CUDA(cudaMemcpy2DAsync(w.Twork, m * 8, A, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (uv) RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
+  Problem P{m, n, bb, q, seed, w.Twork, m, nullptr, m, uv ? V : nullptr, ldv, uv};
+  RUTV_TRY(run_loop(L, w, P, K, with_final));
+  // rho = ||T(k:m, k:n)||_F
+  RUTV_TRY(launch_sumsq(L, m - k, n - k, w.Twork + k + k * m, m, w.red, w.scal));
+  // Tk = T(0:k, :)
+  RUTV_CUDA(cudaMemcpy2DAsync(Tk, ldt * 8, w.Twork, m * 8, k * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (uv) {
+    // U_k = U^(1) ... U^(p) [I_k; 0], backward (A12)
+    RUTV_TRY(launch_set_identity(L, m, k, Uk, ldu));
+    for (i64 j = nrec - 1; j >= 0; --j) {
+      const i64 kj = j * bb;
+      if (kj >= k) continue;
+      const bool fin = with_final && j == nrec - 1;
+      const i64 wj = fin ? n - kj : bb;
+      const i64 rj = m - kj;
+      const bool has_w = !fin || rj > wj;
+      const double* rec = w.lefts + j * (m * bb + 2 * bb * bb);
+      const i64 cols = k - kj;
+      double* X = Uk + kj + kj * ldu;  // rows kj.., cols kj..k
+      // X(0:wj, :) = U_s X(0:wj, :)
+      RUTV_TRY(launch_dgemm(L, false, false, wj, cols, wj, 1.0, rec + m * bb + bb * bb, wj, X, ldu, 0.0, w.Z, wj,
+                            nullptr, 0));
+      RUTV_TRY(launch_copy(L, wj, cols, w.Z, wj, X, ldu));
+      if (has_w) {
+        // X(kj:m) -= W (T (W^T X))
+        RUTV_TRY(launch_dgemm(L, true, false, wj, cols, rj, 1.0, rec, rj, X, ldu, 0.0, w.Z, wj, w.gemm_ws,
+                              w.gemm_ws_elems));
+        RUTV_TRY(launch_dgemm(L, false, false, wj, cols, wj, 1.0, rec + m * bb, wj, w.Z, wj, 0.0, w.Z2, wj,
+                              nullptr, 0));
+        RUTV_TRY(launch_dgemm(L, false, false, rj, cols, wj, -1.0, rec, rj, w.Z2, wj, 1.0, X, ldu, nullptr, 0));
+      }
+    }
+  }
+  double ss = 0.0;
+  RUTV_CUDA(cudaMemcpyAsync(&ss, w.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  const int st = finish(ctx, w);
+  *resid_fro = std::sqrt(ss);
+  if (st == 0) ctx->stats.factorizations++;
+  return st;
+}
+
+// ----------------------------------------------------------------- literal form
+
+static std::mutex g_lit_mu;
+static randutv_ctx* g_lit_ctx[64];
+
+static int literal_ctx(randutv_ctx** out) {
+  int dev = 0;
+  RUTV_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return RANDUTV_ERR_CTX;
+  std::lock_guard<std::mutex> lk(g_lit_mu);
+  if (!g_lit_ctx[dev]) RUTV_TRY(randutv_create(&g_lit_ctx[dev], dev, nullptr));
+  *out = g_lit_ctx[dev];
+  return 0;
+}
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int q, uint64_t seed,
+                               double* U, double* T, double* V) {
+  if (n < 1) return -2;
+  if (m < n) return -1;
+  if (!A) return -3;
+  if (lda < m) return -4;
+  if (b < 1) return -5;
+  if (q < 0) return -6;
+  if (!U) return -8;
+  if (!T) return -9;
+  if (!V) return -10;
+  randutv_ctx* ctx = nullptr;
+  RUTV_TRY(literal_ctx(&ctx));
+  const bool dev = is_device_ptr(A);
+  if (dev != is_device_ptr(T) || dev != is_device_ptr(U) || dev != is_device_ptr(V)) return -9;
+  if (dev) return randutv_factor_ex(ctx, m, n, A, lda, b, q, seed, 0u, U, m, T, m, V, n);
+  // host pointers: stage through device memory (A -> dT in place, U, V)
+  const size_t need = ((size_t)m * n + (size_t)m * m + (size_t)n * n) * sizeof(double);
+  if (ctx->stage_bytes < need) {
+    if (ctx->stage) cudaFree(ctx->stage);
+    ctx->stage = nullptr;
+    ctx->stage_bytes = 0;
+    cudaError_t e = cudaMalloc(&ctx->stage, need);
+    if (e != cudaSuccess) {
+      rutv::set_last_error("cudaMalloc(stage)", e);
+      cudaGetLastError();
+      return RANDUTV_ERR_ALLOC;
+    }
+    ctx->stage_bytes = need;
+  }
+  double* dT = ctx->stage;
+  double* dU = dT + (size_t)m * n;
+  double* dV = dU + (size_t)m * m;
+  RUTV_CUDA(cudaMemcpy2DAsync(dT, m * 8, A, lda * 8, m * 8, n, cudaMemcpyHostToDevice, ctx->stream));
+  ctx->stats.h2d_bytes += (int64_t)m * n * 8;
+  int st = randutv_factor_ex(ctx, m, n, dT, m, b, q, seed, 0u, dU, m, dT, m, dV, n);
+  if (st < 0 || st >= 1000) return st;
+  RUTV_CUDA(cudaMemcpyAsync(T, dT, (size_t)m * n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RUTV_CUDA(cudaMemcpyAsync(U, dU, (size_t)m * m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RUTV_CUDA(cudaMemcpyAsync(V, dV, (size_t)n * n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->stats.d2h_bytes += (int64_t)((size_t)m * n + (size_t)m * m + (size_t)n * n) * 8;
+  return st;
+}
+
+// --------------------------------------------------------------- step entries
+
+RANDUTV_API int randutv_gaussian(randutv_ctx* ctx, uint64_t seed, int64_t it, int64_t rows, int64_t cols, double* G,
+                                 int64_t ldg) {
+  RUTV_TRY(begin_call(ctx));
+  if (it < 0) return -3;
+  if (rows < 0) return -4;
+  if (cols < 0) return -5;
+  if (!G && rows * cols > 0) return -6;
+  if (ldg < rows || ldg < 1) return -7;
+  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  RUTV_TRY(launch_gaussian(L, seed, it, rows, cols, G, ldg));
+  RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+RANDUTV_API int randutv_dgemm(randutv_ctx* ctx, int transa, int transb, int64_t M, int64_t N, int64_t K,
+                              double alpha, const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                              double* C, int64_t ldc) {
+  RUTV_TRY(begin_call(ctx));
+  if (transa != 0 && transa != 1) return -2;
+  if (transb != 0 && transb != 1) return -3;
+  if (M < 0) return -4;
+  if (N < 0) return -5;
+  if (K < 0) return -6;
+  const i64 arows = transa ? K : M, brows = transb ? N : K;
+  if (lda < (arows > 1 ? arows : 1)) return -9;
+  if (ldb < (brows > 1 ? brows : 1)) return -11;
+  if (ldc < (M > 1 ? M : 1)) return -14;
+  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  // split-K scratch from the workspace
+  const size_t need = (size_t)4 * (size_t)(M > 0 ? M : 1) * (size_t)(N > 0 ? N : 1) * 8 + (1 << 20);
+  RUTV_TRY(ensure_ws(ctx, need));
+  RUTV_TRY(launch_dgemm(L, transa != 0, transb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
+                        (double*)ctx->ws, (i64)(ctx->ws_bytes / 8)));
+  RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+RANDUTV_API int randutv_panel_qr(randutv_ctx* ctx, int64_t h, int64_t wdt, double* P, int64_t ldp, double* tau,
+                                 double* Tf, int64_t ldtf) {
+  RUTV_TRY(begin_call(ctx));
+  if (wdt < 1) return -3;
+  if (h < wdt) return -2;
+  if (!P) return -4;
+  if (ldp < h) return -5;
+  if (!tau) return -6;
+  if (!Tf) return -7;
+  if (ldtf < wdt) return -8;
+  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Work w;
+  RUTV_TRY(prepare(ctx, w, h, wdt, wdt, 0, false));
+  RUTV_TRY(panel_qr(L, h, wdt, P, ldp, tau, w.Wu, h, Tf, ldtf, w.qw));
+  RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+  RUTV_CUDA(cudaGetLastError());
+  return 0;
+}
+
+RANDUTV_API int randutv_small_svd(randutv_ctx* ctx, int64_t wdt, const double* B, int64_t ldb, double* Us, double* d,
+                                  double* Vs) {
+  RUTV_TRY(begin_call(ctx));
+  if (wdt < 1) return -2;
+  if (!B) return -3;
+  if (ldb < wdt) return -4;
+  if (!Us) return -5;
+  if (!d) return -6;
+  if (!Vs) return -7;
+  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Work w;
+  RUTV_TRY(prepare(ctx, w, wdt, wdt, wdt, 0, false));
+  RUTV_TRY(start_status(ctx, w));
+  RUTV_TRY(launch_jacobi_svd(L, wdt, B, ldb, Us, d, Vs, w.status, 1, w.jac, w.jac_elems));
+  return finish(ctx, w);
+}
+
+}  // extern "C"

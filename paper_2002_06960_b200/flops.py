@@ -1,0 +1,64 @@
+"""Algorithmic flop model of randUTV -- measurement only.
+
+Counts what the method computes per sampled step i (k = i b, r = m - k,
+s = n - k), following the steps of Sec. 3.1 / Fig. fig:FLArandutv:
+  sample         2 (1 + 2q) r s b
+  QR(Y)          3 s b^2 - b^3   (Householder, ~2(sb^2 - b^3/3) + T factor)
+  right update   4 m s b + m b^2                       (all m rows)
+  V update       4 n s b + n b^2
+  QR(col)        3 r b^2 - b^3
+  left update    4 r (s-b) b + (s-b) b^2
+  U update       4 m r b + m b^2   (forward m x m U)
+  folds          2 b^2 (k + s - b) for T, 2 b^2 (m + n) for U, V
+final step (s <= b): 3 r s^2 - s^3 + 4 m r s + m s^2 if tall, folds 2 s^2 (k + m + n).
+Truncated (K sampled steps) with U_k by backward accumulation replaces the
+forward U term by sum_j 4 (m - k_j)(k - k_j) b + 2 b^2 (k - k_j).
+The Jacobi SVD (O(b^3) per step) and the RNG are not counted.
+Square asymptotics: (12 + 4q)/3 n^3 (T only) + 4 n^3 (U and V).
+"""
+
+
+def sampled_steps(n, b):
+    return (n - b + b - 1) // b if n > b else 0
+
+
+def randutv_flops(m, n, b, q, build_uv=True, k=None):
+    b = min(b, n)
+    nsamp = sampled_steps(n, b)
+    K = nsamp
+    with_final = True
+    if k is not None:
+        K = -(-k // b)
+        if K > nsamp:
+            K = nsamp
+        else:
+            with_final = False
+    F = 0.0
+    for i in range(K):
+        kk = i * b
+        r, s = m - kk, n - kk
+        F += 2 * (1 + 2 * q) * r * s * b
+        F += 3 * s * b * b - b ** 3
+        F += 4 * m * s * b + m * b * b
+        F += 3 * r * b * b - b ** 3
+        F += 4 * r * (s - b) * b + (s - b) * b * b
+        F += 2 * b * b * (kk + s - b)
+        if build_uv:
+            F += 4 * n * s * b + n * b * b
+            F += 2 * b * b * n
+            if k is None:
+                F += 4 * m * r * b + m * b * b + 2 * b * b * m
+            else:
+                F += 4 * r * max(k - kk, 0) * b + 2 * b * b * max(k - kk, 0)
+    if with_final:
+        kk = K * b
+        r, s = m - kk, n - kk
+        if s > 0:
+            if r > s:
+                F += 3 * r * s * s - s ** 3
+                if build_uv:
+                    F += 4 * m * r * s + m * s * s
+            F += 2 * s * s * kk
+            if build_uv:
+                F += 2 * s * s * (m + n)
+    return float(F)

@@ -1,0 +1,256 @@
+"""Python binding of librandutv.so (include/randutv.h) -- argument marshalling only.
+
+Every arithmetic step of randUTV runs in the CUDA kernels of the shared
+library; this module only converts torch tensors / numpy arrays into pointers,
+leading dimensions and the ctx stream, and raises on a non-zero status.  There
+is no CPU fallback: if the library is missing, importing a compute function
+raises.
+
+Column-major convention: a column-major m x n FP64 matrix on the device is a
+torch tensor of shape (m, n) with strides (1, ld), e.g. ``colmajor(m, n)``.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librandutv.so")
+
+RANDUTV_NO_UV = 1
+RANDUTV_CHECK_FINITE = 2
+RANDUTV_ERR_CUDA = 1000
+RANDUTV_ERR_ALLOC = 1001
+RANDUTV_ERR_NONFINITE = 1002
+RANDUTV_ERR_CTX = 1003
+
+# name -> (restype, argtypes) ; mirrors include/randutv.h
+_i64, _u64, _int, _uint, _dbl, _vp = (ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint,
+                                      ctypes.c_double, ctypes.c_void_p)
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("kernel_launches", ctypes.c_int64), ("factorizations", ctypes.c_int64),
+                ("workspace_bytes", ctypes.c_int64), ("h2d_bytes", ctypes.c_int64),
+                ("d2h_bytes", ctypes.c_int64)]
+
+
+SIGNATURES = {
+    "randutv_create": (_int, [ctypes.POINTER(_vp), _int, _vp]),
+    "randutv_destroy": (_int, [_vp]),
+    "randutv_set_stream": (_int, [_vp, _vp]),
+    "randutv_workspace_bytes": (_int, [_i64, _i64, _i64, _int, _uint, ctypes.POINTER(ctypes.c_size_t)]),
+    "randutv_factor": (_int, [_i64, _i64, _vp, _i64, _i64, _int, _u64, _vp, _vp, _vp]),
+    "randutv_factor_ex": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint,
+                                 _vp, _i64, _vp, _i64, _vp, _i64]),
+    "randutv_factor_rank": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _int, _u64, _uint,
+                                   _vp, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(_dbl)]),
+    "randutv_status_string": (ctypes.c_char_p, [_int]),
+    "randutv_last_error": (ctypes.c_char_p, []),
+    "randutv_get_stats": (_int, [_vp, ctypes.POINTER(Stats)]),
+    "randutv_reset_stats": (_int, [_vp]),
+    "randutv_gaussian": (_int, [_vp, _u64, _i64, _i64, _i64, _vp, _i64]),
+    "randutv_dgemm": (_int, [_vp, _int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64]),
+    "randutv_panel_qr": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64]),
+    "randutv_small_svd": (_int, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
+}
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load librandutv.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                           " (there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class RandUTVError(RuntimeError):
+    def __init__(self, fn, status):
+        lib = load_library()
+        msg = lib.randutv_status_string(status).decode()
+        if status == RANDUTV_ERR_CUDA:
+            msg += ": " + lib.randutv_last_error().decode()
+        super().__init__(f"{fn} returned {status} ({msg})")
+        self.status = status
+
+
+def _check(fn, status, allow_positive=False):
+    if status != 0 and not (allow_positive and 0 < status < 1000):
+        raise RandUTVError(fn, status)
+    return status
+
+
+# ----------------------------------------------------------------------------- tensors
+
+def colmajor(m, n, device="cuda", fill=None):
+    """Column-major m x n float64 tensor (shape (m, n), strides (1, m))."""
+    import torch
+    t = torch.empty((n, m), dtype=torch.float64, device=device).t()
+    if fill is not None:
+        t.fill_(fill)
+    return t
+
+
+def as_colmajor(X):
+    """Column-major copy (or the tensor itself if already column-major with ld >= rows)."""
+    import torch
+    m, n = X.shape
+    if X.dtype == torch.float64 and X.stride(0) == 1 and X.stride(1) >= max(m, 1):
+        return X
+    Y = colmajor(m, n, device=X.device)
+    Y.copy_(X)
+    return Y
+
+
+def _ld(X):
+    if X.dim() != 2 or X.stride(0) != 1:
+        raise ValueError("expected a column-major 2-D float64 tensor (stride(0) == 1)")
+    return max(X.stride(1), 1) if X.shape[1] > 1 else max(X.shape[0], 1)
+
+
+def _ptr(X):
+    return ctypes.c_void_p(X.data_ptr()) if X is not None else None
+
+
+class Context:
+    """A randutv_ctx bound to a CUDA device and stream (torch's current stream by default)."""
+
+    def __init__(self, device=None, stream=None):
+        import torch
+        self.lib = load_library()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        h = ctypes.c_void_p()
+        _check("randutv_create", self.lib.randutv_create(ctypes.byref(h), self.device,
+                                                          ctypes.c_void_p(stream.cuda_stream)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.randutv_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stats(self):
+        s = Stats()
+        _check("randutv_get_stats", self.lib.randutv_get_stats(self.h, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+    def reset_stats(self):
+        _check("randutv_reset_stats", self.lib.randutv_reset_stats(self.h))
+
+    # ---------------------------------------------------------------- factorisations
+    def randutv_factor_ex(self, A, b, q, seed, build_uv=True, U=None, T=None, V=None, flags=0,
+                          allow_nonconvergence=False):
+        """Full randUTV of the column-major device matrix A: returns (U, T, V, status)."""
+        m, n = A.shape
+        if not build_uv:
+            flags |= RANDUTV_NO_UV
+        if T is None:
+            T = colmajor(m, n, device=A.device)
+        if build_uv:
+            U = colmajor(m, m, device=A.device) if U is None else U
+            V = colmajor(n, n, device=A.device) if V is None else V
+        st = self.lib.randutv_factor_ex(self.h, m, n, _ptr(A), _ld(A), int(b), int(q), int(seed) & (2**64 - 1),
+                                        flags, _ptr(U), _ld(U) if U is not None else 1, _ptr(T), _ld(T),
+                                        _ptr(V), _ld(V) if V is not None else 1)
+        _check("randutv_factor_ex", st, allow_positive=allow_nonconvergence)
+        return U, T, V, st
+
+    def randutv_factor_rank(self, A, k, b, q, seed, build_uv=True, flags=0):
+        """Truncated randUTV: returns (Uk, Tk, V, rho)."""
+        m, n = A.shape
+        if not build_uv:
+            flags |= RANDUTV_NO_UV
+        Tk = colmajor(k, n, device=A.device)
+        Uk = colmajor(m, k, device=A.device) if build_uv else None
+        V = colmajor(n, n, device=A.device) if build_uv else None
+        rho = ctypes.c_double()
+        st = self.lib.randutv_factor_rank(self.h, m, n, _ptr(A), _ld(A), int(k), int(b), int(q),
+                                          int(seed) & (2**64 - 1), flags, _ptr(Uk), _ld(Uk) if Uk is not None else 1,
+                                          _ptr(Tk), _ld(Tk), _ptr(V), _ld(V) if V is not None else 1,
+                                          ctypes.byref(rho))
+        _check("randutv_factor_rank", st)
+        return Uk, Tk, V, rho.value
+
+    # ---------------------------------------------------------------- step entries
+    def randutv_gaussian(self, seed, it, rows, cols, G=None):
+        G = colmajor(rows, cols) if G is None else G
+        _check("randutv_gaussian", self.lib.randutv_gaussian(self.h, int(seed) & (2**64 - 1), int(it), rows, cols,
+                                                             _ptr(G), max(rows, 1) if G.shape[1] <= 1 else _ld(G)))
+        return G
+
+    def randutv_dgemm(self, transa, transb, A, B, C, alpha=1.0, beta=0.0):
+        M, N = C.shape
+        K = A.shape[0] if transa else A.shape[1]
+        _check("randutv_dgemm", self.lib.randutv_dgemm(self.h, int(transa), int(transb), M, N, K, float(alpha),
+                                                       _ptr(A), _ld(A), _ptr(B), _ld(B), float(beta), _ptr(C),
+                                                       _ld(C)))
+        return C
+
+    def randutv_panel_qr(self, P):
+        """In-place Householder QR of the column-major panel P: returns (P, tau, Tf)."""
+        import torch
+        h, w = P.shape
+        tau = torch.empty(w, dtype=torch.float64, device=P.device)
+        Tf = colmajor(w, w, device=P.device)
+        _check("randutv_panel_qr", self.lib.randutv_panel_qr(self.h, h, w, _ptr(P), _ld(P), _ptr(tau), _ptr(Tf),
+                                                             _ld(Tf)))
+        return P, tau, Tf
+
+    def randutv_small_svd(self, B, allow_nonconvergence=False):
+        import torch
+        w = B.shape[0]
+        Us = colmajor(w, w, device=B.device)
+        Vs = colmajor(w, w, device=B.device)
+        d = torch.empty(w, dtype=torch.float64, device=B.device)
+        st = self.lib.randutv_small_svd(self.h, w, _ptr(B), _ld(B), _ptr(Us), _ptr(d), _ptr(Vs))
+        _check("randutv_small_svd", st, allow_positive=allow_nonconvergence)
+        return Us, d, Vs, st
+
+
+def randutv_factor(m, n, A, lda, b, q, seed, U, T, V):
+    """The literal north-star entry: all four matrices on the device (torch tensors)
+    or all on the host (numpy Fortran-ordered float64 arrays, ideally pinned)."""
+    lib = load_library()
+
+    def p(X):
+        if isinstance(X, np.ndarray):
+            if not X.flags.f_contiguous or X.dtype != np.float64:
+                raise ValueError("host arrays must be Fortran-ordered float64")
+            return ctypes.c_void_p(X.ctypes.data)
+        if hasattr(X, "data_ptr"):
+            return ctypes.c_void_p(X.data_ptr())
+        return ctypes.c_void_p(int(X))
+
+    st = lib.randutv_factor(int(m), int(n), p(A), int(lda), int(b), int(q), int(seed) & (2**64 - 1),
+                            p(U), p(T), p(V))
+    _check("randutv_factor", st)
+    return st
+
+
+def randutv_workspace_bytes(m, n, b, q, flags=0):
+    lib = load_library()
+    out = ctypes.c_size_t()
+    _check("randutv_workspace_bytes", lib.randutv_workspace_bytes(m, n, b, q, flags, ctypes.byref(out)))
+    return out.value

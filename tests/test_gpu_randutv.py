@@ -1,0 +1,185 @@
+"""GPU randUTV (through the C ABI) against the CPU oracle on the same seeded A and G.
+
+North-star bar (BASELINE.json): reconstruction <= 1e-12, orthogonality <= 1e-12
+(spectral norm, reading A17), |diag T| within 1e-9 relative (with the absolute
+floor of reading A16), truncated ||A - A_k|| within 1e-9 relative of the
+oracle's.  Additionally, because the two sides use the same G bits, reflector
+convention and power formula, |T|, |U|, |V| agree ELEMENTWISE (singular-vector
+sign choices of the small SVD flip rows/columns of a block pairwise and change no
+magnitude); a convention mismatch would show up as O(1e-2) differences.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from gpu_util import diag_parity, recon_error, spectral_orth_error, to_dev, to_np  # noqa: E402
+from oracle.randutv import randutv as oracle_randutv  # noqa: E402
+from paper_2002_06960_b200.inputs import make_numpy, sigma_powspec  # noqa: E402
+
+ELEM_TOL = 1e-11  # |Delta| / ||A||_F, elementwise on |T|, |U|, |V|
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    assert torch.cuda.is_available(), "the -m gpu tests need a CUDA device"
+    from paper_2002_06960_b200.randutv import Context
+    c = Context()
+    yield c
+    c.close()
+
+
+def _gpu_full(ctx, A, b, q, seed):
+    U, T, V, st = ctx.randutv_factor_ex(to_dev(A), b, q, seed)
+    assert st == 0
+    return to_np(U), to_np(T), to_np(V)
+
+
+def _check_full(A, U, T, V, o, elementwise=True):
+    nA = np.linalg.norm(A)
+    assert recon_error(A, U, T, V) <= 1e-12
+    assert spectral_orth_error(U) <= 1e-12
+    assert spectral_orth_error(V) <= 1e-12
+    assert np.all(np.tril(T, -1) == 0.0)
+    assert diag_parity(np.diag(T), np.diag(o["T"])) <= 1.0
+    if elementwise:
+        for X, key in ((T, "T"), (U, "U"), (V, "V")):
+            scale = nA if key == "T" else 1.0
+            err = np.max(np.abs(np.abs(X) - np.abs(o[key]))) / scale
+            assert err <= ELEM_TOL, (key, err)
+
+
+@pytest.mark.parametrize("m,n,b,q", [
+    (64, 64, 16, 1), (200, 200, 32, 2), (333, 333, 64, 1),   # ragged final block
+    (300, 170, 40, 2),                                       # tall, ragged
+    (129, 129, 128, 0),                                      # final block of 1 column
+    (96, 96, 96, 1), (80, 50, 100, 1),                       # b >= n: SVD only (tall: QR + SVD)
+    (40, 40, 1, 1),                                          # b = 1
+    (257, 257, 32, 0),
+])
+def test_random_parity(ctx, m, n, b, q):
+    rng = np.random.default_rng(m * 1000 + n + b + q)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    U, T, V = _gpu_full(ctx, A, b, q, 99)
+    o = oracle_randutv(A, b, q, 99)
+    _check_full(A, U, T, V, o)
+    assert np.all(T[n:, :] == 0.0)
+
+
+@pytest.fixture(scope="module")
+def c1_pair(ctx):
+    A = make_numpy("powspec", 512, 512, cfg_index=1)
+    U, T, V = _gpu_full(ctx, A, 64, 2, 2001)
+    o = oracle_randutv(A, 64, 2, 2001)
+    return A, (U, T, V), o
+
+
+def test_c1_full_parity(c1_pair):
+    A, (U, T, V), o = c1_pair
+    _check_full(A, U, T, V, o)
+    # closed form: sum log10 |T_kk| = sum log10 sigma_k = -2048 (tests/golden/small_cases.txt)
+    assert abs(np.sum(np.log10(np.abs(np.diag(T)))) + 2048.0) <= 1e-6
+
+
+@pytest.mark.parametrize("k", [64, 128])
+def test_c1_rank_k(ctx, c1_pair, k):
+    A, (U, T, V), o = c1_pair
+    Uk, Tk, Vk, rho = ctx.randutv_factor_rank(to_dev(A), k, 64, 2, 2001)
+    Uk, Tk, Vk = to_np(Uk), to_np(Tk), to_np(Vk)
+    Ak = Uk @ Tk @ Vk.T
+    err_f = np.linalg.norm(A - Ak)
+    err_2 = np.linalg.norm(A - Ak, 2)
+    to = oracle_randutv(A, 64, 2, 2001, k=k, thin_u=True)
+    Ak_o = to["Uk"] @ to["Tk"] @ to["V"].T
+    err_f_o = np.linalg.norm(A - Ak_o)
+    err_2_o = np.linalg.norm(A - Ak_o, 2)
+    assert abs(rho - to["rho"]) <= 1e-9 * to["rho"]
+    assert abs(err_f - err_f_o) <= 1e-9 * err_f_o
+    assert abs(err_2 - err_2_o) <= 1e-9 * err_2_o
+    assert abs(rho - err_f) <= 1e-12 * np.linalg.norm(A)
+    # the full GPU run gives the same A_k (later steps do not change U(:, :k) T(:k, :) V^T)
+    Ak_full = U[:, :k] @ T[:k, :] @ V.T
+    assert np.linalg.norm(Ak_full - Ak) <= 1e-12 * np.linalg.norm(A)
+    assert 1.0 - 1e-9 <= err_2 / sigma_powspec(512)[k] <= 1.5
+    assert spectral_orth_error(Uk) <= 1e-12
+
+
+def test_truncated_tall_parity(ctx):
+    A = make_numpy("lowrank", 3000, 600, cfg_index=4, rank=100)
+    k, b, q = 160, 64, 2
+    Uk, Tk, V, rho = ctx.randutv_factor_rank(to_dev(A), k, b, q, 2004)
+    Uk, Tk, V = to_np(Uk), to_np(Tk), to_np(V)
+    to = oracle_randutv(A, b, q, 2004, k=k, thin_u=True)
+    assert abs(rho - to["rho"]) <= 1e-9 * to["rho"]
+    assert diag_parity(np.diag(Tk), np.diag(to["Tk"])) <= 1.0
+    assert np.max(np.abs(np.abs(Tk) - np.abs(to["Tk"]))) <= ELEM_TOL * np.linalg.norm(A)
+    assert np.max(np.abs(np.abs(Uk) - np.abs(to["Uk"]))) <= ELEM_TOL
+    assert spectral_orth_error(Uk) <= 1e-12 and spectral_orth_error(V) <= 1e-12
+    Ak = Uk @ Tk @ V.T
+    assert abs(np.linalg.norm(A - Ak) - rho) <= 1e-12 * np.linalg.norm(A)
+
+
+def test_c2_full_parity(ctx):
+    A = make_numpy("gauss", 4096, 4096, cfg_index=2)
+    U, T, V = _gpu_full(ctx, A, 128, 1, 2002)
+    o = oracle_randutv(A, 128, 1, 2002)
+    _check_full(A, U, T, V, o)
+
+
+def test_determinism_and_stats(ctx):
+    rng = np.random.default_rng(11)
+    A = np.asfortranarray(rng.standard_normal((700, 600)))
+    ctx.reset_stats()
+    r1 = _gpu_full(ctx, A, 64, 1, 5)
+    st = ctx.stats()
+    r2 = _gpu_full(ctx, A, 64, 1, 5)
+    for a, b in zip(r1, r2):
+        assert np.array_equal(a, b)
+    assert st["kernel_launches"] > 0 and st["factorizations"] == 1
+
+
+def test_literal_entry_host_and_device(ctx):
+    import torch
+    from paper_2002_06960_b200.randutv import randutv_factor
+    rng = np.random.default_rng(12)
+    m, n = 300, 250
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    Uh = np.zeros((m, m), order="F")
+    Th = np.zeros((m, n), order="F")
+    Vh = np.zeros((n, n), order="F")
+    randutv_factor(m, n, A, m, 32, 1, 77, Uh, Th, Vh)
+    Ad = to_dev(A)
+    from paper_2002_06960_b200.randutv import colmajor
+    Ud, Td, Vd = colmajor(m, m), colmajor(m, n), colmajor(n, n)
+    randutv_factor(m, n, Ad, m, 32, 1, 77, Ud, Td, Vd)
+    torch.cuda.synchronize()
+    assert np.array_equal(Th, to_np(Td)) and np.array_equal(Uh, to_np(Ud)) and np.array_equal(Vh, to_np(Vd))
+    o = oracle_randutv(A, 32, 1, 77)
+    _check_full(A, Uh, Th, Vh, o)
+
+
+def test_in_place_alias_and_no_uv(ctx):
+    rng = np.random.default_rng(13)
+    A = np.asfortranarray(rng.standard_normal((256, 256)))
+    U, T, V, _ = ctx.randutv_factor_ex(to_dev(A), 32, 1, 3)
+    Ad = to_dev(A)
+    _, T2, _, _ = ctx.randutv_factor_ex(Ad, 32, 1, 3, build_uv=False, T=Ad)
+    assert np.array_equal(to_np(T2), to_np(T))   # T alone does not depend on U, V
+
+
+def test_error_codes(ctx):
+    import ctypes
+    from paper_2002_06960_b200.randutv import RANDUTV_CHECK_FINITE, RANDUTV_ERR_NONFINITE, RandUTVError
+    A = to_dev(np.ones((8, 8)))
+    with pytest.raises(RandUTVError) as e:
+        ctx.randutv_factor_ex(A, 0, 1, 1)
+    assert e.value.status == -6
+    lib = ctx.lib
+    assert lib.randutv_factor_ex(ctx.h, 4, 8, ctypes.c_void_p(A.data_ptr()), 8, 2, 1, 1, 1, None, 1,
+                                 ctypes.c_void_p(A.data_ptr()), 8, None, 1) == -2
+    Bn = np.ones((8, 8))
+    Bn[3, 4] = np.nan
+    with pytest.raises(RandUTVError) as e:
+        ctx.randutv_factor_ex(to_dev(Bn), 2, 1, 1, flags=RANDUTV_CHECK_FINITE)
+    assert e.value.status == RANDUTV_ERR_NONFINITE

@@ -70,3 +70,33 @@ def test_nonconvergence_reported():
     rng = np.random.default_rng(1)
     with pytest.raises(JacobiNonConvergence):
         one_sided_jacobi(rng.standard_normal((8, 8)), max_sweeps=1)
+
+
+@pytest.mark.parametrize("b,kind", [(64, "graded"), (128, "gauss_r"), (33, "dense")])
+def test_svd_block_transposed_variant(b, kind):
+    # svd_block = one-sided Jacobi on B^T (reading A10); same pins as the column variant
+    from oracle.jacobi import svd_block
+    rng = np.random.default_rng(b)
+    B = rng.standard_normal((b, b))
+    if kind == "gauss_r":
+        B = np.linalg.qr(B)[1]
+    elif kind == "graded":
+        Q1 = np.linalg.qr(rng.standard_normal((b, b)))[0]
+        Q2 = np.linalg.qr(rng.standard_normal((b, b)))[0]
+        B = np.linalg.qr((Q1 * 10.0 ** (-8.0 * np.arange(b) / b)) @ Q2.T)[1]
+    Us, d, Vs, sweeps = svd_block(B)
+    s = np.linalg.svd(B, compute_uv=False)
+    assert np.max(np.abs(d - s)) <= 10 * b * U * s[0]
+    assert np.linalg.norm(B - (Us * d) @ Vs.T) <= 1e-13 * np.linalg.norm(B)
+    assert np.linalg.norm(Us.T @ Us - np.eye(b), 2) <= 1e-13
+    assert np.linalg.norm(Vs.T @ Vs - np.eye(b), 2) <= 1e-13
+    if kind == "graded":
+        assert sweeps <= 12
+
+
+def test_svd_block_golden_and_zero():
+    from oracle.jacobi import svd_block
+    Us, d, Vs, _ = svd_block(np.diag([3.0, 1.0, 2.0]))
+    assert np.array_equal(d, [3.0, 2.0, 1.0])
+    Us, d, Vs, _ = svd_block(np.zeros((3, 3)))
+    assert np.array_equal(Us, np.eye(3)) and np.array_equal(Vs, np.eye(3))
