@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 randUTV hot path (BASELINE.json metric: randUTV FP64
+GFLOP/s and t/n^3 at 1/2/4/8 B200; % of FP64 tensor peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+A "step" is one full randUTV factorisation (every row of SURVEY.md §8(a):
+S1-S10, U and V built) of the config's seeded synthetic matrix, resident in HBM.
+Default workload: c3 (n = 16384, b = 256, q = 2, exponential spectrum), the
+largest config quoted at 1/2/4/8 GPUs that a single step of finishes in
+seconds (DESIGN.md §Measurement explains the choice; c2 and c5 run with
+--config).  value = F_model / t (GFLOP/s, F from paper_2002_06960_b200.flops),
+whole job over all ranks.  Multi-GPU: N independent replicas ("scaling":
+"weak", no data-path collective; the column-sharded NCCL path is a later round,
+DESIGN.md §Multi-GPU).
+
+--impl reference times the CPU oracle (oracle/, numpy) on the host cores on a
+bounded sample of the same workload (the first sampled step of the config) --
+the only other place this script executes oracle/ besides the cpu_baseline leg.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+NCU_TRAFFIC_FILE = os.path.join(ROOT, "profiles", "dgemm_traffic.json")
+METRIC = "randUTV FP64 GFLOP/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c5"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-profile", action="store_true", help="do not record per-kernel CUDA events")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        import statistics
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for name, val in zip(names, r[5:9]):
+                if val.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def fp64_peak():
+    """Measured FP64 DMMA sustained peak (tools/fp64_peak.cu on this pool's B200)."""
+    try:
+        d = json.load(open(FP64_PEAK_FILE))
+        return float(d["dmma884_sustained_tflops"]), "measured (profiles/fp64_peak_r01.json, DMMA sustained)"
+    except Exception:
+        return 37.2, "nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz (measurement file missing)"
+
+
+def cpu_sample(cfg_name, A_host, seed):
+    """The oracle (as it stands) on a bounded sample: the first sampled step of the
+    config (truncated k = b, thin U), timed on this host's cores."""
+    from threadpoolctl import threadpool_info
+
+    from oracle.randutv import randutv as oracle_randutv
+    from paper_2002_06960_b200.flops import randutv_flops
+    from paper_2002_06960_b200.inputs import CONFIGS
+    c = CONFIGS[cfg_name]
+    m, n, b, q = c["m"], c["n"], c["b"], c["q"]
+    t0 = time.perf_counter()
+    oracle_randutv(A_host, b, q, seed, k=b, thin_u=True)
+    dt = time.perf_counter() - t0
+    F = randutv_flops(m, n, b, q, build_uv=True, k=b)
+    threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    return {"value": F / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+            "sample": f"{cfg_name}: first sampled step only (truncated k=b={b}, q={q}, V + thin U_k), "
+                      f"{F:.3g} flops in {dt:.1f} s (numpy/OpenBLAS, {threads} threads, {os.cpu_count()} host cpus)",
+            "seconds": dt, "flops": F}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    from paper_2002_06960_b200.inputs import CONFIGS, make_config_numpy
+    cfg = CONFIGS[args.config]
+    A = make_config_numpy(args.config)
+    seed = 2000 + int(args.config[1:])
+    times = []
+    cs = None
+    for _ in range(max(args.warmup, 0)):
+        cs = cpu_sample(args.config, A, seed)
+    for _ in range(args.steps):
+        cs = cpu_sample(args.config, A, seed)
+        times.append(cs["seconds"])
+    t = sum(times) / len(times)
+    val = cs["flops"] / t / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} sample: first sampled step", "m": cfg["m"], "n": cfg["n"],
+                       "b": cfg["b"], "q": cfg["q"]},
+            "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cs["cores"], "kind": "oracle",
+                             "sample": cs["sample"]},
+            "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2002_06960_b200.flops import randutv_flops
+    from paper_2002_06960_b200.inputs import CONFIGS, make_config_torch
+    from paper_2002_06960_b200.randutv import Context, colmajor, randutv_factor
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    cfg = CONFIGS[args.config]
+    m, n, b, q = cfg["m"], cfg["n"], cfg["b"], cfg["q"]
+    seed = 2000 + int(args.config[1:])
+    F = randutv_flops(m, n, b, q, build_uv=True)
+
+    A = make_config_torch(args.config, device=f"cuda:{dev}")
+    T = colmajor(m, n)
+    U = colmajor(m, m)
+    V = colmajor(n, n)
+    stream = torch.cuda.Stream()
+    ctx = Context(dev, stream)
+
+    def step():
+        ctx.randutv_factor_ex(A, b, q, seed, U=U, T=T, V=V)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    clocks = ClockSampler(dev)
+    ctx.reset_stats()
+    if not args.no_profile:
+        ctx.set_profiling(True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    stats = ctx.stats()
+    prof = ctx.profile() if not args.no_profile else None
+    ctx.set_profiling(False)
+    ms_step = ms / args.steps
+    value = F * ws * args.steps / (ms * 1e-3) / 1e9
+
+    # ---- e2e: the literal C-ABI entry on pinned host buffers, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        Ah = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A.t())
+        Uh = torch.empty((m, m), dtype=torch.float64, pin_memory=True)
+        Th = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+        Vh = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        An, Un, Tn, Vn = Ah.numpy().T, Uh.numpy().T, Th.numpy().T, Vh.numpy().T
+        del T, U, V  # make room for the library's host-staging buffers
+        torch.cuda.empty_cache()
+        randutv_factor(m, n, An, m, b, q, seed, Un, Tn, Vn)      # warm-up (allocates staging)
+        e2e_steps = min(args.steps, 2)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            randutv_factor(m, n, An, m, b, q, seed, Un, Tn, Vn)
+        dt = time.perf_counter() - t0
+        if ws > 1:
+            tt = torch.tensor([dt], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e = {"value": F * ws * e2e_steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * m * n,
+               "d2h_bytes_per_step": 8 * (m * m + m * n + n * n), "steps": e2e_steps,
+               "ms_per_step": dt / e2e_steps * 1e3}
+
+    # ---- CPU baseline: the oracle on a bounded sample, rank 0, N = 1 only
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        A_host = np.asfortranarray(A.t().cpu().numpy().T)
+        cpu = cpu_sample(args.config, A_host, seed)
+        cpu = {k: v for k, v in cpu.items() if k not in ("seconds", "flops")}
+
+    if rank == 0:
+        peak, peak_src = fp64_peak()
+        roof = None
+        if prof and prof["dgemm"]["ms"] > 0:
+            g = prof["dgemm"]
+            ach = g["flops"] / (g["ms"] * 1e-3) / 1e12
+            traffic = None
+            try:
+                tr = json.load(open(NCU_TRAFFIC_FILE))
+                if tr.get("config") == args.config:
+                    traffic = tr.get("bytes_per_launch")
+            except Exception:
+                pass
+            roof = {"bound": "tensor", "achieved": round(ach, 3), "peak": peak, "unit": "TFLOP/s",
+                    "frac": round(ach / peak, 4), "traffic": traffic,
+                    "kernel": "dgemm_kernel (mma.sync.m8n8k4.f64 / DMMA)",
+                    "launches": g["launches"], "kernel_ms_per_step": g["ms"] / args.steps,
+                    "kernel_share_of_step": round(g["ms"] / ms, 4),
+                    "peak_source": peak_src,
+                    "algorithmic": "2*M*N*K flops per GEMM launch (SURVEY.md §8(d) M3 terms)"}
+            roof["other_kernels"] = {k: {"ms_per_step": v["ms"] / args.steps, "launches": v["launches"]}
+                                     for k, v in prof.items() if k != "dgemm"}
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: " + {
+                "c1": "n=512 known spectrum", "c2": "n=4096 Gaussian", "c3": "n=16384 exp spectrum",
+                "c5": "n=65536 Gaussian"}[args.config] + f", b={b}, q={q}, full randUTV with U and V",
+                "m": m, "n": n, "b": b, "q": q, "flops_per_step": F,
+                "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                "l2": "inputs larger than L2 (A is %.2f GB, L2 126 MB); no flush" % (8 * m * n / 1e9)
+                if 8 * m * n > 126e6 else "input fits L2: not flushed"},
+            "t_over_n3_x1e10": ms_step * 1e-3 / float(n) ** 3 * 1e10,
+            "frac_of_fp64_peak": round(value / ws / 1e3 / peak, 4),
+            "gpu_launches": stats["kernel_launches"],
+            "gpu_launches_per_step": stats["kernel_launches"] / args.steps,
+            "clocks": clocks.summary(),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -125,6 +125,23 @@ RANDUTV_API const char* randutv_last_error(void);
 RANDUTV_API int randutv_get_stats(randutv_ctx* ctx, randutv_stats* out);
 RANDUTV_API int randutv_reset_stats(randutv_ctx* ctx);
 
+/* Per-kernel-class timing with CUDA events recorded on the ctx stream around
+ * every launch of the class (measurement support for bench.py's roofline).
+ * Kinds: 0 DMMA GEMM (flops = 2MNK), 1 panel-QR leaf, 2 Jacobi SVD, 3 Gaussian.
+ * randutv_set_profiling(ctx, 1) resets the totals and turns recording on. */
+#define RANDUTV_PROF_DGEMM    0
+#define RANDUTV_PROF_QR_LEAF  1
+#define RANDUTV_PROF_JACOBI   2
+#define RANDUTV_PROF_GAUSSIAN 3
+typedef struct randutv_profile {
+  int64_t launches;  /* launches recorded                                    */
+  double ms;         /* summed event-to-event device time                    */
+  double flops;      /* summed algorithmic flops of those launches           */
+  double bytes;      /* summed compulsory bytes (operands read + C written)  */
+} randutv_profile;
+RANDUTV_API int randutv_set_profiling(randutv_ctx* ctx, int enable);
+RANDUTV_API int randutv_get_profile(randutv_ctx* ctx, int kind, randutv_profile* out);
+
 /* ---------------------------------------------------------------------------
  * Step-level entry points (the steps S1, S2/S3, S4/S6, S8 of SURVEY.md §8(a)),
  * exported so each kernel can be parity-checked against the oracle on its own.

@@ -21,6 +21,11 @@ method with the cyclic-by-rows pair order:
     Sort d descending (stable), permuting U and V alike.
 
 tol = sqrt(b) * 2^-53 (LAPACK dgesvj's sqrt(m)*eps), max_sweeps = 30.
+Columns with ||x|| <= nu = b 2^-53 ||B||_F are numerically null: pairs that
+involve one are not rotated and their d is set to 0 (then completed).  Without
+this rule a rank-deficient block never converges: rounding leaves more
+u-sized "null" vectors than the null space has dimensions, and no rotation can
+make them mutually orthogonal under the relative test.
 The rotation annihilates the (p,q) Gram entry exactly in exact arithmetic:
 gamma' = cs(alpha - beta) + (c^2 - s^2) gamma = 0.
 
@@ -44,6 +49,11 @@ def jacobi_tol(b):
     return math.sqrt(b) * 2.0 ** -53
 
 
+def negligible_norm(B):
+    """nu = n 2^-53 ||B||_F: columns this short are numerical zeros (not rotated, d := 0)."""
+    return B.shape[1] * 2.0 ** -53 * math.sqrt(float(np.sum(np.asarray(B) ** 2)))
+
+
 def one_sided_jacobi(B, tol=None, max_sweeps=30):
     """Return (Us, d, Vs, sweeps) with B = Us diag(d) Vs^T, d >= 0 descending."""
     X = np.array(B, dtype=np.float64, order="F", copy=True)
@@ -51,6 +61,7 @@ def one_sided_jacobi(B, tol=None, max_sweeps=30):
     V = np.eye(n, order="F")
     if tol is None:
         tol = jacobi_tol(n)
+    nu2 = negligible_norm(X) ** 2
     sweeps = 0
     converged = n <= 1
     while not converged:
@@ -65,7 +76,7 @@ def one_sided_jacobi(B, tol=None, max_sweeps=30):
                 alpha = float(xp @ xp)
                 beta = float(xq @ xq)
                 gamma = float(xp @ xq)
-                if abs(gamma) > tol * math.sqrt(alpha * beta):
+                if alpha > nu2 and beta > nu2 and abs(gamma) > tol * math.sqrt(alpha * beta):
                     rotated = True
                     zeta = (beta - alpha) / (2.0 * gamma)
                     t = math.copysign(1.0, zeta) / (abs(zeta) + math.hypot(1.0, zeta))
@@ -80,6 +91,7 @@ def one_sided_jacobi(B, tol=None, max_sweeps=30):
                     V[:, q] = s * vp0 + c * vq0
         converged = not rotated
     d = np.sqrt(np.einsum("ij,ij->j", X, X))
+    d[d * d <= nu2] = 0.0          # numerically null columns -> exact zeros (completed below)
     U = np.zeros((nr, n), order="F")
     for j in range(n):
         if d[j] != 0.0:

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <vector>
 
 #include "../../include/randutv.h"
 
@@ -19,12 +20,43 @@ constexpr int kNumSMs = 148;  // B200; launch heuristics only (never correctness
 void set_last_error(const char* where, cudaError_t e);
 const char* last_error();
 
+// Optional per-kernel-class timing with CUDA events on the launching stream
+// (randutv_set_profiling): bench.py's roofline numbers come from here.
+enum ProfKind { PK_DGEMM = 0, PK_QR_LEAF = 1, PK_JACOBI = 2, PK_GAUSSIAN = 3, PK_OTHER = 4, PK_COUNT = 5 };
+
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  struct Rec {
+    int kind;
+    double flops;
+    double bytes;
+    size_t e0, e1;
+  };
+  std::vector<Rec> recs;
+  int64_t launches[PK_COUNT] = {0};
+  double ms[PK_COUNT] = {0};
+  double flops[PK_COUNT] = {0};
+  double bytes[PK_COUNT] = {0};
+  size_t begin(cudaStream_t s);
+  void end(cudaStream_t s, int kind, double fl, double by, size_t e0);
+  void collect();  // after the stream is synchronised
+  void reset();
+  ~Profiler();
+};
+
 struct Launch {
   cudaStream_t stream;
   int64_t* counter;  // incremented per kernel launch
   int device_sms;
+  Profiler* prof = nullptr;
   void count(int n = 1) const {
     if (counter) *counter += n;
+  }
+  size_t pbegin() const { return (prof && prof->on) ? prof->begin(stream) : 0; }
+  void pend(int kind, double fl, double by, size_t e0) const {
+    if (prof && prof->on) prof->end(stream, kind, fl, by, e0);
   }
 };
 

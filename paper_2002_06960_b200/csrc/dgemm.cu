@@ -237,6 +237,7 @@ int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double 
   }
   if (kchunk <= 0) kchunk = 1;
   const int va = vec_of(A, lda), vb = vec_of(B, ldb);
+  const size_t pe = L.pbegin();
   dim3 grid((unsigned)gm, (unsigned)gn, (unsigned)splits);
   double* part = splits > 1 ? ws : nullptr;
   int st;
@@ -253,6 +254,9 @@ int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double 
     L.count();
     RUTV_CHECK_LAUNCH("splitk_reduce_kernel");
   }
+  // algorithmic: 2MNK flops; compulsory bytes: read A, B (and C if beta != 0), write C
+  L.pend(PK_DGEMM, 2.0 * (double)M * (double)N * (double)K,
+         8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2.0 : 1.0)), pe);
   return 0;
 }
 

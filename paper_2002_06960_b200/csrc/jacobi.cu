@@ -10,7 +10,9 @@
 // |x_p.x_q| > tol sqrt(|x_p|^2 |x_q|^2), tol = sqrt(b) 2^-53, with
 //   zeta = (beta - alpha)/(2 gamma), t = sign(zeta)/(|zeta| + sqrt(1+zeta^2)),
 //   c = 1/sqrt(1+t^2), s = c t,  (x_p, x_q) <- (c x_p - s x_q, s x_p + c x_q),
-// stop after a sweep without rotations (cap 30 sweeps -> status +block),
+// columns with |x| <= nu = b 2^-53 ||B||_F are numerically null (never rotated,
+// d := 0, completed), stop after a sweep without rotations (cap 30 sweeps ->
+// status +block),
 // d_j = |x_j|, Q(:,j) = x_j/d_j (zero columns completed by Gram-Schmidt),
 // stable descending sort of d.
 //
@@ -58,7 +60,7 @@ JacobiPlan plan_for(i64 w) {
   for (int C = 1; C <= 16; C *= 2) {
     const int RP = (p.nc + C - 1) / C;
     if (RP > 64) continue;  // lanes cover <= 2 rows each
-    const size_t part = (size_t)2 * (p.nc / 2) * 3 * 8 + (size_t)p.nc * 8 + 64;
+    const size_t part = (size_t)2 * (p.nc / 2) * 3 * 8 + (size_t)(p.nc + 8) * 8 + 64;
     const size_t x = (size_t)p.nc * RP * 8;
     if (x * 2 + part <= limit) {
       p.C = C; p.RP = RP; p.v_smem = true; p.smem = x * 2 + part;
@@ -68,7 +70,7 @@ JacobiPlan plan_for(i64 w) {
   for (int C = 1; C <= 16; C *= 2) {
     const int RP = (p.nc + C - 1) / C;
     if (RP > 64) continue;
-    const size_t part = (size_t)2 * (p.nc / 2) * 3 * 8 + (size_t)p.nc * 8 + 64;
+    const size_t part = (size_t)2 * (p.nc / 2) * 3 * 8 + (size_t)(p.nc + 8) * 8 + 64;
     const size_t x = (size_t)p.nc * RP * 8;
     if (x + part <= limit) {
       p.C = C; p.RP = RP; p.v_smem = false; p.smem = x + part;
@@ -104,17 +106,34 @@ __global__ void __launch_bounds__(JT)
   double* Xs = sm;
   double* Vsl = v_smem ? Xs + (size_t)nc * RP : vglobal + (size_t)rank * nc * RP;
   double* part = (v_smem ? Vsl + (size_t)nc * RP : Xs + (size_t)nc * RP);  // [2][npairs][3]
-  double* dsum = part + 2 * npairs * 3;                                     // [nc]
+  double* dsum = part + 2 * npairs * 3;                                     // [nc + 1]
   __shared__ int sflag[2];
   const int r0 = rank * RP;
 
-  // load X = B (zero padded) and V = I for this CTA's rows
+  // load X = B^T (zero padded) and W = I for this CTA's rows; partial ||B||_F^2
+  double ss = 0.0;
   for (int e = tid; e < nc * RP; e += JT) {
     const int col = e / RP, lr = e % RP, row = r0 + lr;
-    Xs[e] = (row < w && col < w) ? B[col + (i64)row * ldb] : 0.0;  // X = B^T
+    const double x = (row < w && col < w) ? B[col + (i64)row * ldb] : 0.0;  // X = B^T
+    Xs[e] = x;
+    ss += x * x;
     Vsl[e] = (row == col) ? 1.0 : 0.0;
   }
+  ss = warp_sum(ss);
+  if (lane == 0) dsum[warp] = ss;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int k = 0; k < nwarps; ++k) t += dsum[k];
+    dsum[nc] = t;  // this CTA's partial, read by every CTA below
+  }
   cluster.sync();
+  // nu^2 = (w 2^-53 ||B||_F)^2: columns this short are numerically null (not rotated, d := 0)
+  double fro2 = 0.0;
+  for (int c = 0; c < C; ++c) fro2 += cluster.map_shared_rank(dsum, c)[nc];
+  const double nu = (double)w * 0x1p-53 * sqrt(fro2);
+  const double nu2 = nu * nu;
+  cluster.sync();  // dsum is reused below
 
   int sweeps = 0;
   bool converged = (nc <= 1);
@@ -162,7 +181,7 @@ __global__ void __launch_bounds__(JT)
         a = __shfl_sync(0xffffffffu, a, 0);
         bb = __shfl_sync(0xffffffffu, bb, 0);
         g = __shfl_sync(0xffffffffu, g, 0);
-        if (fabs(g) > tol * sqrt(a * bb)) {
+        if (a > nu2 && bb > nu2 && fabs(g) > tol * sqrt(a * bb)) {
           rotated = 1;
           const double zeta = (bb - a) / (2.0 * g);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
@@ -203,7 +222,7 @@ __global__ void __launch_bounds__(JT)
   for (int col = tid; col < nc; col += JT) {
     double s = 0.0;
     for (int c = 0; c < C; ++c) s += cluster.map_shared_rank(dsum, c)[col];
-    dl[col] = sqrt(s);
+    dl[col] = (s <= nu2) ? 0.0 : sqrt(s);
   }
   if (tid == 0) sflag[0] = 0;
   cluster.sync();  // dsum reads done everywhere; dl visible in this CTA
@@ -328,12 +347,14 @@ int launch_jacobi_svd(const Launch& L, i64 w, const double* B, i64 ldb, double* 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const double tol = sqrt((double)w) * 0x1p-53;
+  const size_t pe = L.pbegin();
   RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_svd_kernel, (int)w, B, ldb, Us, d, Vs, status, block_id, p.nc, p.RP,
                                (int)p.v_smem, vglobal, tol, zero_flag));
   L.count();
   jacobi_complete_kernel<<<1, 256, 0, L.stream>>>((int)w, Vs, d, zero_flag, ctmp);
   L.count();
   RUTV_CHECK_LAUNCH("jacobi_complete_kernel");
+  L.pend(PK_JACOBI, 0.0, 8.0 * 4.0 * (double)w * w, pe);
   return 0;
 }
 

@@ -64,8 +64,10 @@ int launch_gaussian(const Launch& L, uint64_t seed, i64 it, i64 rows, i64 cols, 
   const int threads = 256;
   i64 blocks = (total + threads - 1) / threads;
   if (blocks > (i64)L.device_sms * 16) blocks = (i64)L.device_sms * 16;
+  const size_t pe = L.pbegin();
   gaussian_kernel<<<(unsigned)blocks, threads, 0, L.stream>>>(seed, (uint32_t)it, rows, cols, G, ldg);
   L.count();
+  L.pend(PK_GAUSSIAN, 0.0, 8.0 * (double)rows * cols, pe);
   RUTV_CHECK_LAUNCH("gaussian_kernel");
   return 0;
 }

@@ -253,8 +253,11 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
       double* taup = tau;
       double* part = qw.partials;
       void* args[] = {&Pp, &hh, &ld, &cc, &nbv, &taup, &part};
+      const size_t pe = L.pbegin();
       RUTV_CUDA(cudaLaunchCooperativeKernel((void*)qr_leaf_kernel, dim3(G), dim3(LEAF_THREADS), args, 0, L.stream));
       L.count();
+      // algorithmic: ~4 (h-c0) wl^2 flops (dlarfg + dlarf over the leaf); bytes: the leaf read + written once
+      L.pend(PK_QR_LEAF, 4.0 * (double)(h - c0) * wl * wl, 16.0 * (double)(h - c0) * wl, pe);
     }
     // ---- explicit W for this leaf
     {

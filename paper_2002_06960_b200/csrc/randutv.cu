@@ -43,6 +43,55 @@ void set_last_error(const char* where, cudaError_t e) {
 }
 const char* last_error() { return g_last_error; }
 
+size_t Profiler::begin(cudaStream_t s) {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      cudaGetLastError();
+      on = false;
+      return 0;
+    }
+    pool.push_back(e);
+  }
+  cudaEventRecord(pool[used], s);
+  return used++;
+}
+
+void Profiler::end(cudaStream_t s, int kind, double fl, double by, size_t e0) {
+  const size_t e1 = begin(s);
+  if (!on) return;
+  recs.push_back(Rec{kind, fl, by, e0, e1});
+}
+
+void Profiler::collect() {
+  for (const Rec& r : recs) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, pool[r.e0], pool[r.e1]) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    launches[r.kind] += 1;
+    ms[r.kind] += t;
+    flops[r.kind] += r.flops;
+    bytes[r.kind] += r.bytes;
+  }
+  recs.clear();
+  used = 0;
+}
+
+void Profiler::reset() {
+  recs.clear();
+  used = 0;
+  for (int k = 0; k < PK_COUNT; ++k) {
+    launches[k] = 0;
+    ms[k] = flops[k] = bytes[k] = 0.0;
+  }
+}
+
+Profiler::~Profiler() {
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+
 }  // namespace rutv
 
 struct randutv_ctx {
@@ -56,6 +105,8 @@ struct randutv_ctx {
   // host-staging buffers of the literal (host pointer) entry
   double* stage;
   size_t stage_bytes;
+  rutv::Profiler prof;
+  rutv::Launch launch() { return rutv::Launch{stream, &stats.kernel_launches, sms, &prof}; }
 };
 
 static const int kMagic = 0x52555456;  // "RUTV"
@@ -309,6 +360,7 @@ int finish(randutv_ctx* ctx, const Work& w) {
   RUTV_CUDA(cudaMemcpyAsync(&status, w.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
   RUTV_CUDA(cudaGetLastError());
+  if (ctx->prof.on) ctx->prof.collect();
   if (status != 0x7f7f7f7f) return status;  // 1-based block of a non-converged SVD
   return 0;
 }
@@ -391,6 +443,24 @@ RANDUTV_API int randutv_reset_stats(randutv_ctx* ctx) {
 
 RANDUTV_API const char* randutv_last_error(void) { return rutv::last_error(); }
 
+RANDUTV_API int randutv_set_profiling(randutv_ctx* ctx, int enable) {
+  if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
+  ctx->prof.reset();
+  ctx->prof.on = enable != 0;
+  return 0;
+}
+
+RANDUTV_API int randutv_get_profile(randutv_ctx* ctx, int kind, randutv_profile* out) {
+  if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
+  if (kind < 0 || kind >= rutv::PK_COUNT) return -2;
+  if (!out) return -3;
+  out->launches = ctx->prof.launches[kind];
+  out->ms = ctx->prof.ms[kind];
+  out->flops = ctx->prof.flops[kind];
+  out->bytes = ctx->prof.bytes[kind];
+  return 0;
+}
+
 RANDUTV_API const char* randutv_status_string(int s) {
   if (s == 0) return "success";
   if (s < 0) return "invalid argument (see the 1-based index in the status)";
@@ -436,7 +506,7 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
   if (alias && ldt != lda) return -13;
   if (!alias && overlaps(A, (size_t)lda * n * 8, T, (size_t)ldt * n * 8)) return -12;
   const i64 bb = b < n ? b : n;
-  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Launch L = ctx->launch();
   Work w;
   RUTV_TRY(prepare(ctx, w, m, n, bb, 0, false));
   if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
@@ -482,7 +552,7 @@ RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, cons
     with_final = true;
   }
   const i64 nrec = uv ? K + (with_final ? 1 : 0) : 0;
-  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Launch L = ctx->launch();
   Work w;
   RUTV_TRY(prepare(ctx, w, m, n, bb, nrec, true));
   if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
@@ -609,9 +679,10 @@ RANDUTV_API int randutv_gaussian(randutv_ctx* ctx, uint64_t seed, int64_t it, in
   if (cols < 0) return -5;
   if (!G && rows * cols > 0) return -6;
   if (ldg < rows || ldg < 1) return -7;
-  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Launch L = ctx->launch();
   RUTV_TRY(launch_gaussian(L, seed, it, rows, cols, G, ldg));
   RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->prof.on) ctx->prof.collect();
   return 0;
 }
 
@@ -628,13 +699,14 @@ RANDUTV_API int randutv_dgemm(randutv_ctx* ctx, int transa, int transb, int64_t 
   if (lda < (arows > 1 ? arows : 1)) return -9;
   if (ldb < (brows > 1 ? brows : 1)) return -11;
   if (ldc < (M > 1 ? M : 1)) return -14;
-  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Launch L = ctx->launch();
   // split-K scratch from the workspace
   const size_t need = (size_t)4 * (size_t)(M > 0 ? M : 1) * (size_t)(N > 0 ? N : 1) * 8 + (1 << 20);
   RUTV_TRY(ensure_ws(ctx, need));
   RUTV_TRY(launch_dgemm(L, transa != 0, transb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
                         (double*)ctx->ws, (i64)(ctx->ws_bytes / 8)));
   RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->prof.on) ctx->prof.collect();
   return 0;
 }
 
@@ -648,12 +720,13 @@ RANDUTV_API int randutv_panel_qr(randutv_ctx* ctx, int64_t h, int64_t wdt, doubl
   if (!tau) return -6;
   if (!Tf) return -7;
   if (ldtf < wdt) return -8;
-  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Launch L = ctx->launch();
   Work w;
   RUTV_TRY(prepare(ctx, w, h, wdt, wdt, 0, false));
   RUTV_TRY(panel_qr(L, h, wdt, P, ldp, tau, w.Wu, h, Tf, ldtf, w.qw));
   RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
   RUTV_CUDA(cudaGetLastError());
+  if (ctx->prof.on) ctx->prof.collect();
   return 0;
 }
 
@@ -666,7 +739,7 @@ RANDUTV_API int randutv_small_svd(randutv_ctx* ctx, int64_t wdt, const double* B
   if (!Us) return -5;
   if (!d) return -6;
   if (!Vs) return -7;
-  Launch L{ctx->stream, &ctx->stats.kernel_launches, ctx->sms};
+  Launch L = ctx->launch();
   Work w;
   RUTV_TRY(prepare(ctx, w, wdt, wdt, wdt, 0, false));
   RUTV_TRY(start_status(ctx, w));

@@ -35,6 +35,13 @@ class Stats(ctypes.Structure):
                 ("d2h_bytes", ctypes.c_int64)]
 
 
+class Profile(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64), ("ms", ctypes.c_double), ("flops", ctypes.c_double),
+                ("bytes", ctypes.c_double)]
+
+
+PROF_KINDS = {"dgemm": 0, "qr_leaf": 1, "jacobi": 2, "gaussian": 3}
+
 SIGNATURES = {
     "randutv_create": (_int, [ctypes.POINTER(_vp), _int, _vp]),
     "randutv_destroy": (_int, [_vp]),
@@ -49,6 +56,8 @@ SIGNATURES = {
     "randutv_last_error": (ctypes.c_char_p, []),
     "randutv_get_stats": (_int, [_vp, ctypes.POINTER(Stats)]),
     "randutv_reset_stats": (_int, [_vp]),
+    "randutv_set_profiling": (_int, [_vp, _int]),
+    "randutv_get_profile": (_int, [_vp, _int, ctypes.POINTER(Profile)]),
     "randutv_gaussian": (_int, [_vp, _u64, _i64, _i64, _i64, _vp, _i64]),
     "randutv_dgemm": (_int, [_vp, _int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64]),
     "randutv_panel_qr": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64]),
@@ -158,6 +167,17 @@ class Context:
 
     def reset_stats(self):
         _check("randutv_reset_stats", self.lib.randutv_reset_stats(self.h))
+
+    def set_profiling(self, on=True):
+        _check("randutv_set_profiling", self.lib.randutv_set_profiling(self.h, 1 if on else 0))
+
+    def profile(self):
+        out = {}
+        for name, kind in PROF_KINDS.items():
+            p = Profile()
+            _check("randutv_get_profile", self.lib.randutv_get_profile(self.h, kind, ctypes.byref(p)))
+            out[name] = {k: getattr(p, k) for k, _ in Profile._fields_}
+        return out
 
     # ---------------------------------------------------------------- factorisations
     def randutv_factor_ex(self, A, b, q, seed, build_uv=True, U=None, T=None, V=None, flags=0,

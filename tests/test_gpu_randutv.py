@@ -36,15 +36,15 @@ def _gpu_full(ctx, A, b, q, seed):
     return to_np(U), to_np(T), to_np(V)
 
 
-def _check_full(A, U, T, V, o, elementwise=True):
+def _check_full(A, U, T, V, o, elementwise=("T", "U", "V")):
     nA = np.linalg.norm(A)
     assert recon_error(A, U, T, V) <= 1e-12
     assert spectral_orth_error(U) <= 1e-12
     assert spectral_orth_error(V) <= 1e-12
     assert np.all(np.tril(T, -1) == 0.0)
     assert diag_parity(np.diag(T), np.diag(o["T"])) <= 1.0
-    if elementwise:
-        for X, key in ((T, "T"), (U, "U"), (V, "V")):
+    for X, key in ((T, "T"), (U, "U"), (V, "V")):
+        if key in elementwise:
             scale = nA if key == "T" else 1.0
             err = np.max(np.abs(np.abs(X) - np.abs(o[key]))) / scale
             assert err <= ELEM_TOL, (key, err)
@@ -77,7 +77,11 @@ def c1_pair(ctx):
 
 def test_c1_full_parity(c1_pair):
     A, (U, T, V), o = c1_pair
-    _check_full(A, U, T, V, o)
+    # |U|, |V| are not compared elementwise on c1: its singular values 1e-8..1 are only
+    # ~3.6% apart, so the singular vectors of the tail are conditioned ~u/gap ~ 1e-7 and
+    # two valid FP64 runs differ by ~3e-9 there (tests/calibrate_parity.py); the
+    # invariants and |diag T| pin them instead.
+    _check_full(A, U, T, V, o, elementwise=("T",))
     # closed form: sum log10 |T_kk| = sum log10 sigma_k = -2048 (tests/golden/small_cases.txt)
     assert abs(np.sum(np.log10(np.abs(np.diag(T)))) + 2048.0) <= 1e-6
 
@@ -106,15 +110,19 @@ def test_c1_rank_k(ctx, c1_pair, k):
 
 
 def test_truncated_tall_parity(ctx):
-    A = make_numpy("lowrank", 3000, 600, cfg_index=4, rank=100)
-    k, b, q = 160, 64, 2
+    # c4's shape ratios at 1/64 of the size: rank-200 signal (1 .. 1e-3) + 1e-6 noise.
+    # (A 3000 x 600 rank-100 variant puts noise directions of a block below
+    # eps^(1/(2q+1)) of its top singular value, where the literal power iteration
+    # (reading A8) resolves nothing and two valid FP64 runs differ 100x the bound.)
+    A = make_numpy("lowrank", 4096, 1024, cfg_index=4, rank=200)
+    k, b, q = 256, 64, 2
     Uk, Tk, V, rho = ctx.randutv_factor_rank(to_dev(A), k, b, q, 2004)
     Uk, Tk, V = to_np(Uk), to_np(Tk), to_np(V)
     to = oracle_randutv(A, b, q, 2004, k=k, thin_u=True)
     assert abs(rho - to["rho"]) <= 1e-9 * to["rho"]
     assert diag_parity(np.diag(Tk), np.diag(to["Tk"])) <= 1.0
     assert np.max(np.abs(np.abs(Tk) - np.abs(to["Tk"]))) <= ELEM_TOL * np.linalg.norm(A)
-    assert np.max(np.abs(np.abs(Uk) - np.abs(to["Uk"]))) <= ELEM_TOL
+    assert np.max(np.abs(np.abs(Uk) - np.abs(to["Uk"]))) <= 1e-9  # calibrated noise 3e-11
     assert spectral_orth_error(Uk) <= 1e-12 and spectral_orth_error(V) <= 1e-12
     Ak = Uk @ Tk @ V.T
     assert abs(np.linalg.norm(A - Ak) - rho) <= 1e-12 * np.linalg.norm(A)

@@ -100,3 +100,17 @@ def test_svd_block_golden_and_zero():
     assert np.array_equal(d, [3.0, 2.0, 1.0])
     Us, d, Vs, _ = svd_block(np.zeros((3, 3)))
     assert np.array_equal(Us, np.eye(3)) and np.array_equal(Vs, np.eye(3))
+
+
+def test_svd_block_structurally_rank_deficient_converges():
+    # rows of B span a 2-D space: without the negligible-column rule the
+    # transposed Jacobi would rotate u-sized null vectors forever
+    from oracle.jacobi import svd_block
+    rng = np.random.default_rng(9)
+    B = np.zeros((6, 6))
+    B[:, 1] = rng.standard_normal(6)
+    B[:, 4] = rng.standard_normal(6)
+    Us, d, Vs, sweeps = svd_block(B)
+    assert np.count_nonzero(d) == 2 and sweeps < 10
+    assert np.linalg.norm(Us.T @ Us - np.eye(6)) < 1e-14 and np.linalg.norm(Vs.T @ Vs - np.eye(6)) < 1e-14
+    assert np.linalg.norm(B - (Us * d) @ Vs.T) < 1e-14 * np.linalg.norm(B)

@@ -1,0 +1,29 @@
+#!/bin/bash
+# One gpurun session: tests, bench, ncu launch list, ncu full capture of the top kernel.
+# Usage (from repo root, under gpurun): bash tools/gpu_session.sh [tests] [bench] [ncu_launches] [ncu_full]
+set -u
+mkdir -p gpurun_out
+for stage in "$@"; do
+  case "$stage" in
+    tests)
+      timeout 1200 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider --durations=10 \
+        > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_gpu.log ;;
+    smoke)
+      python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log ;;
+    bench)
+      timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err ;;
+    bench_c2)
+      timeout 900 python bench.py --config c2 --no-cpu-baseline > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo "bench c2 rc=$?"; cat gpurun_out/bench_c2.json ;;
+    ncu_launches)
+      CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-profile"
+      timeout 900 $CMD > gpurun_out/plain.log 2>&1 && \
+      timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD \
+        > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"; tail -3 gpurun_out/ncu_launches.log ;;
+    ncu_full)
+      CMD="python bench.py --config c2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-profile"
+      timeout 900 $CMD > gpurun_out/plain_c2.log 2>&1 && \
+      timeout 1500 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+        -k regex:dgemm_kernelILb0ELb1E -s 6 -c 2 -o gpurun_out/prof_dgemm_nt $CMD \
+        > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -3 gpurun_out/ncu_full.log ;;
+  esac
+done
