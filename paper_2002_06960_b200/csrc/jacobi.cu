@@ -29,8 +29,11 @@
 //      rank order (bitwise identical totals, hence identical rotations and
 //      identical convergence decisions, in every CTA), rotate its own rows.
 // One cluster barrier + one CTA barrier per round; no global memory traffic
-// until the factors are written.  Latency-bound (~b^2/2 pair steps per sweep
-// spread over 8 warps); off the GEMM critical path.
+// until the factors are written.  Per round: partial Gram entries (thread per
+// pair), cluster barrier, the owner CTA of each pair (l mod C) sums the C
+// partials in rank order and forms the rotation, cluster barrier, every CTA
+// gathers all rotations (one DSMEM load per thread) and rotates its rows.
+// Latency-bound: ~2 cluster barriers per round, (b-1) rounds per sweep.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -48,36 +51,40 @@ struct JacobiPlan {
   int nc;        // columns incl. phantom (even)
   int C;         // cluster size
   int RP;        // rows per CTA
-  bool v_smem;   // V slab in shared memory
+  int LDS;       // slab column stride (RP + 1: conflict-free when lanes walk columns)
+  bool v_smem;   // W slab in shared memory
   size_t smem;   // dynamic smem bytes
 };
+
+// shared-memory bytes besides the slabs: part[np][3], rot[np][2], grot[np][2],
+// flags (2 x np ints), dsum[nc + 8]
+size_t aux_bytes(int nc) {
+  const size_t np = nc / 2;
+  return np * 3 * 8 + np * 2 * 8 * 2 + np * 4 * 2 + (size_t)(nc + 8) * 8 + 256;
+}
 
 JacobiPlan plan_for(i64 w) {
   JacobiPlan p;
   p.nc = (int)(w + (w & 1));
   const size_t limit = 200 * 1024;
-  p.C = 0;
-  for (int C = 1; C <= 16; C *= 2) {
-    const int RP = (p.nc + C - 1) / C;
-    if (RP > 64) continue;  // lanes cover <= 2 rows each
-    const size_t part = (size_t)2 * (p.nc / 2) * 3 * 8 + (size_t)(p.nc + 8) * 8 + 64;
-    const size_t x = (size_t)p.nc * RP * 8;
-    if (x * 2 + part <= limit) {
-      p.C = C; p.RP = RP; p.v_smem = true; p.smem = x * 2 + part;
-      return p;
-    }
-  }
-  for (int C = 1; C <= 16; C *= 2) {
-    const int RP = (p.nc + C - 1) / C;
-    if (RP > 64) continue;
-    const size_t part = (size_t)2 * (p.nc / 2) * 3 * 8 + (size_t)(p.nc + 8) * 8 + 64;
-    const size_t x = (size_t)p.nc * RP * 8;
-    if (x + part <= limit) {
-      p.C = C; p.RP = RP; p.v_smem = false; p.smem = x + part;
-      return p;
-    }
-  }
   p.C = -1;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int C = 1; C <= 16; C *= 2) {
+      const int RP = (p.nc + C - 1) / C;
+      if (RP > 64) continue;  // apply phase: lanes cover <= 2 rows each
+      if ((p.nc / 2 + C - 1) / C > JT) continue;
+      const size_t x = (size_t)p.nc * (RP + 1) * 8;
+      const size_t need = (pass == 0 ? 2 * x : x) + aux_bytes(p.nc);
+      if (need <= limit) {
+        p.C = C;
+        p.RP = RP;
+        p.LDS = RP + 1;
+        p.v_smem = pass == 0;
+        p.smem = need;
+        return p;
+      }
+    }
+  }
   return p;
 }
 
@@ -92,11 +99,12 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// X (nc x nc, zero padded) slab: Xs[col * RP + lrow];  V slab likewise (Vsl).
+// X = B^T (nc x nc, zero padded) split by rows: this CTA holds rows [r0, r0+RP)
+// as Xs[col * LDS + lr]; the accumulated rotations W likewise (Ws).
 __global__ void __launch_bounds__(JT)
     jacobi_svd_kernel(int w, const double* __restrict__ B, i64 ldb, double* __restrict__ Us, double* __restrict__ d,
-                      double* __restrict__ Vs, int* status, int block_id, int nc, int RP, int v_smem,
-                      double* __restrict__ vglobal, double tol, int* zero_flag) {
+                      double* __restrict__ Vs, int* status, int block_id, int nc, int RP, int LDS, int v_smem,
+                      double* __restrict__ wglobal, double tol, int* zero_flag) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double sm[];
   const int rank = (int)cluster.block_rank();
@@ -104,9 +112,13 @@ __global__ void __launch_bounds__(JT)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = JT / 32;
   const int npairs = nc / 2;
   double* Xs = sm;
-  double* Vsl = v_smem ? Xs + (size_t)nc * RP : vglobal + (size_t)rank * nc * RP;
-  double* part = (v_smem ? Vsl + (size_t)nc * RP : Xs + (size_t)nc * RP);  // [2][npairs][3]
-  double* dsum = part + 2 * npairs * 3;                                     // [nc + 1]
+  double* Ws = v_smem ? Xs + (size_t)nc * LDS : wglobal + (size_t)rank * nc * LDS;
+  double* part = v_smem ? Ws + (size_t)nc * LDS : Xs + (size_t)nc * LDS;  // [npairs][3] this CTA's partials
+  double* rot = part + npairs * 3;                                        // [npairs][2] owned pairs
+  double* grot = rot + npairs * 2;                                        // [npairs][2] gathered
+  int* rflag = reinterpret_cast<int*>(grot + npairs * 2);                 // [npairs] owned
+  int* gflag = rflag + npairs;                                            // [npairs] gathered
+  double* dsum = reinterpret_cast<double*>(gflag + npairs + (npairs & 1)); // [nc + 8]
   __shared__ int sflag[2];
   const int r0 = rank * RP;
 
@@ -115,9 +127,9 @@ __global__ void __launch_bounds__(JT)
   for (int e = tid; e < nc * RP; e += JT) {
     const int col = e / RP, lr = e % RP, row = r0 + lr;
     const double x = (row < w && col < w) ? B[col + (i64)row * ldb] : 0.0;  // X = B^T
-    Xs[e] = x;
+    Xs[col * LDS + lr] = x;
     ss += x * x;
-    Vsl[e] = (row == col) ? 1.0 : 0.0;
+    Ws[col * LDS + lr] = (row == col) ? 1.0 : 0.0;
   }
   ss = warp_sum(ss);
   if (lane == 0) dsum[warp] = ss;
@@ -137,71 +149,81 @@ __global__ void __launch_bounds__(JT)
 
   int sweeps = 0;
   bool converged = (nc <= 1);
-  int buf = 0;
+  const int nown = (npairs - rank + C - 1) / C;  // pairs l = rank + C j owned by this CTA
   while (!converged) {
     if (sweeps >= MAX_SWEEPS) break;
     ++sweeps;
     int rotated = 0;
     for (int round = 0; round < nc - 1; ++round) {
-      double* pb = part + buf * npairs * 3;
-      // phase 1: partial Gram entries of this warp's pairs over own rows
-      for (int l = warp; l < npairs; l += nwarps) {
+      // 1. partial Gram entries of every pair over this CTA's rows (thread per pair)
+      for (int l = tid; l < npairs; l += JT) {
         const int p = rr_col(l, round, nc), q = rr_col(nc - 1 - l, round, nc);
-        const double* xp = Xs + (size_t)p * RP;
-        const double* xq = Xs + (size_t)q * RP;
+        const double* xp = Xs + p * LDS;
+        const double* xq = Xs + q * LDS;
         double a = 0.0, bb = 0.0, g = 0.0;
-        for (int lr = lane; lr < RP; lr += 32) {
+        for (int lr = 0; lr < RP; ++lr) {
           const double u = xp[lr], v = xq[lr];
-          a += u * u;
-          bb += v * v;
-          g += u * v;
+          a = fma(u, u, a);
+          bb = fma(v, v, bb);
+          g = fma(u, v, g);
         }
-        a = warp_sum(a);
-        bb = warp_sum(bb);
-        g = warp_sum(g);
-        if (lane == 0) {
-          pb[l * 3 + 0] = a;
-          pb[l * 3 + 1] = bb;
-          pb[l * 3 + 2] = g;
-        }
+        part[l * 3 + 0] = a;
+        part[l * 3 + 1] = bb;
+        part[l * 3 + 2] = g;
       }
       cluster.sync();
-      // phase 2: cluster totals (rank order), rotation, apply to own rows
-      for (int l = warp; l < npairs; l += nwarps) {
-        const int p = rr_col(l, round, nc), q = rr_col(nc - 1 - l, round, nc);
+      // 2. owners: totals over the cluster in rank order -> rotation of each owned pair
+      for (int j = tid; j < nown; j += JT) {
+        const int l = rank + C * j;
         double a = 0.0, bb = 0.0, g = 0.0;
-        if (lane == 0) {
-          for (int c = 0; c < C; ++c) {
-            const double* rp = cluster.map_shared_rank(pb + l * 3, c);
-            a += rp[0];
-            bb += rp[1];
-            g += rp[2];
-          }
+        for (int c = 0; c < C; ++c) {
+          const double* rp = cluster.map_shared_rank(part + l * 3, c);
+          a += rp[0];
+          bb += rp[1];
+          g += rp[2];
         }
-        a = __shfl_sync(0xffffffffu, a, 0);
-        bb = __shfl_sync(0xffffffffu, bb, 0);
-        g = __shfl_sync(0xffffffffu, g, 0);
+        int f = 0;
+        double cs = 1.0, sn = 0.0;
         if (a > nu2 && bb > nu2 && fabs(g) > tol * sqrt(a * bb)) {
-          rotated = 1;
           const double zeta = (bb - a) / (2.0 * g);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t);
-          const double s = c * t;
-          double* xp = Xs + (size_t)p * RP;
-          double* xq = Xs + (size_t)q * RP;
-          double* vp = Vsl + (size_t)p * RP;
-          double* vq = Vsl + (size_t)q * RP;
-          for (int lr = lane; lr < RP; lr += 32) {
-            const double u = xp[lr], v = xq[lr];
-            xp[lr] = c * u - s * v;
-            xq[lr] = s * u + c * v;
-            const double uu = vp[lr], vv = vq[lr];
-            vp[lr] = c * uu - s * vv;
-            vq[lr] = s * uu + c * vv;
-          }
+          cs = 1.0 / sqrt(1.0 + t * t);
+          sn = cs * t;
+          f = 1;
+        }
+        rot[l * 2 + 0] = cs;
+        rot[l * 2 + 1] = sn;
+        rflag[l] = f;
+      }
+      cluster.sync();
+      // 3. gather every pair's rotation from its owner
+      for (int l = tid; l < npairs; l += JT) {
+        const int owner = l % C;
+        const double* rp = cluster.map_shared_rank(rot + l * 2, owner);
+        grot[l * 2 + 0] = rp[0];
+        grot[l * 2 + 1] = rp[1];
+        gflag[l] = *cluster.map_shared_rank(rflag + l, owner);
+      }
+      __syncthreads();
+      // 4. rotate this CTA's rows of X and W (warp per pair, lanes over rows)
+      for (int l = warp; l < npairs; l += nwarps) {
+        if (!gflag[l]) continue;
+        rotated = 1;
+        const int p = rr_col(l, round, nc), q = rr_col(nc - 1 - l, round, nc);
+        const double c = grot[l * 2 + 0], s = grot[l * 2 + 1];
+        double* xp = Xs + p * LDS;
+        double* xq = Xs + q * LDS;
+        double* vp = Ws + p * LDS;
+        double* vq = Ws + q * LDS;
+        for (int lr = lane; lr < RP; lr += 32) {
+          const double u = xp[lr], v = xq[lr];
+          xp[lr] = c * u - s * v;
+          xq[lr] = s * u + c * v;
+          const double uu = vp[lr], vv = vq[lr];
+          vp[lr] = c * uu - s * vv;
+          vq[lr] = s * uu + c * vv;
         }
       }
-      buf ^= 1;
       __syncthreads();
     }
     converged = __syncthreads_or(rotated) == 0;
@@ -209,20 +231,19 @@ __global__ void __launch_bounds__(JT)
   if (!converged && rank == 0 && tid == 0) atomicMin(status, block_id);
 
   // column norms over the cluster
-  for (int col = warp; col < nc; col += nwarps) {
-    const double* xc = Xs + (size_t)col * RP;
-    double s = 0.0;
-    for (int lr = lane; lr < RP; lr += 32) s += xc[lr] * xc[lr];
-    s = warp_sum(s);
-    if (lane == 0) dsum[col] = s;
+  for (int col = tid; col < nc; col += JT) {
+    const double* xc = Xs + col * LDS;
+    double s2 = 0.0;
+    for (int lr = 0; lr < RP; ++lr) s2 = fma(xc[lr], xc[lr], s2);
+    dsum[col] = s2;
   }
   cluster.sync();
   // every CTA: totals in rank order -> d; ranks for the stable descending sort
-  double* dl = part;  // reuse: [nc] totals
+  double* dl = part;  // reuse: [nc] totals (part holds 3 npairs >= nc doubles)
   for (int col = tid; col < nc; col += JT) {
-    double s = 0.0;
-    for (int c = 0; c < C; ++c) s += cluster.map_shared_rank(dsum, c)[col];
-    dl[col] = (s <= nu2) ? 0.0 : sqrt(s);
+    double s2 = 0.0;
+    for (int c = 0; c < C; ++c) s2 += cluster.map_shared_rank(dsum, c)[col];
+    dl[col] = (s2 <= nu2) ? 0.0 : sqrt(s2);
   }
   if (tid == 0) sflag[0] = 0;
   cluster.sync();  // dsum reads done everywhere; dl visible in this CTA
@@ -236,8 +257,8 @@ __global__ void __launch_bounds__(JT)
     if (rank == 0) d[rk] = dj;
     if (dj == 0.0) sflag[0] = 1;
     const double inv = dj != 0.0 ? 1.0 / dj : 0.0;
-    const double* xc = Xs + (size_t)col * RP;
-    const double* vc = Vsl + (size_t)col * RP;
+    const double* xc = Xs + col * LDS;
+    const double* vc = Ws + col * LDS;
     for (int lr = 0; lr < RP; ++lr) {
       const int row = r0 + lr;
       if (row >= w) break;
@@ -314,7 +335,7 @@ __global__ void jacobi_complete_kernel(int w, double* __restrict__ Us, const dou
 
 i64 jacobi_scratch_elems(i64 w) {
   const JacobiPlan p = plan_for(w);
-  const i64 vg = p.v_smem ? 0 : (i64)p.C * p.nc * p.RP;
+  const i64 vg = p.v_smem ? 0 : (i64)p.C * p.nc * p.LDS;
   return vg + w + 64;  // + completion temp + flag
 }
 
@@ -325,7 +346,7 @@ int launch_jacobi_svd(const Launch& L, i64 w, const double* B, i64 ldb, double* 
   if (p.C <= 0) return -2;
   if (scratch_elems < jacobi_scratch_elems(w)) return -10;
   double* vglobal = p.v_smem ? nullptr : scratch;
-  double* ctmp = scratch + (p.v_smem ? 0 : (i64)p.C * p.nc * p.RP);
+  double* ctmp = scratch + (p.v_smem ? 0 : (i64)p.C * p.nc * p.LDS);
   int* zero_flag = reinterpret_cast<int*>(ctmp + w);
   static bool attr_done = false;
   if (!attr_done) {
@@ -349,7 +370,7 @@ int launch_jacobi_svd(const Launch& L, i64 w, const double* B, i64 ldb, double* 
   const double tol = sqrt((double)w) * 0x1p-53;
   const size_t pe = L.pbegin();
   RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_svd_kernel, (int)w, B, ldb, Us, d, Vs, status, block_id, p.nc, p.RP,
-                               (int)p.v_smem, vglobal, tol, zero_flag));
+                               p.LDS, (int)p.v_smem, vglobal, tol, zero_flag));
   L.count();
   jacobi_complete_kernel<<<1, 256, 0, L.stream>>>((int)w, Vs, d, zero_flag, ctmp);
   L.count();

@@ -106,7 +106,11 @@ struct randutv_ctx {
   double* stage;
   size_t stage_bytes;
   rutv::Profiler prof;
+  // side stream (high priority) for the small SVD + folds, and its two events
+  cudaStream_t side;
+  cudaEvent_t eR, eF;
   rutv::Launch launch() { return rutv::Launch{stream, &stats.kernel_launches, sms, &prof}; }
+  rutv::Launch side_launch() { return rutv::Launch{side, &stats.kernel_launches, sms, &prof}; }
 };
 
 static const int kMagic = 0x52555456;  // "RUTV"
@@ -142,6 +146,7 @@ struct Work {
   double* lefts;  // truncated-U records
   i64 lefts_elems;
   double* Twork;  // m x n working T for the truncated variant
+  double* Zf;     // fold temporaries of the side stream (max(m,n) x b)
 };
 
 i64 gemm_ws_elems_for(i64 m, i64 n, i64 b) {
@@ -160,6 +165,7 @@ size_t carve(Carver& c, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork) {
   w.Y = c.take<double>(n * b);
   w.Z = c.take<double>(mx * b);
   w.Z2 = c.take<double>(mx * b);
+  w.Zf = c.take<double>(mx * b);
   w.Wv = c.take<double>(n * b);
   w.Wu = c.take<double>(m * b);
   w.TV = c.take<double>(b * b);
@@ -230,6 +236,11 @@ struct Problem {
   double* V;  // n x n (may be null)
   i64 ldv;
   bool record_lefts;
+  // S8/S9 of step i run on a side stream and overlap S1-S4 of step i+1
+  // (SURVEY.md §8(a) "Commutation"): eR = R and T12 of step i ready (main),
+  // eF = folds of step i done (side); S5 of step i+1 waits for eF.
+  Launch side;
+  cudaEvent_t eR, eF;
 };
 
 i64 sampled_steps(i64 n, i64 b) { return n > b ? (n - b + b - 1) / b : 0; }
@@ -254,19 +265,18 @@ int apply_left_t(const Launch& L, Work& w, i64 r, i64 c, i64 bw, double* X, i64 
   return 0;
 }
 
-// X(rows x bw) := X M  (M bw x bw), via Z
-int right_mult_inplace(const Launch& L, Work& w, i64 rows, i64 bw, double* X, i64 ldx, const double* M, i64 ldm) {
+// X(rows x bw) := X M  (M bw x bw), via the temporary Zt
+int right_mult_inplace(const Launch& L, double* Zt, i64 rows, i64 bw, double* X, i64 ldx, const double* M, i64 ldm) {
   if (rows <= 0) return 0;
-  RUTV_TRY(launch_dgemm(L, false, false, rows, bw, bw, 1.0, X, ldx, M, ldm, 0.0, w.Z, rows, nullptr, 0));
-  return launch_copy(L, rows, bw, w.Z, rows, X, ldx);
+  RUTV_TRY(launch_dgemm(L, false, false, rows, bw, bw, 1.0, X, ldx, M, ldm, 0.0, Zt, rows, nullptr, 0));
+  return launch_copy(L, rows, bw, Zt, rows, X, ldx);
 }
 
 // X(bw x cols) := M^T X
-int left_mult_t_inplace(const Launch& L, Work& w, i64 bw, i64 cols, double* X, i64 ldx, const double* M, i64 ldm) {
+int left_mult_t_inplace(const Launch& L, double* Zt, i64 bw, i64 cols, double* X, i64 ldx, const double* M, i64 ldm) {
   if (cols <= 0) return 0;
-  RUTV_TRY(launch_dgemm(L, true, false, bw, cols, bw, 1.0, M, ldm, X, ldx, 0.0, w.Z, bw, w.gemm_ws,
-                        w.gemm_ws_elems));
-  return launch_copy(L, bw, cols, w.Z, bw, X, ldx);
+  RUTV_TRY(launch_dgemm(L, true, false, bw, cols, bw, 1.0, M, ldm, X, ldx, 0.0, Zt, bw, nullptr, 0));
+  return launch_copy(L, bw, cols, Zt, bw, X, ldx);
 }
 
 // S8 + S9 for a bw x bw diagonal block at (kk, kk).  `B` is the block to
@@ -275,22 +285,26 @@ int svd_and_fold(const Launch& L, Work& w, const Problem& P, i64 kk, i64 bw, int
   double* T11 = P.T + kk + kk * P.ldt;
   RUTV_TRY(launch_jacobi_svd(L, bw, T11, P.ldt, w.Us, w.d, w.Vs, w.status, block_id, w.jac, w.jac_elems));
   RUTV_TRY(launch_set_diag(L, bw, w.d, T11, P.ldt));
-  RUTV_TRY(right_mult_inplace(L, w, kk, bw, P.T + kk * P.ldt, P.ldt, w.Vs, bw));                 // A01 V_s
-  RUTV_TRY(left_mult_t_inplace(L, w, bw, P.n - kk - bw, P.T + kk + (kk + bw) * P.ldt, P.ldt, w.Us, bw));  // U_s^T A12
-  if (P.U) RUTV_TRY(right_mult_inplace(L, w, P.m, bw, P.U + kk * P.ldu, P.ldu, w.Us, bw));         // U1 U_s
-  if (P.V) RUTV_TRY(right_mult_inplace(L, w, P.n, bw, P.V + kk * P.ldv, P.ldv, w.Vs, bw));         // V1 V_s
+  RUTV_TRY(right_mult_inplace(L, w.Zf, kk, bw, P.T + kk * P.ldt, P.ldt, w.Vs, bw));                 // A01 V_s
+  RUTV_TRY(left_mult_t_inplace(L, w.Zf, bw, P.n - kk - bw, P.T + kk + (kk + bw) * P.ldt, P.ldt, w.Us, bw));  // U_s^T A12
+  if (P.U) RUTV_TRY(right_mult_inplace(L, w.Zf, P.m, bw, P.U + kk * P.ldu, P.ldu, w.Us, bw));         // U1 U_s
+  if (P.V) RUTV_TRY(right_mult_inplace(L, w.Zf, P.n, bw, P.V + kk * P.ldv, P.ldv, w.Vs, bw));         // V1 V_s
   return 0;
 }
 
-int record_left(const Launch& L, Work& w, const Problem& P, int step, i64 r, i64 bw, bool has_w) {
-  const i64 b = P.b;
-  double* rec = w.lefts + (i64)step * (P.m * b + 2 * b * b);
-  if (has_w) {
-    RUTV_TRY(launch_copy(L, r, bw, w.Wu, r, rec, r));
-    RUTV_TRY(launch_copy(L, bw, bw, w.TU, b, rec + P.m * b, bw));
-  }
-  RUTV_TRY(launch_copy(L, bw, bw, w.Us, bw, rec + P.m * b + b * b, bw));
-  return 0;
+double* left_record(Work& w, const Problem& P, int step) { return w.lefts + (i64)step * (P.m * P.b + 2 * P.b * P.b); }
+
+// (W_U, T_U) of a step for the backward U_k accumulation: on the main stream
+// (the next step's S6 overwrites them there)
+int record_left_w(const Launch& L, Work& w, const Problem& P, int step, i64 r, i64 bw) {
+  double* rec = left_record(w, P, step);
+  RUTV_TRY(launch_copy(L, r, bw, w.Wu, r, rec, r));
+  return launch_copy(L, bw, bw, w.TU, P.b, rec + P.m * P.b, bw);
+}
+
+// U_s of a step: on the stream that ran its SVD
+int record_left_us(const Launch& L, Work& w, const Problem& P, int step, i64 bw) {
+  return launch_copy(L, bw, bw, w.Us, bw, left_record(w, P, step) + P.m * P.b + P.b * P.b, bw);
 }
 
 int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
@@ -307,7 +321,9 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   }
   // S4
   RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
-  // S5: all m rows of T(:, k:n); V(:, k:n)
+  // S5: all m rows of T(:, k:n); V(:, k:n).  Row block i-1 of T(:, k:n) is
+  // written by the side stream's U_s^T T12 fold of step i-1: wait for it.
+  RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
   RUTV_TRY(apply_right(L, w, m, s, b, P.T + kk * P.ldt, P.ldt, w.Wv, s, w.TV, b));
   if (P.V) RUTV_TRY(apply_right(L, w, n, s, b, P.V + kk * P.ldv, P.ldv, w.Wv, s, w.TV, b));
   // S6: QR of the column block in place; keep R, zero below
@@ -317,9 +333,13 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   // S7
   RUTV_TRY(apply_left_t(L, w, r, s - b, b, At + b * P.ldt, P.ldt, w.Wu, r, w.TU, b));
   if (P.U) RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
-  // S8, S9
-  RUTV_TRY(svd_and_fold(L, w, P, kk, b, (int)(i + 1)));
-  if (P.record_lefts) RUTV_TRY(record_left(L, w, P, (int)i, r, b, true));
+  if (P.record_lefts) RUTV_TRY(record_left_w(L, w, P, (int)i, r, b));
+  // S8, S9 on the side stream, overlapping S1-S4 of step i+1
+  RUTV_CUDA(cudaEventRecord(P.eR, L.stream));
+  RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eR, 0));
+  RUTV_TRY(svd_and_fold(P.side, w, P, kk, b, (int)(i + 1)));
+  if (P.record_lefts) RUTV_TRY(record_left_us(P.side, w, P, (int)i, b));
+  RUTV_CUDA(cudaEventRecord(P.eF, P.side.stream));
   return 0;
 }
 
@@ -328,6 +348,7 @@ int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   if (s <= 0) return 0;
   double* At = P.T + kk + kk * P.ldt;
   const bool tall = r > s;
+  RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));  // previous step's folds
   if (tall) {
     RUTV_TRY(panel_qr(L, r, s, At, P.ldt, w.tauU, w.Wu, r, w.TU, P.b, w.qw));
     RUTV_TRY(launch_triu(L, s, s, At, P.ldt));
@@ -336,22 +357,31 @@ int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   }
   RUTV_TRY(svd_and_fold(L, w, P, kk, s, (int)(i + 1)));
   if (P.record_lefts) {
-    // T_U of the final step has leading dimension b in w.TU; record_left copies with ld b
-    RUTV_TRY(record_left(L, w, P, (int)i, r, s, tall));
+    if (tall) RUTV_TRY(record_left_w(L, w, P, (int)i, r, s));  // T_U has ld b in w.TU
+    RUTV_TRY(record_left_us(L, w, P, (int)i, s));
   }
   return 0;
 }
 
-// Runs steps [0, nsteps) (sampled) and the final step if `with_final`.
+// Runs steps [0, nsteps) (sampled) and the final step if `with_final`; joins
+// the side stream back into the main stream at the end.
 int run_loop(const Launch& L, Work& w, const Problem& P, i64 nsteps, bool with_final) {
   for (i64 i = 0; i < nsteps; ++i) RUTV_TRY(sampled_step(L, w, P, i));
   if (with_final) RUTV_TRY(final_step(L, w, P, nsteps));
+  RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
   return 0;
 }
 
 int begin_call(randutv_ctx* ctx) {
   if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
   RUTV_CUDA(cudaSetDevice(ctx->device));
+  if (!ctx->side) {
+    int lo = 0, hi = 0;
+    RUTV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    RUTV_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eR, cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eF, cudaEventDisableTiming));
+  }
   return 0;
 }
 
@@ -413,8 +443,14 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
   if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->side) cudaStreamSynchronize(ctx->side);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->stage) cudaFree(ctx->stage);
+  if (ctx->side) {
+    cudaEventDestroy(ctx->eR);
+    cudaEventDestroy(ctx->eF);
+    cudaStreamDestroy(ctx->side);
+  }
   ctx->magic = 0;
   delete ctx;
   return 0;
@@ -516,7 +552,8 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
     RUTV_TRY(launch_set_identity(L, m, m, U, ldu));
     RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
   }
-  Problem P{m, n, bb, q, seed, T, ldt, uv ? U : nullptr, ldu, uv ? V : nullptr, ldv, false};
+  Problem P{m, n, bb, q, seed, T, ldt, uv ? U : nullptr, ldu, uv ? V : nullptr, ldv, false,
+            ctx->side_launch(), ctx->eR, ctx->eF};
   const i64 nsamp = sampled_steps(n, bb);
   RUTV_TRY(run_loop(L, w, P, nsamp, true));
   const int st = finish(ctx, w);
@@ -559,7 +596,8 @@ RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, cons
   RUTV_TRY(start_status(ctx, w));
   RUTV_CUDA(cudaMemcpy2DAsync(w.Twork, m * 8, A, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
   if (uv) RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
-  Problem P{m, n, bb, q, seed, w.Twork, m, nullptr, m, uv ? V : nullptr, ldv, uv};
+  Problem P{m, n, bb, q, seed, w.Twork, m, nullptr, m, uv ? V : nullptr, ldv, uv,
+            ctx->side_launch(), ctx->eR, ctx->eF};
   RUTV_TRY(run_loop(L, w, P, K, with_final));
   // rho = ||T(k:m, k:n)||_F
   RUTV_TRY(launch_sumsq(L, m - k, n - k, w.Twork + k + k * m, m, w.red, w.scal));
