@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(JT)
   double* grot = rot + npairs * 2;                                        // [npairs][2] gathered
   int* rflag = reinterpret_cast<int*>(grot + npairs * 2);                 // [npairs] owned
   int* gflag = rflag + npairs;                                            // [npairs] gathered
-  double* dsum = reinterpret_cast<double*>(gflag + npairs + (npairs & 1)); // [nc + 8]
+  double* dsum = reinterpret_cast<double*>(gflag + npairs);                // [nc + 8] (2 npairs ints: 8-B aligned)
   __shared__ int sflag[2];
   const int r0 = rank * RP;
 
