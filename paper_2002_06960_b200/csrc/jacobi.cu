@@ -2,38 +2,30 @@
 //
 // Paper: "Compute the SVD of (U22(:,1:b))* T22 V22(:,1:b) = U_SVD D V_SVD*"
 // (Sec. 3.1); FLAME "[A11, U_SVD, V_SVD] := SVD(A11)";
-// task Svd_of_block.  The algorithm is reading A10 of DESIGN.md:
-// one-sided (Hestenes) Jacobi applied to X = B^T (the ROWS of B are
-// orthogonalised, Drmac-Veselic transposition: fast on the row-graded R of a
-// randUTV step); at convergence B^T W = Q diag(d), so U_SVD = W, V_SVD = Q.
-// A pair (p, q) of columns of X is rotated when
-// |x_p.x_q| > tol sqrt(|x_p|^2 |x_q|^2), tol = sqrt(b) 2^-53, with
+// task Svd_of_block.  The algorithm is reading A10/A23/A24 of
+// DESIGN.md: one-sided (Hestenes) Jacobi applied to X = B^T (the ROWS of B are
+// orthogonalised); at convergence B^T W = Q diag(d), so U_SVD = W, V_SVD = Q.
+// A pair (p, q) of columns of X is rotated when both columns are longer than
+// nu = b 2^-53 ||B||_F and |x_p.x_q| > tol sqrt(|x_p|^2 |x_q|^2),
+// tol = sqrt(b) 2^-53, with
 //   zeta = (beta - alpha)/(2 gamma), t = sign(zeta)/(|zeta| + sqrt(1+zeta^2)),
-//   c = 1/sqrt(1+t^2), s = c t,  (x_p, x_q) <- (c x_p - s x_q, s x_p + c x_q),
-// columns with |x| <= nu = b 2^-53 ||B||_F are numerically null (never rotated,
-// d := 0, completed), stop after a sweep without rotations (cap 30 sweeps ->
-// status +block),
-// d_j = |x_j|, Q(:,j) = x_j/d_j (zero columns completed by Gram-Schmidt),
-// stable descending sort of d.
+//   c = 1/sqrt(1+t^2), s = c t,  (x_p, x_q) <- (c x_p - s x_q, s x_p + c x_q);
+// stop after a sweep without rotations (cap 30 sweeps -> status +block);
+// d_j = |x_j| (0 if |x_j| <= nu), Q(:,j) = x_j/d_j (zero columns completed by
+// Gram-Schmidt); stable descending sort of d.
 //
-// B200 design.  The oracle visits pairs cyclic-by-rows; here each sweep is the
-// b-1 rounds of a round-robin tournament, b/2 disjoint pairs per round, which
-// converges to the same d (unique) and to U, V equal up to the signs of
-// singular-vector pairs (which no parity metric sees).  X = B^T and
-// W = I are split by ROWS over a thread-block cluster of C CTAs (C <= 16,
-// chosen so the row slabs fit in shared memory): every column operation is
-// row-separable, so each round is
-//   1. every CTA: partial (alpha, beta, gamma) of each pair over its rows,
-//   2. cluster barrier,
-//   3. every CTA: read the C partials of each pair through DSMEM, sum them in
-//      rank order (bitwise identical totals, hence identical rotations and
-//      identical convergence decisions, in every CTA), rotate its own rows.
-// One cluster barrier + one CTA barrier per round; no global memory traffic
-// until the factors are written.  Per round: partial Gram entries (thread per
-// pair), cluster barrier, the owner CTA of each pair (l mod C) sums the C
-// partials in rank order and forms the rotation, cluster barrier, every CTA
-// gathers all rotations (one DSMEM load per thread) and rotates its rows.
-// Latency-bound: ~2 cluster barriers per round, (b-1) rounds per sweep.
+// B200 design: BLOCK one-sided Jacobi (reading A25: a different, equally valid
+// cyclic pair order than the oracle's; same d, U/V up to singular-vector signs).
+// The nc columns of X (b padded to a multiple of 2 nb with zero columns) form
+// nblk = nc/nb column blocks; P = nblk/2 CTAs of a cooperative grid each take a
+// pair of blocks per block round (round-robin tournament over blocks, nblk-1
+// block rounds per sweep), stage their 2 nb columns of X and of W in shared
+// memory, and perform every cross pair (p in I, q in J) as nb inner rounds of
+// nb disjoint rotations (intra-block pairs in the first block round of a
+// sweep) -- warp per pair, lanes over rows, so the per-rotation barrier is a
+// CTA barrier, not a grid/cluster one.  One grid barrier per block round.
+// Every pair is visited once per sweep; each dot product is one warp's fixed
+// lane-strided sum + xor butterfly (bitwise identical on every lane and run).
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -48,49 +40,20 @@ constexpr int JT = 256;  // threads per CTA
 constexpr int MAX_SWEEPS = 30;
 
 struct JacobiPlan {
-  int nc;        // columns incl. phantom (even)
-  int C;         // cluster size
-  int RP;        // rows per CTA
-  int LDS;       // slab column stride (RP + 1: conflict-free when lanes walk columns)
-  bool v_smem;   // W slab in shared memory
-  size_t smem;   // dynamic smem bytes
+  int nb;      // columns per block
+  int nc;      // padded column count (multiple of 2 nb)
+  int P;       // CTAs = nblk / 2
+  size_t smem; // dynamic shared memory
 };
-
-// shared-memory bytes besides the slabs: part[np][3], rot[np][2], grot[np][2],
-// flags (2 x np ints), dsum[nc + 8]
-size_t aux_bytes(int nc) {
-  const size_t np = nc / 2;
-  return np * 3 * 8 + np * 2 * 8 * 2 + np * 4 * 2 + (size_t)(nc + 8) * 8 + 256;
-}
 
 JacobiPlan plan_for(i64 w) {
   JacobiPlan p;
-  p.nc = (int)(w + (w & 1));
-  const size_t limit = 200 * 1024;
-  p.C = -1;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int C = 1; C <= 16; C *= 2) {
-      const int RP = (p.nc + C - 1) / C;
-      if (RP > 64) continue;  // apply phase: lanes cover <= 2 rows each
-      if ((p.nc / 2 + C - 1) / C > JT) continue;
-      const size_t x = (size_t)p.nc * (RP + 1) * 8;
-      const size_t need = (pass == 0 ? 2 * x : x) + aux_bytes(p.nc);
-      if (need <= limit) {
-        p.C = C;
-        p.RP = RP;
-        p.LDS = RP + 1;
-        p.v_smem = pass == 0;
-        p.smem = need;
-        return p;
-      }
-    }
-  }
+  p.nb = w <= 256 ? 16 : 8;
+  const i64 ww = w < 1 ? 1 : w;
+  p.nc = (int)((ww + 2 * p.nb - 1) / (2 * p.nb) * (2 * p.nb));
+  p.P = p.nc / p.nb / 2;
+  p.smem = (size_t)2 * p.nb * ((size_t)ww + p.nc) * sizeof(double);
   return p;
-}
-
-// round-robin tournament: position 0 fixed, positions 1..nc-1 rotate by `round`
-__device__ __forceinline__ int rr_col(int pos, int round, int nc) {
-  return pos == 0 ? 0 : 1 + (pos - 1 + round) % (nc - 1);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -99,175 +62,170 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// X = B^T (nc x nc, zero padded) split by rows: this CTA holds rows [r0, r0+RP)
-// as Xs[col * LDS + lr]; the accumulated rotations W likewise (Ws).
-__global__ void __launch_bounds__(JT)
-    jacobi_svd_kernel(int w, const double* __restrict__ B, i64 ldb, double* __restrict__ Us, double* __restrict__ d,
-                      double* __restrict__ Vs, int* status, int block_id, int nc, int RP, int LDS, int v_smem,
-                      double* __restrict__ wglobal, double tol, int* zero_flag) {
-  cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ __align__(16) double sm[];
-  const int rank = (int)cluster.block_rank();
-  const int C = (int)cluster.num_blocks();
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = JT / 32;
-  const int npairs = nc / 2;
-  double* Xs = sm;
-  double* Ws = v_smem ? Xs + (size_t)nc * LDS : wglobal + (size_t)rank * nc * LDS;
-  double* part = v_smem ? Ws + (size_t)nc * LDS : Xs + (size_t)nc * LDS;  // [npairs][3] this CTA's partials
-  double* rot = part + npairs * 3;                                        // [npairs][2] owned pairs
-  double* grot = rot + npairs * 2;                                        // [npairs][2] gathered
-  int* rflag = reinterpret_cast<int*>(grot + npairs * 2);                 // [npairs] owned
-  int* gflag = rflag + npairs;                                            // [npairs] gathered
-  double* dsum = reinterpret_cast<double*>(gflag + npairs);                // [nc + 8] (2 npairs ints: 8-B aligned)
-  __shared__ int sflag[2];
-  const int r0 = rank * RP;
+// round-robin tournament over `n` (even) slots: slot 0 fixed, others rotate
+__device__ __forceinline__ int rr(int pos, int round, int n) {
+  return pos == 0 ? 0 : 1 + (pos - 1 + round) % (n - 1);
+}
 
-  // load X = B^T (zero padded) and W = I for this CTA's rows; partial ||B||_F^2
+// One warp: test and (maybe) rotate the column pair (xp, xq) of X (w rows) and
+// (wp, wq) of W (nc rows).  Returns 1 if rotated.
+__device__ __forceinline__ int jacobi_pair(double* xp, double* xq, double* wp, double* wq, int w, int nc,
+                                           double tol, double nu2, int lane) {
+  double a = 0.0, bb = 0.0, g = 0.0;
+  for (int r = lane; r < w; r += 32) {
+    const double u = xp[r], v = xq[r];
+    a = fma(u, u, a);
+    bb = fma(v, v, bb);
+    g = fma(u, v, g);
+  }
+  a = warp_sum(a);
+  bb = warp_sum(bb);
+  g = warp_sum(g);
+  if (!(a > nu2 && bb > nu2 && fabs(g) > tol * sqrt(a * bb))) return 0;
+  const double zeta = (bb - a) / (2.0 * g);
+  const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
+  const double c = 1.0 / sqrt(1.0 + t * t);
+  const double s = c * t;
+  for (int r = lane; r < w; r += 32) {
+    const double u = xp[r], v = xq[r];
+    xp[r] = c * u - s * v;
+    xq[r] = s * u + c * v;
+  }
+  for (int r = lane; r < nc; r += 32) {
+    const double u = wp[r], v = wq[r];
+    wp[r] = c * u - s * v;
+    wq[r] = s * u + c * v;
+  }
+  return 1;
+}
+
+// Xg: w x nc (X = B^T, zero padded columns), Wg: nc x nc, both column-major in
+// global memory (L2 resident).  red: >= 2 P + nc doubles; flags: MAX_SWEEPS+1 ints (zeroed).
+__global__ void __launch_bounds__(JT)
+    jacobi_block_kernel(int w, const double* __restrict__ B, i64 ldb, double* __restrict__ Us, double* __restrict__ d,
+                        double* __restrict__ Vs, int* status, int block_id, int nb, int nc, double* __restrict__ Xg,
+                        double* __restrict__ Wg, double* __restrict__ red, int* __restrict__ flags, double tol,
+                        int* zero_flag) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double wred[JT / 32];
+  __shared__ int srot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = JT / 32;
+  const int cta = blockIdx.x, P = gridDim.x;
+  const int nblk = nc / nb;
+  double* Xs = sm;                       // 2 nb columns x w
+  double* Ws = sm + (size_t)2 * nb * w;  // 2 nb columns x nc
+
+  // ---- X = B^T, W = I; this CTA initialises columns [cta*2nb, (cta+1)*2nb)
   double ss = 0.0;
-  for (int e = tid; e < nc * RP; e += JT) {
-    const int col = e / RP, lr = e % RP, row = r0 + lr;
-    const double x = (row < w && col < w) ? B[col + (i64)row * ldb] : 0.0;  // X = B^T
-    Xs[col * LDS + lr] = x;
-    ss += x * x;
-    Ws[col * LDS + lr] = (row == col) ? 1.0 : 0.0;
+  for (int cl = 0; cl < 2 * nb; ++cl) {
+    const int col = cta * 2 * nb + cl;
+    for (int r = tid; r < w; r += JT) {
+      const double x = col < w ? B[col + (i64)r * ldb] : 0.0;
+      Xg[r + (i64)col * w] = x;
+      ss = fma(x, x, ss);
+    }
+    for (int r = tid; r < nc; r += JT) Wg[r + (i64)col * nc] = (r == col) ? 1.0 : 0.0;
   }
   ss = warp_sum(ss);
-  if (lane == 0) dsum[warp] = ss;
+  if (lane == 0) wred[warp] = ss;
   __syncthreads();
   if (tid == 0) {
     double t = 0.0;
-    for (int k = 0; k < nwarps; ++k) t += dsum[k];
-    dsum[nc] = t;  // this CTA's partial, read by every CTA below
+    for (int k = 0; k < nwarps; ++k) t += wred[k];
+    red[cta] = t;
   }
-  cluster.sync();
-  // nu^2 = (w 2^-53 ||B||_F)^2: columns this short are numerically null (not rotated, d := 0)
+  grid.sync();
   double fro2 = 0.0;
-  for (int c = 0; c < C; ++c) fro2 += cluster.map_shared_rank(dsum, c)[nc];
+  for (int c = 0; c < P; ++c) fro2 += red[c];  // same order in every CTA
   const double nu = (double)w * 0x1p-53 * sqrt(fro2);
   const double nu2 = nu * nu;
-  cluster.sync();  // dsum is reused below
 
   int sweeps = 0;
-  bool converged = (nc <= 1);
-  const int nown = (npairs - rank + C - 1) / C;  // pairs l = rank + C j owned by this CTA
+  bool converged = (w <= 1);
   while (!converged) {
     if (sweeps >= MAX_SWEEPS) break;
-    ++sweeps;
     int rotated = 0;
-    for (int round = 0; round < nc - 1; ++round) {
-      // 1. partial Gram entries of every pair over this CTA's rows (thread per pair)
-      for (int l = tid; l < npairs; l += JT) {
-        const int p = rr_col(l, round, nc), q = rr_col(nc - 1 - l, round, nc);
-        const double* xp = Xs + p * LDS;
-        const double* xq = Xs + q * LDS;
-        double a = 0.0, bb = 0.0, g = 0.0;
-        for (int lr = 0; lr < RP; ++lr) {
-          const double u = xp[lr], v = xq[lr];
-          a = fma(u, u, a);
-          bb = fma(v, v, bb);
-          g = fma(u, v, g);
-        }
-        part[l * 3 + 0] = a;
-        part[l * 3 + 1] = bb;
-        part[l * 3 + 2] = g;
-      }
-      cluster.sync();
-      // 2. owners: totals over the cluster in rank order -> rotation of each owned pair
-      for (int j = tid; j < nown; j += JT) {
-        const int l = rank + C * j;
-        double a = 0.0, bb = 0.0, g = 0.0;
-        for (int c = 0; c < C; ++c) {
-          const double* rp = cluster.map_shared_rank(part + l * 3, c);
-          a += rp[0];
-          bb += rp[1];
-          g += rp[2];
-        }
-        int f = 0;
-        double cs = 1.0, sn = 0.0;
-        if (a > nu2 && bb > nu2 && fabs(g) > tol * sqrt(a * bb)) {
-          const double zeta = (bb - a) / (2.0 * g);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-          cs = 1.0 / sqrt(1.0 + t * t);
-          sn = cs * t;
-          f = 1;
-        }
-        rot[l * 2 + 0] = cs;
-        rot[l * 2 + 1] = sn;
-        rflag[l] = f;
-      }
-      cluster.sync();
-      // 3. gather every pair's rotation from its owner
-      for (int l = tid; l < npairs; l += JT) {
-        const int owner = l % C;
-        const double* rp = cluster.map_shared_rank(rot + l * 2, owner);
-        grot[l * 2 + 0] = rp[0];
-        grot[l * 2 + 1] = rp[1];
-        gflag[l] = *cluster.map_shared_rank(rflag + l, owner);
+    for (int r = 0; r < nblk - 1; ++r) {
+      const int I = rr(cta, r, nblk), J = rr(nblk - 1 - cta, r, nblk);
+      // stage blocks I and J of X and W
+      for (int cl = 0; cl < 2 * nb; ++cl) {
+        const int col = (cl < nb ? I * nb + cl : J * nb + cl - nb);
+        for (int e = tid; e < w; e += JT) Xs[(size_t)cl * w + e] = Xg[e + (i64)col * w];
+        for (int e = tid; e < nc; e += JT) Ws[(size_t)cl * nc + e] = Wg[e + (i64)col * nc];
       }
       __syncthreads();
-      // 4. rotate this CTA's rows of X and W (warp per pair, lanes over rows)
-      for (int l = warp; l < npairs; l += nwarps) {
-        if (!gflag[l]) continue;
-        rotated = 1;
-        const int p = rr_col(l, round, nc), q = rr_col(nc - 1 - l, round, nc);
-        const double c = grot[l * 2 + 0], s = grot[l * 2 + 1];
-        double* xp = Xs + p * LDS;
-        double* xq = Xs + q * LDS;
-        double* vp = Ws + p * LDS;
-        double* vq = Ws + q * LDS;
-        for (int lr = lane; lr < RP; lr += 32) {
-          const double u = xp[lr], v = xq[lr];
-          xp[lr] = c * u - s * v;
-          xq[lr] = s * u + c * v;
-          const double uu = vp[lr], vv = vq[lr];
-          vp[lr] = c * uu - s * vv;
-          vq[lr] = s * uu + c * vv;
+      if (r == 0) {
+        // intra-block pairs of both blocks: nb-1 inner rounds, nb/2 pairs per block each
+        for (int t = 0; t < nb - 1; ++t) {
+          for (int pi = warp; pi < nb; pi += nwarps) {
+            const int blk = pi / (nb / 2), k = pi % (nb / 2);
+            const int p = blk * nb + rr(k, t, nb), q = blk * nb + rr(nb - 1 - k, t, nb);
+            rotated |= jacobi_pair(Xs + (size_t)p * w, Xs + (size_t)q * w, Ws + (size_t)p * nc, Ws + (size_t)q * nc,
+                                   w, nc, tol, nu2, lane);
+          }
+          __syncthreads();
         }
       }
-      __syncthreads();
+      // cross pairs (a in I, (a + t) mod nb in J): nb inner rounds of nb disjoint pairs
+      for (int t = 0; t < nb; ++t) {
+        for (int a = warp; a < nb; a += nwarps) {
+          const int p = a, q = nb + (a + t) % nb;
+          rotated |= jacobi_pair(Xs + (size_t)p * w, Xs + (size_t)q * w, Ws + (size_t)p * nc, Ws + (size_t)q * nc, w,
+                                 nc, tol, nu2, lane);
+        }
+        __syncthreads();
+      }
+      for (int cl = 0; cl < 2 * nb; ++cl) {
+        const int col = (cl < nb ? I * nb + cl : J * nb + cl - nb);
+        for (int e = tid; e < w; e += JT) Xg[e + (i64)col * w] = Xs[(size_t)cl * w + e];
+        for (int e = tid; e < nc; e += JT) Wg[e + (i64)col * nc] = Ws[(size_t)cl * nc + e];
+      }
+      grid.sync();
     }
-    converged = __syncthreads_or(rotated) == 0;
+    if (tid == 0) srot = 0;
+    __syncthreads();
+    if (rotated) atomicOr(&srot, 1);
+    __syncthreads();
+    if (tid == 0 && srot) atomicOr(&flags[sweeps], 1);
+    grid.sync();
+    converged = (*(volatile int*)&flags[sweeps]) == 0;
+    ++sweeps;
   }
-  if (!converged && rank == 0 && tid == 0) atomicMin(status, block_id);
+  if (!converged && cta == 0 && tid == 0) atomicMin(status, block_id);
 
-  // column norms over the cluster
-  for (int col = tid; col < nc; col += JT) {
-    const double* xc = Xs + col * LDS;
+  // ---- column norms (thread per column, sequential over rows), d, stable descending sort
+  double* dn = red + 2 * P;  // [nc]
+  for (int col = cta * JT + tid; col < nc; col += P * JT) {
+    const double* xc = Xg + (i64)col * w;
     double s2 = 0.0;
-    for (int lr = 0; lr < RP; ++lr) s2 = fma(xc[lr], xc[lr], s2);
-    dsum[col] = s2;
+    for (int e = 0; e < w; ++e) s2 = fma(xc[e], xc[e], s2);
+    dn[col] = (s2 <= nu2) ? 0.0 : sqrt(s2);
   }
-  cluster.sync();
-  // every CTA: totals in rank order -> d; ranks for the stable descending sort
-  double* dl = part;  // reuse: [nc] totals (part holds 3 npairs >= nc doubles)
-  for (int col = tid; col < nc; col += JT) {
-    double s2 = 0.0;
-    for (int c = 0; c < C; ++c) s2 += cluster.map_shared_rank(dsum, c)[col];
-    dl[col] = (s2 <= nu2) ? 0.0 : sqrt(s2);
-  }
-  if (tid == 0) sflag[0] = 0;
-  cluster.sync();  // dsum reads done everywhere; dl visible in this CTA
-  for (int col = tid; col < w; col += JT) {
-    const double dj = dl[col];
+  grid.sync();
+  int anyzero = 0;
+  for (int col = cta; col < w; col += P) {  // CTA per column
+    const double dj = dn[col];
     int rk = 0;
-    for (int i = 0; i < nc; ++i) {
-      const double di = dl[i];
+    for (int i = tid; i < nc; i += JT) {
+      const double di = dn[i];
       rk += (di > dj) || (di == dj && i < col);
     }
-    if (rank == 0) d[rk] = dj;
-    if (dj == 0.0) sflag[0] = 1;
+    rk = __reduce_add_sync(0xffffffffu, rk);
+    if (lane == 0) wred[warp] = (double)rk;
+    __syncthreads();
+    int rank = 0;
+    for (int k = 0; k < nwarps; ++k) rank += (int)wred[k];
+    __syncthreads();
+    if (tid == 0) d[rank] = dj;
+    anyzero |= (dj == 0.0);
     const double inv = dj != 0.0 ? 1.0 / dj : 0.0;
-    const double* xc = Xs + col * LDS;
-    const double* vc = Ws + col * LDS;
-    for (int lr = 0; lr < RP; ++lr) {
-      const int row = r0 + lr;
-      if (row >= w) break;
-      Vs[row + (i64)rk * w] = dj != 0.0 ? xc[lr] * inv : 0.0;  // V_SVD = Q = X / d
-      Us[row + (i64)rk * w] = vc[lr];                         // U_SVD = W (rotations)
+    for (int e = tid; e < w; e += JT) {
+      Vs[e + (i64)rank * w] = dj != 0.0 ? Xg[e + (i64)col * w] * inv : 0.0;  // V_SVD = Q = X / d
+      Us[e + (i64)rank * w] = Wg[e + (i64)col * nc];                         // U_SVD = W
     }
   }
-  __syncthreads();
-  if (sflag[0] && rank == 0 && tid == 0) atomicExch(zero_flag, 1);
+  if (anyzero && tid == 0) atomicExch(zero_flag, 1);
 }
 
 // Completion of the Q (= V_SVD) columns with d_j == 0 (sorted last): Gram-Schmidt of e_1, e_2, ...
@@ -335,42 +293,36 @@ __global__ void jacobi_complete_kernel(int w, double* __restrict__ Us, const dou
 
 i64 jacobi_scratch_elems(i64 w) {
   const JacobiPlan p = plan_for(w);
-  const i64 vg = p.v_smem ? 0 : (i64)p.C * p.nc * p.LDS;
-  return vg + w + 64;  // + completion temp + flag
+  const i64 ww = w < 1 ? 1 : w;
+  // Xg (w x nc) + Wg (nc x nc) + red (2P + nc) + completion temp (w) + flags/zero flag
+  return ww * p.nc + (i64)p.nc * p.nc + 2 * p.P + p.nc + ww + 64;
 }
 
 int launch_jacobi_svd(const Launch& L, i64 w, const double* B, i64 ldb, double* Us, double* d, double* Vs,
                       int* status, int block_id, double* scratch, i64 scratch_elems) {
   if (w <= 0) return 0;
   const JacobiPlan p = plan_for(w);
-  if (p.C <= 0) return -2;
   if (scratch_elems < jacobi_scratch_elems(w)) return -10;
-  double* vglobal = p.v_smem ? nullptr : scratch;
-  double* ctmp = scratch + (p.v_smem ? 0 : (i64)p.C * p.nc * p.LDS);
-  int* zero_flag = reinterpret_cast<int*>(ctmp + w);
+  double* Xg = scratch;
+  double* Wg = Xg + w * p.nc;
+  double* red = Wg + (i64)p.nc * p.nc;
+  double* ctmp = red + 2 * p.P + p.nc;
+  int* iflags = reinterpret_cast<int*>(ctmp + w);  // [0] zero flag, [1..] sweep flags
+  int* zero_flag = iflags;
+  int* flags = iflags + 1;
   static bool attr_done = false;
   if (!attr_done) {
-    RUTV_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    RUTV_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RUTV_CUDA(cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_done = true;
   }
-  RUTV_CUDA(cudaMemsetAsync(zero_flag, 0, sizeof(int), L.stream));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.C);
-  cfg.blockDim = dim3(JT);
-  cfg.dynamicSmemBytes = p.smem;
-  cfg.stream = L.stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const double tol = sqrt((double)w) * 0x1p-53;
+  RUTV_CUDA(cudaMemsetAsync(iflags, 0, sizeof(int) * (MAX_SWEEPS + 2), L.stream));
   const size_t pe = L.pbegin();
-  RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_svd_kernel, (int)w, B, ldb, Us, d, Vs, status, block_id, p.nc, p.RP,
-                               p.LDS, (int)p.v_smem, vglobal, tol, zero_flag));
+  int wi = (int)w, bid = block_id, nbv = p.nb, ncv = p.nc;
+  i64 ldbv = ldb;
+  double tol = sqrt((double)w) * 0x1p-53;
+  const double* Bv = B;
+  void* args[] = {&wi, &Bv, &ldbv, &Us, &d, &Vs, &status, &bid, &nbv, &ncv, &Xg, &Wg, &red, &flags, &tol, &zero_flag};
+  RUTV_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_block_kernel, dim3(p.P), dim3(JT), args, p.smem, L.stream));
   L.count();
   jacobi_complete_kernel<<<1, 256, 0, L.stream>>>((int)w, Vs, d, zero_flag, ctmp);
   L.count();
