@@ -21,18 +21,32 @@
 //   * Skinny outputs with long K (A_t^T G, W^T X: K up to 262144) use split-K;
 //     partial tiles go to a workspace and a second kernel sums them in a fixed
 //     order, so results are bitwise deterministic run to run.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace rutv {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
-constexpr int PAD = 4;
-constexpr int A_ELEMS = (BK * (BM + PAD) > BM * (BK + PAD)) ? BK * (BM + PAD) : BM * (BK + PAD);
-constexpr int B_ELEMS = (BK * (BN + PAD) > BN * (BK + PAD)) ? BK * (BN + PAD) : BN * (BK + PAD);
-constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
+constexpr int BK = 16, THREADS = 256, PAD = 4;
+
+// Tile configurations (8 warps each):
+//   Cfg<128,128,2,4,1>: warp tile 64x32, 64 accumulators/thread, 4 stages, 1 CTA/SM
+//   Cfg<128, 64,4,3,2>: warp tile 32x32, 32 accumulators/thread, 3 stages, 2 CTAs/SM --
+//                       one CTA's epilogue (C read-modify-write) overlaps the other's
+//                       DMMA main loop; used for the short-K rank-b updates.
+template <int BM_, int BN_, int WM_, int STAGES_, int MINB_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = 8 / WM_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int MI = BM / (WM * 8), NI = BN / (WN * 8);
+  static constexpr int A_ELEMS = (BK * (BM + PAD) > BM * (BK + PAD)) ? BK * (BM + PAD) : BM * (BK + PAD);
+  static constexpr int B_ELEMS = (BK * (BN + PAD) > BN * (BK + PAD)) ? BK * (BN + PAD) : BN * (BK + PAD);
+  static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
+};
+using CfgBig = Cfg<128, 128, 2, 4, 1>;
+using CfgHalf = Cfg<128, 64, 4, 3, 2>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -78,15 +92,17 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
   }
 }
 
-template <bool TA, bool TB, int VA, int VB>
-__global__ void __launch_bounds__(THREADS, 1)
+template <class CF, bool TA, bool TB, int VA, int VB>
+__global__ void __launch_bounds__(THREADS, CF::MINB)
     dgemm_kernel(i64 M, i64 N, i64 K, double alpha, const double* __restrict__ A, i64 lda,
                  const double* __restrict__ B, i64 ldb, double beta, double* __restrict__ C, i64 ldc,
                  i64 kchunk, double* __restrict__ part) {
+  constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, MI = CF::MI, NI = CF::NI;
+  constexpr int A_ELEMS = CF::A_ELEMS, STAGE_ELEMS = CF::STAGE_ELEMS;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp % CF::WM, wn = warp / CF::WM;
   const i64 m0 = (i64)blockIdx.x * BM, n0 = (i64)blockIdx.y * BN;
   const i64 kb = (i64)blockIdx.z * kchunk;
   const i64 ke = (kb + kchunk < K) ? kb + kchunk : K;
@@ -102,11 +118,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     else load_tile<BN, BK, VB>(Bs, B, ldb, n0, k0, N, ke, tid);                 // rows: k, contiguous n
   };
 
-  double acc[8][4][2];
+  double acc[MI][NI][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -127,35 +143,35 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       const int k = kk * 4 + t;
-      double a[8], b[4];
+      double a[MI], b[NI];
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi) {
-        const int row = wm * 64 + mi * 8 + g;
+      for (int mi = 0; mi < MI; ++mi) {
+        const int row = wm * (MI * 8) + mi * 8 + g;
         a[mi] = TA ? As[row * (BK + PAD) + k] : As[k * (BM + PAD) + row];
       }
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) {
-        const int col = wn * 32 + ni * 8 + g;
+      for (int ni = 0; ni < NI; ++ni) {
+        const int col = wn * (NI * 8) + ni * 8 + g;
         b[ni] = TB ? Bs[k * (BN + PAD) + col] : Bs[col * (BK + PAD) + k];
       }
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni], a[mi], b[ni]);
+        for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni], a[mi], b[ni]);
     }
   }
   cp_async_wait<0>();
 
   // epilogue: lane holds C[row g][cols 2t, 2t+1] of each 8x8 tile
 #pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-    const i64 row = m0 + wm * 64 + mi * 8 + g;
+  for (int mi = 0; mi < MI; ++mi) {
+    const i64 row = m0 + wm * (MI * 8) + mi * 8 + g;
     if (row >= M) continue;
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
+    for (int ni = 0; ni < NI; ++ni) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const i64 col = n0 + wn * 32 + ni * 8 + 2 * t + e;
+        const i64 col = n0 + wn * (NI * 8) + ni * 8 + 2 * t + e;
         if (col >= N) continue;
         if (part) {
           part[(i64)blockIdx.z * M * N + row + col * M] = acc[mi][ni][e];
@@ -182,29 +198,58 @@ __global__ void splitk_reduce_kernel(i64 M, i64 N, int splits, double alpha, con
   }
 }
 
-template <bool TA, bool TB, int VA, int VB>
+template <class CF, bool TA, bool TB, int VA, int VB>
 int launch_t(const Launch& L, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
              i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
   static bool attr_set = false;  // per instantiation; first call from any ctx
   if (!attr_set) {
-    RUTV_CUDA(cudaFuncSetAttribute(dgemm_kernel<TA, TB, VA, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)SMEM_BYTES));
+    RUTV_CUDA(cudaFuncSetAttribute(dgemm_kernel<CF, TA, TB, VA, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)CF::SMEM_BYTES));
     attr_set = true;
   }
-  dgemm_kernel<TA, TB, VA, VB><<<grid, THREADS, SMEM_BYTES, L.stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C,
-                                                                       ldc, kchunk, part);
+  dgemm_kernel<CF, TA, TB, VA, VB><<<grid, THREADS, CF::SMEM_BYTES, L.stream>>>(M, N, K, alpha, A, lda, B, ldb,
+                                                                               beta, C, ldc, kchunk, part);
   L.count();
   RUTV_CHECK_LAUNCH("dgemm_kernel");
   return 0;
 }
 
-template <bool TA, bool TB>
+template <class CF, bool TA, bool TB>
 int launch_v(const Launch& L, int va, int vb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
              const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
-  if (va == 2 && vb == 2) return launch_t<TA, TB, 2, 2>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  if (va == 2) return launch_t<TA, TB, 2, 1>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  if (vb == 2) return launch_t<TA, TB, 1, 2>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  return launch_t<TA, TB, 1, 1>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (va == 2 && vb == 2)
+    return launch_t<CF, TA, TB, 2, 2>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (va == 2) return launch_t<CF, TA, TB, 2, 1>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (vb == 2) return launch_t<CF, TA, TB, 1, 2>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  return launch_t<CF, TA, TB, 1, 1>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+}
+
+template <class CF>
+int launch_cfg(const Launch& L, bool ta, bool tb, int va, int vb, i64 M, i64 N, i64 K, double alpha,
+               const double* A, i64 lda, const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid,
+               i64 kchunk, double* part) {
+  if (!ta && !tb) return launch_v<CF, false, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (ta && !tb) return launch_v<CF, true, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (!ta && tb) return launch_v<CF, false, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  return launch_v<CF, true, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+}
+
+// Tile choice: the 128 x 64 two-CTAs-per-SM tile wins on every randUTV shape
+// measured on B200 (tools/bench_kernels.py, profiles/gemm_cfg_r01.txt): rank-b
+// updates 17.4 -> 24.2 TFLOP/s (one CTA's C read-modify-write overlaps the other
+// CTA's main loop), skinny tall-K products 26.3 -> 30.7, square 30.2 -> 32.0.
+// RUTV_GEMM_CFG=0 forces the 128 x 128 one-CTA tile (tuning only).
+int choose_cfg(i64 M, i64 N, i64 K) {
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = getenv("RUTV_GEMM_CFG");
+    forced = e ? atoi(e) : -1;
+  }
+  if (forced == 0 || forced == 1) return forced;
+  (void)M;
+  (void)N;
+  (void)K;
+  return 1;
 }
 
 inline int vec_of(const double* p, i64 ld) {
@@ -216,11 +261,13 @@ inline int vec_of(const double* p, i64 ld) {
 int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                  const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
   if (M <= 0 || N <= 0) return 0;
+  const int cfg = choose_cfg(M, N, K);
+  const i64 BM = 128, BN = cfg == 1 ? 64 : 128;
   const i64 gm = (M + BM - 1) / BM, gn = (N + BN - 1) / BN;
   if (gn > 65535) return -5;
   const i64 tiles = gm * gn;
   i64 splits = 1;
-  const i64 target = 2 * (i64)L.device_sms;
+  const i64 target = (cfg == 1 ? 4 : 2) * (i64)L.device_sms;
   if (ws && K > 0 && tiles < target) {
     splits = (target + tiles - 1) / tiles;
     const i64 maxk = K / (8 * BK);  // at least 128 of K per split
@@ -240,11 +287,9 @@ int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double 
   const size_t pe = L.pbegin();
   dim3 grid((unsigned)gm, (unsigned)gn, (unsigned)splits);
   double* part = splits > 1 ? ws : nullptr;
-  int st;
-  if (!ta && !tb) st = launch_v<false, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  else if (ta && !tb) st = launch_v<true, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  else if (!ta && tb) st = launch_v<false, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  else st = launch_v<true, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  const int st = cfg == 1
+                     ? launch_cfg<CfgHalf>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part)
+                     : launch_cfg<CfgBig>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
   if (st) return st;
   if (splits > 1) {
     const i64 total = M * N;

@@ -56,6 +56,12 @@ JacobiPlan plan_for(i64 w) {
   return p;
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -148,11 +154,22 @@ __global__ void __launch_bounds__(JT)
     int rotated = 0;
     for (int r = 0; r < nblk - 1; ++r) {
       const int I = rr(cta, r, nblk), J = rr(nblk - 1 - cta, r, nblk);
-      // stage blocks I and J of X and W
-      for (int cl = 0; cl < 2 * nb; ++cl) {
-        const int col = (cl < nb ? I * nb + cl : J * nb + cl - nb);
-        for (int e = tid; e < w; e += JT) Xs[(size_t)cl * w + e] = Xg[e + (i64)col * w];
-        for (int e = tid; e < nc; e += JT) Ws[(size_t)cl * nc + e] = Wg[e + (i64)col * nc];
+      // stage blocks I and J of X and W: cp.async, every element in flight at once
+      {
+        const double* xI = Xg + (i64)I * nb * w;
+        const double* xJ = Xg + (i64)J * nb * w;
+        const double* wI = Wg + (i64)I * nb * nc;
+        const double* wJ = Wg + (i64)J * nb * nc;
+        const int nx = nb * w, nw = nb * nc;
+        for (int e = tid; e < nx; e += JT) {
+          cp_async8(Xs + e, xI + e);
+          cp_async8(Xs + nx + e, xJ + e);
+        }
+        for (int e = tid; e < nw; e += JT) {
+          cp_async8(Ws + e, wI + e);
+          cp_async8(Ws + nw + e, wJ + e);
+        }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
       }
       __syncthreads();
       if (r == 0) {
@@ -176,10 +193,20 @@ __global__ void __launch_bounds__(JT)
         }
         __syncthreads();
       }
-      for (int cl = 0; cl < 2 * nb; ++cl) {
-        const int col = (cl < nb ? I * nb + cl : J * nb + cl - nb);
-        for (int e = tid; e < w; e += JT) Xg[e + (i64)col * w] = Xs[(size_t)cl * w + e];
-        for (int e = tid; e < nc; e += JT) Wg[e + (i64)col * nc] = Ws[(size_t)cl * nc + e];
+      {
+        double* xI = Xg + (i64)I * nb * w;
+        double* xJ = Xg + (i64)J * nb * w;
+        double* wI = Wg + (i64)I * nb * nc;
+        double* wJ = Wg + (i64)J * nb * nc;
+        const int nx = nb * w, nw = nb * nc;
+        for (int e = tid; e < nx; e += JT) {
+          xI[e] = Xs[e];
+          xJ[e] = Xs[nx + e];
+        }
+        for (int e = tid; e < nw; e += JT) {
+          wI[e] = Ws[e];
+          wJ[e] = Ws[nw + e];
+        }
       }
       grid.sync();
     }
@@ -196,11 +223,12 @@ __global__ void __launch_bounds__(JT)
 
   // ---- column norms (thread per column, sequential over rows), d, stable descending sort
   double* dn = red + 2 * P;  // [nc]
-  for (int col = cta * JT + tid; col < nc; col += P * JT) {
+  for (int col = cta * nwarps + warp; col < nc; col += P * nwarps) {  // warp per column
     const double* xc = Xg + (i64)col * w;
     double s2 = 0.0;
-    for (int e = 0; e < w; ++e) s2 = fma(xc[e], xc[e], s2);
-    dn[col] = (s2 <= nu2) ? 0.0 : sqrt(s2);
+    for (int e = lane; e < w; e += 32) s2 = fma(xc[e], xc[e], s2);
+    s2 = warp_sum(s2);
+    if (lane == 0) dn[col] = (s2 <= nu2) ? 0.0 : sqrt(s2);
   }
   grid.sync();
   int anyzero = 0;

@@ -51,10 +51,31 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Cross-CTA reduction of the PSTRIDE partial sums of column j: every CTA
+// reads all G records (coalesced, all loads in flight), then warp w sums values
+// e = w, w+8, ... with lanes over CTAs + xor butterfly -- the same fixed order
+// in every CTA, so every CTA obtains bitwise identical totals.
+__device__ __forceinline__ void reduce_partials(const double* __restrict__ pj, int G, double* stage, double* tot,
+                                                int tid, int lane, int warp) {
+  for (int e = tid; e < G * PSTRIDE; e += LEAF_THREADS) stage[e] = pj[e];
+  __syncthreads();
+  for (int e = warp; e < PSTRIDE; e += LEAF_THREADS / 32) {
+    double s = 0.0;
+    for (int c = lane; c < G; c += 32) s += stage[c * PSTRIDE + e];
+    s = warp_sum(s);
+    if (lane == 0) tot[e] = s;
+  }
+  __syncthreads();
+}
+
 // P points at the panel's top-left element (row 0, col 0); the leaf is columns
 // [c0, c0+nb), rows [c0, h).  Rows [c0, c0+nb) form the replicated top block;
-// rows [c0+nb, h) are split into contiguous slabs, one per CTA.
-__global__ void __launch_bounds__(LEAF_THREADS)
+// rows [c0+nb, h) are split into contiguous slabs, one per CTA.  R > 0: each
+// thread keeps its R slab rows of the 32 leaf columns in registers for the whole
+// leaf (one read and one write of the slab); R == 0: rows stay in global memory
+// (L2) -- for panels taller than 128 x 256 x 2 rows.
+template <int R>
+__global__ void __launch_bounds__(LEAF_THREADS, 1)
     qr_leaf_kernel(double* __restrict__ P, i64 h, i64 ldp, i64 c0, int nb, double* __restrict__ tau,
                    double* __restrict__ partials) {
   cg::grid_group grid = cg::this_grid();
@@ -63,6 +84,7 @@ __global__ void __launch_bounds__(LEAF_THREADS)
   __shared__ double tot[PSTRIDE];
   __shared__ double wv[NB];
   __shared__ double sc[4];  // tau, scal, beta, flag
+  __shared__ double stage[LEAF_MAX_CTAS * PSTRIDE];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, cta = blockIdx.x;
@@ -73,57 +95,79 @@ __global__ void __launch_bounds__(LEAF_THREADS)
   i64 re = rb + per;
   if (re > nb + slab_rows) re = nb + slab_rows;
 
+  double v[R > 0 ? R : 1][NB];
+  if constexpr (R > 0) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const i64 r = rb + tid + (i64)k * LEAF_THREADS;
+#pragma unroll
+      for (int l = 0; l < NB; ++l) v[k][l] = (r < re && l < nb) ? L0[r + (i64)l * ldp] : 0.0;
+    }
+  }
   for (int e = tid; e < NB * NB; e += LEAF_THREADS) {
     const int r = e % NB, c = e / NB;
     TB[r][c] = (r < nb && c < nb) ? L0[r + (i64)c * ldp] : 0.0;
   }
   __syncthreads();
 
-  for (int j = 0; j < nb; ++j) {
+#pragma unroll 1
+  for (int jj = 0; jj < NB; jj += 1) {
+    if (jj >= nb) break;
     // ---------------- phase A: partial sums over this CTA's rows
     double acc[PSTRIDE];
 #pragma unroll
     for (int l = 0; l < PSTRIDE; ++l) acc[l] = 0.0;
-    const double* xcol = L0 + (i64)j * ldp;
-    for (i64 r = rb + tid; r < re; r += LEAF_THREADS) {
-      const double x = xcol[r];
-      acc[0] += x * x;
+    if constexpr (R > 0) {
+      // j must be a compile-time index into v: dispatch through a switch-free unrolled scan
 #pragma unroll
-      for (int l = 0; l < NB; ++l)
-        if (l > j && l < nb) acc[1 + l] += x * L0[r + (i64)l * ldp];
-    }
-    if (cta == 0) {  // the top-block rows below the diagonal count once (CTA 0)
-      for (int r = j + 1 + tid; r < nb; r += LEAF_THREADS) {
-        const double x = TB[r][j];
-        acc[0] += x * x;
+      for (int j = 0; j < NB; ++j) {
+        if (j == jj) {
+#pragma unroll
+          for (int k = 0; k < R; ++k) {
+            const double x = v[k][j];
+            acc[0] = fma(x, x, acc[0]);
+#pragma unroll
+            for (int l = j + 1; l < NB; ++l) acc[1 + l] = fma(x, v[k][l], acc[1 + l]);
+          }
+        }
+      }
+    } else {
+      const double* xcol = L0 + (i64)jj * ldp;
+      for (i64 r = rb + tid; r < re; r += LEAF_THREADS) {
+        const double x = xcol[r];
+        acc[0] = fma(x, x, acc[0]);
 #pragma unroll
         for (int l = 0; l < NB; ++l)
-          if (l > j && l < nb) acc[1 + l] += x * TB[r][l];
+          if (l > jj && l < nb) acc[1 + l] = fma(x, L0[r + (i64)l * ldp], acc[1 + l]);
+      }
+    }
+    if (cta == 0) {  // the top-block rows below the diagonal count once (CTA 0)
+      for (int r = jj + 1 + tid; r < nb; r += LEAF_THREADS) {
+        const double x = TB[r][jj];
+        acc[0] = fma(x, x, acc[0]);
+#pragma unroll
+        for (int l = 0; l < NB; ++l)
+          if (l > jj && l < nb) acc[1 + l] = fma(x, TB[r][l], acc[1 + l]);
       }
     }
 #pragma unroll
     for (int l = 0; l < PSTRIDE; ++l) {
-      const double s = warp_sum(acc[l]);
-      if (lane == 0) wred[warp][l] = s;
+      const double s2 = warp_sum(acc[l]);
+      if (lane == 0) wred[warp][l] = s2;
     }
     __syncthreads();
-    double* pj = partials + (size_t)(j & 1) * G * PSTRIDE;
+    double* pj = partials + (size_t)(jj & 1) * G * PSTRIDE;
     if (tid < PSTRIDE) {
-      double s = 0.0;
+      double s2 = 0.0;
 #pragma unroll
-      for (int w = 0; w < LEAF_THREADS / 32; ++w) s += wred[w][tid];
-      pj[(size_t)cta * PSTRIDE + tid] = s;
+      for (int w = 0; w < LEAF_THREADS / 32; ++w) s2 += wred[w][tid];
+      pj[(size_t)cta * PSTRIDE + tid] = s2;
     }
     grid.sync();
-    // ---------------- phase B: every CTA reduces the partials in CTA order
-    if (tid < PSTRIDE) {
-      double s = 0.0;
-      for (int c = 0; c < G; ++c) s += pj[(size_t)c * PSTRIDE + tid];
-      tot[tid] = s;
-    }
-    __syncthreads();
+    // ---------------- phase B: every CTA reduces the partials in the same order
+    reduce_partials(pj, G, stage, tot, tid, lane, warp);
     if (tid == 0) {
-      const double alpha = TB[j][j];
+      const double alpha = TB[jj][jj];
       const double xi = sqrt(tot[0]);
       if (xi == 0.0) {
         sc[0] = 0.0;
@@ -141,34 +185,60 @@ __global__ void __launch_bounds__(LEAF_THREADS)
     __syncthreads();
     const double t = sc[0], scal = sc[1];
     const bool active = sc[3] != 0.0;
-    if (tid < NB) wv[tid] = (active && tid > j && tid < nb) ? TB[j][tid] + scal * tot[1 + tid] : 0.0;
+    if (tid < NB) wv[tid] = (active && tid > jj && tid < nb) ? TB[jj][tid] + scal * tot[1 + tid] : 0.0;
     __syncthreads();
     if (active) {
-      // own slab rows
-      double* xw = L0 + (i64)j * ldp;
-      for (i64 r = rb + tid; r < re; r += LEAF_THREADS) {
-        const double v = xw[r] * scal;
-        xw[r] = v;
-        const double tv = t * v;
+      if constexpr (R > 0) {
 #pragma unroll
-        for (int l = 0; l < NB; ++l)
-          if (l > j && l < nb) L0[r + (i64)l * ldp] -= tv * wv[l];
+        for (int j = 0; j < NB; ++j) {
+          if (j == jj) {
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              const double vv = v[k][j] * scal;
+              v[k][j] = vv;
+              const double tv = t * vv;
+#pragma unroll
+              for (int l = j + 1; l < NB; ++l) v[k][l] = fma(-tv, wv[l], v[k][l]);
+            }
+          }
+        }
+      } else {
+        double* xw = L0 + (i64)jj * ldp;
+        for (i64 r = rb + tid; r < re; r += LEAF_THREADS) {
+          const double vv = xw[r] * scal;
+          xw[r] = vv;
+          const double tv = t * vv;
+#pragma unroll
+          for (int l = 0; l < NB; ++l)
+            if (l > jj && l < nb) L0[r + (i64)l * ldp] = fma(-tv, wv[l], L0[r + (i64)l * ldp]);
+        }
       }
       // replicated top block: rows > j, then the pivot row j
-      for (int r = j + 1 + tid; r < nb; r += LEAF_THREADS) {
-        const double v = TB[r][j] * scal;
-        TB[r][j] = v;
-        const double tv = t * v;
-        for (int l = j + 1; l < nb; ++l) TB[r][l] -= tv * wv[l];
+      for (int r = jj + 1 + tid; r < nb; r += LEAF_THREADS) {
+        const double vv = TB[r][jj] * scal;
+        TB[r][jj] = vv;
+        const double tv = t * vv;
+        for (int l = jj + 1; l < nb; ++l) TB[r][l] = fma(-tv, wv[l], TB[r][l]);
       }
-      if (tid > j && tid < nb) TB[j][tid] -= t * wv[tid];
+      if (tid > jj && tid < nb) TB[jj][tid] -= t * wv[tid];
     }
     __syncthreads();
     if (tid == 0) {
-      TB[j][j] = sc[2];
-      if (cta == 0) tau[c0 + j] = t;
+      TB[jj][jj] = sc[2];
+      if (cta == 0) tau[c0 + jj] = t;
     }
     __syncthreads();
+  }
+  if constexpr (R > 0) {
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const i64 r = rb + tid + (i64)k * LEAF_THREADS;
+      if (r < re) {
+#pragma unroll
+        for (int l = 0; l < NB; ++l)
+          if (l < nb) L0[r + (i64)l * ldp] = v[k][l];
+      }
+    }
   }
   if (cta == 0) {
     for (int e = tid; e < nb * nb; e += LEAF_THREADS) {
@@ -223,11 +293,25 @@ __global__ void larft_leaf_kernel(const double* __restrict__ S, i64 lds, const d
   }
 }
 
-int leaf_ctas(i64 slab_rows) {
-  i64 g = (slab_rows + LEAF_THREADS - 1) / LEAF_THREADS;
+// Leaf grid: R rows per thread in registers when the slab fits (R = 1, 2),
+// otherwise rows in L2 (R = 0).  G depends on the panel height only, so the
+// factorisation is bitwise reproducible.
+void leaf_plan(i64 slab_rows, int* G, int* R) {
+  const i64 cap1 = (i64)LEAF_MAX_CTAS * LEAF_THREADS;
+  i64 g;
+  if (slab_rows <= cap1) {
+    *R = 1;
+    g = (slab_rows + LEAF_THREADS - 1) / LEAF_THREADS;
+  } else if (slab_rows <= 2 * cap1) {
+    *R = 2;
+    g = (slab_rows + 2 * LEAF_THREADS - 1) / (2 * LEAF_THREADS);
+  } else {
+    *R = 0;
+    g = LEAF_MAX_CTAS;
+  }
   if (g < 1) g = 1;
   if (g > LEAF_MAX_CTAS) g = LEAF_MAX_CTAS;
-  return (int)g;
+  *G = (int)g;
 }
 
 }  // namespace
@@ -246,7 +330,8 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
     const int wl = (int)((w - c0) < NB ? (w - c0) : NB);
     // ---- leaf factorisation (cooperative grid)
     {
-      const int G = leaf_ctas(h - c0 - wl);
+      int G = 1, R = 1;
+      leaf_plan(h - c0 - wl, &G, &R);
       double* Pp = P;
       i64 hh = h, ld = ldp, cc = c0;
       int nbv = wl;
@@ -254,7 +339,8 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
       double* part = qw.partials;
       void* args[] = {&Pp, &hh, &ld, &cc, &nbv, &taup, &part};
       const size_t pe = L.pbegin();
-      RUTV_CUDA(cudaLaunchCooperativeKernel((void*)qr_leaf_kernel, dim3(G), dim3(LEAF_THREADS), args, 0, L.stream));
+      void* fn = R == 1 ? (void*)qr_leaf_kernel<1> : (R == 2 ? (void*)qr_leaf_kernel<2> : (void*)qr_leaf_kernel<0>);
+      RUTV_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(LEAF_THREADS), args, 0, L.stream));
       L.count();
       // algorithmic: ~4 (h-c0) wl^2 flops (dlarfg + dlarf over the leaf); bytes: the leaf read + written once
       L.pend(PK_QR_LEAF, 4.0 * (double)(h - c0) * wl * wl, 16.0 * (double)(h - c0) * wl, pe);
