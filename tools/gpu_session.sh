@@ -15,15 +15,17 @@ for stage in "$@"; do
     bench_c2)
       timeout 900 python bench.py --config c2 --no-cpu-baseline > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo "bench c2 rc=$?"; cat gpurun_out/bench_c2.json ;;
     ncu_launches)
-      CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-profile"
+      # first 3000 launches of one c3 step (ncu costs ~40 ms per launch; a step has ~13.7k)
+      CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-profile"
       timeout 900 $CMD > gpurun_out/plain.log 2>&1 && \
-      timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD \
+      timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv $CMD \
         > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"; tail -3 gpurun_out/ncu_launches.log ;;
     ncu_full)
-      CMD="python bench.py --config c2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-profile"
-      timeout 900 $CMD > gpurun_out/plain_c2.log 2>&1 && \
+      # the dominant kernel: the S5 rank-b update X -= Z2 W^T (dgemm NT) of c3, iteration >= 1
+      CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-profile"
+      timeout 900 $CMD > gpurun_out/plain_full.log 2>&1 && \
       timeout 1500 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
-        -k regex:dgemm_kernelILb0ELb1E -s 6 -c 2 -o gpurun_out/prof_dgemm_nt $CMD \
+        -k regex:dgemm_kernel.*Lb0ELb1E -s 2 -c 1 -o gpurun_out/prof_dgemm_nt $CMD \
         > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"; tail -3 gpurun_out/ncu_full.log ;;
   esac
 done
