@@ -15,10 +15,11 @@ for stage in "$@"; do
     bench_c2)
       timeout 900 python bench.py --config c2 --no-cpu-baseline > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo "bench c2 rc=$?"; cat gpurun_out/bench_c2.json ;;
     ncu_launches)
-      # first 3000 launches of one c3 step (ncu costs ~40 ms per launch; a step has ~13.7k)
+      # every librandutv launch of one c3 step (ncu costs ~40 ms per launch; a step has ~13.7k)
       CMD="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-profile"
       timeout 900 $CMD > gpurun_out/plain.log 2>&1 && \
-      timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv $CMD \
+      timeout 2400 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base mangled -k regex:4rutv \
+        --csv --log-file gpurun_out/launches.csv $CMD \
         > gpurun_out/ncu_launches.log 2>&1; echo "ncu launches rc=$?"; tail -3 gpurun_out/ncu_launches.log ;;
     ncu_full)
       # the dominant kernel: the S5 rank-b update X -= Z2 W^T (dgemm NT) of c3, iteration >= 1
