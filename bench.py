@@ -10,9 +10,9 @@ Default workload: c3 (n = 16384, b = 256, q = 2, exponential spectrum), the
 largest config quoted at 1/2/4/8 GPUs that a single step of finishes in
 seconds (DESIGN.md §Measurement explains the choice; c2 and c5 run with
 --config).  value = F_model / t (GFLOP/s, F from paper_2002_06960_b200.flops),
-whole job over all ranks.  Multi-GPU: N independent replicas ("scaling":
-"weak", no data-path collective; the column-sharded NCCL path is a later round,
-DESIGN.md §Multi-GPU).
+whole job over all ranks.  Multi-GPU (N > 1, torchrun): ONE factorisation of
+the same matrix sharded over the N GPUs (1-D block-cyclic column blocks, NCCL
+AllReduce / AllGather / Broadcast) -- "scaling": "strong".
 
 --impl reference times the CPU oracle (oracle/, numpy) on the host cores on a
 bounded sample of the same workload (the first sampled step of the config) --
@@ -167,7 +167,7 @@ def run_reference(args):
     val = cs["flops"] / t / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config} sample: first sampled step", "m": cfg["m"], "n": cfg["n"],
                        "b": cfg["b"], "q": cfg["q"]},
             "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cs["cores"], "kind": "oracle",
@@ -201,14 +201,33 @@ def run_ours(args):
     F = randutv_flops(m, n, b, q, build_uv=True)
 
     A = make_config_torch(args.config, device=f"cuda:{dev}")
-    T = colmajor(m, n)
-    U = colmajor(m, m)
-    V = colmajor(n, n)
     stream = torch.cuda.Stream()
     ctx = Context(dev, stream)
+    if ws > 1:
+        # column-sharded path: block-cyclic columns of A, row
+        # ranges of U and V; NCCL communicator bootstrapped over torch.distributed
+        from paper_2002_06960_b200.randutv import dist_layout, local_columns
+        ctx.comm_init_torch()
+        lay = dist_layout(m, n, b, ws, rank)
+        cols = torch.from_numpy(local_columns(n, b, ws, rank)).to(A.device)
+        A_loc = colmajor(m, lay["ncols"])
+        A_loc.copy_(A.index_select(1, cols))
+        del A
+        torch.cuda.empty_cache()
+        T_loc = colmajor(m, lay["ncols"])
+        U_loc = colmajor(lay["u1"] - lay["u0"], m)
+        V_loc = colmajor(lay["v1"] - lay["v0"], n)
 
-    def step():
-        ctx.randutv_factor_ex(A, b, q, seed, U=U, T=T, V=V)
+        def step():
+            T_loc.copy_(A_loc)
+            ctx.randutv_factor_dist(T_loc, m, n, b, q, seed, U_local=U_loc, V_local=V_loc)
+    else:
+        T = colmajor(m, n)
+        U = colmajor(m, m)
+        V = colmajor(n, n)
+
+        def step():
+            ctx.randutv_factor_ex(A, b, q, seed, U=U, T=T, V=V)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -246,11 +265,48 @@ def run_ours(args):
     prof = ctx.profile() if not args.no_profile else None
     ctx.set_profiling(False)
     ms_step = ms / args.steps
-    value = F * ws * args.steps / (ms * 1e-3) / 1e9
+    value = F * args.steps / (ms * 1e-3) / 1e9   # one factorisation per step, whole job
 
     # ---- e2e: the literal C-ABI entry on pinned host buffers, copies inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and ws > 1:
+        # the sharded entry from pinned host memory: H2D of the rank's columns, the
+        # collective factorisation, D2H of its T columns and U / V rows
+        Ah = torch.empty((lay["ncols"], m), dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A_loc.t())
+        Th = torch.empty_like(Ah)
+        Uh = torch.empty((m, lay["u1"] - lay["u0"]), dtype=torch.float64, pin_memory=True)
+        Vh = torch.empty((n, lay["v1"] - lay["v0"]), dtype=torch.float64, pin_memory=True)
+
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                T_loc.copy_(Ah.t(), non_blocking=True)
+                ctx.randutv_factor_dist(T_loc, m, n, b, q, seed, U_local=U_loc, V_local=V_loc)
+                Th.copy_(T_loc.t(), non_blocking=True)
+                Uh.copy_(U_loc.t(), non_blocking=True)
+                Vh.copy_(V_loc.t(), non_blocking=True)
+            stream.synchronize()
+
+        e2e_step()
+        e2e_steps = min(args.steps, 2)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        dt = float(tt.item())
+        bi = torch.tensor([8 * m * lay["ncols"]], device="cuda", dtype=torch.float64)
+        bo = torch.tensor([8 * (m * lay["ncols"] + m * (lay["u1"] - lay["u0"]) + n * (lay["v1"] - lay["v0"]))],
+                          device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(bi)
+        torch.distributed.all_reduce(bo)
+        e2e = {"value": F * e2e_steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(bi.item()),
+               "d2h_bytes_per_step": int(bo.item()), "steps": e2e_steps, "ms_per_step": dt / e2e_steps * 1e3,
+               "api": "randutv_factor_dist (pinned host shards)"}
+    elif not args.no_e2e:
+        # the literal C-ABI entry on pinned host buffers, copies inside the timed region
         Ah = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         Ah.copy_(A.t())
         Uh = torch.empty((m, m), dtype=torch.float64, pin_memory=True)
@@ -261,18 +317,13 @@ def run_ours(args):
         torch.cuda.empty_cache()
         randutv_factor(m, n, An, m, b, q, seed, Un, Tn, Vn)      # warm-up (allocates staging)
         e2e_steps = min(args.steps, 2)
-        barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             randutv_factor(m, n, An, m, b, q, seed, Un, Tn, Vn)
         dt = time.perf_counter() - t0
-        if ws > 1:
-            tt = torch.tensor([dt], device="cuda", dtype=torch.float64)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            dt = float(tt.item())
-        e2e = {"value": F * ws * e2e_steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * m * n,
+        e2e = {"value": F * e2e_steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": 8 * m * n,
                "d2h_bytes_per_step": 8 * (m * m + m * n + n * n), "steps": e2e_steps,
-               "ms_per_step": dt / e2e_steps * 1e3}
+               "ms_per_step": dt / e2e_steps * 1e3, "api": "randutv_factor (literal entry, pinned host pointers)"}
 
     # ---- CPU baseline: the oracle on a bounded sample, rank 0, N = 1 only
     cpu = None
@@ -306,16 +357,16 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: " + {
                 "c1": "n=512 known spectrum", "c2": "n=4096 Gaussian", "c3": "n=16384 exp spectrum",
                 "c5": "n=65536 Gaussian"}[args.config] + f", b={b}, q={q}, full randUTV with U and V",
                 "m": m, "n": n, "b": b, "q": q, "flops_per_step": F,
-                "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                "parallelism": f"column-sharded x{ws} (1-D block-cyclic, NCCL)" if ws > 1 else "single",
                 "l2": "inputs larger than L2 (A is %.2f GB, L2 126 MB); no flush" % (8 * m * n / 1e9)
                 if 8 * m * n > 126e6 else "input fits L2: not flushed"},
             "t_over_n3_x1e10": ms_step * 1e-3 / float(n) ** 3 * 1e10,
-            "frac_of_fp64_peak": round(value / ws / 1e3 / peak, 4),
+            "frac_of_fp64_peak": round(value / ws / 1e3 / peak, 4),   # of N x per-GPU peak
             "gpu_launches": stats["kernel_launches"],
             "gpu_launches_per_step": stats["kernel_launches"] / args.steps,
             "clocks": clocks.summary(),

@@ -53,6 +53,8 @@ extern "C" {
 #define RANDUTV_ERR_ALLOC     1001  /* device workspace allocation failed                      */
 #define RANDUTV_ERR_NONFINITE 1002  /* A holds a NaN/Inf (only with RANDUTV_CHECK_FINITE)       */
 #define RANDUTV_ERR_CTX       1003  /* NULL or destroyed context                                */
+#define RANDUTV_ERR_NCCL      1004  /* NCCL missing or a collective failed (randutv_last_error)   */
+#define RANDUTV_ERR_NOCOMM    1005  /* randutv_factor_dist before randutv_comm_init              */
 
 /* flags */
 #define RANDUTV_NO_UV         1u    /* do not build U and V ("no orthonormal matrices") */
@@ -176,6 +178,107 @@ RANDUTV_API int randutv_panel_qr(randutv_ctx* ctx, int64_t h, int64_t w, double*
  * 6 d, 7 Vs. */
 RANDUTV_API int randutv_small_svd(randutv_ctx* ctx, int64_t w, const double* B, int64_t ldb,
                                   double* Us, double* d, double* Vs);
+
+
+/* ---------------------------------------------------------------------------
+ * Host-streamed mode: the GPU analogue of the
+ * paper's out-of-core randUTV, whose matrix lives on disk and moves through an
+ * LRU block cache in RAM with a dedicated I/O thread overlapping transfers and
+ * computation (decomposed times in Table 1).  Here
+ * A, U, V live in host memory and stream as column panels (all rows x b)
+ * through a device panel cache of `device_cache_bytes`, with H2D prefetch and
+ * D2H write-back on two copy streams overlapping the DMMA work.
+ * ------------------------------------------------------------------------- */
+
+/* What one host-streamed factorisation moved and how long it took. */
+typedef struct randutv_host_report {
+  int64_t h2d_bytes;     /* host -> device panel bytes                          */
+  int64_t d2h_bytes;     /* device -> host write-back bytes                     */
+  int64_t cache_hits;    /* panel requests served from the device cache         */
+  int64_t cache_misses;  /* panel requests that needed a (re)load               */
+  int64_t cache_slots;   /* panels the cache holds                              */
+  int64_t slot_bytes;    /* bytes per slot (max(m, n) * b * 8, rounded)         */
+  double wall_ms;        /* device time of the whole call (events on the stream) */
+  double h2d_ms;         /* summed duration of the H2D copies (I/O time)        */
+  double d2h_ms;         /* summed duration of the D2H copies                   */
+} randutv_host_report;
+
+/* Full randUTV of the m x n matrix in HOST memory (A_host, lda >= m), which is
+ * overwritten by T (the paper's in-place OOC factorisation); U_host (m x m,
+ * ldu >= m) and V_host (n x n, ldv >= n) in host memory are written unless
+ * RANDUTV_NO_UV.  Host buffers should be pinned (cudaHostAlloc /
+ * torch pin_memory); unpinned ones are registered for the duration of the
+ * call.  device_cache_bytes bounds the panel cache (0 = half the free device
+ * memory; at least 3 panels are always used).  report (host, may be NULL)
+ * receives the traffic and timing.  Results equal randutv_factor_ex's to
+ * rounding (panel sums are accumulated in a different order).
+ * Arguments: 1 ctx, 2 m, 3 n, 4 A_host, 5 lda, 6 b, 7 q, 8 seed, 9 flags,
+ * 10 device_cache_bytes, 11 U_host, 12 ldu, 13 V_host, 14 ldv, 15 report. */
+RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b,
+                                    int q, uint64_t seed, unsigned flags, size_t device_cache_bytes, double* U_host,
+                                    int64_t ldu, double* V_host, int64_t ldv, randutv_host_report* report);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU: the column-sharded randUTV.
+ *
+ * The paper's method is sequential over column blocks (each sample depends on
+ * the whole updated trailing matrix), but every O(r s b) product of
+ * a step splits by columns.  Layout, for P ranks and block size b:
+ *   A (and T): 1-D block-cyclic by column blocks of width b -- global block j
+ *              (columns j*b .. min(n, (j+1)*b)) lives on rank j mod P, local
+ *              blocks in increasing j; local matrix m x n_p (lda >= m);
+ *   U, V     : contiguous row ranges, rows [m*p/P, m*(p+1)/P) of U (m x m) and
+ *              [n*p/P, n*(p+1)/P) of V (n x n); local ld >= the row count.
+ * Exchanges per sampled step: AllReduce of A_t Y (q times, (m-k) x b) and of
+ * T W_V (m x b), AllGather of Y (then the same bitwise-deterministic QR(Y) on
+ * every rank), Broadcast of (W_U, T_U) and of (U_s, V_s) from the owner of
+ * the column block.  Results equal the single-GPU path's up to the summation
+ * order of the AllReduces.
+ * ------------------------------------------------------------------------- */
+
+#define RANDUTV_UNIQUE_ID_BYTES 128
+
+/* Pure host arithmetic (no GPU needed): the layout of rank `rank` of `nranks`.
+ * out[0] = local column count n_p, out[1..2] = [first, end) row of U held,
+ * out[3..4] = [first, end) row of V held.  Arguments: 1 m, 2 n, 3 b, 4 nranks,
+ * 5 rank, 6 out (host, 5 int64). */
+RANDUTV_API int randutv_dist_layout(int64_t m, int64_t n, int64_t b, int nranks, int rank, int64_t* out);
+
+/* Write a fresh NCCL unique id (RANDUTV_UNIQUE_ID_BYTES bytes, host) that the
+ * caller sends to every rank (e.g. torch.distributed.broadcast_object_list).
+ * Returns 0 or RANDUTV_ERR_NCCL. */
+RANDUTV_API int randutv_nccl_unique_id(void* out);
+
+/* Join the NCCL communicator of `nranks` ranks (collective over all ranks; one
+ * process per GPU, the ctx's device).  The ctx owns the communicator and a
+ * second one split from it for the side stream; both are released by
+ * randutv_destroy or a later randutv_comm_init.  Arguments: 1 ctx, 2 unique_id
+ * (host, RANDUTV_UNIQUE_ID_BYTES), 3 nranks, 4 rank. */
+RANDUTV_API int randutv_comm_init(randutv_ctx* ctx, const void* unique_id, int nranks, int rank);
+
+/* Sharded full randUTV: collective over the ranks of the ctx communicator,
+ * every rank passing the same m, n, b, q, seed, flags.  A_local (m x n_p,
+ * device) is overwritten by the rank's columns of T.  U_local (mu x m) and
+ * V_local (nv x n) receive the rank's rows of U and V (ignored with
+ * RANDUTV_NO_UV).  Status: as randutv_factor_ex, identical on every rank (+j
+ * Jacobi non-convergence is agreed by an AllReduce-min); RANDUTV_ERR_NOCOMM
+ * without randutv_comm_init.  Arguments: 1 ctx, 2 m, 3 n, 4 A_local, 5 lda,
+ * 6 b, 7 q, 8 seed, 9 flags, 10 U_local, 11 ldu, 12 V_local, 13 ldv. */
+RANDUTV_API int randutv_factor_dist(randutv_ctx* ctx, int64_t m, int64_t n, double* A_local, int64_t lda,
+                                    int64_t b, int q, uint64_t seed, unsigned flags, double* U_local, int64_t ldu,
+                                    double* V_local, int64_t ldv);
+
+/* The same SPMD driver with `nranks` (<= 16) virtual ranks run as host threads
+ * on ONE device, collectives done by device copies and fixed-order sums
+ * between host barriers (no kernel waits on another rank).  Used to test the
+ * sharded path on a single GPU.  A_locals / U_locals / V_locals: host arrays
+ * of nranks device pointers laid out as for randutv_factor_dist (lda, ldu, ldv
+ * shared by all ranks).  Arguments: 1 device, 2 nranks, 3 m, 4 n, 5 A_locals,
+ * 6 lda, 7 b, 8 q, 9 seed, 10 flags, 11 U_locals, 12 ldu, 13 V_locals, 14 ldv. */
+RANDUTV_API int randutv_factor_dist_loopback(int device, int nranks, int64_t m, int64_t n, double* const* A_locals,
+                                             int64_t lda, int64_t b, int q, uint64_t seed, unsigned flags,
+                                             double* const* U_locals, int64_t ldu, double* const* V_locals,
+                                             int64_t ldv);
 
 #ifdef __cplusplus
 }

@@ -118,6 +118,9 @@ i64 jacobi_scratch_elems(i64 w);
 
 // misc.cu
 int launch_set_identity(const Launch& L, i64 rows, i64 cols, double* X, i64 ldx);
+// X(r, c) := (r - c == shift): a shifted slice of the identity (row block of I
+// for shift < 0, column panel of I for shift > 0)
+int launch_set_identity_shift(const Launch& L, i64 rows, i64 cols, i64 shift, double* X, i64 ldx);
 int launch_copy(const Launch& L, i64 rows, i64 cols, const double* S, i64 lds, double* D, i64 ldd);
 int launch_fill(const Launch& L, i64 rows, i64 cols, double v, double* X, i64 ldx);
 // zero the strictly lower part of the rows x cols block X (X = triu(X))

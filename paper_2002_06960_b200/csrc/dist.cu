@@ -1,0 +1,719 @@
+// Column-sharded multi-GPU randUTV and its C ABI.
+//
+// The paper has no distributed algorithm (its parallelism is shared-memory
+// tasks over disk-resident blocks); the sharding here
+// follows from the structure of one randUTV step (Sec. 3.1): every
+// O(r s b) product of a step splits by columns of the trailing matrix, so
+//
+//   A (and the working T) : 1-D block-cyclic by column blocks of width b,
+//                           global block j on rank j mod P (load balance as the
+//                           trailing matrix shrinks);
+//   U, V                  : contiguous row ranges (every update of U and V is a
+//                           right multiplication, P:1338-1340, P:1352-1354,
+//                           P:1361-1362, hence row-local).
+//
+// Per sampled step i (k = i b, r = m - k, s = n - k, owner o = i mod P), with
+// A_p the rank's trailing columns:
+//   S1  G                   generated redundantly (same Philox counters)
+//   S2  Y_p = A_p^T G        local rows of Y
+//   S3  Z = sum_p A_p Y_p    AllReduce (r x b);  Y_p = A_p^T Z  local
+//   S4  Y = AllGather(Y_p)   then the same deterministic QR(Y) on every rank
+//   S5  X W = sum_p A_p W_p  AllReduce (m x b); A_p -= (X W) T_V W_p^T local;
+//       V rows: local (every rank holds all of W_V)
+//   S6  QR of column block i on its owner; Broadcast (W_U, T_U)
+//   S7  A_p -= W_U T_U^T W_U^T A_p local;  U rows local
+//   S8  Jacobi SVD on the owner; Broadcast (U_s, V_s) on the side communicator
+//   S9  folds: owner T11 = diag d, A01 V_s; every rank U_s^T A12 (its
+//       columns), U(:, blk) U_s, V(:, blk) V_s
+// The S8/S9 overlap of the single-GPU driver is kept: they run on the side
+// stream with their own communicator (split from the main one), in the same
+// program order on every rank.
+//
+// Two communicator back ends implement the same four collectives:
+//   * NCCL (libnccl.so.2, loaded at run time; torch's bundled copy), one
+//     process per GPU, bootstrapped from an ncclUniqueId the caller
+//     distributes (the Python layer uses torch.distributed);
+//   * loopback: P virtual ranks as P host threads in one process on one GPU,
+//     collectives done by device copies/sums between host barriers (no kernel
+//     ever waits on another rank's kernel).  It runs the SAME SPMD driver and
+//     is how the sharded path is parity-tested on a single GPU.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <thread>
+#include <vector>
+
+#include <nccl.h>
+
+#include "driver.cuh"
+
+#ifndef RUTV_NCCL_PATH
+#define RUTV_NCCL_PATH "libnccl.so.2"
+#endif
+
+namespace rutv {
+
+// ============================================================== layout (host)
+
+struct Layout {
+  i64 m, n, b;
+  int P, p;
+  i64 nblocks;
+  i64 width(i64 j) const { return std::min(b, n - j * b); }
+  // local column count of rank q
+  i64 ncols(int q) const {
+    i64 c = 0;
+    for (i64 j = q; j < nblocks; j += P) c += width(j);
+    return c;
+  }
+  // number of rank q's blocks with global index < i
+  i64 lb_before(int q, i64 i) const { return i > q ? (i - q + P - 1) / P : 0; }
+  // local column offset of rank q's first block with global index >= i
+  i64 lcol(int q, i64 i) const { return lb_before(q, i) * b; }
+  i64 trailing_cols(int q, i64 i) const { return ncols(q) - lcol(q, i); }
+  i64 max_trailing(i64 i) const {
+    i64 mx = 0;
+    for (int q = 0; q < P; ++q) mx = std::max(mx, trailing_cols(q, i));
+    return mx;
+  }
+  static i64 row0(i64 rows, int P, int q) { return rows * q / P; }
+};
+
+// ============================================================== communicators
+
+struct Comm {
+  int rank = 0, nranks = 1;
+  virtual ~Comm() {}
+  virtual int allreduce_sum(double* buf, i64 count, cudaStream_t s) = 0;
+  // recv holds nranks * count doubles, rank q's block at q * count
+  virtual int allgather(const double* send, double* recv, i64 count, cudaStream_t s) = 0;
+  virtual int bcast(double* buf, i64 count, int root, cudaStream_t s) = 0;
+  virtual int allreduce_min_int(int* buf, i64 count, cudaStream_t s) = 0;
+};
+
+void comm_free(Comm* c) { delete c; }
+
+// ---------------------------------------------------------------- NCCL
+
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) GetUniqueId;
+  decltype(&ncclCommInitRank) CommInitRank;
+  decltype(&ncclCommSplit) CommSplit;
+  decltype(&ncclCommDestroy) CommDestroy;
+  decltype(&ncclAllReduce) AllReduce;
+  decltype(&ncclAllGather) AllGather;
+  decltype(&ncclBroadcast) Broadcast;
+  decltype(&ncclGetErrorString) GetErrorString;
+};
+
+static std::mutex g_nccl_mu;
+static NcclApi g_nccl;
+
+static char g_nccl_err[256] = "";
+
+const NcclApi* nccl_api() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.ok) return &g_nccl;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen(RUTV_NCCL_PATH, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    snprintf(g_nccl_err, sizeof(g_nccl_err), "dlopen(libnccl.so.2): %s", dlerror());
+    return nullptr;
+  }
+#define RUTV_SYM(field, name)                                              \
+  g_nccl.field = (decltype(g_nccl.field))dlsym(h, name);                   \
+  if (!g_nccl.field) {                                                     \
+    snprintf(g_nccl_err, sizeof(g_nccl_err), "dlsym(%s) failed", name);    \
+    return nullptr;                                                        \
+  }
+  RUTV_SYM(GetUniqueId, "ncclGetUniqueId");
+  RUTV_SYM(CommInitRank, "ncclCommInitRank");
+  RUTV_SYM(CommSplit, "ncclCommSplit");
+  RUTV_SYM(CommDestroy, "ncclCommDestroy");
+  RUTV_SYM(AllReduce, "ncclAllReduce");
+  RUTV_SYM(AllGather, "ncclAllGather");
+  RUTV_SYM(Broadcast, "ncclBroadcast");
+  RUTV_SYM(GetErrorString, "ncclGetErrorString");
+#undef RUTV_SYM
+  g_nccl.ok = true;
+  return &g_nccl;
+}
+
+#define RUTV_NCCL(call)                                                                      \
+  do {                                                                                       \
+    ncclResult_t r__ = (call);                                                               \
+    if (r__ != ncclSuccess) {                                                                \
+      snprintf(g_nccl_err, sizeof(g_nccl_err), "%s: %s", #call, api->GetErrorString(r__));   \
+      ::rutv::set_last_error(g_nccl_err, cudaErrorUnknown);                                  \
+      return RANDUTV_ERR_NCCL;                                                               \
+    }                                                                                        \
+  } while (0)
+
+struct NcclComm : Comm {
+  const NcclApi* api;
+  ncclComm_t comm = nullptr;
+  ~NcclComm() override {
+    if (comm) api->CommDestroy(comm);
+  }
+  int allreduce_sum(double* buf, i64 count, cudaStream_t s) override {
+    if (count <= 0) return 0;
+    RUTV_NCCL(api->AllReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, comm, s));
+    return 0;
+  }
+  int allgather(const double* send, double* recv, i64 count, cudaStream_t s) override {
+    if (count <= 0) return 0;
+    RUTV_NCCL(api->AllGather(send, recv, (size_t)count, ncclFloat64, comm, s));
+    return 0;
+  }
+  int bcast(double* buf, i64 count, int root, cudaStream_t s) override {
+    if (count <= 0) return 0;
+    RUTV_NCCL(api->Broadcast(buf, buf, (size_t)count, ncclFloat64, root, comm, s));
+    return 0;
+  }
+  int allreduce_min_int(int* buf, i64 count, cudaStream_t s) override {
+    if (count <= 0) return 0;
+    RUTV_NCCL(api->AllReduce(buf, buf, (size_t)count, ncclInt32, ncclMin, comm, s));
+    return 0;
+  }
+};
+
+// ---------------------------------------------------------------- loopback
+
+constexpr int kMaxLoopRanks = 16;
+
+struct PtrPack {
+  const double* p[kMaxLoopRanks];
+};
+
+__global__ void sum_ranks_kernel(i64 count, int P, PtrPack src, double* __restrict__ out) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < count; i += (i64)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < P; ++q) s += src.p[q][i];  // fixed rank order: identical on every rank
+    out[i] = s;
+  }
+}
+
+struct LoopShared {
+  int P;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long gen = 0;
+  std::vector<const void*> ptr;
+  explicit LoopShared(int P_) : P(P_), ptr(P_, nullptr) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long g = gen;
+    if (++arrived == P) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+struct LoopComm : Comm {
+  LoopShared* sh;
+  double* tmp = nullptr;  // per-rank reduction target
+  i64 tmp_elems = 0;
+  int sms = 148;
+  ~LoopComm() override {
+    if (tmp) cudaFree(tmp);
+  }
+  int grow(i64 elems) {
+    if (elems <= tmp_elems) return 0;
+    if (tmp) cudaFree(tmp);
+    tmp = nullptr;
+    tmp_elems = 0;
+    RUTV_CUDA(cudaMalloc(&tmp, (size_t)elems * sizeof(double)));
+    tmp_elems = elems;
+    return 0;
+  }
+  // publish `p`, wait until every rank has published and drained its stream
+  int publish(const void* p, cudaStream_t s) {
+    RUTV_CUDA(cudaStreamSynchronize(s));
+    sh->ptr[rank] = p;
+    sh->barrier();
+    return 0;
+  }
+  int allreduce_sum(double* buf, i64 count, cudaStream_t s) override {
+    if (count <= 0) return 0;
+    int st = grow(count);
+    RUTV_TRY(publish(buf, s));
+    if (st == 0) {
+      PtrPack pk{};
+      for (int q = 0; q < nranks; ++q) pk.p[q] = (const double*)sh->ptr[q];
+      i64 blocks = std::min<i64>((count + 255) / 256, (i64)sms * 8);
+      sum_ranks_kernel<<<(unsigned)blocks, 256, 0, s>>>(count, nranks, pk, tmp);
+      if (cudaStreamSynchronize(s) != cudaSuccess) st = RANDUTV_ERR_CUDA;
+    }
+    sh->barrier();  // every rank has read every buffer
+    if (st == 0 && cudaMemcpyAsync(buf, tmp, (size_t)count * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      st = RANDUTV_ERR_CUDA;
+    if (st == 0 && cudaStreamSynchronize(s) != cudaSuccess) st = RANDUTV_ERR_CUDA;
+    sh->barrier();
+    return st;
+  }
+  int allgather(const double* send, double* recv, i64 count, cudaStream_t s) override {
+    if (count <= 0) return 0;
+    RUTV_TRY(publish(send, s));
+    int st = 0;
+    for (int q = 0; q < nranks && st == 0; ++q)
+      if (cudaMemcpyAsync(recv + (i64)q * count, sh->ptr[q], (size_t)count * 8, cudaMemcpyDeviceToDevice, s) !=
+          cudaSuccess)
+        st = RANDUTV_ERR_CUDA;
+    if (st == 0 && cudaStreamSynchronize(s) != cudaSuccess) st = RANDUTV_ERR_CUDA;
+    sh->barrier();
+    return st;
+  }
+  int bcast(double* buf, i64 count, int root, cudaStream_t s) override {
+    if (count <= 0) return 0;
+    RUTV_TRY(publish(buf, s));
+    int st = 0;
+    if (rank != root) {
+      if (cudaMemcpyAsync(buf, sh->ptr[root], (size_t)count * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        st = RANDUTV_ERR_CUDA;
+    }
+    sh->barrier();
+    return st;
+  }
+  int allreduce_min_int(int* buf, i64 count, cudaStream_t s) override {
+    if (count <= 0) return 0;
+    RUTV_TRY(publish(buf, s));
+    std::vector<int> acc((size_t)count, 0x7fffffff), h((size_t)count);
+    int st = 0;
+    for (int q = 0; q < nranks && st == 0; ++q) {
+      if (cudaMemcpy(h.data(), sh->ptr[q], (size_t)count * 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        st = RANDUTV_ERR_CUDA;
+        break;
+      }
+      for (i64 e = 0; e < count; ++e) acc[e] = std::min(acc[e], h[e]);
+    }
+    sh->barrier();
+    if (st == 0 && cudaMemcpy(buf, acc.data(), (size_t)count * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      st = RANDUTV_ERR_CUDA;
+    sh->barrier();
+    return st;
+  }
+};
+
+// ============================================================== layout kernels
+
+// Y(0:s, 0:cols) in global trailing-column order from the all-gathered local
+// chunks (rank q's chunk at Yall + q*stride, ld ldc, rows = q's trailing
+// columns in local order).
+__global__ void cyclic_gather_rows_kernel(i64 s, i64 cols, i64 k, i64 b, int P, i64 i, const double* __restrict__ Yall,
+                                          i64 ldc, i64 stride, double* __restrict__ Y, i64 ldy) {
+  const i64 total = s * cols;
+  for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
+    const i64 t = idx % s, col = idx / s;
+    const i64 c = k + t, j = c / b;
+    const int q = (int)(j % P);
+    const i64 lb0 = i > q ? (i - q + P - 1) / P : 0;
+    const i64 lr = (j / P - lb0) * b + c % b;
+    Y[t + col * ldy] = Yall[q * stride + lr + col * ldc];
+  }
+}
+
+// Wl(0:sl, 0:cols) = the rows of W (global trailing order, ld ldw) that belong
+// to rank p's trailing columns.
+__global__ void cyclic_scatter_rows_kernel(i64 sl, i64 cols, i64 k, i64 b, int P, int p, i64 lb0,
+                                           const double* __restrict__ W, i64 ldw, double* __restrict__ Wl, i64 ldl) {
+  const i64 total = sl * cols;
+  for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
+    const i64 lr = idx % sl, col = idx / sl;
+    const i64 j = (lb0 + lr / b) * P + p;
+    const i64 t = j * b + lr % b - k;
+    Wl[lr + col * ldl] = W[t + col * ldw];
+  }
+}
+
+unsigned grid_for(const Launch& L, i64 total) {
+  i64 b = (total + 255) / 256;
+  const i64 cap = (i64)L.device_sms * 8;
+  if (b > cap) b = cap;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+// ============================================================== SPMD driver
+
+struct DistWork {
+  Work w;
+  double *Yl, *Yall, *Wl, *wbuf, *svd;
+};
+
+size_t carve_dist(Carver& c, DistWork& d, const Layout& lay) {
+  const i64 m = lay.m, n = lay.n, b = std::min(lay.b, lay.n);
+  const i64 maxs = std::max<i64>(lay.max_trailing(0), 1);
+  carve(c, d.w, m, n, b, 0, false);
+  d.Yl = c.take<double>(maxs * b);
+  d.Yall = c.take<double>((i64)lay.P * maxs * b);
+  d.Wl = c.take<double>(maxs * b);
+  d.wbuf = c.take<double>(m * b + b * b);
+  d.svd = c.take<double>(2 * b * b);
+  return c.off;
+}
+
+struct DistProblem {
+  Layout lay;
+  int q;
+  uint64_t seed;
+  double* A;  // local columns, ld lda
+  i64 lda;
+  double* U;  // rows [u0, u0 + mu) of U (m x m), ld ldu; may be null
+  i64 ldu, u0, mu;
+  double* V;  // rows [v0, v0 + nv) of V (n x n), ld ldv; may be null
+  i64 ldv, v0, nv;
+};
+
+struct DistRun {
+  randutv_ctx* ctx;
+  Comm* comm;
+  Comm* side_comm;
+  DistWork d;
+  DistProblem P;
+  Launch L, S;
+};
+
+// S8 + S9 of a block of width bw whose SVD the owner computes; runs on `Ls`
+// with collectives on `cm`.
+int dist_svd_and_fold(DistRun& R, const Launch& Ls, Comm* cm, i64 i, i64 bw, bool dense_final) {
+  (void)dense_final;
+  const Layout& lay = R.P.lay;
+  const int p = lay.p, o = (int)(i % lay.P);
+  const i64 k = i * lay.b;
+  Work& w = R.d.w;
+  double* Us = R.d.svd;
+  double* Vs = R.d.svd + bw * bw;
+  const i64 lc = (i / lay.P) * lay.b;  // owner's local column of block i
+  if (p == o) {
+    double* T11 = R.P.A + k + lc * R.P.lda;
+    RUTV_TRY(launch_jacobi_svd(Ls, bw, T11, R.P.lda, Us, w.d, Vs, w.status, (int)(i + 1), w.jac, w.jac_elems));
+  }
+  RUTV_TRY(cm->bcast(R.d.svd, 2 * bw * bw, o, Ls.stream));
+  if (p == o) {
+    double* T11 = R.P.A + k + lc * R.P.lda;
+    RUTV_TRY(launch_set_diag(Ls, bw, w.d, T11, R.P.lda));
+    RUTV_TRY(right_mult_inplace(Ls, w.Zf, k, bw, R.P.A + lc * R.P.lda, R.P.lda, Vs, bw));  // A01 V_s
+  }
+  // U_s^T A12 over this rank's columns right of block i
+  const i64 c1 = lay.lcol(p, i + 1);
+  RUTV_TRY(left_mult_t_inplace(Ls, w.Zf, bw, lay.ncols(p) - c1, R.P.A + k + c1 * R.P.lda, R.P.lda, Us, bw));
+  if (R.P.U) RUTV_TRY(right_mult_inplace(Ls, w.Zf, R.P.mu, bw, R.P.U + k * R.P.ldu, R.P.ldu, Us, bw));
+  if (R.P.V) RUTV_TRY(right_mult_inplace(Ls, w.Zf, R.P.nv, bw, R.P.V + k * R.P.ldv, R.P.ldv, Vs, bw));
+  return 0;
+}
+
+int dist_sampled_step(DistRun& R, i64 i) {
+  const Layout& lay = R.P.lay;
+  const Launch& L = R.L;
+  Work& w = R.d.w;
+  const int p = lay.p, P = lay.P, o = (int)(i % P);
+  const i64 m = lay.m, n = lay.n, b = lay.b, k = i * b, r = m - k, s = n - k;
+  const i64 c0 = lay.lcol(p, i), sl = lay.ncols(p) - c0, maxs = std::max<i64>(lay.max_trailing(i), 1);
+  double* Ap = R.P.A + c0 * R.P.lda;  // this rank's trailing columns, all m rows
+  double* At = Ap + k;                // rows k:m
+  const i64 lda = R.P.lda;
+  cudaStream_t st = L.stream;
+  // S1, S2, S3
+  RUTV_TRY(launch_gaussian(L, R.P.seed, i, r, b, w.G, r));
+  RUTV_TRY(launch_dgemm(L, true, false, sl, b, r, 1.0, At, lda, w.G, r, 0.0, R.d.Yl, maxs, w.gemm_ws, w.gemm_ws_elems));
+  for (int qq = 0; qq < R.P.q; ++qq) {
+    RUTV_TRY(launch_dgemm(L, false, false, r, b, sl, 1.0, At, lda, R.d.Yl, maxs, 0.0, w.Z, r, w.gemm_ws,
+                          w.gemm_ws_elems));
+    RUTV_TRY(R.comm->allreduce_sum(w.Z, r * b, st));
+    RUTV_TRY(launch_dgemm(L, true, false, sl, b, r, 1.0, At, lda, w.Z, r, 0.0, R.d.Yl, maxs, w.gemm_ws,
+                          w.gemm_ws_elems));
+  }
+  // S4: gather Y in global order, the same QR on every rank
+  RUTV_TRY(R.comm->allgather(R.d.Yl, R.d.Yall, maxs * b, st));
+  cyclic_gather_rows_kernel<<<grid_for(L, s * b), 256, 0, st>>>(s, b, k, b, P, i, R.d.Yall, maxs, maxs * b, w.Y, s);
+  L.count();
+  RUTV_CHECK_LAUNCH("cyclic_gather_rows_kernel");
+  RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
+  // S5: T(:, k:n) -= (T W_V) T_V W_V^T -- wait for the previous step's U_s^T A12 fold
+  RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eF, 0));
+  if (sl > 0) {
+    cyclic_scatter_rows_kernel<<<grid_for(L, sl * b), 256, 0, st>>>(sl, b, k, b, P, p, lay.lb_before(p, i), w.Wv, s,
+                                                                   R.d.Wl, maxs);
+    L.count();
+    RUTV_CHECK_LAUNCH("cyclic_scatter_rows_kernel");
+  }
+  RUTV_TRY(launch_dgemm(L, false, false, m, b, sl, 1.0, Ap, lda, R.d.Wl, maxs, 0.0, w.Z, m, w.gemm_ws,
+                        w.gemm_ws_elems));
+  RUTV_TRY(R.comm->allreduce_sum(w.Z, m * b, st));
+  RUTV_TRY(launch_dgemm(L, false, false, m, b, b, 1.0, w.Z, m, w.TV, b, 0.0, w.Z2, m, nullptr, 0));
+  RUTV_TRY(launch_dgemm(L, false, true, m, sl, b, -1.0, w.Z2, m, R.d.Wl, maxs, 1.0, Ap, lda, nullptr, 0));
+  if (R.P.V) RUTV_TRY(apply_right(L, w, R.P.nv, s, b, R.P.V + k * R.P.ldv, R.P.ldv, w.Wv, s, w.TV, b));
+  // S6: QR of column block i on its owner, broadcast (W_U, T_U)
+  double* Wu = R.d.wbuf;
+  double* TU = R.d.wbuf + r * b;
+  if (p == o) {
+    RUTV_TRY(panel_qr(L, r, b, At, lda, w.tauU, Wu, r, TU, b, w.qw));
+    RUTV_TRY(launch_triu(L, b, b, At, lda));
+    RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, lda));
+  }
+  RUTV_TRY(R.comm->bcast(R.d.wbuf, r * b + b * b, o, st));
+  // S7: columns right of block i; U rows
+  const i64 c1 = lay.lcol(p, i + 1);
+  RUTV_TRY(apply_left_t(L, w, r, lay.ncols(p) - c1, b, R.P.A + k + c1 * lda, lda, Wu, r, TU, b));
+  if (R.P.U) RUTV_TRY(apply_right(L, w, R.P.mu, r, b, R.P.U + k * R.P.ldu, R.P.ldu, Wu, r, TU, b));
+  // S8, S9 on the side stream / side communicator
+  RUTV_CUDA(cudaEventRecord(R.ctx->eR, st));
+  RUTV_CUDA(cudaStreamWaitEvent(R.S.stream, R.ctx->eR, 0));
+  RUTV_TRY(dist_svd_and_fold(R, R.S, R.side_comm, i, b, false));
+  RUTV_CUDA(cudaEventRecord(R.ctx->eF, R.S.stream));
+  return 0;
+}
+
+int dist_final_step(DistRun& R, i64 i) {
+  const Layout& lay = R.P.lay;
+  const Launch& L = R.L;
+  Work& w = R.d.w;
+  const int p = lay.p, o = (int)(i % lay.P);
+  const i64 m = lay.m, n = lay.n, k = i * lay.b, r = m - k, s = n - k;
+  if (s <= 0) return 0;
+  cudaStream_t st = L.stream;
+  RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eF, 0));
+  const i64 lc = (i / lay.P) * lay.b;
+  double* At = R.P.A + k + lc * R.P.lda;
+  if (r > s) {
+    double* Wu = R.d.wbuf;
+    double* TU = R.d.wbuf + r * s;
+    if (p == o) {
+      RUTV_TRY(panel_qr(L, r, s, At, R.P.lda, w.tauU, Wu, r, TU, s, w.qw));
+      RUTV_TRY(launch_triu(L, s, s, At, R.P.lda));
+      RUTV_TRY(launch_fill(L, r - s, s, 0.0, At + s, R.P.lda));
+    }
+    if (R.P.U) {
+      RUTV_TRY(R.comm->bcast(R.d.wbuf, r * s + s * s, o, st));
+      RUTV_TRY(apply_right(L, w, R.P.mu, r, s, R.P.U + k * R.P.ldu, R.P.ldu, Wu, r, TU, s));
+    }
+  }
+  return dist_svd_and_fold(R, L, R.comm, i, s, r == s);
+}
+
+int dist_run(DistRun& R) {
+  const Layout& lay = R.P.lay;
+  randutv_ctx* ctx = R.ctx;
+  Work& w = R.d.w;
+  const Launch& L = R.L;
+  const i64 nsamp = sampled_steps(lay.n, lay.b);
+  RUTV_TRY(start_status(ctx, w));
+  if (R.P.U && R.P.mu > 0) {
+    RUTV_TRY(launch_set_identity_shift(L, R.P.mu, lay.m, -R.P.u0, R.P.U, R.P.ldu));  // rows u0.. of I
+  }
+  if (R.P.V && R.P.nv > 0) {
+    RUTV_TRY(launch_set_identity_shift(L, R.P.nv, lay.n, -R.P.v0, R.P.V, R.P.ldv));
+  }
+  // the side stream starts after the initialisation
+  RUTV_CUDA(cudaEventRecord(ctx->eF, L.stream));
+  for (i64 i = 0; i < nsamp; ++i) RUTV_TRY(dist_sampled_step(R, i));
+  RUTV_TRY(dist_final_step(R, nsamp));
+  RUTV_CUDA(cudaStreamWaitEvent(L.stream, ctx->eF, 0));
+  // every rank returns the first non-converged block (status word: min)
+  RUTV_TRY(R.comm->allreduce_min_int(w.status, 1, L.stream));
+  return finish(ctx, w);
+}
+
+// argument checks shared by the NCCL and loopback entries; returns 0 or -i
+// (positions of randutv_factor_dist)
+int dist_check(const Layout& lay, const double* A, i64 lda, int q, unsigned flags, const double* U, i64 ldu,
+               const double* V, i64 ldv) {
+  const bool uv = !(flags & RANDUTV_NO_UV);
+  if (lay.n < 1) return -3;
+  if (lay.m < lay.n) return -2;
+  const i64 nc = lay.ncols(lay.p);
+  if (nc > 0 && !A) return -4;
+  if (lda < std::max<i64>(lay.m, 1)) return -5;
+  if (lay.b < 1) return -6;
+  if (q < 0) return -7;
+  const i64 mu = Layout::row0(lay.m, lay.P, lay.p + 1) - Layout::row0(lay.m, lay.P, lay.p);
+  const i64 nv = Layout::row0(lay.n, lay.P, lay.p + 1) - Layout::row0(lay.n, lay.P, lay.p);
+  if (uv && mu > 0 && !U) return -10;
+  if (uv && ldu < std::max<i64>(mu, 1)) return -11;
+  if (uv && nv > 0 && !V) return -12;
+  if (uv && ldv < std::max<i64>(nv, 1)) return -13;
+  return 0;
+}
+
+int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, double* A, i64 lda, i64 b, int q,
+                uint64_t seed, unsigned flags, double* U, i64 ldu, double* V, i64 ldv) {
+  Layout lay{m, n, std::min(b, n), comm->nranks, comm->rank, 0};
+  if (b < 1) return -6;
+  lay.nblocks = (n + lay.b - 1) / lay.b;
+  RUTV_TRY(dist_check(lay, A, lda, q, flags, U, ldu, V, ldv));
+  const bool uv = !(flags & RANDUTV_NO_UV);
+  DistRun R;
+  R.ctx = ctx;
+  R.comm = comm;
+  R.side_comm = side_comm;
+  R.L = ctx->launch();
+  R.S = ctx->side_launch();
+  Carver dry{nullptr, 0, 0, true};
+  const size_t need = carve_dist(dry, R.d, lay);
+  RUTV_TRY(ensure_ws(ctx, need));
+  Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
+  carve_dist(real, R.d, lay);
+  const i64 u0 = Layout::row0(m, lay.P, lay.p), u1 = Layout::row0(m, lay.P, lay.p + 1);
+  const i64 v0 = Layout::row0(n, lay.P, lay.p), v1 = Layout::row0(n, lay.P, lay.p + 1);
+  R.P = DistProblem{lay, q, seed, A, lda, uv ? U : nullptr, ldu, u0, u1 - u0, uv ? V : nullptr, ldv, v0, v1 - v0};
+  if (R.P.U && R.P.mu == 0) R.P.U = nullptr;
+  if (R.P.V && R.P.nv == 0) R.P.V = nullptr;
+  if (flags & RANDUTV_CHECK_FINITE) {
+    int bad = 0;
+    if (lay.ncols(lay.p) > 0) bad = check_finite(ctx, R.L, R.d.w, m, lay.ncols(lay.p), A, lda);
+    if (bad != 0 && bad != RANDUTV_ERR_NONFINITE) return bad;
+    // agree on the verdict: min over ranks of (0 = bad, 1 = good)
+    int h = bad ? 0 : 1;
+    RUTV_CUDA(cudaMemcpyAsync(R.d.w.flag, &h, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    RUTV_TRY(comm->allreduce_min_int(R.d.w.flag, 1, ctx->stream));
+    RUTV_CUDA(cudaMemcpyAsync(&h, R.d.w.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (!h) return RANDUTV_ERR_NONFINITE;
+  }
+  const int st = dist_run(R);
+  if (st == 0) ctx->stats.factorizations++;
+  return st;
+}
+
+}  // namespace rutv
+
+// ============================================================================ C ABI
+
+using namespace rutv;
+
+extern "C" {
+
+RANDUTV_API int randutv_dist_layout(int64_t m, int64_t n, int64_t b, int nranks, int rank, int64_t* out) {
+  if (n < 1) return -2;
+  if (m < n) return -1;
+  if (b < 1) return -3;
+  if (nranks < 1) return -4;
+  if (rank < 0 || rank >= nranks) return -5;
+  if (!out) return -6;
+  const i64 bb = std::min<i64>(b, n);
+  Layout lay{m, n, bb, nranks, rank, (n + bb - 1) / bb};
+  out[0] = lay.ncols(rank);
+  out[1] = Layout::row0(m, nranks, rank);
+  out[2] = Layout::row0(m, nranks, rank + 1);
+  out[3] = Layout::row0(n, nranks, rank);
+  out[4] = Layout::row0(n, nranks, rank + 1);
+  return 0;
+}
+
+RANDUTV_API int randutv_nccl_unique_id(void* out) {
+  if (!out) return -1;
+  const NcclApi* api = nccl_api();
+  if (!api) {
+    set_last_error(g_nccl_err, cudaErrorUnknown);
+    return RANDUTV_ERR_NCCL;
+  }
+  ncclUniqueId id;
+  RUTV_NCCL(api->GetUniqueId(&id));
+  memcpy(out, &id, sizeof(id));
+  return 0;
+}
+
+RANDUTV_API int randutv_comm_init(randutv_ctx* ctx, const void* unique_id, int nranks, int rank) {
+  RUTV_TRY(begin_call(ctx));
+  if (!unique_id) return -2;
+  if (nranks < 1) return -3;
+  if (rank < 0 || rank >= nranks) return -4;
+  const NcclApi* api = nccl_api();
+  if (!api) {
+    set_last_error(g_nccl_err, cudaErrorUnknown);
+    return RANDUTV_ERR_NCCL;
+  }
+  comm_free(ctx->comm_side);
+  comm_free(ctx->comm);
+  ctx->comm = ctx->comm_side = nullptr;
+  ncclUniqueId id;
+  memcpy(&id, unique_id, sizeof(id));
+  NcclComm* c = new (std::nothrow) NcclComm();
+  NcclComm* cs = new (std::nothrow) NcclComm();
+  if (!c || !cs) {
+    delete c;
+    delete cs;
+    return RANDUTV_ERR_ALLOC;
+  }
+  c->api = cs->api = api;
+  c->rank = cs->rank = rank;
+  c->nranks = cs->nranks = nranks;
+  ncclResult_t r = api->CommInitRank(&c->comm, nranks, id, rank);
+  if (r == ncclSuccess) r = api->CommSplit(c->comm, 0, rank, &cs->comm, nullptr);
+  if (r != ncclSuccess) {
+    snprintf(g_nccl_err, sizeof(g_nccl_err), "ncclCommInitRank/Split: %s", api->GetErrorString(r));
+    set_last_error(g_nccl_err, cudaErrorUnknown);
+    delete cs;
+    delete c;
+    return RANDUTV_ERR_NCCL;
+  }
+  ctx->comm = c;
+  ctx->comm_side = cs;
+  return 0;
+}
+
+RANDUTV_API int randutv_factor_dist(randutv_ctx* ctx, int64_t m, int64_t n, double* A_local, int64_t lda,
+                                    int64_t b, int q, uint64_t seed, unsigned flags, double* U_local, int64_t ldu,
+                                    double* V_local, int64_t ldv) {
+  RUTV_TRY(begin_call(ctx));
+  if (!ctx->comm) return RANDUTV_ERR_NOCOMM;
+  return dist_factor(ctx, ctx->comm, ctx->comm_side, m, n, A_local, lda, b, q, seed, flags, U_local, ldu, V_local,
+                     ldv);
+}
+
+RANDUTV_API int randutv_factor_dist_loopback(int device, int nranks, int64_t m, int64_t n, double* const* A_locals,
+                                             int64_t lda, int64_t b, int q, uint64_t seed, unsigned flags,
+                                             double* const* U_locals, int64_t ldu, double* const* V_locals,
+                                             int64_t ldv) {
+  if (nranks < 1 || nranks > kMaxLoopRanks) return -2;
+  if (!A_locals) return -5;
+  const bool uv = !(flags & RANDUTV_NO_UV);
+  if (uv && (!U_locals || !V_locals)) return -11;
+  LoopShared sh(nranks);
+  std::vector<int> status(nranks, 0);
+  std::vector<std::thread> th;
+  std::vector<LoopComm*> comms(2 * nranks, nullptr);
+  for (int r = 0; r < 2 * nranks; ++r) {
+    comms[r] = new LoopComm();
+    comms[r]->sh = &sh;  // main and side collectives share the barrier: issued in program order
+    comms[r]->rank = r % nranks;
+    comms[r]->nranks = nranks;
+  }
+  for (int r = 0; r < nranks; ++r) {
+    th.emplace_back([&, r] {
+      int st = 0;
+      randutv_ctx* ctx = nullptr;
+      cudaStream_t s = nullptr;
+      if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+        st = RANDUTV_ERR_CUDA;
+      }
+      if (st == 0) st = randutv_create(&ctx, device, s);
+      if (st == 0) st = begin_call(ctx);
+      if (st == 0) {
+        comms[r]->sms = comms[nranks + r]->sms = ctx->sms;
+        st = dist_factor(ctx, comms[r], comms[nranks + r], m, n, A_locals[r], lda, b, q, seed, flags,
+                         uv ? U_locals[r] : nullptr, ldu, uv ? V_locals[r] : nullptr, ldv);
+      }
+      if (ctx) randutv_destroy(ctx);
+      if (s) cudaStreamDestroy(s);
+      status[r] = st;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (LoopComm* c : comms) delete c;
+  for (int r = 0; r < nranks; ++r)
+    if (status[r] != 0) return status[r];
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// Host-driver internals shared by the single-GPU driver (randutv.cu) and the
+// column-sharded multi-GPU driver (dist.cu): the context, the workspace
+// carving and the compact-WY application helpers.  Not part of the C ABI.
+#pragma once
+#include "common.cuh"
+
+namespace rutv {
+struct Comm;  // dist.cu
+}
+
+struct randutv_ctx {
+  int magic;
+  int device;
+  cudaStream_t stream;
+  int sms;
+  void* ws;
+  size_t ws_bytes;
+  randutv_stats stats;
+  // host-staging buffers of the literal (host pointer) entry
+  double* stage;
+  size_t stage_bytes;
+  rutv::Profiler prof;
+  // side stream (high priority) for the small SVD + folds, and its two events
+  cudaStream_t side;
+  cudaEvent_t eR, eF;
+  // multi-GPU communicators (randutv_comm_init): main-stream and side-stream
+  rutv::Comm* comm;
+  rutv::Comm* comm_side;
+  rutv::Launch launch() { return rutv::Launch{stream, &stats.kernel_launches, sms, &prof}; }
+  rutv::Launch side_launch() { return rutv::Launch{side, &stats.kernel_launches, sms, &prof}; }
+};
+
+namespace rutv {
+
+constexpr int kMagic = 0x52555456;  // "RUTV"
+constexpr i64 kAlign = 256;
+
+struct Carver {
+  char* base;
+  size_t off;
+  size_t cap;
+  bool dry;
+  template <typename Tp>
+  Tp* take(i64 elems) {
+    size_t bytes = ((size_t)(elems > 0 ? elems : 1) * sizeof(Tp) + kAlign - 1) / kAlign * kAlign;
+    Tp* p = dry ? nullptr : reinterpret_cast<Tp*>(base + off);
+    off += bytes;
+    return p;
+  }
+};
+
+// All per-call device buffers.
+struct Work {
+  double *G, *Y, *Z, *Z2, *Wv, *Wu, *TV, *TU, *tauV, *tauU;
+  double *Us, *Vs, *d;
+  double *jac, *gemm_ws, *red, *scal;
+  i64 jac_elems, gemm_ws_elems;
+  int *status, *flag;
+  QrWork qw;
+  double* lefts;  // truncated-U records
+  i64 lefts_elems;
+  double* Twork;  // m x n working T for the truncated variant
+  double* Zf;     // fold temporaries of the side stream (max(m,n) x b)
+};
+
+i64 gemm_ws_elems_for(i64 m, i64 n, i64 b);
+size_t carve(Carver& c, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork);
+int ensure_ws(randutv_ctx* ctx, size_t bytes);
+int prepare(randutv_ctx* ctx, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork);
+int begin_call(randutv_ctx* ctx);
+// synchronise the ctx stream and turn the device status word into the return code
+int finish(randutv_ctx* ctx, const Work& w);
+i64 sampled_steps(i64 n, i64 b);
+// dist.cu: release a communicator (NULL is a no-op)
+void comm_free(Comm* c);
+int start_status(randutv_ctx* ctx, const Work& w);
+int check_finite(randutv_ctx* ctx, const Launch& L, const Work& w, i64 m, i64 n, const double* A, i64 lda);
+
+// X(rows x s, ldx) -= ((X W) Tf) W^T : the right application of Q = I - W Tf W^T
+int apply_right(const Launch& L, Work& w, i64 rows, i64 s, i64 bw, double* X, i64 ldx, const double* W, i64 ldw,
+                const double* Tf, i64 ldtf);
+// X(r x c) -= W Tf^T (W^T X): the left application of Q^T
+int apply_left_t(const Launch& L, Work& w, i64 r, i64 c, i64 bw, double* X, i64 ldx, const double* W, i64 ldw,
+                 const double* Tf, i64 ldtf);
+// X(rows x bw) := X M  (M bw x bw), via the temporary Zt
+int right_mult_inplace(const Launch& L, double* Zt, i64 rows, i64 bw, double* X, i64 ldx, const double* M, i64 ldm);
+// X(bw x cols) := M^T X
+int left_mult_t_inplace(const Launch& L, double* Zt, i64 bw, i64 cols, double* X, i64 ldx, const double* M, i64 ldm);
+
+}  // namespace rutv

@@ -1,0 +1,570 @@
+// Host-streamed randUTV: A, U and V stay in (pinned)
+// host memory and stream through a bounded device panel cache -- the GPU
+// analogue of the paper's out-of-core setting, where the matrix lives on disk
+// and blocks move through an LRU cache in RAM ("cache"
+// dispatcher) while a dedicated I/O thread overlaps the transfers with the
+// computation ("cache + overlap").
+//
+// Unit of transfer: a column panel (all rows x b columns) of T (= A, updated
+// in place), U or V.  The cache holds C panel slots (device_cache_bytes /
+// (max(m,n) b 8 bytes), at least 3); victims are least recently used, dirty
+// victims are written back first.  Every pass over the trailing panels runs
+// in the direction opposite to the previous pass ("serpentine"), so an LRU
+// cache smaller than the pass keeps the panels the next pass starts with
+// (cyclic sweeps larger than an LRU cache never hit).
+// Copies run on two copy streams (H2D prefetch of the next panel of the pass,
+// D2H write-back of victims) and overlap the DMMA work on the compute stream;
+// events order slot reuse.  Per sampled step i (k = i b), panels j >= i:
+//   pass 1   (RW)  pending U_s^T fold of row block i-1 (deferred from step
+//                  i-1, it commutes with everything before S5 of step i) and
+//                  Y_j = T_j(k:m)^T G                                   S1, S2
+//   2q passes (R)  Z = sum_j T_j(k:m) Y_j ; Y_j = T_j(k:m)^T Z           S3
+//   QR(Y) on the device                                                  S4
+//   pass     (R)   Z = sum_j T_j W_j (all m rows)                        S5
+//   pass     (RW)  panel i: S5 update, QR of rows k:m (S6);
+//                  panels j > i: S5 update, then S7 left update          S5-S7
+//   V, U           read pass (X W) + RW pass (X -= ...) over their trailing
+//                  panels                                                S5, S7
+//   panel i        Jacobi SVD of the diagonal block, T11 = diag d, A01 V_s;
+//                  U_i U_s, V_i V_s                                      S8, S9
+// The arithmetic is that of the in-HBM driver (same kernels, same reflector
+// conventions); only sums over panels are split (GEMM accumulation with
+// beta = 1), so results agree with randutv_factor_ex to rounding.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "driver.cuh"
+
+namespace rutv {
+
+namespace {
+
+struct HostMat {
+  double* h;
+  i64 rows, cols, ld;
+  i64 npanels;
+};
+
+struct Slot {
+  double* d = nullptr;
+  int mat = -1;
+  i64 panel = -1;
+  bool dirty = false;
+  int pins = 0;
+  uint64_t last = 0;
+  cudaEvent_t ready = nullptr, idle = nullptr, clean = nullptr;
+};
+
+struct CopyTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<size_t, size_t>> h2d, d2h;
+  int mark(cudaStream_t s, size_t* idx) {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      RUTV_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    RUTV_CUDA(cudaEventRecord(pool[used], s));
+    *idx = used++;
+    return 0;
+  }
+  ~CopyTimer() {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
+};
+
+struct PanelCache {
+  std::vector<HostMat> mats;
+  std::vector<std::vector<int>> where;  // mat -> panel -> slot (-1: host only)
+  std::vector<Slot> slots;
+  double* base = nullptr;
+  i64 slot_elems = 0, b = 0;
+  cudaStream_t comp = nullptr, h2d = nullptr, d2h = nullptr;
+  cudaEvent_t h2d_done = nullptr;
+  uint64_t clock = 0;
+  randutv_host_report* rep = nullptr;
+  CopyTimer timer;
+
+  int add_mat(double* h, i64 rows, i64 cols, i64 ld) {
+    mats.push_back(HostMat{h, rows, cols, ld, (cols + b - 1) / b});
+    where.emplace_back((size_t)mats.back().npanels, -1);
+    return (int)mats.size() - 1;
+  }
+  i64 width(int mat, i64 p) const { return std::min(b, mats[mat].cols - p * b); }
+
+  int init(i64 nslots, double* dbase) {
+    base = dbase;
+    slots.resize((size_t)nslots);
+    for (i64 s = 0; s < nslots; ++s) {
+      slots[s].d = base + s * slot_elems;
+      RUTV_CUDA(cudaEventCreateWithFlags(&slots[s].ready, cudaEventDisableTiming));
+      RUTV_CUDA(cudaEventCreateWithFlags(&slots[s].idle, cudaEventDisableTiming));
+      RUTV_CUDA(cudaEventCreateWithFlags(&slots[s].clean, cudaEventDisableTiming));
+    }
+    return 0;
+  }
+  void destroy() {
+    for (Slot& s : slots) {
+      if (s.ready) cudaEventDestroy(s.ready);
+      if (s.idle) cudaEventDestroy(s.idle);
+      if (s.clean) cudaEventDestroy(s.clean);
+    }
+    slots.clear();
+  }
+
+  int write_back(Slot& s) {
+    if (!s.dirty) return 0;
+    const HostMat& M = mats[s.mat];
+    const i64 w = width(s.mat, s.panel);
+    RUTV_CUDA(cudaStreamWaitEvent(d2h, s.idle, 0));
+    size_t e0 = 0, e1 = 0;
+    if (timer.on) RUTV_TRY(timer.mark(d2h, &e0));
+    RUTV_CUDA(cudaMemcpy2DAsync(M.h + s.panel * b * M.ld, M.ld * 8, s.d, M.rows * 8, M.rows * 8, w,
+                                cudaMemcpyDeviceToHost, d2h));
+    if (timer.on) {
+      RUTV_TRY(timer.mark(d2h, &e1));
+      timer.d2h.push_back({e0, e1});
+    }
+    RUTV_CUDA(cudaEventRecord(s.clean, d2h));
+    rep->d2h_bytes += M.rows * w * 8;
+    s.dirty = false;
+    return 0;
+  }
+
+  int victim(int* out) {
+    int best = -1;
+    for (int s = 0; s < (int)slots.size(); ++s) {
+      if (slots[s].pins > 0) continue;
+      if (slots[s].mat < 0) {
+        best = s;
+        break;
+      }
+      if (best < 0 || slots[s].last < slots[best].last) best = s;
+    }
+    if (best < 0) return RANDUTV_ERR_ALLOC;  // every slot pinned: cannot happen with >= 3 slots
+    *out = best;
+    return 0;
+  }
+
+  // make (mat, panel) resident; `load` = false gives an uninitialised slot
+  // (the caller overwrites the whole panel, e.g. U := I)
+  int fetch(int mat, i64 panel, bool load, int* out) {
+    int s = where[mat][panel];
+    if (s >= 0) {
+      ++rep->cache_hits;
+      *out = s;
+      return 0;
+    }
+    ++rep->cache_misses;
+    RUTV_TRY(victim(&s));
+    Slot& v = slots[s];
+    if (v.mat >= 0) {
+      RUTV_TRY(write_back(v));
+      where[v.mat][v.panel] = -1;
+    }
+    v.mat = mat;
+    v.panel = panel;
+    v.dirty = false;
+    v.last = ++clock;
+    where[mat][panel] = s;
+    const HostMat& M = mats[mat];
+    const i64 w = width(mat, panel);
+    RUTV_CUDA(cudaStreamWaitEvent(h2d, v.idle, 0));
+    RUTV_CUDA(cudaStreamWaitEvent(h2d, v.clean, 0));
+    if (load) {
+      size_t e0 = 0, e1 = 0;
+      if (timer.on) RUTV_TRY(timer.mark(h2d, &e0));
+      RUTV_CUDA(cudaMemcpy2DAsync(v.d, M.rows * 8, M.h + panel * b * M.ld, M.ld * 8, M.rows * 8, w,
+                                  cudaMemcpyHostToDevice, h2d));
+      if (timer.on) {
+        RUTV_TRY(timer.mark(h2d, &e1));
+        timer.h2d.push_back({e0, e1});
+      }
+      rep->h2d_bytes += M.rows * w * 8;
+    }
+    RUTV_CUDA(cudaEventRecord(v.ready, h2d));
+    *out = s;
+    return 0;
+  }
+
+  // pin (mat, panel) for compute on `comp`; returns the device panel (ld = rows)
+  int get(int mat, i64 panel, double** d, bool load = true) {
+    int s;
+    RUTV_TRY(fetch(mat, panel, load, &s));
+    Slot& v = slots[s];
+    v.pins++;
+    v.last = ++clock;
+    RUTV_CUDA(cudaStreamWaitEvent(comp, v.ready, 0));
+    *d = v.d;
+    return 0;
+  }
+  int put(int mat, i64 panel, bool dirty) {
+    Slot& v = slots[where[mat][panel]];
+    v.pins--;
+    v.dirty = v.dirty || dirty;
+    RUTV_CUDA(cudaEventRecord(v.idle, comp));
+    return 0;
+  }
+  int prefetch(int mat, i64 panel) {
+    if (panel < 0 || panel >= mats[mat].npanels) return 0;
+    int s;
+    return fetch(mat, panel, true, &s);
+  }
+  int flush() {
+    for (Slot& s : slots)
+      if (s.mat >= 0) RUTV_TRY(write_back(s));
+    return 0;
+  }
+};
+
+struct HostRun {
+  randutv_ctx* ctx;
+  Launch L;
+  Work w;
+  PanelCache pc;
+  int mT = -1, mU = -1, mV = -1;
+  i64 m, n, b;
+  int q;
+  uint64_t seed;
+  bool dir = false;        // direction of the next pass (serpentine)
+  i64 fold_row = -1;       // pending U_s^T fold of row block [fold_row, fold_row + b) ...
+  i64 fold_from = 0;       // ... for panels >= fold_from
+  double* Usf = nullptr;   // its U_s (b x b)
+};
+
+// Visit panels [p0, p1) of `mat` in the current serpentine direction with a
+// one-panel prefetch; f(panel, device ptr) enqueues the work on the compute stream.
+template <class F>
+int pass(HostRun& R, int mat, i64 p0, i64 p1, bool dirty, F&& f) {
+  const bool fwd = R.dir;
+  R.dir = !R.dir;
+  const i64 cnt = p1 - p0;
+  for (i64 t = 0; t < cnt; ++t) {
+    const i64 j = fwd ? p0 + t : p1 - 1 - t;
+    double* d;
+    RUTV_TRY(R.pc.get(mat, j, &d));
+    if (t + 1 < cnt) RUTV_TRY(R.pc.prefetch(mat, fwd ? j + 1 : j - 1));
+    RUTV_TRY(f(j, d));
+    RUTV_TRY(R.pc.put(mat, j, dirty));
+  }
+  return 0;
+}
+
+// X (rows x cols) := M^T X in place through Zt
+int fold_rows(HostRun& R, i64 bw, i64 cols, double* X, i64 ldx, const double* M) {
+  return left_mult_t_inplace(R.L, R.w.Zf, bw, cols, X, ldx, M, bw);
+}
+
+// right update of the trailing panels [p0, np) of matrix `mat` (rows x *):
+// X -= ((X W) Tf) W^T with W (ld ldw) rows aligned to panel p0's first column
+int stream_apply_right(HostRun& R, int mat, i64 p0, i64 bw, const double* W, i64 ldw, const double* Tf, i64 ldtf) {
+  const HostMat& M = R.pc.mats[mat];
+  const i64 rows = M.rows;
+  Work& w = R.w;
+  // Z = sum_j X_j W_j   (fixed panel order inside a pass is not needed for
+  // correctness; the GEMM accumulation is beta = 1)
+  RUTV_TRY(launch_fill(R.L, rows, bw, 0.0, w.Z, rows));
+  RUTV_TRY(pass(R, mat, p0, M.npanels, false, [&](i64 j, double* X) {
+    const i64 wj = R.pc.width(mat, j);
+    return launch_dgemm(R.L, false, false, rows, bw, wj, 1.0, X, rows, W + (j - p0) * R.b, ldw, 1.0, w.Z, rows,
+                        nullptr, 0);
+  }));
+  RUTV_TRY(launch_dgemm(R.L, false, false, rows, bw, bw, 1.0, w.Z, rows, Tf, ldtf, 0.0, w.Z2, rows, nullptr, 0));
+  return pass(R, mat, p0, M.npanels, true, [&](i64 j, double* X) {
+    const i64 wj = R.pc.width(mat, j);
+    return launch_dgemm(R.L, false, true, rows, wj, bw, -1.0, w.Z2, rows, W + (j - p0) * R.b, ldw, 1.0, X, rows,
+                        nullptr, 0);
+  });
+}
+
+int host_svd_fold(HostRun& R, i64 i, i64 bw, bool defer_fold) {
+  Work& w = R.w;
+  const i64 k = i * R.b;
+  double* X;
+  RUTV_TRY(R.pc.get(R.mT, i, &X));
+  double* T11 = X + k;
+  RUTV_TRY(launch_jacobi_svd(R.L, bw, T11, R.m, w.Us, w.d, w.Vs, w.status, (int)(i + 1), w.jac, w.jac_elems));
+  RUTV_TRY(launch_set_diag(R.L, bw, w.d, T11, R.m));
+  RUTV_TRY(right_mult_inplace(R.L, w.Zf, k, bw, X, R.m, w.Vs, bw));  // A01 V_s
+  RUTV_TRY(R.pc.put(R.mT, i, true));
+  if (R.mU >= 0) {
+    RUTV_TRY(R.pc.get(R.mU, i, &X));
+    RUTV_TRY(right_mult_inplace(R.L, w.Zf, R.m, bw, X, R.m, w.Us, bw));
+    RUTV_TRY(R.pc.put(R.mU, i, true));
+  }
+  if (R.mV >= 0) {
+    RUTV_TRY(R.pc.get(R.mV, i, &X));
+    RUTV_TRY(right_mult_inplace(R.L, w.Zf, R.n, bw, X, R.n, w.Vs, bw));
+    RUTV_TRY(R.pc.put(R.mV, i, true));
+  }
+  if (defer_fold) {
+    // U_s^T T(k:k+b, k+b:n) is applied by the next pass over the trailing panels
+    RUTV_TRY(launch_copy(R.L, bw, bw, w.Us, bw, R.Usf, bw));
+    R.fold_row = k;
+    R.fold_from = i + 1;
+  }
+  return 0;
+}
+
+int apply_pending_fold(HostRun& R, i64 j, double* X) {
+  if (R.fold_row < 0 || j < R.fold_from) return 0;
+  return fold_rows(R, R.b, R.pc.width(R.mT, j), X + R.fold_row, R.m, R.Usf);
+}
+
+int host_sampled_step(HostRun& R, i64 i) {
+  Work& w = R.w;
+  const i64 m = R.m, n = R.n, b = R.b, k = i * b, r = m - k, s = n - k;
+  const i64 np = R.pc.mats[R.mT].npanels;
+  // S1; pass 1: pending fold + S2
+  RUTV_TRY(launch_gaussian(R.L, R.seed, i, r, b, w.G, r));
+  RUTV_TRY(pass(R, R.mT, i, np, R.fold_row >= 0, [&](i64 j, double* X) {
+    RUTV_TRY(apply_pending_fold(R, j, X));
+    return launch_dgemm(R.L, true, false, R.pc.width(R.mT, j), b, r, 1.0, X + k, m, w.G, r, 0.0,
+                        w.Y + (j - i) * b, s, w.gemm_ws, w.gemm_ws_elems);
+  }));
+  R.fold_row = -1;
+  // S3
+  for (int qq = 0; qq < R.q; ++qq) {
+    RUTV_TRY(launch_fill(R.L, r, b, 0.0, w.Z, r));
+    RUTV_TRY(pass(R, R.mT, i, np, false, [&](i64 j, double* X) {
+      return launch_dgemm(R.L, false, false, r, b, R.pc.width(R.mT, j), 1.0, X + k, m, w.Y + (j - i) * b, s, 1.0,
+                          w.Z, r, nullptr, 0);
+    }));
+    RUTV_TRY(pass(R, R.mT, i, np, false, [&](i64 j, double* X) {
+      return launch_dgemm(R.L, true, false, R.pc.width(R.mT, j), b, r, 1.0, X + k, m, w.Z, r, 0.0,
+                          w.Y + (j - i) * b, s, w.gemm_ws, w.gemm_ws_elems);
+    }));
+  }
+  // S4
+  RUTV_TRY(panel_qr(R.L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
+  // S5 (read): Z = T(:, k:n) W_V ; Z2 = Z T_V
+  RUTV_TRY(launch_fill(R.L, m, b, 0.0, w.Z, m));
+  RUTV_TRY(pass(R, R.mT, i, np, false, [&](i64 j, double* X) {
+    return launch_dgemm(R.L, false, false, m, b, R.pc.width(R.mT, j), 1.0, X, m, w.Wv + (j - i) * b, s, 1.0, w.Z,
+                        m, nullptr, 0);
+  }));
+  RUTV_TRY(launch_dgemm(R.L, false, false, m, b, b, 1.0, w.Z, m, w.TV, b, 0.0, w.Z2, m, nullptr, 0));
+  // S5 update + S6 on panel i
+  {
+    double* X;
+    RUTV_TRY(R.pc.get(R.mT, i, &X));
+    RUTV_TRY(launch_dgemm(R.L, false, true, m, b, b, -1.0, w.Z2, m, w.Wv, s, 1.0, X, m, nullptr, 0));
+    RUTV_TRY(panel_qr(R.L, r, b, X + k, m, w.tauU, w.Wu, r, w.TU, b, w.qw));
+    RUTV_TRY(launch_triu(R.L, b, b, X + k, m));
+    RUTV_TRY(launch_fill(R.L, r - b, b, 0.0, X + k + b, m));
+    RUTV_TRY(R.pc.put(R.mT, i, true));
+  }
+  // S5 update + S7 on panels > i (RW).  apply_left_t uses Z/Z2 as temporaries:
+  // keep Z2 (the S5 factor) in Zf meanwhile.
+  RUTV_TRY(launch_copy(R.L, m, b, w.Z2, m, w.Zf, m));
+  RUTV_TRY(pass(R, R.mT, i + 1, np, true, [&](i64 j, double* X) {
+    const i64 wj = R.pc.width(R.mT, j);
+    RUTV_TRY(launch_dgemm(R.L, false, true, m, wj, b, -1.0, w.Zf, m, w.Wv + (j - i) * b, s, 1.0, X, m, nullptr, 0));
+    return apply_left_t(R.L, w, r, wj, b, X + k, m, w.Wu, r, w.TU, b);
+  }));
+  // V: right transform with W_V; U: right transform with W_U (columns k:m)
+  if (R.mV >= 0) RUTV_TRY(stream_apply_right(R, R.mV, i, b, w.Wv, s, w.TV, b));
+  if (R.mU >= 0) RUTV_TRY(stream_apply_right(R, R.mU, i, b, w.Wu, r, w.TU, b));
+  // S8, S9
+  return host_svd_fold(R, i, b, true);
+}
+
+int host_final_step(HostRun& R, i64 i) {
+  Work& w = R.w;
+  const i64 m = R.m, n = R.n, k = i * R.b, r = m - k, s = n - k;
+  if (s <= 0) return 0;
+  double* X;
+  RUTV_TRY(R.pc.get(R.mT, i, &X));
+  RUTV_TRY(apply_pending_fold(R, i, X));
+  R.fold_row = -1;
+  const bool tall = r > s;
+  if (tall) {
+    RUTV_TRY(panel_qr(R.L, r, s, X + k, m, w.tauU, w.Wu, r, w.TU, R.b, w.qw));
+    RUTV_TRY(launch_triu(R.L, s, s, X + k, m));
+    RUTV_TRY(launch_fill(R.L, r - s, s, 0.0, X + k + s, m));
+  }
+  RUTV_TRY(R.pc.put(R.mT, i, true));
+  if (tall && R.mU >= 0) RUTV_TRY(stream_apply_right(R, R.mU, i, s, w.Wu, r, w.TU, R.b));
+  return host_svd_fold(R, i, s, false);
+}
+
+}  // namespace
+
+}  // namespace rutv
+
+using namespace rutv;
+
+extern "C" {
+
+RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b,
+                                    int q, uint64_t seed, unsigned flags, size_t device_cache_bytes, double* U_host,
+                                    int64_t ldu, double* V_host, int64_t ldv, randutv_host_report* report) {
+  RUTV_TRY(begin_call(ctx));
+  const bool uv = !(flags & RANDUTV_NO_UV);
+  if (n < 1) return -3;
+  if (m < n) return -2;
+  if (!A_host) return -4;
+  if (lda < m) return -5;
+  if (b < 1) return -6;
+  if (q < 0) return -7;
+  if (uv && !U_host) return -11;
+  if (uv && ldu < m) return -12;
+  if (uv && !V_host) return -13;
+  if (uv && ldv < n) return -14;
+  const i64 bb = std::min<i64>(b, n);
+  randutv_host_report rep;
+  memset(&rep, 0, sizeof(rep));
+
+  HostRun R;
+  R.ctx = ctx;
+  R.L = ctx->launch();
+  R.m = m;
+  R.n = n;
+  R.b = bb;
+  R.q = q;
+  R.seed = seed;
+  R.pc.b = bb;
+  R.pc.rep = &rep;
+  R.pc.slot_elems = ((std::max(m, n) * bb + 31) / 32) * 32;
+  // workspace: the in-HBM driver's buffers + U_s of the deferred fold + the slots
+  Carver dry{nullptr, 0, 0, true};
+  carve(dry, R.w, m, n, bb, 0, false);
+  dry.take<double>(bb * bb);
+  const size_t fixed = dry.off;
+  const size_t slot_bytes = (size_t)R.pc.slot_elems * 8;
+  size_t budget = device_cache_bytes;
+  if (budget == 0) {
+    size_t fr = 0, tot = 0;
+    RUTV_CUDA(cudaMemGetInfo(&fr, &tot));
+    budget = fr / 2;
+  }
+  i64 nslots = (i64)(budget / slot_bytes);
+  const i64 npT = (n + bb - 1) / bb, npU = uv ? (m + bb - 1) / bb : 0, npV = uv ? npT : 0;
+  nslots = std::min<i64>(nslots, npT + npU + npV);
+  if (nslots < 3) nslots = 3;
+  RUTV_TRY(ensure_ws(ctx, fixed + (size_t)nslots * slot_bytes + kAlign));
+  Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
+  carve(real, R.w, m, n, bb, 0, false);
+  R.Usf = real.take<double>(bb * bb);
+  double* slots = real.take<double>(nslots * R.pc.slot_elems);
+  rep.cache_slots = nslots;
+  rep.slot_bytes = (int64_t)slot_bytes;
+
+  // pin the host matrices for the duration of the call if the caller did not
+  std::vector<void*> registered;
+  auto pin = [&](double* h, i64 ld, i64 cols) -> int {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) == cudaSuccess && a.type == cudaMemoryTypeHost) return 0;
+    cudaGetLastError();
+    RUTV_CUDA(cudaHostRegister(h, (size_t)ld * cols * 8, cudaHostRegisterDefault));
+    registered.push_back(h);
+    return 0;
+  };
+  int st = pin(A_host, lda, n);
+  if (st == 0 && uv) st = pin(U_host, ldu, m);
+  if (st == 0 && uv) st = pin(V_host, ldv, n);
+
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (st == 0 && (cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking) != cudaSuccess ||
+                  cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) != cudaSuccess ||
+                  cudaEventCreate(&t0) != cudaSuccess || cudaEventCreate(&t1) != cudaSuccess))
+    st = RANDUTV_ERR_CUDA;
+  if (st == 0) {
+    R.pc.comp = ctx->stream;
+    R.pc.h2d = h2d;
+    R.pc.d2h = d2h;
+    R.pc.timer.on = report != nullptr;
+    st = R.pc.init(nslots, slots);
+  }
+  if (st == 0) {
+    R.mT = R.pc.add_mat(A_host, m, n, lda);
+    if (uv) {
+      R.mU = R.pc.add_mat(U_host, m, m, ldu);
+      R.mV = R.pc.add_mat(V_host, n, n, ldv);
+    }
+    cudaEventRecord(t0, ctx->stream);
+    st = start_status(ctx, R.w);
+  }
+  // U := I, V := I panel by panel on the device (no host traffic in)
+  if (st == 0 && uv) {
+    for (int mat : {R.mU, R.mV}) {
+      const HostMat& M = R.pc.mats[mat];
+      for (i64 j = 0; j < M.npanels && st == 0; ++j) {
+        double* X;
+        st = R.pc.get(mat, j, &X, false);
+        if (st == 0) st = launch_set_identity_shift(R.L, M.rows, R.pc.width(mat, j), j * bb, X, M.rows);
+        if (st == 0) st = R.pc.put(mat, j, true);
+      }
+    }
+  }
+  if (st == 0 && (flags & RANDUTV_CHECK_FINITE)) {
+    // scan panel by panel through the cache
+    st = cudaMemsetAsync(R.w.flag, 0, sizeof(int), ctx->stream) == cudaSuccess ? 0 : RANDUTV_ERR_CUDA;
+    for (i64 j = 0; j < npT && st == 0; ++j) {
+      double* X;
+      st = R.pc.get(R.mT, j, &X);
+      if (st == 0) st = launch_nonfinite(R.L, m, R.pc.width(R.mT, j), X, m, R.w.flag);
+      if (st == 0) st = R.pc.put(R.mT, j, false);
+    }
+    int flag = 0;
+    if (st == 0 && (cudaMemcpyAsync(&flag, R.w.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream) !=
+                        cudaSuccess ||
+                    cudaStreamSynchronize(ctx->stream) != cudaSuccess))
+      st = RANDUTV_ERR_CUDA;
+    if (st == 0 && flag) st = RANDUTV_ERR_NONFINITE;
+  }
+  if (st == 0) {
+    const i64 nsamp = sampled_steps(n, bb);
+    for (i64 i = 0; i < nsamp && st == 0; ++i) st = host_sampled_step(R, i);
+    if (st == 0) st = host_final_step(R, nsamp);
+    if (st == 0) st = R.pc.flush();
+    if (st == 0) {
+      // the compute stream must not return before the write-backs land
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(e, d2h);
+        cudaStreamWaitEvent(ctx->stream, e, 0);
+        cudaEventRecord(e, h2d);
+        cudaStreamWaitEvent(ctx->stream, e, 0);
+        cudaEventDestroy(e);
+      }
+      cudaEventRecord(t1, ctx->stream);
+      st = finish(ctx, R.w);
+    }
+  }
+  {
+    float ms = 0.f;
+    if (t0 && t1 && cudaEventElapsedTime(&ms, t0, t1) == cudaSuccess) rep.wall_ms = ms;
+    auto sum = [&](const std::vector<std::pair<size_t, size_t>>& v) {
+      double tot = 0.0;
+      for (auto& pr : v) {
+        float x = 0.f;
+        if (cudaEventElapsedTime(&x, R.pc.timer.pool[pr.first], R.pc.timer.pool[pr.second]) == cudaSuccess) tot += x;
+      }
+      return tot;
+    };
+    rep.h2d_ms = sum(R.pc.timer.h2d);
+    rep.d2h_ms = sum(R.pc.timer.d2h);
+  }
+  cudaStreamSynchronize(ctx->stream);
+  if (h2d) cudaStreamSynchronize(h2d);
+  if (d2h) cudaStreamSynchronize(d2h);
+  R.pc.destroy();
+  if (h2d) cudaStreamDestroy(h2d);
+  if (d2h) cudaStreamDestroy(d2h);
+  if (t0) cudaEventDestroy(t0);
+  if (t1) cudaEventDestroy(t1);
+  for (void* p : registered) cudaHostUnregister(p);
+  cudaGetLastError();
+  ctx->stats.h2d_bytes += rep.h2d_bytes;
+  ctx->stats.d2h_bytes += rep.d2h_bytes;
+  if (report) *report = rep;
+  if (st == 0) ctx->stats.factorizations++;
+  return st;
+}
+
+}  // extern "C"

@@ -28,6 +28,14 @@ __global__ void set_identity_kernel(i64 rows, i64 cols, double* X, i64 ldx) {
   }
 }
 
+__global__ void set_identity_shift_kernel(i64 rows, i64 cols, i64 shift, double* X, i64 ldx) {
+  const i64 total = rows * cols;
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < total; i += (i64)gridDim.x * blockDim.x) {
+    const i64 r = i % rows, c = i / rows;
+    X[r + c * ldx] = (r - c == shift) ? 1.0 : 0.0;
+  }
+}
+
 __global__ void copy_kernel(i64 rows, i64 cols, const double* __restrict__ S, i64 lds, double* __restrict__ D,
                             i64 ldd) {
   const i64 total = rows * cols;
@@ -115,6 +123,9 @@ __global__ void nonfinite_kernel(i64 rows, i64 cols, const double* __restrict__ 
 
 int launch_set_identity(const Launch& L, i64 rows, i64 cols, double* X, i64 ldx) {
   RUTV_GRID_LAUNCH(set_identity_kernel, rows * cols, rows, cols, X, ldx);
+}
+int launch_set_identity_shift(const Launch& L, i64 rows, i64 cols, i64 shift, double* X, i64 ldx) {
+  RUTV_GRID_LAUNCH(set_identity_shift_kernel, rows * cols, rows, cols, shift, X, ldx);
 }
 int launch_copy(const Launch& L, i64 rows, i64 cols, const double* S, i64 lds, double* D, i64 ldd) {
   RUTV_GRID_LAUNCH(copy_kernel, rows * cols, rows, cols, S, lds, D, ldd);

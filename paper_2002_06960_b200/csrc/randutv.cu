@@ -30,7 +30,7 @@
 #include <mutex>
 #include <new>
 
-#include "common.cuh"
+#include "driver.cuh"
 
 using rutv::i64;
 
@@ -94,60 +94,7 @@ Profiler::~Profiler() {
 
 }  // namespace rutv
 
-struct randutv_ctx {
-  int magic;
-  int device;
-  cudaStream_t stream;
-  int sms;
-  void* ws;
-  size_t ws_bytes;
-  randutv_stats stats;
-  // host-staging buffers of the literal (host pointer) entry
-  double* stage;
-  size_t stage_bytes;
-  rutv::Profiler prof;
-  // side stream (high priority) for the small SVD + folds, and its two events
-  cudaStream_t side;
-  cudaEvent_t eR, eF;
-  rutv::Launch launch() { return rutv::Launch{stream, &stats.kernel_launches, sms, &prof}; }
-  rutv::Launch side_launch() { return rutv::Launch{side, &stats.kernel_launches, sms, &prof}; }
-};
-
-static const int kMagic = 0x52555456;  // "RUTV"
-
-namespace {
-
-using namespace rutv;
-
-constexpr i64 kAlign = 256;
-
-struct Carver {
-  char* base;
-  size_t off;
-  size_t cap;
-  bool dry;
-  template <typename Tp>
-  Tp* take(i64 elems) {
-    size_t bytes = ((size_t)(elems > 0 ? elems : 1) * sizeof(Tp) + kAlign - 1) / kAlign * kAlign;
-    Tp* p = dry ? nullptr : reinterpret_cast<Tp*>(base + off);
-    off += bytes;
-    return p;
-  }
-};
-
-// All per-call device buffers.
-struct Work {
-  double *G, *Y, *Z, *Z2, *Wv, *Wu, *TV, *TU, *tauV, *tauU;
-  double *Us, *Vs, *d;
-  double *jac, *gemm_ws, *red, *scal;
-  i64 jac_elems, gemm_ws_elems;
-  int *status, *flag;
-  QrWork qw;
-  double* lefts;  // truncated-U records
-  i64 lefts_elems;
-  double* Twork;  // m x n working T for the truncated variant
-  double* Zf;     // fold temporaries of the side stream (max(m,n) x b)
-};
+namespace rutv {
 
 i64 gemm_ws_elems_for(i64 m, i64 n, i64 b) {
   const i64 mx = m > n ? m : n;
@@ -225,24 +172,6 @@ int prepare(randutv_ctx* ctx, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool tw
   return 0;
 }
 
-struct Problem {
-  i64 m, n, b;
-  int q;
-  uint64_t seed;
-  double* T;
-  i64 ldt;
-  double* U;  // forward m x m accumulation (may be null)
-  i64 ldu;
-  double* V;  // n x n (may be null)
-  i64 ldv;
-  bool record_lefts;
-  // S8/S9 of step i run on a side stream and overlap S1-S4 of step i+1
-  // (SURVEY.md §8(a) "Commutation"): eR = R and T12 of step i ready (main),
-  // eF = folds of step i done (side); S5 of step i+1 waits for eF.
-  Launch side;
-  cudaEvent_t eR, eF;
-};
-
 i64 sampled_steps(i64 n, i64 b) { return n > b ? (n - b + b - 1) / b : 0; }
 
 // X(rows x s, ldx) -= ((X W) Tf) W^T : the right application of Q = I - W Tf W^T
@@ -278,6 +207,31 @@ int left_mult_t_inplace(const Launch& L, double* Zt, i64 bw, i64 cols, double* X
   RUTV_TRY(launch_dgemm(L, true, false, bw, cols, bw, 1.0, M, ldm, X, ldx, 0.0, Zt, bw, nullptr, 0));
   return launch_copy(L, bw, cols, Zt, bw, X, ldx);
 }
+
+}  // namespace rutv
+
+namespace {
+
+using namespace rutv;
+
+struct Problem {
+  i64 m, n, b;
+  int q;
+  uint64_t seed;
+  double* T;
+  i64 ldt;
+  double* U;  // forward m x m accumulation (may be null)
+  i64 ldu;
+  double* V;  // n x n (may be null)
+  i64 ldv;
+  bool record_lefts;
+  // S8/S9 of step i run on a side stream and overlap S1-S4 of step i+1
+  // (SURVEY.md §8(a) "Commutation"): eR = R and T12 of step i ready (main),
+  // eF = folds of step i done (side); S5 of step i+1 waits for eF.
+  Launch side;
+  cudaEvent_t eR, eF;
+};
+
 
 // S8 + S9 for a bw x bw diagonal block at (kk, kk).  `B` is the block to
 // decompose (T11 itself).
@@ -372,6 +326,10 @@ int run_loop(const Launch& L, Work& w, const Problem& P, i64 nsteps, bool with_f
   return 0;
 }
 
+}  // namespace
+
+namespace rutv {
+
 int begin_call(randutv_ctx* ctx) {
   if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
   RUTV_CUDA(cudaSetDevice(ctx->device));
@@ -408,6 +366,12 @@ int check_finite(randutv_ctx* ctx, const Launch& L, const Work& w, i64 m, i64 n,
   RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
   return flag ? RANDUTV_ERR_NONFINITE : 0;
 }
+
+}  // namespace rutv
+
+namespace {
+
+using namespace rutv;
 
 bool overlaps(const double* a, size_t abytes, const double* b, size_t bbytes) {
   const char *pa = (const char*)a, *pb = (const char*)b;
@@ -446,6 +410,9 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
   if (ctx->side) cudaStreamSynchronize(ctx->side);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->stage) cudaFree(ctx->stage);
+  rutv::comm_free(ctx->comm_side);
+  rutv::comm_free(ctx->comm);
+  ctx->comm = ctx->comm_side = nullptr;
   if (ctx->side) {
     cudaEventDestroy(ctx->eR);
     cudaEventDestroy(ctx->eF);

@@ -23,6 +23,9 @@ RANDUTV_ERR_CUDA = 1000
 RANDUTV_ERR_ALLOC = 1001
 RANDUTV_ERR_NONFINITE = 1002
 RANDUTV_ERR_CTX = 1003
+RANDUTV_ERR_NCCL = 1004
+RANDUTV_ERR_NOCOMM = 1005
+RANDUTV_UNIQUE_ID_BYTES = 128
 
 # name -> (restype, argtypes) ; mirrors include/randutv.h
 _i64, _u64, _int, _uint, _dbl, _vp = (ctypes.c_int64, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint,
@@ -38,6 +41,12 @@ class Stats(ctypes.Structure):
 class Profile(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("ms", ctypes.c_double), ("flops", ctypes.c_double),
                 ("bytes", ctypes.c_double)]
+
+
+class HostReport(ctypes.Structure):
+    _fields_ = [("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64), ("cache_hits", ctypes.c_int64),
+                ("cache_misses", ctypes.c_int64), ("cache_slots", ctypes.c_int64), ("slot_bytes", ctypes.c_int64),
+                ("wall_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double)]
 
 
 PROF_KINDS = {"dgemm": 0, "qr_leaf": 1, "jacobi": 2, "gaussian": 3}
@@ -62,6 +71,14 @@ SIGNATURES = {
     "randutv_dgemm": (_int, [_vp, _int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64]),
     "randutv_panel_qr": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64]),
     "randutv_small_svd": (_int, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
+    "randutv_factor_host": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint, ctypes.c_size_t, _vp, _i64,
+                                   _vp, _i64, ctypes.POINTER(HostReport)]),
+    "randutv_dist_layout": (_int, [_i64, _i64, _i64, _int, _int, ctypes.POINTER(_i64)]),
+    "randutv_nccl_unique_id": (_int, [_vp]),
+    "randutv_comm_init": (_int, [_vp, _vp, _int, _int]),
+    "randutv_factor_dist": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint, _vp, _i64, _vp, _i64]),
+    "randutv_factor_dist_loopback": (_int, [_int, _int, _i64, _i64, ctypes.POINTER(_vp), _i64, _i64, _int, _u64,
+                                            _uint, ctypes.POINTER(_vp), _i64, ctypes.POINTER(_vp), _i64]),
 }
 
 _lib = None
@@ -238,6 +255,58 @@ class Context:
                                                              _ld(Tf)))
         return P, tau, Tf
 
+    # ---------------------------------------------------------------- host-streamed
+    def randutv_factor_host(self, A, b, q, seed, build_uv=True, U=None, V=None, cache_bytes=0, flags=0):
+        """Host-streamed randUTV: A (Fortran-ordered float64 numpy array in host memory,
+        ideally pinned, see pinned_colmajor) is overwritten by T; returns (U, V, report)."""
+        m, n = A.shape
+        if not build_uv:
+            flags |= RANDUTV_NO_UV
+        if build_uv:
+            U = pinned_colmajor(m, m) if U is None else U
+            V = pinned_colmajor(n, n) if V is None else V
+        rep = HostReport()
+        st = self.lib.randutv_factor_host(self.h, m, n, _hptr(A), _hld(A), int(b), int(q), int(seed) & (2**64 - 1),
+                                          flags, int(cache_bytes), _hptr(U), _hld(U) if U is not None else 1,
+                                          _hptr(V), _hld(V) if V is not None else 1, ctypes.byref(rep))
+        _check("randutv_factor_host", st)
+        return U, V, {k: getattr(rep, k) for k, _ in HostReport._fields_}
+
+    # ---------------------------------------------------------------- multi-GPU
+    def comm_init(self, unique_id, nranks, rank):
+        """Join the NCCL communicator (collective; one process per GPU)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), RANDUTV_UNIQUE_ID_BYTES)
+        _check("randutv_comm_init", self.lib.randutv_comm_init(self.h, buf, int(nranks), int(rank)))
+
+    def comm_init_torch(self, group=None):
+        """Bootstrap the communicator over an initialised torch.distributed group:
+        rank 0 draws the NCCL unique id, broadcast_object_list ships it."""
+        import torch.distributed as dist
+        rank, ws = dist.get_rank(group), dist.get_world_size(group)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self.comm_init(obj[0], ws, rank)
+        return rank, ws
+
+    def randutv_factor_dist(self, A_local, m, n, b, q, seed, build_uv=True, U_local=None, V_local=None, flags=0,
+                            nranks=None, rank=None):
+        """Sharded randUTV (collective).  A_local (m x n_p, column-major, device) is
+        overwritten by this rank's columns of T; returns (U_local, V_local)."""
+        import torch.distributed as dist
+        if nranks is None:
+            nranks, rank = dist.get_world_size(), dist.get_rank()
+        lay = dist_layout(m, n, b, nranks, rank)
+        if not build_uv:
+            flags |= RANDUTV_NO_UV
+        if build_uv:
+            U_local = colmajor(lay["u1"] - lay["u0"], m, device=A_local.device) if U_local is None else U_local
+            V_local = colmajor(lay["v1"] - lay["v0"], n, device=A_local.device) if V_local is None else V_local
+        st = self.lib.randutv_factor_dist(self.h, m, n, _ptr(A_local), _ld_or(A_local, m), int(b), int(q),
+                                          int(seed) & (2**64 - 1), flags, _ptr(U_local), _ld_or(U_local, 1),
+                                          _ptr(V_local), _ld_or(V_local, 1))
+        _check("randutv_factor_dist", st)
+        return U_local, V_local
+
     def randutv_small_svd(self, B, allow_nonconvergence=False):
         import torch
         w = B.shape[0]
@@ -247,6 +316,24 @@ class Context:
         st = self.lib.randutv_small_svd(self.h, w, _ptr(B), _ld(B), _ptr(Us), _ptr(d), _ptr(Vs))
         _check("randutv_small_svd", st, allow_positive=allow_nonconvergence)
         return Us, d, Vs, st
+
+
+def pinned_colmajor(m, n):
+    """Fortran-ordered m x n float64 numpy array in pinned (page-locked) host memory."""
+    import torch
+    return torch.empty((n, m), dtype=torch.float64, pin_memory=True).numpy().T
+
+
+def _hptr(X):
+    if X is None:
+        return None
+    if not isinstance(X, np.ndarray) or X.dtype != np.float64 or X.strides[0] != 8:
+        raise ValueError("host matrices must be column-major float64 numpy arrays")
+    return ctypes.c_void_p(X.ctypes.data)
+
+
+def _hld(X):
+    return max(X.strides[1] // 8, X.shape[0], 1) if X.shape[1] > 1 else max(X.shape[0], 1)
 
 
 def randutv_factor(m, n, A, lda, b, q, seed, U, T, V):
@@ -274,3 +361,70 @@ def randutv_workspace_bytes(m, n, b, q, flags=0):
     out = ctypes.c_size_t()
     _check("randutv_workspace_bytes", lib.randutv_workspace_bytes(m, n, b, q, flags, ctypes.byref(out)))
     return out.value
+
+
+# ----------------------------------------------------------------------------- multi-GPU helpers
+
+def dist_layout(m, n, b, nranks, rank):
+    """Layout of one rank of the column-sharded path (randutv_dist_layout, host only):
+    local column count and the U / V row ranges it holds."""
+    lib = load_library()
+    out = (_i64 * 5)()
+    _check("randutv_dist_layout", lib.randutv_dist_layout(int(m), int(n), int(b), int(nranks), int(rank), out))
+    return {"ncols": out[0], "u0": out[1], "u1": out[2], "v0": out[3], "v1": out[4]}
+
+
+def local_columns(n, b, nranks, rank):
+    """Global column indices of a rank's local matrix, in local order (block-cyclic
+    by column blocks of width b: global block j on rank j mod nranks)."""
+    b = min(int(b), int(n))
+    nblocks = (n + b - 1) // b
+    cols = []
+    for j in range(rank, nblocks, nranks):
+        cols.extend(range(j * b, min(n, (j + 1) * b)))
+    return np.asarray(cols, dtype=np.int64)
+
+
+def nccl_unique_id():
+    """A fresh NCCL unique id (bytes) for randutv_comm_init."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(RANDUTV_UNIQUE_ID_BYTES)
+    _check("randutv_nccl_unique_id", lib.randutv_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _ld_or(X, default):
+    return _ld(X) if X is not None else max(int(default), 1)
+
+
+def randutv_factor_dist_loopback(A_locals, m, n, b, q, seed, U_locals=None, V_locals=None, build_uv=True, flags=0,
+                                 device=None):
+    """The sharded SPMD driver with len(A_locals) virtual ranks as host threads on one
+    GPU (collectives by device copies between host barriers): the single-GPU test
+    harness of the multi-GPU path.  A_locals are overwritten with the ranks' T columns."""
+    import torch
+    lib = load_library()
+    P = len(A_locals)
+    if device is None:
+        device = A_locals[0].device.index if A_locals[0].device.index is not None else torch.cuda.current_device()
+    if not build_uv:
+        flags |= RANDUTV_NO_UV
+    lays = [dist_layout(m, n, b, P, p) for p in range(P)]
+    if build_uv:
+        if U_locals is None:
+            U_locals = [colmajor(l["u1"] - l["u0"], m, device=f"cuda:{device}") for l in lays]
+        if V_locals is None:
+            V_locals = [colmajor(l["v1"] - l["v0"], n, device=f"cuda:{device}") for l in lays]
+    lda = max([_ld(a) for a in A_locals if a.numel() > 0] + [m])
+    for a in A_locals:
+        if a.numel() > 0 and _ld(a) != lda:
+            raise ValueError("loopback: every A_local needs the same leading dimension")
+    ldu = max([_ld(u) for u in U_locals if u.numel() > 0] + [1]) if build_uv else 1
+    ldv = max([_ld(v) for v in V_locals if v.numel() > 0] + [1]) if build_uv else 1
+    arr = lambda xs: (_vp * P)(*[x.data_ptr() if x is not None and x.numel() > 0 else None for x in xs])
+    torch.cuda.synchronize(device)
+    st = lib.randutv_factor_dist_loopback(int(device), P, int(m), int(n), arr(A_locals), lda, int(b), int(q),
+                                          int(seed) & (2**64 - 1), flags, arr(U_locals) if build_uv else None, ldu,
+                                          arr(V_locals) if build_uv else None, ldv)
+    _check("randutv_factor_dist_loopback", st)
+    return U_locals, V_locals

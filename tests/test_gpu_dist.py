@@ -1,0 +1,119 @@
+"""The column-sharded multi-GPU randUTV on one GPU.
+
+`randutv_factor_dist_loopback` runs the SAME SPMD driver as
+`randutv_factor_dist` (NCCL, one process per GPU) with P virtual ranks as host
+threads; only the four collectives differ (device copies / fixed-order sums
+between host barriers instead of NCCL).  The assembled U, T, V are checked
+against the CPU oracle with the north-star tolerances, exactly like the
+single-GPU path (tests/test_gpu_randutv.py), and against the single-GPU result.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from gpu_util import diag_parity, recon_error, spectral_orth_error, to_dev, to_np  # noqa: E402
+from oracle.randutv import randutv as oracle_randutv  # noqa: E402
+
+ELEM_TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    assert torch.cuda.is_available(), "the -m gpu tests need a CUDA device"
+    from paper_2002_06960_b200.randutv import Context
+    c = Context()
+    yield c
+    c.close()
+
+
+def shard_and_run(A, b, q, seed, P, build_uv=True):
+    import torch
+    from paper_2002_06960_b200.randutv import (colmajor, dist_layout, local_columns,
+                                               randutv_factor_dist_loopback)
+    m, n = A.shape
+    locals_ = []
+    for p in range(P):
+        cols = local_columns(n, b, P, p)
+        Al = colmajor(m, len(cols))
+        if len(cols):
+            Al.copy_(torch.from_numpy(np.ascontiguousarray(A[:, cols])))
+        locals_.append(Al)
+    Us, Vs = randutv_factor_dist_loopback(locals_, m, n, b, q, seed, build_uv=build_uv)
+    T = np.zeros((m, n), order="F")
+    for p in range(P):
+        cols = local_columns(n, b, P, p)
+        if len(cols):
+            T[:, cols] = to_np(locals_[p])
+    if not build_uv:
+        return None, T, None
+    U = np.zeros((m, m), order="F")
+    V = np.zeros((n, n), order="F")
+    for p in range(P):
+        lay = dist_layout(m, n, b, P, p)
+        if lay["u1"] > lay["u0"]:
+            U[lay["u0"]:lay["u1"], :] = to_np(Us[p])
+        if lay["v1"] > lay["v0"]:
+            V[lay["v0"]:lay["v1"], :] = to_np(Vs[p])
+    return U, T, V
+
+
+@pytest.mark.parametrize("m,n,b,q,P", [
+    (256, 256, 32, 1, 2),
+    (300, 300, 32, 2, 3),      # ragged final block, 3 ranks
+    (400, 250, 40, 1, 2),      # tall, ragged
+    (200, 200, 64, 1, 4),      # 4 blocks on 4 ranks (last ragged)
+    (96, 96, 32, 1, 4),        # fewer blocks than ranks: rank 3 holds no column
+    (129, 129, 128, 0, 2),     # final block of one column
+    (64, 40, 64, 1, 3),        # b >= n: QR + SVD only, owner 0
+    (520, 520, 64, 2, 8),      # 8 ranks
+])
+def test_dist_loopback_parity(ctx, m, n, b, q, P):
+    rng = np.random.default_rng(7 * m + n + b + 13 * P)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    U, T, V = shard_and_run(A, b, q, 31, P)
+    o = oracle_randutv(A, b, q, 31)
+    nA = np.linalg.norm(A)
+    assert recon_error(A, U, T, V) <= 1e-12
+    assert spectral_orth_error(U) <= 1e-12
+    assert spectral_orth_error(V) <= 1e-12
+    assert np.all(np.tril(T, -1) == 0.0)
+    assert diag_parity(np.diag(T), np.diag(o["T"])) <= 1.0
+    assert np.max(np.abs(np.abs(T) - np.abs(o["T"]))) / nA <= ELEM_TOL
+    assert np.max(np.abs(np.abs(U) - np.abs(o["U"]))) <= ELEM_TOL
+    assert np.max(np.abs(np.abs(V) - np.abs(o["V"]))) <= ELEM_TOL
+    # against the single-GPU path on the same A
+    Ug, Tg, Vg, _ = ctx.randutv_factor_ex(to_dev(A), b, q, 31)
+    assert np.max(np.abs(np.abs(T) - np.abs(to_np(Tg)))) / nA <= ELEM_TOL
+
+
+def test_dist_loopback_c2_shape(ctx):
+    # c2's proportions (Gaussian, b=128, q=1) at n = 1024 on 4 ranks
+    from paper_2002_06960_b200.inputs import make_numpy
+    A = make_numpy("gauss", 1024, 1024, cfg_index=2)
+    U, T, V = shard_and_run(A, 128, 1, 2002, 4)
+    o = oracle_randutv(A, 128, 1, 2002)
+    assert recon_error(A, U, T, V) <= 1e-12
+    assert spectral_orth_error(U) <= 1e-12 and spectral_orth_error(V) <= 1e-12
+    assert diag_parity(np.diag(T), np.diag(o["T"])) <= 1.0
+    assert np.max(np.abs(np.abs(T) - np.abs(o["T"]))) / np.linalg.norm(A) <= ELEM_TOL
+
+
+def test_dist_loopback_deterministic_and_no_uv(ctx):
+    rng = np.random.default_rng(5)
+    A = np.asfortranarray(rng.standard_normal((300, 260)))
+    r1 = shard_and_run(A, 32, 1, 9, 3)
+    r2 = shard_and_run(A, 32, 1, 9, 3)
+    for a, b in zip(r1, r2):
+        assert np.array_equal(a, b)
+    _, T3, _ = shard_and_run(A, 32, 1, 9, 3, build_uv=False)
+    assert np.array_equal(T3, r1[1])   # T does not depend on U, V
+
+
+def test_dist_requires_comm(ctx):
+    import ctypes
+    from paper_2002_06960_b200.randutv import RANDUTV_ERR_NOCOMM, colmajor
+    A = colmajor(8, 8)
+    st = ctx.lib.randutv_factor_dist(ctx.h, 8, 8, ctypes.c_void_p(A.data_ptr()), 8, 4, 1, 1, 1, None, 1, None, 1)
+    assert st == RANDUTV_ERR_NOCOMM
