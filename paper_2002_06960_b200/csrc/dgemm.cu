@@ -92,6 +92,13 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
   }
 }
 
+// One CTA walks the output tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
+// (tile t = (t % gm, t / gm): consecutive CTAs share the B panel in L2) for the
+// K-split blockIdx.y.  The cp.async ring runs over the flattened sequence of
+// (tile, k-tile) iterations, so the loads of the next tile's first k-tiles are
+// in flight while the current tile's epilogue (C read-modify-write) runs: with
+// a persistent grid (one wave of resident CTAs) the per-tile prologue latency
+// disappears and the epilogue overlaps the copies.
 template <class CF, bool TA, bool TB, int VA, int VB>
 __global__ void __launch_bounds__(THREADS, CF::MINB)
     dgemm_kernel(i64 M, i64 N, i64 K, double alpha, const double* __restrict__ A, i64 lda,
@@ -103,12 +110,17 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % CF::WM, wn = warp / CF::WM;
-  const i64 m0 = (i64)blockIdx.x * BM, n0 = (i64)blockIdx.y * BN;
-  const i64 kb = (i64)blockIdx.z * kchunk;
+  const i64 gm = (M + BM - 1) / BM, gn = (N + BN - 1) / BN, tiles = gm * gn;
+  const i64 kb = (i64)blockIdx.y * kchunk;
   const i64 ke = (kb + kchunk < K) ? kb + kchunk : K;
   const int ktiles = ke > kb ? (int)((ke - kb + BK - 1) / BK) : 0;
+  const i64 my_tiles = tiles > (i64)blockIdx.x ? (tiles - 1 - (i64)blockIdx.x) / gridDim.x + 1 : 0;
+  const i64 total = my_tiles * ktiles;
 
-  auto load_stage = [&](int stage, int kt) {
+  auto load_stage = [&](int stage, i64 it) {
+    const i64 tile = (i64)blockIdx.x + (it / ktiles) * gridDim.x;
+    const int kt = (int)(it % ktiles);
+    const i64 m0 = (tile % gm) * BM, n0 = (tile / gm) * BN;
     double* As = smem + stage * STAGE_ELEMS;
     double* Bs = As + A_ELEMS;
     const i64 k0 = kb + (i64)kt * BK;
@@ -124,21 +136,52 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // epilogue of one tile: lane holds C[row g][cols 2t, 2t+1] of each 8x8 tile
+  auto epilogue = [&](i64 tile) {
+    const i64 m0 = (tile % gm) * BM, n0 = (tile / gm) * BN;
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const i64 row = m0 + wm * (MI * 8) + mi * 8 + g;
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const i64 col = n0 + wn * (NI * 8) + ni * 8 + 2 * t + e;
+          if (row < M && col < N) {
+            if (part) {
+              part[(i64)blockIdx.y * M * N + row + col * M] = acc[mi][ni][e];
+            } else {
+              double* cp = C + row + col * ldc;
+              const double v = alpha * acc[mi][ni][e];
+              *cp = (beta == 0.0) ? v : v + beta * (*cp);
+            }
+          }
+          acc[mi][ni][e] = 0.0;
+        }
+      }
+    }
+  };
+
+  if (ktiles == 0) {  // empty reduction: C = beta C (or zero partials)
+    for (i64 j = 0; j < my_tiles; ++j) epilogue((i64)blockIdx.x + j * gridDim.x);
+    return;
+  }
+
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_stage(s, s);
+    if (s < total) load_stage(s, s);
     cp_async_commit();
   }
 
-  for (int kt = 0; kt < ktiles; ++kt) {
+  for (i64 it = 0; it < total; ++it) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
-      const int nk = kt + STAGES - 1;
-      if (nk < ktiles) load_stage(nk % STAGES, nk);
+      const i64 nk = it + STAGES - 1;
+      if (nk < total) load_stage((int)(nk % STAGES), nk);
       cp_async_commit();
     }
-    const double* As = smem + (kt % STAGES) * STAGE_ELEMS;
+    const double* As = smem + (int)(it % STAGES) * STAGE_ELEMS;
     const double* Bs = As + A_ELEMS;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
@@ -159,30 +202,9 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni], a[mi], b[ni]);
     }
+    if ((int)(it % ktiles) == ktiles - 1) epilogue((i64)blockIdx.x + (it / ktiles) * gridDim.x);
   }
   cp_async_wait<0>();
-
-  // epilogue: lane holds C[row g][cols 2t, 2t+1] of each 8x8 tile
-#pragma unroll
-  for (int mi = 0; mi < MI; ++mi) {
-    const i64 row = m0 + wm * (MI * 8) + mi * 8 + g;
-    if (row >= M) continue;
-#pragma unroll
-    for (int ni = 0; ni < NI; ++ni) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const i64 col = n0 + wn * (NI * 8) + ni * 8 + 2 * t + e;
-        if (col >= N) continue;
-        if (part) {
-          part[(i64)blockIdx.z * M * N + row + col * M] = acc[mi][ni][e];
-        } else {
-          double* cp = C + row + col * ldc;
-          const double v = alpha * acc[mi][ni][e];
-          *cp = (beta == 0.0) ? v : v + beta * (*cp);
-        }
-      }
-    }
-  }
 }
 
 __global__ void splitk_reduce_kernel(i64 M, i64 N, int splits, double alpha, const double* __restrict__ part,
@@ -252,6 +274,16 @@ int choose_cfg(i64 M, i64 N, i64 K) {
   return 1;
 }
 
+// RUTV_GEMM_PERSIST=0 launches one CTA per tile (tuning comparison only)
+bool persistent_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_GEMM_PERSIST");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 inline int vec_of(const double* p, i64 ld) {
   return (((uintptr_t)p & 15) == 0 && (ld % 2) == 0) ? 2 : 1;
 }
@@ -264,7 +296,6 @@ int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double 
   const int cfg = choose_cfg(M, N, K);
   const i64 BM = 128, BN = cfg == 1 ? 64 : 128;
   const i64 gm = (M + BM - 1) / BM, gn = (N + BN - 1) / BN;
-  if (gn > 65535) return -5;
   const i64 tiles = gm * gn;
   i64 splits = 1;
   const i64 target = (cfg == 1 ? 4 : 2) * (i64)L.device_sms;
@@ -285,7 +316,11 @@ int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double 
   if (kchunk <= 0) kchunk = 1;
   const int va = vec_of(A, lda), vb = vec_of(B, ldb);
   const size_t pe = L.pbegin();
-  dim3 grid((unsigned)gm, (unsigned)gn, (unsigned)splits);
+  // persistent grid: at most one wave of resident CTAs per split
+  const i64 resident = (i64)(cfg == 1 ? 2 : 1) * L.device_sms;
+  i64 ctas = tiles;
+  if (persistent_on() && splits == 1 && ctas > resident) ctas = resident;
+  dim3 grid((unsigned)ctas, (unsigned)splits, 1);
   double* part = splits > 1 ? ws : nullptr;
   const int st = cfg == 1
                      ? launch_cfg<CfgHalf>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part)

@@ -49,6 +49,24 @@ def gemm_cases(ctx):
         del A, B, C
 
 
+def gemm_diag(ctx):
+    """Separates main-loop from per-tile (prologue + epilogue) cost of the rank-b update."""
+    M = N = 16384
+    for K in (64, 128, 256, 512, 1024, 2048):
+        for beta in (0.0, 1.0):
+            A = colmajor(M, K)
+            B = colmajor(N, K)
+            C = colmajor(M, N)
+            A.normal_()
+            B.normal_()
+            C.normal_()
+            p = timed(ctx, lambda: ctx.randutv_dgemm(0, 1, A, B, C, alpha=-1.0, beta=beta), "dgemm")
+            ms = p["ms"] / 5
+            print(json.dumps({"kernel": "dgemm_diag", "M": M, "N": N, "K": K, "beta": beta, "ms": round(ms, 4),
+                              "tflops": round(2 * M * N * K / (ms * 1e-3) / 1e12, 3)}))
+            del A, B, C
+
+
 def qr_cases(ctx):
     for h, w in [(16384, 256), (65536, 512), (4096, 128)]:
         P0 = colmajor(h, w)
@@ -92,6 +110,8 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["gemm", "qr", "svd"]
     if "gemm" in which:
         gemm_cases(ctx)
+    if "gemmdiag" in which:
+        gemm_diag(ctx)
     if "qr" in which:
         qr_cases(ctx)
     if "svd" in which:
