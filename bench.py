@@ -40,7 +40,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c5"])
+    p.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -123,25 +123,65 @@ def fp64_peak():
         return 37.2, "nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz (measurement file missing)"
 
 
+SAMPLE_FLOPS = 6e11  # ~20 s of the numpy oracle on a 16-32 core host
+
+
+def sample_shape(cfg_name):
+    """Leading m_s x n_s block of the config (its aspect ratio, b and q) whose first
+    sampled step costs about SAMPLE_FLOPS under the flop model."""
+    from paper_2002_06960_b200.flops import randutv_flops
+    from paper_2002_06960_b200.inputs import CONFIGS
+    c = CONFIGS[cfg_name]
+    m, n, b, q = c["m"], c["n"], c["b"], c["q"]
+    f = 1.0
+    while True:
+        ms, ns = max(int(m * f) // b * b, 2 * b), max(int(n * f) // b * b, 2 * b)
+        if randutv_flops(ms, ns, b, q, build_uv=True, k=b) <= SAMPLE_FLOPS or ns <= 2 * b:
+            return ms, ns
+        f *= 0.9
+
+
 def cpu_sample(cfg_name, A_host, seed):
-    """The oracle (as it stands) on a bounded sample: the first sampled step of the
-    config (truncated k = b, thin U), timed on this host's cores."""
+    """The oracle (as it stands) on a bounded sample of the workload: the first
+    sampled step (truncated k = b, thin U) of the config's leading m_s x n_s block,
+    timed on this host's cores."""
     from threadpoolctl import threadpool_info
 
     from oracle.randutv import randutv as oracle_randutv
     from paper_2002_06960_b200.flops import randutv_flops
     from paper_2002_06960_b200.inputs import CONFIGS
     c = CONFIGS[cfg_name]
-    m, n, b, q = c["m"], c["n"], c["b"], c["q"]
+    b, q = c["b"], c["q"]
+    import numpy as np
+    ms, ns = sample_shape(cfg_name)
+    As = np.asfortranarray(A_host[:ms, :ns])
     t0 = time.perf_counter()
-    oracle_randutv(A_host, b, q, seed, k=b, thin_u=True)
+    oracle_randutv(As, b, q, seed, k=b, thin_u=True)
     dt = time.perf_counter() - t0
-    F = randutv_flops(m, n, b, q, build_uv=True, k=b)
+    F = randutv_flops(ms, ns, b, q, build_uv=True, k=b)
     threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     return {"value": F / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
-            "sample": f"{cfg_name}: first sampled step only (truncated k=b={b}, q={q}, V + thin U_k), "
-                      f"{F:.3g} flops in {dt:.1f} s (numpy/OpenBLAS, {threads} threads, {os.cpu_count()} host cpus)",
+            "sample": f"{cfg_name}: first sampled step (truncated k=b={b}, q={q}, V + thin U_k) of the leading "
+                      f"{ms}x{ns} block, {F:.3g} flops in {dt:.1f} s (numpy/OpenBLAS, {threads} threads, "
+                      f"{os.cpu_count()} host cpus)",
             "seconds": dt, "flops": F}
+
+
+def config_dict(name, ws):
+    """The workload description shared by both arms."""
+    from paper_2002_06960_b200.flops import randutv_flops
+    from paper_2002_06960_b200.inputs import CONFIGS
+    c = CONFIGS[name]
+    m, n, b, q = c["m"], c["n"], c["b"], c["q"]
+    k = c.get("k") if not c.get("full", True) else None
+    return {"workload": f"{name}: " + {
+        "c1": "n=512 known spectrum", "c2": "n=4096 Gaussian", "c3": "n=16384 exp spectrum",
+        "c4": "262144x8192 low-rank + noise", "c5": "n=65536 Gaussian"}[name]
+        + f", b={b}, q={q}, " + (f"truncated rank-{k} randUTV (U_k, T_k, V)" if k else "full randUTV with U and V"),
+        "m": m, "n": n, "b": b, "q": q, "flops_per_step": randutv_flops(m, n, b, q, build_uv=True, k=k),
+        "parallelism": f"column-sharded x{ws} (1-D block-cyclic, NCCL)" if ws > 1 else "single",
+        "l2": "inputs larger than L2 (A is %.2f GB, L2 126 MB); no flush" % (8 * m * n / 1e9)
+        if 8 * m * n > 126e6 else "input fits L2: not flushed"}
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -152,9 +192,12 @@ def run_reference(args):
         return 0
     import numpy as np
 
-    from paper_2002_06960_b200.inputs import CONFIGS, make_config_numpy
+    from paper_2002_06960_b200.inputs import CONFIGS, make_numpy
     cfg = CONFIGS[args.config]
-    A = make_config_numpy(args.config)
+    # the config's recipe (kind, seeds) at the bounded sample size: a leading
+    # block of the full matrix would need its n x n Haar factors on the host
+    ms, ns = sample_shape(args.config)
+    A = make_numpy(cfg["kind"], ms, ns, cfg_index=int(args.config[1:]))
     seed = 2000 + int(args.config[1:])
     times = []
     cs = None
@@ -168,8 +211,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} sample: first sampled step", "m": cfg["m"], "n": cfg["n"],
-                       "b": cfg["b"], "q": cfg["q"]},
+            "config": config_dict(args.config, ws),
             "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cs["cores"], "kind": "oracle",
                              "sample": cs["sample"]},
             "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -198,7 +240,8 @@ def run_ours(args):
     cfg = CONFIGS[args.config]
     m, n, b, q = cfg["m"], cfg["n"], cfg["b"], cfg["q"]
     seed = 2000 + int(args.config[1:])
-    F = randutv_flops(m, n, b, q, build_uv=True)
+    trunc_k = cfg.get("k") if not cfg.get("full", True) else None
+    F = randutv_flops(m, n, b, q, build_uv=True, k=trunc_k)
 
     A = make_config_torch(args.config, device=f"cuda:{dev}")
     stream = torch.cuda.Stream()
@@ -221,6 +264,12 @@ def run_ours(args):
         def step():
             T_loc.copy_(A_loc)
             ctx.randutv_factor_dist(T_loc, m, n, b, q, seed, U_local=U_loc, V_local=V_loc)
+    elif trunc_k is not None:
+        if ws > 1:
+            raise SystemExit("the truncated config runs on one GPU (the sharded path is full-factorisation only)")
+
+        def step():
+            ctx.randutv_factor_rank(A, trunc_k, b, q, seed)
     else:
         T = colmajor(m, n)
         U = colmajor(m, m)
@@ -305,7 +354,7 @@ def run_ours(args):
         e2e = {"value": F * e2e_steps / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(bi.item()),
                "d2h_bytes_per_step": int(bo.item()), "steps": e2e_steps, "ms_per_step": dt / e2e_steps * 1e3,
                "api": "randutv_factor_dist (pinned host shards)"}
-    elif not args.no_e2e:
+    elif not args.no_e2e and trunc_k is None:
         # the literal C-ABI entry on pinned host buffers, copies inside the timed region
         Ah = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         Ah.copy_(A.t())
@@ -328,7 +377,8 @@ def run_ours(args):
     # ---- CPU baseline: the oracle on a bounded sample, rank 0, N = 1 only
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        A_host = np.asfortranarray(A.t().cpu().numpy().T)
+        ms, ns = sample_shape(args.config)
+        A_host = np.asfortranarray(A[:ms, :ns].cpu().numpy())
         cpu = cpu_sample(args.config, A_host, seed)
         cpu = {k: v for k, v in cpu.items() if k not in ("seconds", "flops")}
 
@@ -358,13 +408,7 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: " + {
-                "c1": "n=512 known spectrum", "c2": "n=4096 Gaussian", "c3": "n=16384 exp spectrum",
-                "c5": "n=65536 Gaussian"}[args.config] + f", b={b}, q={q}, full randUTV with U and V",
-                "m": m, "n": n, "b": b, "q": q, "flops_per_step": F,
-                "parallelism": f"column-sharded x{ws} (1-D block-cyclic, NCCL)" if ws > 1 else "single",
-                "l2": "inputs larger than L2 (A is %.2f GB, L2 126 MB); no flush" % (8 * m * n / 1e9)
-                if 8 * m * n > 126e6 else "input fits L2: not flushed"},
+            "config": config_dict(args.config, ws),
             "t_over_n3_x1e10": ms_step * 1e-3 / float(n) ** 3 * 1e10,
             "frac_of_fp64_peak": round(value / ws / 1e3 / peak, 4),   # of N x per-GPU peak
             "gpu_launches": stats["kernel_launches"],

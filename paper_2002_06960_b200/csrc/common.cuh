@@ -51,6 +51,9 @@ struct Launch {
   int64_t* counter;  // incremented per kernel launch
   int device_sms;
   Profiler* prof = nullptr;
+  // two device ints (tile counter, finished-CTA counter) private to this
+  // stream: the persistent GEMM's dynamic tile scheduler (null: static tiles)
+  int* sched = nullptr;
   void count(int n = 1) const {
     if (counter) *counter += n;
   }

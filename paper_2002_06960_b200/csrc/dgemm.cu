@@ -92,34 +92,43 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
   }
 }
 
-// One CTA walks the output tiles t = blockIdx.x, blockIdx.x + gridDim.x, ...
-// (tile t = (t % gm, t / gm): consecutive CTAs share the B panel in L2) for the
-// K-split blockIdx.y.  The cp.async ring runs over the flattened sequence of
-// (tile, k-tile) iterations, so the loads of the next tile's first k-tiles are
-// in flight while the current tile's epilogue (C read-modify-write) runs: with
-// a persistent grid (one wave of resident CTAs) the per-tile prologue latency
-// disappears and the epilogue overlaps the copies.
+// Persistent tile loop.  The work items are w = 0 .. tiles*splits-1 (tile
+// w % tiles = (t % gm, t / gm), K-split w / tiles; consecutive items share the
+// B panel in L2).  With `sched` (two device ints, zero between launches) the
+// CTAs claim items dynamically with atomicAdd -- CTAs that become resident late
+// (e.g. while the side stream's Jacobi SVD holds SMs) simply take fewer items,
+// so the grid never waits on a straggler; the last CTA to finish re-zeroes the
+// counters for the next launch on the stream.  Without it, CTA c takes items
+// c, c + gridDim.x, ...  The cp.async ring runs over the flattened sequence of
+// (item, k-tile) iterations, so the next item's first k-tiles are loading
+// while the current item's epilogue (C read-modify-write) runs.
+constexpr int RING = 8;  // in-flight item ids (>= STAGES + 1)
+
 template <class CF, bool TA, bool TB, int VA, int VB>
 __global__ void __launch_bounds__(THREADS, CF::MINB)
     dgemm_kernel(i64 M, i64 N, i64 K, double alpha, const double* __restrict__ A, i64 lda,
                  const double* __restrict__ B, i64 ldb, double beta, double* __restrict__ C, i64 ldc,
-                 i64 kchunk, double* __restrict__ part) {
+                 i64 kchunk, int splits, double* __restrict__ part, int* __restrict__ sched) {
   constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, MI = CF::MI, NI = CF::NI;
   constexpr int A_ELEMS = CF::A_ELEMS, STAGE_ELEMS = CF::STAGE_ELEMS;
   extern __shared__ __align__(16) double smem[];
+  __shared__ i64 ring[RING];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % CF::WM, wn = warp / CF::WM;
   const i64 gm = (M + BM - 1) / BM, gn = (N + BN - 1) / BN, tiles = gm * gn;
-  const i64 kb = (i64)blockIdx.y * kchunk;
-  const i64 ke = (kb + kchunk < K) ? kb + kchunk : K;
-  const int ktiles = ke > kb ? (int)((ke - kb + BK - 1) / BK) : 0;
-  const i64 my_tiles = tiles > (i64)blockIdx.x ? (tiles - 1 - (i64)blockIdx.x) / gridDim.x + 1 : 0;
-  const i64 total = my_tiles * ktiles;
+  const i64 items = tiles * splits;
+  const int ktiles = (int)((kchunk + BK - 1) / BK);  // every split has kchunk (last: ragged, masked)
 
-  auto load_stage = [&](int stage, i64 it) {
-    const i64 tile = (i64)blockIdx.x + (it / ktiles) * gridDim.x;
-    const int kt = (int)(it % ktiles);
+  // item id of sequence number `seq` of this CTA (thread 0 only)
+  auto claim = [&](i64 seq) -> i64 {
+    if (sched) return (i64)atomicAdd(sched, 1);
+    return (i64)blockIdx.x + seq * gridDim.x;
+  };
+
+  auto load_stage = [&](int stage, i64 item, int kt) {
+    const i64 tile = item % tiles, split = item / tiles;
+    const i64 kb = split * kchunk, ke = (kb + kchunk < K) ? kb + kchunk : K;
     const i64 m0 = (tile % gm) * BM, n0 = (tile / gm) * BN;
     double* As = smem + stage * STAGE_ELEMS;
     double* Bs = As + A_ELEMS;
@@ -136,8 +145,9 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // epilogue of one tile: lane holds C[row g][cols 2t, 2t+1] of each 8x8 tile
-  auto epilogue = [&](i64 tile) {
+  // epilogue of one item: lane holds C[row g][cols 2t, 2t+1] of each 8x8 tile
+  auto epilogue = [&](i64 item) {
+    const i64 tile = item % tiles, split = item / tiles;
     const i64 m0 = (tile % gm) * BM, n0 = (tile / gm) * BN;
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
@@ -149,7 +159,7 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
           const i64 col = n0 + wn * (NI * 8) + ni * 8 + 2 * t + e;
           if (row < M && col < N) {
             if (part) {
-              part[(i64)blockIdx.y * M * N + row + col * M] = acc[mi][ni][e];
+              part[split * M * N + row + col * M] = acc[mi][ni][e];
             } else {
               double* cp = C + row + col * ldc;
               const double v = alpha * acc[mi][ni][e];
@@ -162,24 +172,41 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
     }
   };
 
-  if (ktiles == 0) {  // empty reduction: C = beta C (or zero partials)
-    for (i64 j = 0; j < my_tiles; ++j) epilogue((i64)blockIdx.x + j * gridDim.x);
+  if (ktiles == 0) {  // K == 0: C = beta C
+    for (i64 w = blockIdx.x; w < items; w += gridDim.x) epilogue(w);
     return;
   }
 
+  // item ids for the loads of iterations 0 .. STAGES-1
+  const int pre = (STAGES - 1) / ktiles + 1;  // sequence numbers 0 .. pre-1
+  if (tid == 0)
+    for (int q = 0; q < pre; ++q) ring[q % RING] = claim(q);
+  i64 claimed = pre;
+  __syncthreads();
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < total) load_stage(s, s);
+    const i64 item = ring[(s / ktiles) % RING];
+    if (item < items) load_stage(s, item, s % ktiles);
     cp_async_commit();
   }
 
-  for (i64 it = 0; it < total; ++it) {
+  for (i64 it = 0;; ++it) {
+    const i64 item = ring[(it / ktiles) % RING];
+    if (item >= items) break;
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
       const i64 nk = it + STAGES - 1;
-      if (nk < total) load_stage((int)(nk % STAGES), nk);
+      const i64 nitem = ring[(nk / ktiles) % RING];
+      if (nitem < items) load_stage((int)(nk % STAGES), nitem, (int)(nk % ktiles));
       cp_async_commit();
+      // the next iteration's load may start a new sequence number: claim it now
+      // (published by that iteration's barrier)
+      const i64 nseq = (nk + 1) / ktiles;
+      if (nseq >= claimed) {
+        if (tid == 0) ring[nseq % RING] = (nitem < items) ? claim(nseq) : items;
+        claimed = nseq + 1;
+      }
     }
     const double* As = smem + (int)(it % STAGES) * STAGE_ELEMS;
     const double* Bs = As + A_ELEMS;
@@ -202,9 +229,21 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
 #pragma unroll
         for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni], a[mi], b[ni]);
     }
-    if ((int)(it % ktiles) == ktiles - 1) epilogue((i64)blockIdx.x + (it / ktiles) * gridDim.x);
+    if ((int)(it % ktiles) == ktiles - 1) epilogue(item);
   }
   cp_async_wait<0>();
+  if (sched) {
+    __syncthreads();
+    if (tid == 0) {
+      // every claim of this launch happened-before this CTA's arrival
+      __threadfence();
+      if (atomicAdd(sched + 1, 1) == (int)gridDim.x - 1) {
+        sched[0] = 0;
+        sched[1] = 0;
+        __threadfence();
+      }
+    }
+  }
 }
 
 __global__ void splitk_reduce_kernel(i64 M, i64 N, int splits, double alpha, const double* __restrict__ part,
@@ -220,9 +259,20 @@ __global__ void splitk_reduce_kernel(i64 M, i64 N, int splits, double alpha, con
   }
 }
 
+// RUTV_GEMM_SCHED=0 disables the dynamic tile scheduler (static item order)
+bool use_sched(const Launch& L) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_GEMM_SCHED");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0 && L.sched != nullptr;
+}
+
 template <class CF, bool TA, bool TB, int VA, int VB>
 int launch_t(const Launch& L, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
              i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
+  const int splits = (int)((K + kchunk - 1) / (kchunk > 0 ? kchunk : 1));
   static bool attr_set = false;  // per instantiation; first call from any ctx
   if (!attr_set) {
     RUTV_CUDA(cudaFuncSetAttribute(dgemm_kernel<CF, TA, TB, VA, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -230,7 +280,8 @@ int launch_t(const Launch& L, i64 M, i64 N, i64 K, double alpha, const double* A
     attr_set = true;
   }
   dgemm_kernel<CF, TA, TB, VA, VB><<<grid, THREADS, CF::SMEM_BYTES, L.stream>>>(M, N, K, alpha, A, lda, B, ldb,
-                                                                               beta, C, ldc, kchunk, part);
+                                                                               beta, C, ldc, kchunk, splits < 1 ? 1 : splits, part,
+                                                                               use_sched(L) ? L.sched : nullptr);
   L.count();
   RUTV_CHECK_LAUNCH("dgemm_kernel");
   return 0;
@@ -316,11 +367,11 @@ int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double 
   if (kchunk <= 0) kchunk = 1;
   const int va = vec_of(A, lda), vb = vec_of(B, ldb);
   const size_t pe = L.pbegin();
-  // persistent grid: at most one wave of resident CTAs per split
+  // persistent grid: at most one wave of resident CTAs over all tiles x splits
   const i64 resident = (i64)(cfg == 1 ? 2 : 1) * L.device_sms;
-  i64 ctas = tiles;
-  if (persistent_on() && splits == 1 && ctas > resident) ctas = resident;
-  dim3 grid((unsigned)ctas, (unsigned)splits, 1);
+  i64 ctas = tiles * splits;
+  if (persistent_on() && ctas > resident) ctas = resident;
+  dim3 grid((unsigned)ctas, 1, 1);
   double* part = splits > 1 ? ws : nullptr;
   const int st = cfg == 1
                      ? launch_cfg<CfgHalf>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part)

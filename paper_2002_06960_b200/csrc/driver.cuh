@@ -26,8 +26,10 @@ struct randutv_ctx {
   // multi-GPU communicators (randutv_comm_init): main-stream and side-stream
   rutv::Comm* comm;
   rutv::Comm* comm_side;
-  rutv::Launch launch() { return rutv::Launch{stream, &stats.kernel_launches, sms, &prof}; }
-  rutv::Launch side_launch() { return rutv::Launch{side, &stats.kernel_launches, sms, &prof}; }
+  // GEMM tile-scheduler counters: [0..1] main stream, [2..3] side stream (zeroed once)
+  int* sched;
+  rutv::Launch launch() { return rutv::Launch{stream, &stats.kernel_launches, sms, &prof, sched}; }
+  rutv::Launch side_launch() { return rutv::Launch{side, &stats.kernel_launches, sms, &prof, sched ? sched + 2 : nullptr}; }
 };
 
 namespace rutv {

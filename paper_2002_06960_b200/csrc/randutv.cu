@@ -399,6 +399,10 @@ RANDUTV_API int randutv_create(randutv_ctx** out, int device, void* stream) {
   c->device = device;
   c->stream = (cudaStream_t)stream;
   c->sms = sms;
+  if (cudaMalloc(&c->sched, 4 * sizeof(int)) != cudaSuccess || cudaMemset(c->sched, 0, 4 * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    c->sched = nullptr;  // static tile order
+  }
   *out = c;
   return 0;
 }
@@ -410,6 +414,7 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
   if (ctx->side) cudaStreamSynchronize(ctx->side);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->stage) cudaFree(ctx->stage);
+  if (ctx->sched) cudaFree(ctx->sched);
   rutv::comm_free(ctx->comm_side);
   rutv::comm_free(ctx->comm);
   ctx->comm = ctx->comm_side = nullptr;
