@@ -63,6 +63,8 @@ struct Work {
   i64 lefts_elems;
   double* Twork;  // m x n working T for the truncated variant
   double* Zf;     // fold temporaries of the side stream (max(m,n) x b)
+  double* Acat;   // fused S5/S7 update operands: [Z2(k:m) | W_U]  (m x 2b)
+  double* Bt;     //                              [W2 | Y^T]       (n x 2b)
 };
 
 i64 gemm_ws_elems_for(i64 m, i64 n, i64 b);
