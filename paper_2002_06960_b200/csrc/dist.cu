@@ -439,7 +439,9 @@ int dist_sampled_step(DistRun& R, i64 i) {
   L.count();
   RUTV_CHECK_LAUNCH("cyclic_gather_rows_kernel");
   RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
-  // S5: T(:, k:n) -= (T W_V) T_V W_V^T -- wait for the previous step's U_s^T A12 fold
+  // S5 for the V rows first (every rank holds all of W_V; V is not touched by the folds of T)
+  if (R.P.V) RUTV_TRY(apply_right(L, w, R.P.nv, s, b, R.P.V + k * R.P.ldv, R.P.ldv, w.Wv, s, w.TV, b));
+  // S5 for T: Z2 = (T W_V) T_V (AllReduce) -- wait for the previous step's U_s^T A12 fold
   RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eF, 0));
   if (sl > 0) {
     cyclic_scatter_rows_kernel<<<grid_for(L, sl * b), 256, 0, st>>>(sl, b, k, b, P, p, lay.lb_before(p, i), w.Wv, s,
@@ -451,8 +453,10 @@ int dist_sampled_step(DistRun& R, i64 i) {
                         w.gemm_ws_elems));
   RUTV_TRY(R.comm->allreduce_sum(w.Z, m * b, st));
   RUTV_TRY(launch_dgemm(L, false, false, m, b, b, 1.0, w.Z, m, w.TV, b, 0.0, w.Z2, m, nullptr, 0));
-  RUTV_TRY(launch_dgemm(L, false, true, m, sl, b, -1.0, w.Z2, m, R.d.Wl, maxs, 1.0, Ap, lda, nullptr, 0));
-  if (R.P.V) RUTV_TRY(apply_right(L, w, R.P.nv, s, b, R.P.V + k * R.P.ldv, R.P.ldv, w.Wv, s, w.TV, b));
+  const bool fuse = fuse_left();
+  // (unfused: the S5 update of every trailing column now; fused: of block i only)
+  RUTV_TRY(launch_dgemm(L, false, true, m, fuse ? (p == o ? b : 0) : sl, b, -1.0, w.Z2, m, R.d.Wl, maxs, 1.0, Ap,
+                        lda, nullptr, 0));
   // S6: QR of column block i on its owner, broadcast (W_U, T_U)
   double* Wu = R.d.wbuf;
   double* TU = R.d.wbuf + r * b;
@@ -462,9 +466,13 @@ int dist_sampled_step(DistRun& R, i64 i) {
     RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, lda));
   }
   RUTV_TRY(R.comm->bcast(R.d.wbuf, r * b + b * b, o, st));
-  // S7: columns right of block i; U rows
+  // S7 (fused with the rest of S5 when enabled): columns right of block i; U rows
   const i64 c1 = lay.lcol(p, i + 1);
-  RUTV_TRY(apply_left_t(L, w, r, lay.ncols(p) - c1, b, R.P.A + k + c1 * lda, lda, Wu, r, TU, b));
+  if (fuse)
+    RUTV_TRY(fused_right_left(L, w, m, r, b, k, lay.ncols(p) - c1, R.P.A + c1 * lda, lda, R.d.Wl + (c1 - c0), maxs,
+                              w.Z2, m, Wu, r, TU, b));
+  else
+    RUTV_TRY(apply_left_t(L, w, r, lay.ncols(p) - c1, b, R.P.A + k + c1 * lda, lda, Wu, r, TU, b));
   if (R.P.U) RUTV_TRY(apply_right(L, w, R.P.mu, r, b, R.P.U + k * R.P.ldu, R.P.ldu, Wu, r, TU, b));
   // S8, S9 on the side stream / side communicator
   RUTV_CUDA(cudaEventRecord(R.ctx->eR, st));

@@ -210,6 +210,53 @@ int left_mult_t_inplace(const Launch& L, double* Zt, i64 bw, i64 cols, double* X
   return launch_copy(L, bw, cols, Zt, bw, X, ldx);
 }
 
+// The S5 right update of the columns right of block i and the S7 left update
+// as ONE rank-2b update of T (same algebra, P:1333-1336 then P:1348-1350):
+// with X = T(:, cols right of block i) before S5, W2 = the rows of W_V for
+// those columns and Z2 = (T W_V) T_V,
+//   X'  = X - Z2 W2^T                              (S5)
+//   X'' = X' - W_U T_U^T W_U^T X'(k:m)   rows k:m   (S7)
+// and W_U^T X' = W_U^T X - (W_U^T Z2(k:m)) W2^T, so with
+//   Y^T = (X(k:m)^T W_U - W2 (Z2(k:m)^T W_U)) T_U        (c x b)
+//   X(0:k)  -= Z2(0:k) W2^T                               (K = b)
+//   X(k:m)  -= [Z2(k:m) | W_U] [W2 | Y^T]^T               (K = 2b)
+// one read pass (X^T W_U) and one read-modify-write pass replace the two
+// read-modify-write passes and one read pass of the unfused form.
+// Temporaries: w.Z (c x b), w.Bt, w.Acat.
+int fused_right_left(const Launch& L, Work& w, i64 m, i64 r, i64 b, i64 kk, i64 c, double* X, i64 ldx,
+                     const double* W2, i64 ldw2, const double* Z2, i64 ldz, const double* Wu, i64 ldwu,
+                     const double* TU, i64 ldtu) {
+  (void)m;
+  if (c <= 0) return 0;
+  double* Ytr = w.Bt + c * b;  // second half of Bt: Y^T (c x b, ld c)
+  // Pt = X(k:m)^T W_U  (c x b, K = r) -> w.Z (ld c)
+  RUTV_TRY(launch_dgemm(L, true, false, c, b, r, 1.0, X + kk, ldx, Wu, ldwu, 0.0, w.Z, c, w.gemm_ws,
+                        w.gemm_ws_elems));
+  // Qt = Z2(k:m)^T W_U (b x b; scratch in Bt's first half), then Pt -= W2 Qt
+  RUTV_TRY(launch_dgemm(L, true, false, b, b, r, 1.0, Z2 + kk, ldz, Wu, ldwu, 0.0, w.Bt, b, w.gemm_ws,
+                        w.gemm_ws_elems));
+  RUTV_TRY(launch_dgemm(L, false, false, c, b, b, -1.0, W2, ldw2, w.Bt, b, 1.0, w.Z, c, nullptr, 0));
+  // Y^T = Pt T_U
+  RUTV_TRY(launch_dgemm(L, false, false, c, b, b, 1.0, w.Z, c, TU, ldtu, 0.0, Ytr, c, nullptr, 0));
+  // Bt(:, 0:b) = W2 ; Acat = [Z2(k:m) | W_U]
+  RUTV_TRY(launch_copy(L, c, b, W2, ldw2, w.Bt, c));
+  RUTV_TRY(launch_copy(L, r, b, Z2 + kk, ldz, w.Acat, r));
+  RUTV_TRY(launch_copy(L, r, b, Wu, ldwu, w.Acat + r * b, r));
+  // X(0:k) -= Z2(0:k) W2^T ; X(k:m) -= Acat Bt^T
+  if (kk > 0) RUTV_TRY(launch_dgemm(L, false, true, kk, c, b, -1.0, Z2, ldz, W2, ldw2, 1.0, X, ldx, nullptr, 0));
+  return launch_dgemm(L, false, true, r, c, 2 * b, -1.0, w.Acat, r, w.Bt, c, 1.0, X + kk, ldx, nullptr, 0);
+}
+
+// RUTV_FUSE_LEFT=0 restores the separate S5 / S7 passes over T (comparison only)
+bool fuse_left() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_FUSE_LEFT");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 }  // namespace rutv
 
 namespace {
@@ -273,41 +320,6 @@ bool fuse_left() {
   return v != 0;
 }
 
-// The S5 right update of the columns right of block i and the S7 left update
-// as ONE rank-2b update of T (same algebra, P:1333-1336 then P:1348-1350):
-// with X = T(:, k+b:n) before S5, W2 = W_V(b:s, :) and Z2 = (T W_V) T_V,
-//   X'  = X - Z2 W2^T                              (S5)
-//   X'' = X' - W_U T_U^T W_U^T X'(k:m)   rows k:m   (S7)
-// and W_U^T X' = W_U^T X - (W_U^T Z2(k:m)) W2^T, so with
-//   Y^T = (X(k:m)^T W_U - W2 (Z2(k:m)^T W_U)) T_U        ((s-b) x b)
-//   X(0:k)  -= Z2(0:k) W2^T                               (K = b)
-//   X(k:m)  -= [Z2(k:m) | W_U] [W2 | Y^T]^T               (K = 2b)
-// one read pass (X^T W_U) and one read-modify-write pass replace the two
-// read-modify-write passes and one read pass of the unfused form.
-int fused_right_left(const Launch& L, Work& w, const Problem& P, i64 kk, i64 r, i64 s) {
-  const i64 m = P.m, b = P.b, c = s - b;
-  if (c <= 0) return 0;
-  double* X = P.T + (kk + b) * P.ldt;  // T(0:m, k+b:n), ld ldt
-  const double* W2 = w.Wv + b;         // rows b..s of W_V, ld s
-  double* Ytr = w.Bt + c * b;          // second half of Bt: Y^T ((s-b) x b, ld c)
-  // Pt = X(k:m)^T W_U   ((s-b) x b, K = r)  -> w.Z (ld c)
-  RUTV_TRY(launch_dgemm(L, true, false, c, b, r, 1.0, X + kk, P.ldt, w.Wu, r, 0.0, w.Z, c, w.gemm_ws,
-                        w.gemm_ws_elems));
-  // Qt = Z2(k:m)^T W_U  (b x b) -> w.Bt first half as scratch, then Pt -= W2 Qt
-  RUTV_TRY(launch_dgemm(L, true, false, b, b, r, 1.0, w.Z2 + kk, m, w.Wu, r, 0.0, w.Bt, b, w.gemm_ws,
-                        w.gemm_ws_elems));
-  RUTV_TRY(launch_dgemm(L, false, false, c, b, b, -1.0, W2, s, w.Bt, b, 1.0, w.Z, c, nullptr, 0));
-  // Y^T = Pt T_U
-  RUTV_TRY(launch_dgemm(L, false, false, c, b, b, 1.0, w.Z, c, w.TU, b, 0.0, Ytr, c, nullptr, 0));
-  // Bt(:, 0:b) = W2 ; Acat = [Z2(k:m) | W_U]
-  RUTV_TRY(launch_copy(L, c, b, W2, s, w.Bt, c));
-  RUTV_TRY(launch_copy(L, r, b, w.Z2 + kk, m, w.Acat, r));
-  RUTV_TRY(launch_copy(L, r, b, w.Wu, r, w.Acat + r * b, r));
-  // X(0:k) -= Z2(0:k) W2^T ; X(k:m) -= Acat Bt^T
-  if (kk > 0) RUTV_TRY(launch_dgemm(L, false, true, kk, c, b, -1.0, w.Z2, m, W2, s, 1.0, X, P.ldt, nullptr, 0));
-  return launch_dgemm(L, false, true, r, c, 2 * b, -1.0, w.Acat, r, w.Bt, c, 1.0, X + kk, P.ldt, nullptr, 0);
-}
-
 int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   const i64 m = P.m, n = P.n, b = P.b, kk = i * b, r = m - kk, s = n - kk;
   double* At = P.T + kk + kk * P.ldt;
@@ -345,7 +357,8 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
     RUTV_TRY(panel_qr(L, r, b, At, P.ldt, w.tauU, w.Wu, r, w.TU, b, w.qw));
     RUTV_TRY(launch_triu(L, b, b, At, P.ldt));
     RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, P.ldt));
-    RUTV_TRY(fused_right_left(L, w, P, kk, r, s));
+    RUTV_TRY(fused_right_left(L, w, m, r, b, kk, s - b, P.T + (kk + b) * P.ldt, P.ldt, w.Wv + b, s, w.Z2, m, w.Wu, r,
+                              w.TU, b));
   }
   if (P.U) RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
   if (P.record_lefts) RUTV_TRY(record_left_w(L, w, P, (int)i, r, b));

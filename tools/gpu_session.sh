@@ -12,6 +12,18 @@ for stage in "$@"; do
       python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log ;;
     bench)
       timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err ;;
+    kernels)
+      for v in "RUTV_GEMM_PERSIST=1 RUTV_GEMM_SCHED=1" "RUTV_GEMM_PERSIST=1 RUTV_GEMM_SCHED=0" "RUTV_GEMM_PERSIST=0"; do
+        echo "== $v" >> gpurun_out/kernels.log
+        env $v timeout 600 python tools/bench_kernels.py gemm gemmdiag >> gpurun_out/kernels.log 2>&1
+      done
+      timeout 600 python tools/bench_kernels.py qr svd >> gpurun_out/kernels.log 2>&1
+      echo "kernels rc=$?"; tail -40 gpurun_out/kernels.log ;;
+    bench_variants)
+      for v in "RUTV_FUSE_LEFT=1" "RUTV_FUSE_LEFT=0" "RUTV_GEMM_PERSIST=0" "RUTV_GEMM_SCHED=0"; do
+        env $v timeout 900 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_var.json 2>>gpurun_out/bench_var.err
+        echo "$v $(python -c "import json;d=json.load(open('gpurun_out/bench_var.json'));print(d['value'], d['ms_per_step'], d['roofline']['achieved'], d['roofline']['other_kernels'])")" | tee -a gpurun_out/bench_variants.log
+      done ;;
     bench_c2)
       timeout 900 python bench.py --config c2 --no-cpu-baseline > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err; echo "bench c2 rc=$?"; cat gpurun_out/bench_c2.json ;;
     ncu_launches)
