@@ -45,6 +45,11 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="do not record per-kernel CUDA events")
+    p.add_argument("--mode", default="hbm", choices=["hbm", "host"],
+                   help="host: the host-streamed (out-of-core analogue) entry, A/U/V in pinned host memory")
+    p.add_argument("--cache-gib", type=float, default=None,
+                   help="device panel cache for --mode host (default: a quarter of A)")
+    p.add_argument("--no-uv", action="store_true", help="T only (the paper's 'no orthonormal matrices')")
     return p.parse_args()
 
 
@@ -425,10 +430,79 @@ def run_ours(args):
     return 0
 
 
+def run_host_streamed(args):
+    """S12: randutv_factor_host from pinned host memory through a bounded device
+    panel cache, reported like the paper's Table 1: compute time
+    (the same factorisation resident in HBM), I/O time (summed H2D + D2H copy
+    durations), real time, and their ratios."""
+    import numpy as np
+    import torch
+
+    from paper_2002_06960_b200.flops import randutv_flops
+    from paper_2002_06960_b200.inputs import CONFIGS, make_config_torch
+    from paper_2002_06960_b200.randutv import RANDUTV_NO_UV, Context, colmajor, pinned_colmajor
+
+    torch.cuda.set_device(0)
+    cfg = CONFIGS[args.config]
+    m, n, b, q = cfg["m"], cfg["n"], cfg["b"], cfg["q"]
+    seed = 2000 + int(args.config[1:])
+    uv = not args.no_uv
+    F = randutv_flops(m, n, b, q, build_uv=uv)
+    A = make_config_torch(args.config)
+    A0 = pinned_colmajor(m, n)
+    torch.from_numpy(A0.T).copy_(A.t())
+    Ah = pinned_colmajor(m, n)
+    U = pinned_colmajor(m, m) if uv else None
+    V = pinned_colmajor(n, n) if uv else None
+    stream = torch.cuda.Stream()
+    ctx = Context(0, stream)
+    # compute-only reference: the same factorisation resident in HBM
+    with torch.cuda.stream(stream):
+        Td = colmajor(m, n)
+        Ud = colmajor(m, m) if uv else None
+        Vd = colmajor(n, n) if uv else None
+        ctx.randutv_factor_ex(A, b, q, seed, build_uv=uv, U=Ud, T=Td, V=Vd)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.randutv_factor_ex(A, b, q, seed, build_uv=uv, U=Ud, T=Td, V=Vd)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        comp_ms = e0.elapsed_time(e1)
+    del A, Td, Ud, Vd
+    torch.cuda.empty_cache()
+    cache = int((args.cache_gib * 2**30) if args.cache_gib else 8 * m * n // 4)
+    reps = []
+    for it in range(max(args.warmup, 0) + args.steps):
+        np.copyto(Ah, A0)
+        _, _, rep = ctx.randutv_factor_host(Ah, b, q, seed, build_uv=uv, U=U, V=V, cache_bytes=cache)
+        if it >= args.warmup:
+            reps.append(rep)
+    real = sum(r["wall_ms"] for r in reps) / len(reps)
+    io = sum(r["h2d_ms"] + r["d2h_ms"] for r in reps) / len(reps)
+    r0 = reps[-1]
+    line = {"metric": METRIC, "value": round(F / (real * 1e-3) / 1e9, 2), "unit": "GFLOP/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(real, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(config_dict(args.config, 1), mode="host-streamed", build_uv=uv,
+                           device_cache_bytes=cache, cache_slots=r0["cache_slots"]),
+            "table1": {"computational_time_s": comp_ms * 1e-3, "io_time_s": io * 1e-3, "real_time_s": real * 1e-3,
+                       "real_over_comp": real / comp_ms, "comp_over_io": comp_ms / io if io > 0 else None,
+                       "h2d_bytes": r0["h2d_bytes"], "d2h_bytes": r0["d2h_bytes"],
+                       "h2d_GBps": r0["h2d_bytes"] / (r0["h2d_ms"] * 1e-3) / 1e9 if r0["h2d_ms"] > 0 else None,
+                       "cache_hits": r0["cache_hits"], "cache_misses": r0["cache_misses"]},
+            "t_over_n3_x1e10": real * 1e-3 / float(n) ** 3 * 1e10}
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "host":
+        return run_host_streamed(args)
     return run_ours(args)
 
 

@@ -268,17 +268,34 @@ RANDUTV_API int randutv_factor_dist(randutv_ctx* ctx, int64_t m, int64_t n, doub
                                     int64_t b, int q, uint64_t seed, unsigned flags, double* U_local, int64_t ldu,
                                     double* V_local, int64_t ldv);
 
+/* Sharded truncated rank-k randUTV (the c4 workload at 1/2/4/8
+ * GPUs): K = ceil(k/b) sampled steps (k <= b * floor((n-1)/b), else -14), no
+ * final step.  A_local is overwritten by the rank's columns of T (T_k = rows
+ * 0:k); Uk_local (mu x k) receives rows [m*p/P, m*(p+1)/P) of U_k, formed by
+ * backward accumulation of the broadcast (W_U, T_U, U_s) with one AllReduce of
+ * b x (k - k_j) per step (reading A12); V_local as for randutv_factor_dist;
+ * *resid_fro (host) = ||T(k:m, k:n)||_F = ||A - U_k T_k V^T||_F (identical on
+ * every rank).  Invalid arguments use randutv_factor_dist's positions, plus -14
+ * (k) and -15 (resid_fro).  Arguments: 1 ctx, 2 m, 3 n, 4 A_local, 5 lda, 6 k,
+ * 7 b, 8 q, 9 seed, 10 flags, 11 Uk_local, 12 ldu, 13 V_local, 14 ldv,
+ * 15 resid_fro. */
+RANDUTV_API int randutv_factor_dist_rank(randutv_ctx* ctx, int64_t m, int64_t n, double* A_local, int64_t lda,
+                                         int64_t k, int64_t b, int q, uint64_t seed, unsigned flags, double* Uk_local,
+                                         int64_t ldu, double* V_local, int64_t ldv, double* resid_fro);
+
 /* The same SPMD driver with `nranks` (<= 16) virtual ranks run as host threads
  * on ONE device, collectives done by device copies and fixed-order sums
  * between host barriers (no kernel waits on another rank).  Used to test the
  * sharded path on a single GPU.  A_locals / U_locals / V_locals: host arrays
  * of nranks device pointers laid out as for randutv_factor_dist (lda, ldu, ldv
- * shared by all ranks).  Arguments: 1 device, 2 nranks, 3 m, 4 n, 5 A_locals,
- * 6 lda, 7 b, 8 q, 9 seed, 10 flags, 11 U_locals, 12 ldu, 13 V_locals, 14 ldv. */
+ * shared by all ranks).  k = 0: full factorisation; k >= 1: the truncated
+ * variant (U_locals hold rows of U_k, *resid_fro as randutv_factor_dist_rank).
+ * Arguments: 1 device, 2 nranks, 3 m, 4 n, 5 A_locals, 6 lda, 7 b, 8 q, 9 seed,
+ * 10 flags, 11 U_locals, 12 ldu, 13 V_locals, 14 ldv, 15 k, 16 resid_fro. */
 RANDUTV_API int randutv_factor_dist_loopback(int device, int nranks, int64_t m, int64_t n, double* const* A_locals,
                                              int64_t lda, int64_t b, int q, uint64_t seed, unsigned flags,
                                              double* const* U_locals, int64_t ldu, double* const* V_locals,
-                                             int64_t ldv);
+                                             int64_t ldv, int64_t k, double* resid_fro);
 
 #ifdef __cplusplus
 }

@@ -336,6 +336,43 @@ __global__ void cyclic_scatter_rows_kernel(i64 sl, i64 cols, i64 k, i64 b, int P
   }
 }
 
+// out[lc] = sum_{r >= k} X(r, lc)^2 for the local columns whose global index is
+// >= k (0 otherwise): one CTA per column, fixed-order tree (deterministic)
+__global__ void cyclic_colsumsq_kernel(i64 m, i64 nl, i64 k, i64 b, int P, int p, const double* __restrict__ X,
+                                       i64 ldx, double* __restrict__ out) {
+  __shared__ double red[256];
+  for (i64 lc = blockIdx.x; lc < nl; lc += gridDim.x) {
+    const i64 g = ((lc / b) * P + p) * b + lc % b;
+    double acc = 0.0;
+    if (g >= k)
+      for (i64 r = k + threadIdx.x; r < m; r += blockDim.x) {
+        const double v = X[r + lc * ldx];
+        acc = fma(v, v, acc);
+      }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[lc] = red[0];
+    __syncthreads();
+  }
+}
+
+__global__ void sum_vector_kernel(i64 cnt, const double* __restrict__ v, double* __restrict__ out) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (i64 i = threadIdx.x; i < cnt; i += blockDim.x) acc += v[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
 unsigned grid_for(const Launch& L, i64 total) {
   i64 b = (total + 255) / 256;
   const i64 cap = (i64)L.device_sms * 8;
@@ -348,9 +385,12 @@ unsigned grid_for(const Launch& L, i64 total) {
 struct DistWork {
   Work w;
   double *Yl, *Yall, *Wl, *wbuf, *svd;
+  double* lefts;   // truncated: per step W_U (m x b, ld r), T_U (b x b), U_s (b x b)
+  double* colss;   // truncated: per-local-column sums of squares (n_p), then the total
+  double* blk;     // truncated: one row block of U_k (b x k) for the U_s application
 };
 
-size_t carve_dist(Carver& c, DistWork& d, const Layout& lay) {
+size_t carve_dist(Carver& c, DistWork& d, const Layout& lay, i64 K, i64 k) {
   const i64 m = lay.m, n = lay.n, b = std::min(lay.b, lay.n);
   const i64 maxs = std::max<i64>(lay.max_trailing(0), 1);
   carve(c, d.w, m, n, b, 0, false);
@@ -359,6 +399,9 @@ size_t carve_dist(Carver& c, DistWork& d, const Layout& lay) {
   d.Wl = c.take<double>(maxs * b);
   d.wbuf = c.take<double>(m * b + b * b);
   d.svd = c.take<double>(2 * b * b);
+  d.lefts = K > 0 ? c.take<double>(K * (m * b + 2 * b * b)) : nullptr;
+  d.colss = K > 0 ? c.take<double>(lay.ncols(lay.p) + 8) : nullptr;
+  d.blk = K > 0 ? c.take<double>(b * k) : nullptr;
   return c.off;
 }
 
@@ -372,6 +415,7 @@ struct DistProblem {
   i64 ldu, u0, mu;
   double* V;  // rows [v0, v0 + nv) of V (n x n), ld ldv; may be null
   i64 ldv, v0, nv;
+  bool record;  // truncated with U_k: keep (W_U, T_U, U_s) of every step
 };
 
 struct DistRun {
@@ -399,6 +443,11 @@ int dist_svd_and_fold(DistRun& R, const Launch& Ls, Comm* cm, i64 i, i64 bw, boo
     RUTV_TRY(launch_jacobi_svd(Ls, bw, T11, R.P.lda, Us, w.d, Vs, w.status, (int)(i + 1), w.jac, w.jac_elems));
   }
   RUTV_TRY(cm->bcast(R.d.svd, 2 * bw * bw, o, Ls.stream));
+  if (R.P.record) {
+    const i64 bb = lay.b, rec = i * (lay.m * bb + 2 * bb * bb);
+    RUTV_CUDA(cudaMemcpyAsync(R.d.lefts + rec + (lay.m - k) * bb + bb * bb, Us, bw * bw * 8, cudaMemcpyDeviceToDevice,
+                              Ls.stream));
+  }
   if (p == o) {
     double* T11 = R.P.A + k + lc * R.P.lda;
     RUTV_TRY(launch_set_diag(Ls, bw, w.d, T11, R.P.lda));
@@ -466,6 +515,8 @@ int dist_sampled_step(DistRun& R, i64 i) {
     RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, lda));
   }
   RUTV_TRY(R.comm->bcast(R.d.wbuf, r * b + b * b, o, st));
+  if (R.P.record) RUTV_CUDA(cudaMemcpyAsync(R.d.lefts + i * (m * b + 2 * b * b), R.d.wbuf, (r * b + b * b) * 8,
+                                            cudaMemcpyDeviceToDevice, st));
   // S7 (fused with the rest of S5 when enabled): columns right of block i; U rows
   const i64 c1 = lay.lcol(p, i + 1);
   if (fuse)
@@ -509,14 +560,58 @@ int dist_final_step(DistRun& R, i64 i) {
   return dist_svd_and_fold(R, L, R.comm, i, s, r == s);
 }
 
-int dist_run(DistRun& R) {
+// U_k = U(:, 0:k) of the truncated run by backward accumulation (reading A12)
+// over this rank's rows [u0, u0 + mu): X := rows of [I_k; 0]; for j = K-1..0:
+// X[kj:kj+b, kj:k] := U_s^(j) X[...] (the row block is gathered with an
+// AllReduce of the ranks' disjoint rows), then X[kj:m, kj:k] -= W (T (W^T X))
+// with W^T X summed over the ranks (AllReduce, b x (k - kj)).
+int dist_backward_uk(DistRun& R, i64 K, i64 k) {
+  const Layout& lay = R.P.lay;
+  const Launch& L = R.L;
+  Work& w = R.d.w;
+  const i64 m = lay.m, b = lay.b, u0 = R.P.u0, mu = R.P.mu;
+  double* X = R.P.U;
+  const i64 ldx = R.P.ldu;
+  cudaStream_t st = L.stream;
+  RUTV_TRY(launch_set_identity_shift(L, mu, k, -u0, X, ldx));
+  for (i64 j = K - 1; j >= 0; --j) {
+    const i64 kj = j * b, rj = m - kj, cols = k - kj;
+    const double* rec = R.d.lefts + j * (m * b + 2 * b * b);
+    const double* Wj = rec;                   // rj x b, ld rj
+    const double* Tj = rec + rj * b;          // b x b
+    const double* Usj = rec + rj * b + b * b; // b x b
+    // (a) rows kj..kj+b: gather, U_s, scatter back
+    const i64 lo = std::max(u0, kj), hi = std::min(u0 + mu, kj + b);
+    RUTV_TRY(launch_fill(L, b, cols, 0.0, R.d.blk, b));
+    if (hi > lo) RUTV_TRY(launch_copy(L, hi - lo, cols, X + (lo - u0) + kj * ldx, ldx, R.d.blk + (lo - kj), b));
+    RUTV_TRY(R.comm->allreduce_sum(R.d.blk, b * cols, st));
+    if (hi > lo) {
+      RUTV_TRY(launch_dgemm(L, false, false, b, cols, b, 1.0, Usj, b, R.d.blk, b, 0.0, w.Z, b, nullptr, 0));
+      RUTV_TRY(launch_copy(L, hi - lo, cols, w.Z + (lo - kj), b, X + (lo - u0) + kj * ldx, ldx));
+    }
+    // (b) X[kj:m] -= W (T (W^T X[kj:m]))   (local rows >= kj)
+    const i64 l0 = std::max(u0, kj), nrow = u0 + mu - l0;  // local rows in [kj, m)
+    double* Xr = X + (l0 - u0) + kj * ldx;
+    const double* Wr = Wj + (l0 - kj);
+    RUTV_TRY(launch_dgemm(L, true, false, b, cols, nrow > 0 ? nrow : 0, 1.0, Wr, rj, Xr, ldx, 0.0, w.Z, b, w.gemm_ws,
+                          w.gemm_ws_elems));
+    RUTV_TRY(R.comm->allreduce_sum(w.Z, b * cols, st));
+    RUTV_TRY(launch_dgemm(L, false, false, b, cols, b, 1.0, Tj, b, w.Z, b, 0.0, w.Z2, b, nullptr, 0));
+    if (nrow > 0) RUTV_TRY(launch_dgemm(L, false, false, nrow, cols, b, -1.0, Wr, rj, w.Z2, b, 1.0, Xr, ldx, nullptr, 0));
+  }
+  return 0;
+}
+
+// K = -1: full factorisation; K >= 1: truncated after K sampled steps (rank k)
+int dist_run(DistRun& R, i64 K, i64 k, double* resid_fro) {
   const Layout& lay = R.P.lay;
   randutv_ctx* ctx = R.ctx;
   Work& w = R.d.w;
   const Launch& L = R.L;
-  const i64 nsamp = sampled_steps(lay.n, lay.b);
+  const bool trunc = K >= 0;
+  const i64 nsamp = trunc ? K : sampled_steps(lay.n, lay.b);
   RUTV_TRY(start_status(ctx, w));
-  if (R.P.U && R.P.mu > 0) {
+  if (!trunc && R.P.U && R.P.mu > 0) {
     RUTV_TRY(launch_set_identity_shift(L, R.P.mu, lay.m, -R.P.u0, R.P.U, R.P.ldu));  // rows u0.. of I
   }
   if (R.P.V && R.P.nv > 0) {
@@ -524,9 +619,35 @@ int dist_run(DistRun& R) {
   }
   // the side stream starts after the initialisation
   RUTV_CUDA(cudaEventRecord(ctx->eF, L.stream));
+  // (truncated: the U updates are replaced by the records; P.U is the U_k output)
+  double* Uk = R.P.U;
+  if (trunc) R.P.U = nullptr;
   for (i64 i = 0; i < nsamp; ++i) RUTV_TRY(dist_sampled_step(R, i));
-  RUTV_TRY(dist_final_step(R, nsamp));
+  if (!trunc) RUTV_TRY(dist_final_step(R, nsamp));
   RUTV_CUDA(cudaStreamWaitEvent(L.stream, ctx->eF, 0));
+  if (trunc) {
+    R.P.U = Uk;
+    // rho^2 = sum over ranks of ||T(k:m, local columns >= k)||_F^2
+    const i64 nl = lay.ncols(lay.p);
+    RUTV_CUDA(cudaMemsetAsync(R.d.colss + nl, 0, sizeof(double), L.stream));
+    if (nl > 0) {
+      cyclic_colsumsq_kernel<<<(unsigned)std::min<i64>(nl, (i64)L.device_sms * 8), 256, 0, L.stream>>>(
+          lay.m, nl, k, lay.b, lay.P, lay.p, R.P.A, R.P.lda, R.d.colss);
+      L.count();
+      RUTV_CHECK_LAUNCH("cyclic_colsumsq_kernel");
+      sum_vector_kernel<<<1, 256, 0, L.stream>>>(nl, R.d.colss, R.d.colss + nl);
+      L.count();
+      RUTV_CHECK_LAUNCH("sum_vector_kernel");
+    }
+    RUTV_TRY(R.comm->allreduce_sum(R.d.colss + nl, 1, L.stream));
+    if (R.P.record) RUTV_TRY(dist_backward_uk(R, K, k));  // collective: every rank, even without rows
+    double ss = 0.0;
+    RUTV_CUDA(cudaMemcpyAsync(&ss, R.d.colss + nl, sizeof(double), cudaMemcpyDeviceToHost, L.stream));
+    RUTV_TRY(R.comm->allreduce_min_int(w.status, 1, L.stream));
+    const int st = finish(ctx, w);
+    *resid_fro = std::sqrt(ss);
+    return st;
+  }
   // every rank returns the first non-converged block (status word: min)
   RUTV_TRY(R.comm->allreduce_min_int(w.status, 1, L.stream));
   return finish(ctx, w);
@@ -553,13 +674,21 @@ int dist_check(const Layout& lay, const double* A, i64 lda, int q, unsigned flag
   return 0;
 }
 
+// k == 0: full factorisation (U_local: rows of U, m x m); k >= 1: truncated
+// rank-k (U_local: rows of U_k, m x k; *resid_fro = ||T(k:m, k:n)||_F)
 int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, double* A, i64 lda, i64 b, int q,
-                uint64_t seed, unsigned flags, double* U, i64 ldu, double* V, i64 ldv) {
+                uint64_t seed, unsigned flags, double* U, i64 ldu, double* V, i64 ldv, i64 k, double* resid_fro) {
   Layout lay{m, n, std::min(b, n), comm->nranks, comm->rank, 0};
   if (b < 1) return -6;
   lay.nblocks = (n + lay.b - 1) / lay.b;
   RUTV_TRY(dist_check(lay, A, lda, q, flags, U, ldu, V, ldv));
   const bool uv = !(flags & RANDUTV_NO_UV);
+  i64 K = -1;
+  if (k != 0) {
+    K = (k + lay.b - 1) / lay.b;
+    if (k < 0 || K > sampled_steps(n, lay.b)) return -14;  // truncation needs k <= b * (sampled steps)
+    if (!resid_fro) return -15;
+  }
   DistRun R;
   R.ctx = ctx;
   R.comm = comm;
@@ -567,13 +696,14 @@ int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, dou
   R.L = ctx->launch();
   R.S = ctx->side_launch();
   Carver dry{nullptr, 0, 0, true};
-  const size_t need = carve_dist(dry, R.d, lay);
+  const size_t need = carve_dist(dry, R.d, lay, K > 0 ? K : 0, k);
   RUTV_TRY(ensure_ws(ctx, need));
   Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
-  carve_dist(real, R.d, lay);
+  carve_dist(real, R.d, lay, K > 0 ? K : 0, k);
   const i64 u0 = Layout::row0(m, lay.P, lay.p), u1 = Layout::row0(m, lay.P, lay.p + 1);
   const i64 v0 = Layout::row0(n, lay.P, lay.p), v1 = Layout::row0(n, lay.P, lay.p + 1);
-  R.P = DistProblem{lay, q, seed, A, lda, uv ? U : nullptr, ldu, u0, u1 - u0, uv ? V : nullptr, ldv, v0, v1 - v0};
+  R.P = DistProblem{lay, q, seed, A, lda, uv ? U : nullptr, ldu, u0, u1 - u0, uv ? V : nullptr, ldv, v0, v1 - v0,
+                    uv && K > 0};
   if (R.P.U && R.P.mu == 0) R.P.U = nullptr;
   if (R.P.V && R.P.nv == 0) R.P.V = nullptr;
   if (flags & RANDUTV_CHECK_FINITE) {
@@ -588,7 +718,7 @@ int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, dou
     RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
     if (!h) return RANDUTV_ERR_NONFINITE;
   }
-  const int st = dist_run(R);
+  const int st = dist_run(R, K, k, resid_fro);
   if (st == 0) ctx->stats.factorizations++;
   return st;
 }
@@ -676,13 +806,25 @@ RANDUTV_API int randutv_factor_dist(randutv_ctx* ctx, int64_t m, int64_t n, doub
   RUTV_TRY(begin_call(ctx));
   if (!ctx->comm) return RANDUTV_ERR_NOCOMM;
   return dist_factor(ctx, ctx->comm, ctx->comm_side, m, n, A_local, lda, b, q, seed, flags, U_local, ldu, V_local,
-                     ldv);
+                     ldv, 0, nullptr);
+}
+
+RANDUTV_API int randutv_factor_dist_rank(randutv_ctx* ctx, int64_t m, int64_t n, double* A_local, int64_t lda,
+                                         int64_t k, int64_t b, int q, uint64_t seed, unsigned flags, double* Uk_local,
+                                         int64_t ldu, double* V_local, int64_t ldv, double* resid_fro) {
+  RUTV_TRY(begin_call(ctx));
+  if (!ctx->comm) return RANDUTV_ERR_NOCOMM;
+  if (k < 1) return -14;
+  return dist_factor(ctx, ctx->comm, ctx->comm_side, m, n, A_local, lda, b, q, seed, flags, Uk_local, ldu, V_local,
+                     ldv, k, resid_fro);
 }
 
 RANDUTV_API int randutv_factor_dist_loopback(int device, int nranks, int64_t m, int64_t n, double* const* A_locals,
                                              int64_t lda, int64_t b, int q, uint64_t seed, unsigned flags,
                                              double* const* U_locals, int64_t ldu, double* const* V_locals,
-                                             int64_t ldv) {
+                                             int64_t ldv, int64_t k, double* resid_fro) {
+  if (k < 0) return -15;
+  if (k > 0 && !resid_fro) return -16;
   if (nranks < 1 || nranks > kMaxLoopRanks) return -2;
   if (!A_locals) return -5;
   const bool uv = !(flags & RANDUTV_NO_UV);
@@ -709,8 +851,10 @@ RANDUTV_API int randutv_factor_dist_loopback(int device, int nranks, int64_t m, 
       if (st == 0) st = begin_call(ctx);
       if (st == 0) {
         comms[r]->sms = comms[nranks + r]->sms = ctx->sms;
+        double rho = 0.0;
         st = dist_factor(ctx, comms[r], comms[nranks + r], m, n, A_locals[r], lda, b, q, seed, flags,
-                         uv ? U_locals[r] : nullptr, ldu, uv ? V_locals[r] : nullptr, ldv);
+                         uv ? U_locals[r] : nullptr, ldu, uv ? V_locals[r] : nullptr, ldv, k, k > 0 ? &rho : nullptr);
+        if (st == 0 && k > 0 && r == 0) *resid_fro = rho;
       }
       if (ctx) randutv_destroy(ctx);
       if (s) cudaStreamDestroy(s);

@@ -77,8 +77,11 @@ SIGNATURES = {
     "randutv_nccl_unique_id": (_int, [_vp]),
     "randutv_comm_init": (_int, [_vp, _vp, _int, _int]),
     "randutv_factor_dist": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint, _vp, _i64, _vp, _i64]),
+    "randutv_factor_dist_rank": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _int, _u64, _uint, _vp, _i64, _vp,
+                                        _i64, ctypes.POINTER(_dbl)]),
     "randutv_factor_dist_loopback": (_int, [_int, _int, _i64, _i64, ctypes.POINTER(_vp), _i64, _i64, _int, _u64,
-                                            _uint, ctypes.POINTER(_vp), _i64, ctypes.POINTER(_vp), _i64]),
+                                            _uint, ctypes.POINTER(_vp), _i64, ctypes.POINTER(_vp), _i64, _i64,
+                                            ctypes.POINTER(_dbl)]),
 }
 
 _lib = None
@@ -307,6 +310,26 @@ class Context:
         _check("randutv_factor_dist", st)
         return U_local, V_local
 
+    def randutv_factor_dist_rank(self, A_local, m, n, k, b, q, seed, build_uv=True, Uk_local=None, V_local=None,
+                                 flags=0, nranks=None, rank=None):
+        """Sharded truncated randUTV (collective): returns (Uk_local, V_local, rho)."""
+        import torch.distributed as dist
+        if nranks is None:
+            nranks, rank = dist.get_world_size(), dist.get_rank()
+        lay = dist_layout(m, n, b, nranks, rank)
+        if not build_uv:
+            flags |= RANDUTV_NO_UV
+        if build_uv:
+            Uk_local = colmajor(lay["u1"] - lay["u0"], k, device=A_local.device) if Uk_local is None else Uk_local
+            V_local = colmajor(lay["v1"] - lay["v0"], n, device=A_local.device) if V_local is None else V_local
+        rho = ctypes.c_double()
+        st = self.lib.randutv_factor_dist_rank(self.h, m, n, _ptr(A_local), _ld_or(A_local, m), int(k), int(b),
+                                               int(q), int(seed) & (2**64 - 1), flags, _ptr(Uk_local),
+                                               _ld_or(Uk_local, 1), _ptr(V_local), _ld_or(V_local, 1),
+                                               ctypes.byref(rho))
+        _check("randutv_factor_dist_rank", st)
+        return Uk_local, V_local, rho.value
+
     def randutv_small_svd(self, B, allow_nonconvergence=False):
         import torch
         w = B.shape[0]
@@ -398,7 +421,7 @@ def _ld_or(X, default):
 
 
 def randutv_factor_dist_loopback(A_locals, m, n, b, q, seed, U_locals=None, V_locals=None, build_uv=True, flags=0,
-                                 device=None):
+                                 device=None, k=0):
     """The sharded SPMD driver with len(A_locals) virtual ranks as host threads on one
     GPU (collectives by device copies between host barriers): the single-GPU test
     harness of the multi-GPU path.  A_locals are overwritten with the ranks' T columns."""
@@ -410,21 +433,28 @@ def randutv_factor_dist_loopback(A_locals, m, n, b, q, seed, U_locals=None, V_lo
     if not build_uv:
         flags |= RANDUTV_NO_UV
     lays = [dist_layout(m, n, b, P, p) for p in range(P)]
+    # one leading dimension per matrix kind for all virtual ranks (the row counts differ by one)
+    mu = max(l["u1"] - l["u0"] for l in lays)
+    nv = max(l["v1"] - l["v0"] for l in lays)
     if build_uv:
         if U_locals is None:
-            U_locals = [colmajor(l["u1"] - l["u0"], m, device=f"cuda:{device}") for l in lays]
+            U_locals = [colmajor(mu, k if k else m, device=f"cuda:{device}")[:l["u1"] - l["u0"]] for l in lays]
         if V_locals is None:
-            V_locals = [colmajor(l["v1"] - l["v0"], n, device=f"cuda:{device}") for l in lays]
+            V_locals = [colmajor(nv, n, device=f"cuda:{device}")[:l["v1"] - l["v0"]] for l in lays]
     lda = max([_ld(a) for a in A_locals if a.numel() > 0] + [m])
-    for a in A_locals:
-        if a.numel() > 0 and _ld(a) != lda:
-            raise ValueError("loopback: every A_local needs the same leading dimension")
-    ldu = max([_ld(u) for u in U_locals if u.numel() > 0] + [1]) if build_uv else 1
-    ldv = max([_ld(v) for v in V_locals if v.numel() > 0] + [1]) if build_uv else 1
+    ldu = max(mu, 1)
+    ldv = max(nv, 1)
+    for X, ld in [(a, lda) for a in A_locals] + ([(u, ldu) for u in U_locals] + [(v, ldv) for v in V_locals]
+                                                  if build_uv else []):
+        if X.numel() > 0 and X.stride(1) != ld and X.shape[1] > 1:
+            raise ValueError("loopback: every rank's matrix of a kind needs the same leading dimension")
     arr = lambda xs: (_vp * P)(*[x.data_ptr() if x is not None and x.numel() > 0 else None for x in xs])
     torch.cuda.synchronize(device)
+    rho = ctypes.c_double()
     st = lib.randutv_factor_dist_loopback(int(device), P, int(m), int(n), arr(A_locals), lda, int(b), int(q),
                                           int(seed) & (2**64 - 1), flags, arr(U_locals) if build_uv else None, ldu,
-                                          arr(V_locals) if build_uv else None, ldv)
+                                          arr(V_locals) if build_uv else None, ldv, int(k), ctypes.byref(rho))
     _check("randutv_factor_dist_loopback", st)
+    if k:
+        return U_locals, V_locals, rho.value
     return U_locals, V_locals

@@ -117,3 +117,43 @@ def test_dist_requires_comm(ctx):
     A = colmajor(8, 8)
     st = ctx.lib.randutv_factor_dist(ctx.h, 8, 8, ctypes.c_void_p(A.data_ptr()), 8, 4, 1, 1, 1, None, 1, None, 1)
     assert st == RANDUTV_ERR_NOCOMM
+
+
+@pytest.mark.parametrize("m,n,k,b,q,P", [
+    (400, 300, 64, 32, 1, 2),     # k = 2b
+    (600, 240, 100, 40, 2, 3),    # k not a multiple of b, ragged rows over 3 ranks
+    (4096, 1024, 256, 64, 2, 4),  # c4's proportions at 1/64 of the size (as test_truncated_tall_parity)
+])
+def test_dist_loopback_truncated(ctx, m, n, k, b, q, P):
+    import torch
+    from paper_2002_06960_b200.inputs import make_numpy
+    from paper_2002_06960_b200.randutv import colmajor, dist_layout, local_columns, randutv_factor_dist_loopback
+    if m == 4096:
+        A = make_numpy("lowrank", m, n, cfg_index=4, rank=200)
+    else:
+        A = np.asfortranarray(np.random.default_rng(m + n + k).standard_normal((m, n)))
+    locals_ = []
+    for p in range(P):
+        cols = local_columns(n, b, P, p)
+        Al = colmajor(m, len(cols))
+        Al.copy_(torch.from_numpy(np.ascontiguousarray(A[:, cols])))
+        locals_.append(Al)
+    Us, Vs, rho = randutv_factor_dist_loopback(locals_, m, n, b, q, 77, k=k)
+    T = np.zeros((m, n), order="F")
+    Uk = np.zeros((m, k), order="F")
+    V = np.zeros((n, n), order="F")
+    for p in range(P):
+        cols = local_columns(n, b, P, p)
+        T[:, cols] = to_np(locals_[p])
+        lay = dist_layout(m, n, b, P, p)
+        Uk[lay["u0"]:lay["u1"], :] = to_np(Us[p])
+        V[lay["v0"]:lay["v1"], :] = to_np(Vs[p])
+    Tk = T[:k, :]
+    o = oracle_randutv(A, b, q, 77, k=k, thin_u=True)
+    nA = np.linalg.norm(A)
+    assert abs(rho - o["rho"]) <= 1e-9 * o["rho"]
+    assert diag_parity(np.diag(Tk), np.diag(o["Tk"])) <= 1.0
+    assert np.max(np.abs(np.abs(Tk) - np.abs(o["Tk"]))) / nA <= ELEM_TOL
+    assert np.max(np.abs(np.abs(Uk) - np.abs(o["Uk"]))) <= 1e-9
+    assert spectral_orth_error(Uk) <= 1e-12 and spectral_orth_error(V) <= 1e-12
+    assert abs(np.linalg.norm(A - Uk @ Tk @ V.T) - rho) <= 1e-12 * nA
