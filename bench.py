@@ -263,16 +263,16 @@ def run_ours(args):
         del A
         torch.cuda.empty_cache()
         T_loc = colmajor(m, lay["ncols"])
-        U_loc = colmajor(lay["u1"] - lay["u0"], m)
+        U_loc = colmajor(lay["u1"] - lay["u0"], trunc_k if trunc_k else m)
         V_loc = colmajor(lay["v1"] - lay["v0"], n)
 
         def step():
             T_loc.copy_(A_loc)
-            ctx.randutv_factor_dist(T_loc, m, n, b, q, seed, U_local=U_loc, V_local=V_loc)
+            if trunc_k:
+                ctx.randutv_factor_dist_rank(T_loc, m, n, trunc_k, b, q, seed, Uk_local=U_loc, V_local=V_loc)
+            else:
+                ctx.randutv_factor_dist(T_loc, m, n, b, q, seed, U_local=U_loc, V_local=V_loc)
     elif trunc_k is not None:
-        if ws > 1:
-            raise SystemExit("the truncated config runs on one GPU (the sharded path is full-factorisation only)")
-
         def step():
             ctx.randutv_factor_rank(A, trunc_k, b, q, seed)
     else:
@@ -329,13 +329,16 @@ def run_ours(args):
         Ah = torch.empty((lay["ncols"], m), dtype=torch.float64, pin_memory=True)
         Ah.copy_(A_loc.t())
         Th = torch.empty_like(Ah)
-        Uh = torch.empty((m, lay["u1"] - lay["u0"]), dtype=torch.float64, pin_memory=True)
+        Uh = torch.empty((U_loc.shape[1], U_loc.shape[0]), dtype=torch.float64, pin_memory=True)
         Vh = torch.empty((n, lay["v1"] - lay["v0"]), dtype=torch.float64, pin_memory=True)
 
         def e2e_step():
             with torch.cuda.stream(stream):
                 T_loc.copy_(Ah.t(), non_blocking=True)
-                ctx.randutv_factor_dist(T_loc, m, n, b, q, seed, U_local=U_loc, V_local=V_loc)
+                if trunc_k:
+                    ctx.randutv_factor_dist_rank(T_loc, m, n, trunc_k, b, q, seed, Uk_local=U_loc, V_local=V_loc)
+                else:
+                    ctx.randutv_factor_dist(T_loc, m, n, b, q, seed, U_local=U_loc, V_local=V_loc)
                 Th.copy_(T_loc.t(), non_blocking=True)
                 Uh.copy_(U_loc.t(), non_blocking=True)
                 Vh.copy_(V_loc.t(), non_blocking=True)
@@ -352,7 +355,7 @@ def run_ours(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         dt = float(tt.item())
         bi = torch.tensor([8 * m * lay["ncols"]], device="cuda", dtype=torch.float64)
-        bo = torch.tensor([8 * (m * lay["ncols"] + m * (lay["u1"] - lay["u0"]) + n * (lay["v1"] - lay["v0"]))],
+        bo = torch.tensor([8 * (m * lay["ncols"] + U_loc.numel() + V_loc.numel())],
                           device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(bi)
         torch.distributed.all_reduce(bo)
