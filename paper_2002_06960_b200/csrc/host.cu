@@ -79,6 +79,9 @@ struct CopyTimer {
 struct PanelCache {
   std::vector<HostMat> mats;
   std::vector<std::vector<int>> where;  // mat -> panel -> slot (-1: host only)
+  // mat -> panel -> event after the panel's latest write-back (a re-fetch of the
+  // panel must not read host memory before its write-back has landed)
+  std::vector<std::vector<cudaEvent_t>> wbev;
   std::vector<Slot> slots;
   double* base = nullptr;
   i64 slot_elems = 0, b = 0;
@@ -91,6 +94,7 @@ struct PanelCache {
   int add_mat(double* h, i64 rows, i64 cols, i64 ld) {
     mats.push_back(HostMat{h, rows, cols, ld, (cols + b - 1) / b});
     where.emplace_back((size_t)mats.back().npanels, -1);
+    wbev.emplace_back((size_t)mats.back().npanels, nullptr);
     return (int)mats.size() - 1;
   }
   i64 width(int mat, i64 p) const { return std::min(b, mats[mat].cols - p * b); }
@@ -107,6 +111,10 @@ struct PanelCache {
     return 0;
   }
   void destroy() {
+    for (auto& v : wbev)
+      for (cudaEvent_t e : v)
+        if (e) cudaEventDestroy(e);
+    wbev.clear();
     for (Slot& s : slots) {
       if (s.ready) cudaEventDestroy(s.ready);
       if (s.idle) cudaEventDestroy(s.idle);
@@ -129,6 +137,9 @@ struct PanelCache {
       timer.d2h.push_back({e0, e1});
     }
     RUTV_CUDA(cudaEventRecord(s.clean, d2h));
+    cudaEvent_t& we = wbev[s.mat][s.panel];
+    if (!we) RUTV_CUDA(cudaEventCreateWithFlags(&we, cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventRecord(we, d2h));
     rep->d2h_bytes += M.rows * w * 8;
     s.dirty = false;
     return 0;
@@ -175,6 +186,7 @@ struct PanelCache {
     RUTV_CUDA(cudaStreamWaitEvent(h2d, v.idle, 0));
     RUTV_CUDA(cudaStreamWaitEvent(h2d, v.clean, 0));
     if (load) {
+      if (wbev[mat][panel]) RUTV_CUDA(cudaStreamWaitEvent(h2d, wbev[mat][panel], 0));
       size_t e0 = 0, e1 = 0;
       if (timer.on) RUTV_TRY(timer.mark(h2d, &e0));
       RUTV_CUDA(cudaMemcpy2DAsync(v.d, M.rows * 8, M.h + panel * b * M.ld, M.ld * 8, M.rows * 8, w,
