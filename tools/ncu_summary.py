@@ -14,14 +14,17 @@ import sys
 
 def short(name):
     name = re.sub(r"\(.*$", "", name)
-    name = name.replace("(anonymous namespace)::", "").replace("rutv::", "")
+    name = name.replace("(anonymous namespace)::", "").replace("rutv::", "").replace("unnamed>::", "")
     m = re.match(r"void\s+(\w+)(<.*>)?", name)
     base = m.group(1) if m else name
     if base == "dgemm_kernel" and m and m.group(2):
         t = m.group(2)
-        flags = re.findall(r"\b(true|false|0|1)\b", t)
         cfg = "128x64" if "128, 64" in t else ("128x128" if "128, 128" in t else "")
-        return f"dgemm_kernel[{cfg}]"
+        tr = re.search(r">\s*,\s*(\d|true|false)\s*,\s*(\d|true|false)", t)
+        op = ""
+        if tr:
+            op = ("T" if tr.group(1) in ("1", "true") else "N") + ("T" if tr.group(2) in ("1", "true") else "N")
+        return f"dgemm_kernel[{cfg},{op}]"
     return base
 
 
