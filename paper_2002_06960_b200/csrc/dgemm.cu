@@ -112,31 +112,42 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
   constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, MI = CF::MI, NI = CF::NI;
   constexpr int A_ELEMS = CF::A_ELEMS, STAGE_ELEMS = CF::STAGE_ELEMS;
   extern __shared__ __align__(16) double smem[];
-  __shared__ i64 ring[RING];
+  __shared__ int ring[RING];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % CF::WM, wn = warp / CF::WM;
-  const i64 gm = (M + BM - 1) / BM, gn = (N + BN - 1) / BN, tiles = gm * gn;
-  const i64 items = tiles * splits;
+  const int gm = (int)((M + BM - 1) / BM), gn = (int)((N + BN - 1) / BN);
+  const int tiles = gm * gn, items = tiles * splits;
   const int ktiles = (int)((kchunk + BK - 1) / BK);  // every split has kchunk (last: ragged, masked)
 
   // item id of sequence number `seq` of this CTA (thread 0 only)
-  auto claim = [&](i64 seq) -> i64 {
-    if (sched) return (i64)atomicAdd(sched, 1);
-    return (i64)blockIdx.x + seq * gridDim.x;
+  auto claim = [&](int seq) -> int {
+    if (sched) return atomicAdd(sched, 1);
+    return (int)blockIdx.x + seq * (int)gridDim.x;
   };
-
-  auto load_stage = [&](int stage, i64 item, int kt) {
-    const i64 tile = item % tiles, split = item / tiles;
-    const i64 kb = split * kchunk, ke = (kb + kchunk < K) ? kb + kchunk : K;
-    const i64 m0 = (tile % gm) * BM, n0 = (tile / gm) * BN;
+  struct TileP {
+    i64 m0, n0, kb, ke;
+    int split;
+  };
+  // per-item constants (the only integer divisions: once per item, 32-bit)
+  auto params = [&](int item) {
+    const int tile = item % tiles, split = item / tiles;
+    TileP tp;
+    tp.m0 = (i64)(tile % gm) * BM;
+    tp.n0 = (i64)(tile / gm) * BN;
+    tp.kb = (i64)split * kchunk;
+    tp.ke = (tp.kb + kchunk < K) ? tp.kb + kchunk : K;
+    tp.split = split;
+    return tp;
+  };
+  auto load_stage = [&](int stage, const TileP& tp, int kt) {
     double* As = smem + stage * STAGE_ELEMS;
     double* Bs = As + A_ELEMS;
-    const i64 k0 = kb + (i64)kt * BK;
-    if constexpr (!TA) load_tile<BM, BK, VA>(As, A, lda, m0, k0, M, ke, tid);   // rows: k, contiguous m
-    else load_tile<BK, BM, VA>(As, A, lda, k0, m0, ke, M, tid);                 // rows: m, contiguous k
-    if constexpr (!TB) load_tile<BK, BN, VB>(Bs, B, ldb, k0, n0, ke, N, tid);   // rows: n, contiguous k
-    else load_tile<BN, BK, VB>(Bs, B, ldb, n0, k0, N, ke, tid);                 // rows: k, contiguous n
+    const i64 k0 = tp.kb + (i64)kt * BK;
+    if constexpr (!TA) load_tile<BM, BK, VA>(As, A, lda, tp.m0, k0, M, tp.ke, tid);   // rows: k, contiguous m
+    else load_tile<BK, BM, VA>(As, A, lda, k0, tp.m0, tp.ke, M, tid);                 // rows: m, contiguous k
+    if constexpr (!TB) load_tile<BK, BN, VB>(Bs, B, ldb, k0, tp.n0, tp.ke, N, tid);   // rows: n, contiguous k
+    else load_tile<BN, BK, VB>(Bs, B, ldb, tp.n0, k0, N, tp.ke, tid);                 // rows: k, contiguous n
   };
 
   double acc[MI][NI][2];
@@ -145,70 +156,104 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
 #pragma unroll
     for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  // epilogue of one item: lane holds C[row g][cols 2t, 2t+1] of each 8x8 tile
-  auto epilogue = [&](i64 item) {
-    const i64 tile = item % tiles, split = item / tiles;
-    const i64 m0 = (tile % gm) * BM, n0 = (tile / gm) * BN;
+  // epilogue of one item.  The DMMA computes the TRANSPOSED 8x8 tile (the
+  // N-side fragment is fed as the mma's A operand), so lane (g, t) holds
+  // C[rows 2t, 2t+1][col g]: two consecutive rows of one column, i.e. one
+  // 16-byte load/store in column-major C (half the epilogue instructions).
+  const bool cvec = part ? ((M & 1) == 0) : ((((uintptr_t)C & 15) == 0) && ((ldc & 1) == 0));
+  auto epilogue = [&](const TileP& tp) {
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
-      const i64 row = m0 + wm * (MI * 8) + mi * 8 + g;
+      const i64 row = tp.m0 + wm * (MI * 8) + mi * 8 + 2 * t;
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const i64 col = n0 + wn * (NI * 8) + ni * 8 + 2 * t + e;
-          if (row < M && col < N) {
+        const i64 col = tp.n0 + wn * (NI * 8) + ni * 8 + g;
+        double* cp = part ? part + (i64)tp.split * M * N + row + col * M : C + row + col * ldc;
+        if (col < N) {
+          if (cvec && row + 1 < M) {
+            double2 v;
             if (part) {
-              part[split * M * N + row + col * M] = acc[mi][ni][e];
+              v.x = acc[mi][ni][0];
+              v.y = acc[mi][ni][1];
+            } else if (beta == 0.0) {
+              v.x = alpha * acc[mi][ni][0];
+              v.y = alpha * acc[mi][ni][1];
             } else {
-              double* cp = C + row + col * ldc;
-              const double v = alpha * acc[mi][ni][e];
-              *cp = (beta == 0.0) ? v : v + beta * (*cp);
+              const double2 c = *reinterpret_cast<const double2*>(cp);
+              v.x = alpha * acc[mi][ni][0] + beta * c.x;
+              v.y = alpha * acc[mi][ni][1] + beta * c.y;
+            }
+            *reinterpret_cast<double2*>(cp) = v;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              if (row + e < M) {
+                if (part) cp[e] = acc[mi][ni][e];
+                else cp[e] = (beta == 0.0) ? alpha * acc[mi][ni][e] : alpha * acc[mi][ni][e] + beta * cp[e];
+              }
             }
           }
-          acc[mi][ni][e] = 0.0;
         }
+        acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
     }
   };
 
   if (ktiles == 0) {  // K == 0: C = beta C
-    for (i64 w = blockIdx.x; w < items; w += gridDim.x) epilogue(w);
+    for (int w = blockIdx.x; w < items; w += gridDim.x) epilogue(params(w));
     return;
   }
 
-  // item ids for the loads of iterations 0 .. STAGES-1
-  const int pre = (STAGES - 1) / ktiles + 1;  // sequence numbers 0 .. pre-1
+  // ---- prologue: claim the items of the first STAGES-1 loads
+  const int pre = (STAGES - 1) / ktiles + 1;
   if (tid == 0)
     for (int q = 0; q < pre; ++q) ring[q % RING] = claim(q);
-  i64 claimed = pre;
+  int claimed = pre;
   __syncthreads();
+  int p_seq = 0, p_kt = 0, p_stage = 0;  // producer: next (item, k-tile, stage) to load
+  int p_item = ring[0];
+  bool p_need = false;
+  TileP ptp = params(p_item < items ? p_item : 0);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    const i64 item = ring[(s / ktiles) % RING];
-    if (item < items) load_stage(s, item, s % ktiles);
+    if (p_item < items) load_stage(p_stage, ptp, p_kt);
     cp_async_commit();
+    p_stage = p_stage + 1 == STAGES ? 0 : p_stage + 1;
+    if (++p_kt == ktiles) {
+      p_kt = 0;
+      ++p_seq;
+      p_item = ring[p_seq % RING];
+      if (p_item < items) ptp = params(p_item);
+    }
   }
 
-  for (i64 it = 0;; ++it) {
-    const i64 item = ring[(it / ktiles) % RING];
-    if (item >= items) break;
+  // ---- main loop over the flattened (item, k-tile) sequence
+  int c_seq = 0, c_kt = 0, c_stage = 0;  // consumer
+  int c_item = ring[0];
+  TileP ctp = params(c_item < items ? c_item : 0);
+  while (c_item < items) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
-      const i64 nk = it + STAGES - 1;
-      const i64 nitem = ring[(nk / ktiles) % RING];
-      if (nitem < items) load_stage((int)(nk % STAGES), nitem, (int)(nk % ktiles));
+      if (p_need) {  // claimed in the previous iteration, published by the barrier above
+        p_item = ring[p_seq % RING];
+        if (p_item < items) ptp = params(p_item);
+        p_need = false;
+      }
+      if (p_item < items) load_stage(p_stage, ptp, p_kt);
       cp_async_commit();
-      // the next iteration's load may start a new sequence number: claim it now
-      // (published by that iteration's barrier)
-      const i64 nseq = (nk + 1) / ktiles;
-      if (nseq >= claimed) {
-        if (tid == 0) ring[nseq % RING] = (nitem < items) ? claim(nseq) : items;
-        claimed = nseq + 1;
+      p_stage = p_stage + 1 == STAGES ? 0 : p_stage + 1;
+      if (++p_kt == ktiles) {
+        p_kt = 0;
+        ++p_seq;
+        p_need = true;
+        if (p_seq >= claimed) {
+          if (tid == 0) ring[p_seq % RING] = (p_item < items) ? claim(p_seq) : items;
+          claimed = p_seq + 1;
+        }
       }
     }
-    const double* As = smem + (int)(it % STAGES) * STAGE_ELEMS;
+    const double* As = smem + c_stage * STAGE_ELEMS;
     const double* Bs = As + A_ELEMS;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
@@ -227,9 +272,16 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni], a[mi], b[ni]);
+        for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni], b[ni], a[mi]);  // transposed tile
     }
-    if ((int)(it % ktiles) == ktiles - 1) epilogue(item);
+    c_stage = c_stage + 1 == STAGES ? 0 : c_stage + 1;
+    if (++c_kt == ktiles) {
+      epilogue(ctp);
+      c_kt = 0;
+      ++c_seq;
+      c_item = ring[c_seq % RING];  // claimed before the producer needed it
+      if (c_item < items) ctp = params(c_item);
+    }
   }
   cp_async_wait<0>();
   if (sched) {

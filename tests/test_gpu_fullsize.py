@@ -146,7 +146,10 @@ def test_c5_fullsize(ctx):
     del Y1, Y2
     assert _orth_err_power(U) <= 1e-12
     assert _orth_err_power(V) <= 1e-12
-    assert bool((torch.tril(T, -1) == 0).all())
+    del U, V
+    torch.cuda.empty_cache()
+    for c0 in range(0, n, 4096):  # strict lower part exactly zero (in column chunks: no 32 GB temporary)
+        assert bool((torch.tril(T[:, c0:c0 + 4096], -1 - c0) == 0).all())
     assert abs(float(torch.linalg.norm(T)) - nA) <= 1e-12 * nA
     d = torch.diagonal(T).abs()
     assert abs(float(torch.log(d).sum()) - lad) <= 1e-4
