@@ -6,7 +6,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "librandutv.so")
+# RUTV_BUILD_OUT / RUTV_NVCC_EXTRA: build a variant library elsewhere (A/B tuning only)
+OUT = os.environ.get("RUTV_BUILD_OUT", os.path.join(HERE, "librandutv.so"))
+EXTRA = os.environ.get("RUTV_NVCC_EXTRA", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
@@ -31,7 +33,7 @@ def _compile(src, objdir, verbose):
         d = nccl_dir()
         extra = ["-I", os.path.join(d, "include"),
                  f'-DRUTV_NCCL_PATH="{os.path.join(d, "lib", "libnccl.so.2")}"']
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -45,7 +47,7 @@ def build(verbose=False, force=False):
         t = os.path.getmtime(OUT)
         if all(os.path.getmtime(p) < t for p in srcs + hdrs + [__file__]):
             return OUT
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build") if OUT == os.path.join(HERE, "librandutv.so") else OUT + ".objs"
     os.makedirs(objdir, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         results = list(ex.map(lambda s: _compile(s, objdir, verbose), SOURCES))

@@ -21,6 +21,7 @@
 //   * Skinny outputs with long K (A_t^T G, W^T X: K up to 262144) use split-K;
 //     partial tiles go to a workspace and a second kernel sums them in a fixed
 //     order, so results are bitwise deterministic run to run.
+#include <cmath>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -29,24 +30,26 @@ namespace rutv {
 
 namespace {
 
-constexpr int BK = 16, THREADS = 256, PAD = 4;
+constexpr int BK = 16, PAD = 4;
 
 // Tile configurations (8 warps each):
-//   Cfg<128,128,2,4,1>: warp tile 64x32, 64 accumulators/thread, 4 stages, 1 CTA/SM
 //   Cfg<128, 64,4,3,2>: warp tile 32x32, 32 accumulators/thread, 3 stages, 2 CTAs/SM --
 //                       one CTA's epilogue (C read-modify-write) overlaps the other's
 //                       DMMA main loop; used for the short-K rank-b updates.
-template <int BM_, int BN_, int WM_, int STAGES_, int MINB_>
+template <int BM_, int BN_, int WM_, int STAGES_, int MINB_, int NW_ = 8>
 struct Cfg {
-  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = 8 / WM_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = NW_ / WM_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int THREADS = 32 * NW_;
   static constexpr int MI = BM / (WM * 8), NI = BN / (WN * 8);
   static constexpr int A_ELEMS = (BK * (BM + PAD) > BM * (BK + PAD)) ? BK * (BM + PAD) : BM * (BK + PAD);
   static constexpr int B_ELEMS = (BK * (BN + PAD) > BN * (BK + PAD)) ? BK * (BN + PAD) : BN * (BK + PAD);
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
 };
-using CfgBig = Cfg<128, 128, 2, 4, 1>;
 using CfgHalf = Cfg<128, 64, 4, 3, 2>;
+//   Cfg< 64, 64,2,3,3,4>: 4 warps (2 x 2) of 32 x 32, 3 stages, 3 CTAs/SM (the CUTLASS
+//                       d884 64x64 shape cuBLAS picks on B200 at 98 % DMMA-pipe use)
+using CfgSmall = Cfg<64, 64, 2, 3, 3, 4>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -72,7 +75,7 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 
 // Copy one Lc x Lo tile (Lc along the global contiguous dimension) into shared
 // memory rows of length Lc + PAD.  lim_c / lim_o: first invalid global index.
-template <int Lc, int Lo, int VEC>
+template <int Lc, int Lo, int VEC, int THREADS>
 __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__ g, i64 ld, i64 c0, i64 o0,
                                           i64 lim_c, i64 lim_o, int tid) {
   constexpr int CPR = Lc / VEC;           // chunks per row
@@ -92,6 +95,27 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
   }
 }
 
+// Interior fast path of load_tile: `g` is this thread's first chunk source,
+// successive chunks are `gstep` elements apart, no bounds checks (the caller
+// guarantees the tile and the k-tile are fully inside the operand).  ~3
+// instructions per cp.async instead of ~25 for the general path.
+template <int Lc, int Lo, int VEC, int THREADS>
+__device__ __forceinline__ void load_tile_fast(double* sm, const double* __restrict__ g, i64 gstep, int tid) {
+  constexpr int CPR = Lc / VEC, RPI = THREADS / CPR, NIT = CPR * Lo / THREADS;
+  static_assert(THREADS % CPR == 0 && (CPR * Lo) % THREADS == 0, "tile/threads mismatch");
+  const int o = tid / CPR, ci = (tid % CPR) * VEC;
+  double* d = sm + o * (Lc + PAD) + ci;
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) cp_async<VEC>(smem_u32(d + it * RPI * (Lc + PAD)), g + it * gstep, VEC * 8);
+}
+
+// this thread's first chunk within an Lc x Lo tile whose origin is (c0, o0)
+template <int Lc, int VEC, int THREADS>
+__device__ __forceinline__ const double* chunk0(const double* g, i64 ld, i64 c0, i64 o0, int tid) {
+  constexpr int CPR = Lc / VEC;
+  return g + (c0 + (tid % CPR) * VEC) + (o0 + tid / CPR) * ld;
+}
+
 // Persistent tile loop.  The work items are w = 0 .. tiles*splits-1 (tile
 // w % tiles = (t % gm, t / gm), K-split w / tiles; consecutive items share the
 // B panel in L2).  With `sched` (two device ints, zero between launches) the
@@ -104,8 +128,8 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
 // while the current item's epilogue (C read-modify-write) runs.
 constexpr int RING = 8;  // in-flight item ids (>= STAGES + 1)
 
-template <class CF, bool TA, bool TB, int VA, int VB>
-__global__ void __launch_bounds__(THREADS, CF::MINB)
+template <class CF, bool TA, bool TB, int VA, int VB, bool CPF>
+__global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     dgemm_kernel(i64 M, i64 N, i64 K, double alpha, const double* __restrict__ A, i64 lda,
                  const double* __restrict__ B, i64 ldb, double beta, double* __restrict__ C, i64 ldc,
                  i64 kchunk, int splits, double* __restrict__ part, int* __restrict__ sched) {
@@ -133,21 +157,50 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
   auto params = [&](int item) {
     const int tile = item % tiles, split = item / tiles;
     TileP tp;
-    tp.m0 = (i64)(tile % gm) * BM;
-    tp.n0 = (i64)(tile / gm) * BN;
+    // raster along the shorter side: consecutive items share the panel of the
+    // longer side (skinny A_t^T G: the 4 N-tiles of an A_t panel run together
+    // and read it from DRAM once instead of four times)
+    if (gn <= gm) {
+      tp.m0 = (i64)(tile / gn) * BM;
+      tp.n0 = (i64)(tile % gn) * BN;
+    } else {
+      tp.m0 = (i64)(tile % gm) * BM;
+      tp.n0 = (i64)(tile / gm) * BN;
+    }
     tp.kb = (i64)split * kchunk;
     tp.ke = (tp.kb + kchunk < K) ? tp.kb + kchunk : K;
     tp.split = split;
     return tp;
   };
+  // producer-side per-item constants of the fast path: the thread's first chunk
+  // at k-tile 0 of each operand, and whether the tile is interior in M / N
+  constexpr int THR = CF::THREADS;
+  constexpr int RPI_A = THR / ((TA ? BK : BM) / VA), RPI_B = THR / ((TB ? BN : BK) / VB);
+  const i64 gstepA = (i64)RPI_A * lda, gstepB = (i64)RPI_B * ldb;
+  const i64 kstepA = TA ? (i64)BK : (i64)BK * lda, kstepB = TB ? (i64)BK * ldb : (i64)BK;
+  const double* pa0 = A;
+  const double* pb0 = B;
+  bool p_inner = false;
+  auto producer_item = [&](const TileP& tp) {
+    pa0 = TA ? chunk0<BK, VA, THR>(A, lda, tp.kb, tp.m0, tid) : chunk0<BM, VA, THR>(A, lda, tp.m0, tp.kb, tid);
+    pb0 = TB ? chunk0<BN, VB, THR>(B, ldb, tp.n0, tp.kb, tid) : chunk0<BK, VB, THR>(B, ldb, tp.kb, tp.n0, tid);
+    p_inner = tp.m0 + BM <= M && tp.n0 + BN <= N;
+  };
   auto load_stage = [&](int stage, const TileP& tp, int kt) {
     double* As = smem + stage * STAGE_ELEMS;
     double* Bs = As + A_ELEMS;
     const i64 k0 = tp.kb + (i64)kt * BK;
-    if constexpr (!TA) load_tile<BM, BK, VA>(As, A, lda, tp.m0, k0, M, tp.ke, tid);   // rows: k, contiguous m
-    else load_tile<BK, BM, VA>(As, A, lda, k0, tp.m0, tp.ke, M, tid);                 // rows: m, contiguous k
-    if constexpr (!TB) load_tile<BK, BN, VB>(Bs, B, ldb, k0, tp.n0, tp.ke, N, tid);   // rows: n, contiguous k
-    else load_tile<BN, BK, VB>(Bs, B, ldb, tp.n0, k0, N, tp.ke, tid);                 // rows: k, contiguous n
+    if (p_inner && k0 + BK <= tp.ke) {
+      if constexpr (!TA) load_tile_fast<BM, BK, VA, THR>(As, pa0 + kt * kstepA, gstepA, tid);
+      else load_tile_fast<BK, BM, VA, THR>(As, pa0 + kt * kstepA, gstepA, tid);
+      if constexpr (!TB) load_tile_fast<BK, BN, VB, THR>(Bs, pb0 + kt * kstepB, gstepB, tid);
+      else load_tile_fast<BN, BK, VB, THR>(Bs, pb0 + kt * kstepB, gstepB, tid);
+      return;
+    }
+    if constexpr (!TA) load_tile<BM, BK, VA, THR>(As, A, lda, tp.m0, k0, M, tp.ke, tid);   // rows: k, contiguous m
+    else load_tile<BK, BM, VA, THR>(As, A, lda, k0, tp.m0, tp.ke, M, tid);                 // rows: m, contiguous k
+    if constexpr (!TB) load_tile<BK, BN, VB, THR>(Bs, B, ldb, k0, tp.n0, tp.ke, N, tid);   // rows: n, contiguous k
+    else load_tile<BN, BK, VB, THR>(Bs, B, ldb, tp.n0, k0, N, tp.ke, tid);                 // rows: k, contiguous n
   };
 
   double acc[MI][NI][2];
@@ -214,6 +267,7 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
   int p_item = ring[0];
   bool p_need = false;
   TileP ptp = params(p_item < items ? p_item : 0);
+  producer_item(ptp);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (p_item < items) load_stage(p_stage, ptp, p_kt);
@@ -223,21 +277,50 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
       p_kt = 0;
       ++p_seq;
       p_item = ring[p_seq % RING];
-      if (p_item < items) ptp = params(p_item);
+      if (p_item < items) {
+        ptp = params(p_item);
+        producer_item(ptp);
+      }
     }
   }
 
+  const int pf_kt = ktiles > 3 ? ktiles - 3 : 0;  // k-tile at which the C tile is prefetched
+  // fragments of one k-step (4 of K), double-buffered in registers: the loads
+  // for step kk+1 are issued before the DMMAs of step kk, and the per-k-tile
+  // wait + barrier sits before the LAST step's DMMAs (whose fragments are
+  // already in registers), so the barrier overlaps the DMMA pipe's backlog
+  auto load_frags = [&](double (&a)[MI], double (&b)[NI], int stage, int kk) {
+    const double* As = smem + stage * STAGE_ELEMS;
+    const double* Bs = As + A_ELEMS;
+    const int k = kk * 4 + t;
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi) {
+      const int row = wm * (MI * 8) + mi * 8 + g;
+      a[mi] = TA ? As[row * (BK + PAD) + k] : As[k * (BM + PAD) + row];
+    }
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+      const int col = wn * (NI * 8) + ni * 8 + g;
+      b[ni] = TB ? Bs[k * (BN + PAD) + col] : Bs[col * (BK + PAD) + k];
+    }
+  };
   // ---- main loop over the flattened (item, k-tile) sequence
   int c_seq = 0, c_kt = 0, c_stage = 0;  // consumer
   int c_item = ring[0];
   TileP ctp = params(c_item < items ? c_item : 0);
+  double fa[2][MI], fb[2][NI];
+  cp_async_wait<STAGES - 2>();
+  __syncthreads();
+  load_frags(fa[0], fb[0], 0, 0);
   while (c_item < items) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      if (p_need) {  // claimed in the previous iteration, published by the barrier above
+    {  // producer: the copies of stage it + STAGES - 1 (last read in iteration it - 1,
+       // before that iteration's barrier)
+      if (p_need) {  // claimed in the previous iteration, published by its barrier
         p_item = ring[p_seq % RING];
-        if (p_item < items) ptp = params(p_item);
+        if (p_item < items) {
+          ptp = params(p_item);
+          producer_item(ptp);
+        }
         p_need = false;
       }
       if (p_item < items) load_stage(p_stage, ptp, p_kt);
@@ -253,28 +336,34 @@ __global__ void __launch_bounds__(THREADS, CF::MINB)
         }
       }
     }
-    const double* As = smem + c_stage * STAGE_ELEMS;
-    const double* Bs = As + A_ELEMS;
+    const int n_stage = c_stage + 1 == STAGES ? 0 : c_stage + 1;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
-      const int k = kk * 4 + t;
-      double a[MI], b[NI];
-#pragma unroll
-      for (int mi = 0; mi < MI; ++mi) {
-        const int row = wm * (MI * 8) + mi * 8 + g;
-        a[mi] = TA ? As[row * (BK + PAD) + k] : As[k * (BM + PAD) + row];
-      }
-#pragma unroll
-      for (int ni = 0; ni < NI; ++ni) {
-        const int col = wn * (NI * 8) + ni * 8 + g;
-        b[ni] = TB ? Bs[k * (BN + PAD) + col] : Bs[col * (BK + PAD) + k];
+      if (kk == BK / 4 - 1) {
+        cp_async_wait<STAGES - 2>();  // stage n_stage has landed (this thread's copies) ...
+        __syncthreads();              // ... and everyone's
+        load_frags(fa[0], fb[0], n_stage, 0);
+      } else {
+        load_frags(fa[(kk + 1) & 1], fb[(kk + 1) & 1], c_stage, kk + 1);
       }
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni], b[ni], a[mi]);  // transposed tile
+        for (int ni = 0; ni < NI; ++ni) dmma884(acc[mi][ni], fb[kk & 1][ni], fa[kk & 1][mi]);  // transposed tile
     }
-    c_stage = c_stage + 1 == STAGES ? 0 : c_stage + 1;
+    c_stage = n_stage;
+    // the epilogue's C read is latency-bound (ncu: its DFMAs carried ~25 % of the
+    // stall samples): pull the item's C tile into L2 a few k-tiles ahead
+    // (a separate instantiation: the branch alone costs the long-K products ~15 %)
+    if constexpr (CPF) if (c_kt == pf_kt) {
+#pragma unroll
+      for (int h = 0; h < (BM / 16) * BN / CF::THREADS; ++h) {
+        const int line = tid + h * CF::THREADS;           // 128-byte lines: BM/16 per column
+        const int cc = line / (BM / 16), rr = (line % (BM / 16)) * 16;
+        const i64 row = ctp.m0 + rr, col = ctp.n0 + cc;
+        if (row < M && col < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + row + col * ldc));
+      }
+    }
     if (++c_kt == ktiles) {
       epilogue(ctp);
       c_kt = 0;
@@ -321,17 +410,17 @@ bool use_sched(const Launch& L) {
   return v != 0 && L.sched != nullptr;
 }
 
-template <class CF, bool TA, bool TB, int VA, int VB>
+template <class CF, bool TA, bool TB, int VA, int VB, bool CPF>
 int launch_t(const Launch& L, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
              i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
   const int splits = (int)((K + kchunk - 1) / (kchunk > 0 ? kchunk : 1));
   static bool attr_set = false;  // per instantiation; first call from any ctx
   if (!attr_set) {
-    RUTV_CUDA(cudaFuncSetAttribute(dgemm_kernel<CF, TA, TB, VA, VB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RUTV_CUDA(cudaFuncSetAttribute(dgemm_kernel<CF, TA, TB, VA, VB, CPF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)CF::SMEM_BYTES));
     attr_set = true;
   }
-  dgemm_kernel<CF, TA, TB, VA, VB><<<grid, THREADS, CF::SMEM_BYTES, L.stream>>>(M, N, K, alpha, A, lda, B, ldb,
+  dgemm_kernel<CF, TA, TB, VA, VB, CPF><<<grid, CF::THREADS, CF::SMEM_BYTES, L.stream>>>(M, N, K, alpha, A, lda, B, ldb,
                                                                                beta, C, ldc, kchunk, splits < 1 ? 1 : splits, part,
                                                                                use_sched(L) ? L.sched : nullptr);
   L.count();
@@ -339,41 +428,51 @@ int launch_t(const Launch& L, i64 M, i64 N, i64 K, double alpha, const double* A
   return 0;
 }
 
-template <class CF, bool TA, bool TB>
+template <class CF, bool TA, bool TB, bool CPF>
 int launch_v(const Launch& L, int va, int vb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
              const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
   if (va == 2 && vb == 2)
-    return launch_t<CF, TA, TB, 2, 2>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  if (va == 2) return launch_t<CF, TA, TB, 2, 1>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  if (vb == 2) return launch_t<CF, TA, TB, 1, 2>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  return launch_t<CF, TA, TB, 1, 1>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+    return launch_t<CF, TA, TB, 2, 2, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (va == 2)
+    return launch_t<CF, TA, TB, 2, 1, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (vb == 2)
+    return launch_t<CF, TA, TB, 1, 2, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  return launch_t<CF, TA, TB, 1, 1, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+}
+
+template <class CF, bool TA, bool TB>
+int launch_p(const Launch& L, int va, int vb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+             const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
+  // C prefetch instantiation for read-modify-write epilogues (beta != 0, no split-K)
+  if (beta != 0.0 && part == nullptr)
+    return launch_v<CF, TA, TB, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  return launch_v<CF, TA, TB, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
 }
 
 template <class CF>
 int launch_cfg(const Launch& L, bool ta, bool tb, int va, int vb, i64 M, i64 N, i64 K, double alpha,
                const double* A, i64 lda, const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid,
                i64 kchunk, double* part) {
-  if (!ta && !tb) return launch_v<CF, false, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  if (ta && !tb) return launch_v<CF, true, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  if (!ta && tb) return launch_v<CF, false, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  return launch_v<CF, true, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (!ta && !tb) return launch_p<CF, false, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (ta && !tb) return launch_p<CF, true, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  if (!ta && tb) return launch_p<CF, false, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+  return launch_p<CF, true, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
 }
 
-// Tile choice: the 128 x 64 two-CTAs-per-SM tile wins on every randUTV shape
-// measured on B200 (tools/bench_kernels.py, profiles/gemm_cfg_r01.txt): rank-b
-// updates 17.4 -> 24.2 TFLOP/s (one CTA's C read-modify-write overlaps the other
-// CTA's main loop), skinny tall-K products 26.3 -> 30.7, square 30.2 -> 32.0.
-// RUTV_GEMM_CFG=0 forces the 128 x 128 one-CTA tile (tuning only).
+// Tile choice (RUTV_GEMM_CFG = 1 | 2 forces one; tuning only): 2 = 64 x 64 tile,
+// 4 warps, 3 CTAs/SM (default); 1 = 128 x 64 tile, 8 warps, 2 CTAs/SM.  The
+// 128 x 128 one-CTA/SM tile of round 1 lost on every randUTV shape
+// (profiles/gemm_cfg_r01.txt) and is gone.
 int choose_cfg(i64 M, i64 N, i64 K) {
   static int forced = -2;
   if (forced == -2) {
     const char* e = getenv("RUTV_GEMM_CFG");
     forced = e ? atoi(e) : -1;
   }
-  if (forced == 0 || forced == 1) return forced;
   (void)M;
   (void)N;
   (void)K;
+  if (forced == 1 || forced == 2) return forced;
   return 1;
 }
 
@@ -393,23 +492,39 @@ inline int vec_of(const double* p, i64 ld) {
 
 }  // namespace
 
-int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
-                 const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
-  if (M <= 0 || N <= 0) return 0;
-  const int cfg = choose_cfg(M, N, K);
-  const i64 BM = 128, BN = cfg == 1 ? 64 : 128;
-  const i64 gm = (M + BM - 1) / BM, gn = (N + BN - 1) / BN;
+namespace {
+
+template <class CF>
+int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
+  const i64 gm = (M + CF::BM - 1) / CF::BM, gn = (N + CF::BN - 1) / CF::BN;
   const i64 tiles = gm * gn;
+  if (tiles > (i64)1 << 30) return -5;
+  // resident CTAs.  All items cost the same, so the grid runs in waves of
+  // `resident` items and a partial last wave idles the rest of the chip
+  // (skinny A_t^T G: 512 tiles on 296 slots = 1.73 waves).  Choose the K split
+  // minimising a time model: waves x k-tiles per item x (one k-tile of one
+  // item at peak share) + the split-K reduction (partials written + read at
+  // HBM speed, plus a launch).
+  const i64 resident = (i64)CF::MINB * L.device_sms;
   i64 splits = 1;
-  const i64 target = (cfg == 1 ? 4 : 2) * (i64)L.device_sms;
-  if (ws && K > 0 && tiles < target) {
-    splits = (target + tiles - 1) / tiles;
+  if (ws && K > 0) {
     const i64 maxk = K / (8 * BK);  // at least 128 of K per split
-    if (splits > maxk) splits = maxk;
-    const i64 maxws = ws_elems / (M * N);
-    if (splits > maxws) splits = maxws;
-    if (splits > 64) splits = 64;
-    if (splits < 1) splits = 1;
+    i64 maxs = ws_elems / (M * N);
+    if (maxs > maxk) maxs = maxk;
+    if (maxs > 64) maxs = 64;
+    const double t_kt = 2.0 * CF::BM * CF::BN * BK / (37e12 / (double)resident);  // s per k-tile per item
+    double best = 1e30;
+    for (i64 sp = 1; sp <= (maxs > 1 ? maxs : 1); ++sp) {
+      const i64 kch = ((K + sp - 1) / sp + BK - 1) / BK;
+      const double waves = std::ceil((double)(tiles * sp) / (double)resident);
+      double t = waves * (double)kch * t_kt;
+      if (sp > 1) t += (double)(sp + 2) * (double)M * (double)N * 8.0 / 5e12 + 3e-6;
+      if (t < best * (1.0 - 1e-6)) {
+        best = t;
+        splits = sp;
+      }
+    }
   }
   i64 kchunk = K;
   if (splits > 1) {
@@ -420,15 +535,11 @@ int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double 
   const int va = vec_of(A, lda), vb = vec_of(B, ldb);
   const size_t pe = L.pbegin();
   // persistent grid: at most one wave of resident CTAs over all tiles x splits
-  const i64 resident = (i64)(cfg == 1 ? 2 : 1) * L.device_sms;
   i64 ctas = tiles * splits;
   if (persistent_on() && ctas > resident) ctas = resident;
   dim3 grid((unsigned)ctas, 1, 1);
   double* part = splits > 1 ? ws : nullptr;
-  const int st = cfg == 1
-                     ? launch_cfg<CfgHalf>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part)
-                     : launch_cfg<CfgBig>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  if (st) return st;
+  RUTV_TRY(launch_cfg<CF>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part));
   if (splits > 1) {
     const i64 total = M * N;
     i64 blocks = (total + 255) / 256;
@@ -441,6 +552,16 @@ int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double 
   L.pend(PK_DGEMM, 2.0 * (double)M * (double)N * (double)K,
          8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2.0 : 1.0)), pe);
   return 0;
+}
+
+}  // namespace
+
+int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                 const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
+  if (M <= 0 || N <= 0) return 0;
+  if (choose_cfg(M, N, K) == 1)
+    return launch_with<CfgHalf>(L, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_elems);
+  return launch_with<CfgSmall>(L, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_elems);
 }
 
 }  // namespace rutv

@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librandutv.so")
+LIB_PATH = os.environ.get("RUTV_LIB", os.path.join(_HERE, "librandutv.so"))  # RUTV_LIB: A/B variants only
 
 RANDUTV_NO_UV = 1
 RANDUTV_CHECK_FINITE = 2

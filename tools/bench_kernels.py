@@ -49,6 +49,34 @@ def gemm_cases(ctx):
         del A, B, C
 
 
+def cublas_cases():
+    """torch.matmul (cuBLAS DGEMM) on the same shapes: the library-GEMM reference point."""
+    cases = [("S2 Y=At^T G c3", 1, 0, 16384, 256, 16384), ("S5 X-=Z2 W^T c3", 0, 1, 16384, 16384, 256),
+             ("S7 X-=W Z2 c3", 0, 0, 16384, 16128, 256), ("square 8192", 0, 0, 8192, 8192, 8192)]
+    for label, ta, tb, M, N, K in cases:
+        A = colmajor(K, M) if ta else colmajor(M, K)
+        B = colmajor(N, K) if tb else colmajor(K, N)
+        C = colmajor(M, N)
+        A.normal_()
+        B.normal_()
+        C.normal_()
+        opA = A.t() if ta else A
+        opB = B.t() if tb else B
+        f = lambda: C.addmm_(opA, opB, beta=1.0, alpha=-1.0)
+        f()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        print(json.dumps({"kernel": "cublas_dgemm", "case": label, "M": M, "N": N, "K": K, "ms": round(ms, 4),
+                          "tflops": round(2 * M * N * K / (ms * 1e-3) / 1e12, 3)}))
+        del A, B, C
+
+
 def gemm_diag(ctx):
     """Separates main-loop from per-tile (prologue + epilogue) cost of the rank-b update."""
     M = N = 16384
@@ -110,6 +138,8 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["gemm", "qr", "svd"]
     if "gemm" in which:
         gemm_cases(ctx)
+    if "cublas" in which:
+        cublas_cases()
     if "gemmdiag" in which:
         gemm_diag(ctx)
     if "qr" in which:

@@ -1,0 +1,9 @@
+python paper_2002_06960_b200/build.py > /dev/null || exit 1
+timeout 300 python tools/bench_kernels.py gemm cublas 2>&1 | python -c "
+import sys, json
+for l in sys.stdin:
+    if l.startswith('{'):
+        d = json.loads(l); print(f\"{d['kernel']:14s} {d['case']:24s} {d['tflops']:7.2f}\")"
+timeout 600 python bench.py --steps 2 --warmup 2 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "
+import sys, json
+d = json.loads(sys.stdin.read()); print('bench', d['value'], d['ms_per_step'], d['roofline']['achieved'])"
