@@ -10,17 +10,28 @@
 // sm_100a has no FP64 kind of tcgen05.mma (ptxas rejects .kind::f64), so FP64
 // tensor work is the warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4); the
 // measured chip peak is 37.0 TFLOP/s (profiles/fp64_peak_r01.json), equal to
-// the DFMA peak, and DMMA needs 8x fewer issue slots.  Design:
-//   * CTA tile 128 x 128, BK = 16, 256 threads = 8 warps (2 x 4), warp tile
-//     64 x 32 = 8 x 4 DMMA tiles, 64 FP64 accumulators per thread in registers.
-//   * Operands staged global -> shared with cp.async (16 B when the operand is
-//     16 B aligned with an even leading dimension, else 8 B), 4-stage ring.
-//     The shared layout follows the global contiguous dimension (m- or k-major)
-//     with a row pad of 4 doubles, which makes every fragment load conflict-free
-//     (the 16 lanes of each half-warp hit 16 distinct 8-byte bank pairs).
-//   * Skinny outputs with long K (A_t^T G, W^T X: K up to 262144) use split-K;
-//     partial tiles go to a workspace and a second kernel sums them in a fixed
-//     order, so results are bitwise deterministic run to run.
+// the DFMA peak, and DMMA needs 8x fewer issue slots.  Design (each choice
+// measured on B200, profiles/gemm_tuning_r01.txt):
+//   * CTA tile 64 x 64, BK = 16, 128 threads = 4 warps (2 x 2) of 32 x 32
+//     (4 x 4 DMMA tiles, 32 accumulators/thread), 3 cp.async stages, 3 CTAs
+//     per SM -- the shape of the CUTLASS d884 kernel cuBLAS runs at 98 % of the
+//     DMMA pipe.
+//   * Shared layout follows the global contiguous dimension with a 4-double row
+//     pad (conflict-free 64-bit fragment loads); fragments double-buffered in
+//     registers; one wait + barrier per k-tile, placed before the last k-step.
+//   * Interior tiles copy with a bounds-free cp.async path (per-item chunk
+//     pointers, ~3 instructions per 16-byte copy): the general masked path
+//     cost ~25 integer instructions per copy and capped the kernel at ~80 %.
+//   * Persistent grid with a dynamic tile scheduler (per-stream atomic
+//     counter) and a cp.async ring flattened over (item, k-tile), so the next
+//     item's loads overlap the current item's epilogue; the DMMA computes the
+//     transposed 8x8 tile so each lane owns two consecutive rows of C
+//     (16-byte epilogue accesses); read-modify-write epilogues prefetch their C
+//     tile into L2 a few k-tiles ahead.
+//   * Skinny outputs with long K (A_t^T G, W^T X: K up to 262144) split K by a
+//     wave-quantisation time model; partial tiles go to a workspace and a
+//     second kernel sums them in a fixed order, so results are bitwise
+//     deterministic run to run.
 #include <cmath>
 #include <cstdlib>
 
@@ -32,10 +43,8 @@ namespace {
 
 constexpr int BK = 16, PAD = 4;
 
-// Tile configurations (8 warps each):
-//   Cfg<128, 64,4,3,2>: warp tile 32x32, 32 accumulators/thread, 3 stages, 2 CTAs/SM --
-//                       one CTA's epilogue (C read-modify-write) overlaps the other's
-//                       DMMA main loop; used for the short-K rank-b updates.
+// Tile configuration: BM x BN CTA tile, WM x (NW/WM) warps, STAGES-deep ring,
+// MINB CTAs per SM.
 template <int BM_, int BN_, int WM_, int STAGES_, int MINB_, int NW_ = 8>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = NW_ / WM_, STAGES = STAGES_, MINB = MINB_;
@@ -46,7 +55,6 @@ struct Cfg {
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
 };
-using CfgHalf = Cfg<128, 64, 4, 3, 2>;
 //   Cfg< 64, 64,2,3,3,4>: 4 warps (2 x 2) of 32 x 32, 3 stages, 3 CTAs/SM (the CUTLASS
 //                       d884 64x64 shape cuBLAS picks on B200 at 98 % DMMA-pipe use)
 using CfgSmall = Cfg<64, 64, 2, 3, 3, 4>;
@@ -215,6 +223,29 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   // 16-byte load/store in column-major C (half the epilogue instructions).
   const bool cvec = part ? ((M & 1) == 0) : ((((uintptr_t)C & 15) == 0) && ((ldc & 1) == 0));
   auto epilogue = [&](const TileP& tp) {
+    if (!part && cvec && tp.m0 + BM <= M && tp.n0 + BN <= N) {
+      // interior tile: no bounds checks, one base pointer, 16-byte accesses
+      double* cb = C + (tp.m0 + wm * (MI * 8) + 2 * t) + (tp.n0 + wn * (NI * 8) + g) * ldc;
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+          double2* cp = reinterpret_cast<double2*>(cb + mi * 8 + (i64)(ni * 8) * ldc);
+          double2 v;
+          if (beta == 0.0) {
+            v.x = alpha * acc[mi][ni][0];
+            v.y = alpha * acc[mi][ni][1];
+          } else {
+            const double2 c = *cp;
+            v.x = alpha * acc[mi][ni][0] + beta * c.x;
+            v.y = alpha * acc[mi][ni][1] + beta * c.y;
+          }
+          *cp = v;
+          acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        }
+      }
+      return;
+    }
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
       const i64 row = tp.m0 + wm * (MI * 8) + mi * 8 + 2 * t;
@@ -459,23 +490,6 @@ int launch_cfg(const Launch& L, bool ta, bool tb, int va, int vb, i64 M, i64 N, 
   return launch_p<CF, true, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
 }
 
-// Tile choice (RUTV_GEMM_CFG = 1 | 2 forces one; tuning only): 2 = 64 x 64 tile,
-// 4 warps, 3 CTAs/SM (default); 1 = 128 x 64 tile, 8 warps, 2 CTAs/SM.  The
-// 128 x 128 one-CTA/SM tile of round 1 lost on every randUTV shape
-// (profiles/gemm_cfg_r01.txt) and is gone.
-int choose_cfg(i64 M, i64 N, i64 K) {
-  static int forced = -2;
-  if (forced == -2) {
-    const char* e = getenv("RUTV_GEMM_CFG");
-    forced = e ? atoi(e) : -1;
-  }
-  (void)M;
-  (void)N;
-  (void)K;
-  if (forced == 1 || forced == 2) return forced;
-  return 1;
-}
-
 // RUTV_GEMM_PERSIST=0 launches one CTA per tile (tuning comparison only)
 bool persistent_on() {
   static int v = -1;
@@ -559,8 +573,6 @@ int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double a
 int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                  const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
   if (M <= 0 || N <= 0) return 0;
-  if (choose_cfg(M, N, K) == 1)
-    return launch_with<CfgHalf>(L, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_elems);
   return launch_with<CfgSmall>(L, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_elems);
 }
 
