@@ -385,8 +385,8 @@ def run_ours(args):
     # ---- CPU baseline: the oracle on a bounded sample, rank 0, N = 1 only
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        ms, ns = sample_shape(args.config)
-        A_host = np.asfortranarray(A[:ms, :ns].cpu().numpy())
+        sm_, sn_ = sample_shape(args.config)
+        A_host = np.asfortranarray(A[:sm_, :sn_].cpu().numpy())
         cpu = cpu_sample(args.config, A_host, seed)
         cpu = {k: v for k, v in cpu.items() if k not in ("seconds", "flops")}
 
