@@ -33,6 +33,7 @@ struct Profiler {
     double flops;
     double bytes;
     size_t e0, e1;
+    int64_t shape[3];  // GEMM M, N, K (for the RUTV_PROF_DUMP per-launch log)
   };
   std::vector<Rec> recs;
   int64_t launches[PK_COUNT] = {0};
@@ -40,7 +41,7 @@ struct Profiler {
   double flops[PK_COUNT] = {0};
   double bytes[PK_COUNT] = {0};
   size_t begin(cudaStream_t s);
-  void end(cudaStream_t s, int kind, double fl, double by, size_t e0);
+  void end(cudaStream_t s, int kind, double fl, double by, size_t e0, int64_t m = 0, int64_t n = 0, int64_t k = 0);
   void collect();  // after the stream is synchronised
   void reset();
   ~Profiler();
@@ -58,8 +59,8 @@ struct Launch {
     if (counter) *counter += n;
   }
   size_t pbegin() const { return (prof && prof->on) ? prof->begin(stream) : 0; }
-  void pend(int kind, double fl, double by, size_t e0) const {
-    if (prof && prof->on) prof->end(stream, kind, fl, by, e0);
+  void pend(int kind, double fl, double by, size_t e0, int64_t m = 0, int64_t n = 0, int64_t k = 0) const {
+    if (prof && prof->on) prof->end(stream, kind, fl, by, e0, m, n, k);
   }
 };
 

@@ -564,7 +564,7 @@ int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double a
   }
   // algorithmic: 2MNK flops; compulsory bytes: read A, B (and C if beta != 0), write C
   L.pend(PK_DGEMM, 2.0 * (double)M * (double)N * (double)K,
-         8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2.0 : 1.0)), pe);
+         8.0 * ((double)M * K + (double)K * N + (double)M * N * (beta != 0.0 ? 2.0 : 1.0)), pe, M, N, K);
   return 0;
 }
 

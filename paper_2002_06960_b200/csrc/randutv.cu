@@ -57,24 +57,30 @@ size_t Profiler::begin(cudaStream_t s) {
   return used++;
 }
 
-void Profiler::end(cudaStream_t s, int kind, double fl, double by, size_t e0) {
+void Profiler::end(cudaStream_t s, int kind, double fl, double by, size_t e0, int64_t m, int64_t n, int64_t k) {
   const size_t e1 = begin(s);
   if (!on) return;
-  recs.push_back(Rec{kind, fl, by, e0, e1});
+  recs.push_back(Rec{kind, fl, by, e0, e1, {m, n, k}});
 }
 
 void Profiler::collect() {
+  // RUTV_PROF_DUMP=<file>: append one line per recorded launch (tuning only)
+  static const char* dump = getenv("RUTV_PROF_DUMP");
+  FILE* f = dump ? fopen(dump, "a") : nullptr;
   for (const Rec& r : recs) {
     float t = 0.f;
     if (cudaEventElapsedTime(&t, pool[r.e0], pool[r.e1]) != cudaSuccess) {
       cudaGetLastError();
       continue;
     }
+    if (f) fprintf(f, "%d %lld %lld %lld %.6f %.6e\n", r.kind, (long long)r.shape[0], (long long)r.shape[1],
+                   (long long)r.shape[2], t, r.flops);
     launches[r.kind] += 1;
     ms[r.kind] += t;
     flops[r.kind] += r.flops;
     bytes[r.kind] += r.bytes;
   }
+  if (f) fclose(f);
   recs.clear();
   used = 0;
 }
