@@ -151,9 +151,27 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
       }
     }
 #pragma unroll
-    for (int l = 0; l < PSTRIDE; ++l) {
-      const double s2 = warp_sum(acc[l]);
-      if (lane == 0) wred[warp][l] = s2;
+    {
+      // warp reduction of the 32 dot products as a butterfly reduce-scatter:
+      // at stride s every lane sends half of its 2s-value window to lane ^ s and
+      // adds the other half, so after 16+8+4+2+1 = 31 shuffles lane L holds
+      // the warp total of value L (vs 5 x 32 shuffles for 32 separate
+      // all-reductions, which dominated the per-column latency in ncu:
+      // leaf 218 -> 181 us at h = 16384)
+      double* v32 = acc + 1;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        const bool upper = (lane & st) != 0;
+#pragma unroll
+        for (int i = 0; i < st; ++i) {
+          const double send = upper ? v32[i] : v32[i + st];
+          const double keep = upper ? v32[i + st] : v32[i];
+          v32[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
+        }
+      }
+      const double nrm = warp_sum(acc[0]);
+      wred[warp][1 + lane] = v32[0];
+      if (lane == 0) wred[warp][0] = nrm;
     }
     __syncthreads();
     double* pj = partials + (size_t)(jj & 1) * G * PSTRIDE;
