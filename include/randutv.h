@@ -129,12 +129,14 @@ RANDUTV_API int randutv_reset_stats(randutv_ctx* ctx);
 
 /* Per-kernel-class timing with CUDA events recorded on the ctx stream around
  * every launch of the class (measurement support for bench.py's roofline).
- * Kinds: 0 DMMA GEMM (flops = 2MNK), 1 panel-QR leaf, 2 Jacobi SVD, 3 Gaussian.
+ * Kinds: 0 DMMA GEMM (flops = 2MNK), 1 panel-QR leaf, 2 Jacobi SVD, 3 Gaussian,
+ * 4 fold wait (time the main stream waits for the side stream's SVD + folds).
  * randutv_set_profiling(ctx, 1) resets the totals and turns recording on. */
 #define RANDUTV_PROF_DGEMM    0
 #define RANDUTV_PROF_QR_LEAF  1
 #define RANDUTV_PROF_JACOBI   2
 #define RANDUTV_PROF_GAUSSIAN 3
+#define RANDUTV_PROF_FOLD_WAIT 4  /* main stream stalled on the side stream's SVD + folds */
 typedef struct randutv_profile {
   int64_t launches;  /* launches recorded                                    */
   double ms;         /* summed event-to-event device time                    */

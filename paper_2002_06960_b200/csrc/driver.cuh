@@ -89,7 +89,7 @@ int apply_left_t(const Launch& L, Work& w, i64 r, i64 c, i64 bw, double* X, i64 
 // S5 + S7 of the columns right of block i as one rank-2b update (randutv.cu)
 int fused_right_left(const Launch& L, Work& w, i64 m, i64 r, i64 b, i64 kk, i64 c, double* X, i64 ldx,
                      const double* W2, i64 ldw2, const double* Z2, i64 ldz, const double* Wu, i64 ldwu,
-                     const double* TU, i64 ldtu);
+                     const double* TU, i64 ldtu, i64 top = -1);
 bool fuse_left();
 // X(rows x bw) := X M  (M bw x bw), via the temporary Zt
 int right_mult_inplace(const Launch& L, double* Zt, i64 rows, i64 bw, double* X, i64 ldx, const double* M, i64 ldm);

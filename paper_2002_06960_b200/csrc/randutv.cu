@@ -231,8 +231,9 @@ int left_mult_t_inplace(const Launch& L, double* Zt, i64 bw, i64 cols, double* X
 // Temporaries: w.Z (c x b), w.Bt, w.Acat.
 int fused_right_left(const Launch& L, Work& w, i64 m, i64 r, i64 b, i64 kk, i64 c, double* X, i64 ldx,
                      const double* W2, i64 ldw2, const double* Z2, i64 ldz, const double* Wu, i64 ldwu,
-                     const double* TU, i64 ldtu) {
+                     const double* TU, i64 ldtu, i64 top) {
   (void)m;
+  if (top < 0) top = kk;
   if (c <= 0) return 0;
   double* Ytr = w.Bt + c * b;  // second half of Bt: Y^T (c x b, ld c)
   // Pt = X(k:m)^T W_U  (c x b, K = r) -> w.Z (ld c)
@@ -249,7 +250,7 @@ int fused_right_left(const Launch& L, Work& w, i64 m, i64 r, i64 b, i64 kk, i64 
   RUTV_TRY(launch_copy(L, r, b, Z2 + kk, ldz, w.Acat, r));
   RUTV_TRY(launch_copy(L, r, b, Wu, ldwu, w.Acat + r * b, r));
   // X(0:k) -= Z2(0:k) W2^T ; X(k:m) -= Acat Bt^T
-  if (kk > 0) RUTV_TRY(launch_dgemm(L, false, true, kk, c, b, -1.0, Z2, ldz, W2, ldw2, 1.0, X, ldx, nullptr, 0));
+  if (top > 0) RUTV_TRY(launch_dgemm(L, false, true, top, c, b, -1.0, Z2, ldz, W2, ldw2, 1.0, X, ldx, nullptr, 0));
   return launch_dgemm(L, false, true, r, c, 2 * b, -1.0, w.Acat, r, w.Bt, c, 1.0, X + kk, ldx, nullptr, 0);
 }
 
@@ -342,10 +343,13 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
   // S5 for V(:, k:n) first: it does not touch T, so it needs no fold event
   if (P.V) RUTV_TRY(apply_right(L, w, n, s, b, P.V + kk * P.ldv, P.ldv, w.Wv, s, w.TV, b));
-  // S5 for T: all m rows of T(:, k:n) (A2).  Row block i-1 of T(:, k:n) is
-  // written by the side stream's U_s^T T12 fold of step i-1: wait for it.
-  RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
   if (!fuse_left()) {
+    // S5 for T: all m rows of T(:, k:n) (A2).  Row block i-1 of T(:, k:n) is
+    // written by the side stream's U_s^T T12 fold of step i-1: wait for it
+    // (the stall is recorded as profile kind PK_OTHER, "fold wait").
+    const size_t pe = L.pbegin();
+    RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
+    L.pend(PK_OTHER, 0.0, 0.0, pe);
     RUTV_TRY(apply_right(L, w, m, s, b, P.T + kk * P.ldt, P.ldt, w.Wv, s, w.TV, b));
     // S6: QR of the column block in place; keep R, zero below
     RUTV_TRY(panel_qr(L, r, b, At, P.ldt, w.tauU, w.Wu, r, w.TU, b, w.qw));
@@ -353,20 +357,45 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
     RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, P.ldt));
     // S7
     RUTV_TRY(apply_left_t(L, w, r, s - b, b, At + b * P.ldt, P.ldt, w.Wu, r, w.TU, b));
+    if (P.U) RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
   } else {
-    // Z2 = (T(:, k:n) W_V) T_V; the S5 update of column block i alone; S6 on it
+    // The side stream's folds of step i-1 write only row block i-1 of T(:, k:n)
+    // (rows pk = k-b .. k, U_s^T T12), so S5-S7 of every OTHER row run before
+    // waiting for them and the SVD of step i-1 hides behind the whole step:
+    //   rows [0, pk) and [k, m): Z2 = (T W_V) T_V, S5 of column block i, S6 on
+    //   it, the fused S5+S7 rank-2b update, the U update;
+    //   then wait, and S5 of row block i-1 alone (b x s, K = b).
+    const i64 pk = kk > 0 ? kk - b : 0;  // first row of the pending row block
+    const i64 pb = kk - pk;              // its height (0 at step 0)
     double* Tk = P.T + kk * P.ldt;
-    RUTV_TRY(launch_dgemm(L, false, false, m, b, s, 1.0, Tk, P.ldt, w.Wv, s, 0.0, w.Z, m, w.gemm_ws,
+    if (pk > 0)
+      RUTV_TRY(launch_dgemm(L, false, false, pk, b, s, 1.0, Tk, P.ldt, w.Wv, s, 0.0, w.Z, m, w.gemm_ws,
+                            w.gemm_ws_elems));
+    RUTV_TRY(launch_dgemm(L, false, false, r, b, s, 1.0, Tk + kk, P.ldt, w.Wv, s, 0.0, w.Z + kk, m, w.gemm_ws,
                           w.gemm_ws_elems));
-    RUTV_TRY(launch_dgemm(L, false, false, m, b, b, 1.0, w.Z, m, w.TV, b, 0.0, w.Z2, m, nullptr, 0));
-    RUTV_TRY(launch_dgemm(L, false, true, m, b, b, -1.0, w.Z2, m, w.Wv, s, 1.0, Tk, P.ldt, nullptr, 0));
+    if (pk > 0) RUTV_TRY(launch_dgemm(L, false, false, pk, b, b, 1.0, w.Z, m, w.TV, b, 0.0, w.Z2, m, nullptr, 0));
+    RUTV_TRY(launch_dgemm(L, false, false, r, b, b, 1.0, w.Z + kk, m, w.TV, b, 0.0, w.Z2 + kk, m, nullptr, 0));
+    if (pk > 0) RUTV_TRY(launch_dgemm(L, false, true, pk, b, b, -1.0, w.Z2, m, w.Wv, s, 1.0, Tk, P.ldt, nullptr, 0));
+    RUTV_TRY(launch_dgemm(L, false, true, r, b, b, -1.0, w.Z2 + kk, m, w.Wv, s, 1.0, Tk + kk, P.ldt, nullptr, 0));
     RUTV_TRY(panel_qr(L, r, b, At, P.ldt, w.tauU, w.Wu, r, w.TU, b, w.qw));
     RUTV_TRY(launch_triu(L, b, b, At, P.ldt));
     RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, P.ldt));
     RUTV_TRY(fused_right_left(L, w, m, r, b, kk, s - b, P.T + (kk + b) * P.ldt, P.ldt, w.Wv + b, s, w.Z2, m, w.Wu, r,
-                              w.TU, b));
+                              w.TU, b, pk));
+    if (P.U) RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
+    {
+      const size_t pe = L.pbegin();
+      RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
+      L.pend(PK_OTHER, 0.0, 0.0, pe);
+    }
+    if (pb > 0) {
+      // S5 of the pending row block: T(pk:k, k:n) -= ((T(pk:k, k:n) W_V) T_V) W_V^T
+      RUTV_TRY(launch_dgemm(L, false, false, pb, b, s, 1.0, Tk + pk, P.ldt, w.Wv, s, 0.0, w.Z + pk, m, w.gemm_ws,
+                            w.gemm_ws_elems));
+      RUTV_TRY(launch_dgemm(L, false, false, pb, b, b, 1.0, w.Z + pk, m, w.TV, b, 0.0, w.Z2 + pk, m, nullptr, 0));
+      RUTV_TRY(launch_dgemm(L, false, true, pb, s, b, -1.0, w.Z2 + pk, m, w.Wv, s, 1.0, Tk + pk, P.ldt, nullptr, 0));
+    }
   }
-  if (P.U) RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
   if (P.record_lefts) RUTV_TRY(record_left_w(L, w, P, (int)i, r, b));
   // S8, S9 on the side stream, overlapping S1-S4 of step i+1
   RUTV_CUDA(cudaEventRecord(P.eR, L.stream));
@@ -382,7 +411,11 @@ int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   if (s <= 0) return 0;
   double* At = P.T + kk + kk * P.ldt;
   const bool tall = r > s;
-  RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));  // previous step's folds
+  {
+    const size_t pe = L.pbegin();
+    RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));  // previous step's folds
+    L.pend(PK_OTHER, 0.0, 0.0, pe);
+  }
   if (tall) {
     RUTV_TRY(panel_qr(L, r, s, At, P.ldt, w.tauU, w.Wu, r, w.TU, P.b, w.qw));
     RUTV_TRY(launch_triu(L, s, s, At, P.ldt));

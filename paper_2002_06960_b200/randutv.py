@@ -49,7 +49,7 @@ class HostReport(ctypes.Structure):
                 ("wall_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("d2h_ms", ctypes.c_double)]
 
 
-PROF_KINDS = {"dgemm": 0, "qr_leaf": 1, "jacobi": 2, "gaussian": 3}
+PROF_KINDS = {"dgemm": 0, "qr_leaf": 1, "jacobi": 2, "gaussian": 3, "fold_wait": 4}
 
 SIGNATURES = {
     "randutv_create": (_int, [ctypes.POINTER(_vp), _int, _vp]),
