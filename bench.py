@@ -484,10 +484,13 @@ def run_host_streamed(args):
     real = sum(r["wall_ms"] for r in reps) / len(reps)
     io = sum(r["h2d_ms"] + r["d2h_ms"] for r in reps) / len(reps)
     r0 = reps[-1]
+    if not uv:
+        cfgd = config_dict(args.config, 1)
+        cfgd["workload"] = cfgd["workload"].replace("with U and V", "T only (no orthonormal matrices)")
     line = {"metric": METRIC, "value": round(F / (real * 1e-3) / 1e9, 2), "unit": "GFLOP/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(real, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(config_dict(args.config, 1), mode="host-streamed", build_uv=uv,
+            "config": dict(config_dict(args.config, 1) if uv else cfgd, mode="host-streamed", build_uv=uv, flops_per_step=F,
                            device_cache_bytes=cache, cache_slots=r0["cache_slots"]),
             "table1": {"computational_time_s": comp_ms * 1e-3, "io_time_s": io * 1e-3, "real_time_s": real * 1e-3,
                        "real_over_comp": real / comp_ms, "comp_over_io": comp_ms / io if io > 0 else None,

@@ -388,6 +388,7 @@ struct DistWork {
   double* lefts;   // truncated: per step W_U (m x b, ld r), T_U (b x b), U_s (b x b)
   double* colss;   // truncated: per-local-column sums of squares (n_p), then the total
   double* blk;     // truncated: one row block of U_k (b x k) for the U_s application
+  double* blkz;    // the pending row block's partial (T W_V) rows (b x b) for its AllReduce
 };
 
 size_t carve_dist(Carver& c, DistWork& d, const Layout& lay, i64 K, i64 k) {
@@ -402,6 +403,7 @@ size_t carve_dist(Carver& c, DistWork& d, const Layout& lay, i64 K, i64 k) {
   d.lefts = K > 0 ? c.take<double>(K * (m * b + 2 * b * b)) : nullptr;
   d.colss = K > 0 ? c.take<double>(lay.ncols(lay.p) + 8) : nullptr;
   d.blk = K > 0 ? c.take<double>(b * k) : nullptr;
+  d.blkz = c.take<double>(b * b);
   return c.off;
 }
 
@@ -490,22 +492,35 @@ int dist_sampled_step(DistRun& R, i64 i) {
   RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
   // S5 for the V rows first (every rank holds all of W_V; V is not touched by the folds of T)
   if (R.P.V) RUTV_TRY(apply_right(L, w, R.P.nv, s, b, R.P.V + k * R.P.ldv, R.P.ldv, w.Wv, s, w.TV, b));
-  // S5 for T: Z2 = (T W_V) T_V (AllReduce) -- wait for the previous step's U_s^T A12 fold
-  RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eF, 0));
+  const bool fuse = fuse_left();
+  // Fused path: the side stream's folds of step i-1 write only row block i-1
+  // (rows pk .. k) of the trailing columns, so every other row runs S5-S7
+  // before waiting for them (the SVD of step i-1 hides behind the step) and the
+  // pending rows get their S5 afterwards.  Unfused: wait first.
+  const i64 pk = (fuse && k > 0) ? k - b : k, pb = k - pk;
+  if (!fuse) RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eF, 0));
   if (sl > 0) {
     cyclic_scatter_rows_kernel<<<grid_for(L, sl * b), 256, 0, st>>>(sl, b, k, b, P, p, lay.lb_before(p, i), w.Wv, s,
                                                                    R.d.Wl, maxs);
     L.count();
     RUTV_CHECK_LAUNCH("cyclic_scatter_rows_kernel");
   }
-  RUTV_TRY(launch_dgemm(L, false, false, m, b, sl, 1.0, Ap, lda, R.d.Wl, maxs, 0.0, w.Z, m, w.gemm_ws,
+  // Z = T W_V (AllReduce, m x b; the pending rows are zero here and done later)
+  if (pk > 0)
+    RUTV_TRY(launch_dgemm(L, false, false, pk, b, sl, 1.0, Ap, lda, R.d.Wl, maxs, 0.0, w.Z, m, w.gemm_ws,
+                          w.gemm_ws_elems));
+  if (pb > 0) RUTV_TRY(launch_fill(L, pb, b, 0.0, w.Z + pk, m));
+  RUTV_TRY(launch_dgemm(L, false, false, r, b, sl, 1.0, At, lda, R.d.Wl, maxs, 0.0, w.Z + k, m, w.gemm_ws,
                         w.gemm_ws_elems));
   RUTV_TRY(R.comm->allreduce_sum(w.Z, m * b, st));
   RUTV_TRY(launch_dgemm(L, false, false, m, b, b, 1.0, w.Z, m, w.TV, b, 0.0, w.Z2, m, nullptr, 0));
-  const bool fuse = fuse_left();
-  // (unfused: the S5 update of every trailing column now; fused: of block i only)
-  RUTV_TRY(launch_dgemm(L, false, true, m, fuse ? (p == o ? b : 0) : sl, b, -1.0, w.Z2, m, R.d.Wl, maxs, 1.0, Ap,
-                        lda, nullptr, 0));
+  // S5 update: unfused -- every trailing column of every row; fused -- column
+  // block i (its owner) for the rows outside the pending block
+  const i64 ucols = fuse ? (p == o ? b : 0) : sl;
+  if (pk > 0)
+    RUTV_TRY(launch_dgemm(L, false, true, pk, ucols, b, -1.0, w.Z2, m, R.d.Wl, maxs, 1.0, Ap, lda, nullptr, 0));
+  RUTV_TRY(launch_dgemm(L, false, true, m - pk - pb, ucols, b, -1.0, w.Z2 + k, m, R.d.Wl, maxs, 1.0, At, lda,
+                        nullptr, 0));
   // S6: QR of column block i on its owner, broadcast (W_U, T_U)
   double* Wu = R.d.wbuf;
   double* TU = R.d.wbuf + r * b;
@@ -521,10 +536,23 @@ int dist_sampled_step(DistRun& R, i64 i) {
   const i64 c1 = lay.lcol(p, i + 1);
   if (fuse)
     RUTV_TRY(fused_right_left(L, w, m, r, b, k, lay.ncols(p) - c1, R.P.A + c1 * lda, lda, R.d.Wl + (c1 - c0), maxs,
-                              w.Z2, m, Wu, r, TU, b));
+                              w.Z2, m, Wu, r, TU, b, pk));
   else
     RUTV_TRY(apply_left_t(L, w, r, lay.ncols(p) - c1, b, R.P.A + k + c1 * lda, lda, Wu, r, TU, b));
   if (R.P.U) RUTV_TRY(apply_right(L, w, R.P.mu, r, b, R.P.U + k * R.P.ldu, R.P.ldu, Wu, r, TU, b));
+  if (fuse) {
+    RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eF, 0));
+    if (pb > 0) {
+      // S5 of the pending row block over all of this rank's trailing columns
+      RUTV_TRY(launch_dgemm(L, false, false, pb, b, sl, 1.0, Ap + pk, lda, R.d.Wl, maxs, 0.0, w.Z + pk, m,
+                            w.gemm_ws, w.gemm_ws_elems));
+      RUTV_TRY(launch_copy(L, pb, b, w.Z + pk, m, R.d.blkz, pb));
+      RUTV_TRY(R.comm->allreduce_sum(R.d.blkz, pb * b, st));
+      RUTV_TRY(launch_dgemm(L, false, false, pb, b, b, 1.0, R.d.blkz, pb, w.TV, b, 0.0, w.Z2 + pk, m, nullptr, 0));
+      RUTV_TRY(launch_dgemm(L, false, true, pb, sl, b, -1.0, w.Z2 + pk, m, R.d.Wl, maxs, 1.0, Ap + pk, lda, nullptr,
+                            0));
+    }
+  }
   // S8, S9 on the side stream / side communicator
   RUTV_CUDA(cudaEventRecord(R.ctx->eR, st));
   RUTV_CUDA(cudaStreamWaitEvent(R.S.stream, R.ctx->eR, 0));
