@@ -23,8 +23,8 @@
 //                      shared memory and updated identically by all of them.
 //     extract_w        explicit W columns (unit diagonal, zeros above)
 //     S = W^T W_L      DMMA GEMM (K = h - c0, split-K)
-//     larft_leaf       T_L from S_LL and tau (one warp, NB^3/6 flops)
-//     T merge          T(0:c0, L) = -T(0:c0,0:c0) S(0:c0, L) T_L   (2 GEMMs)
+//     t_block          T_L from S_LL and tau (dlarft recurrence, one warp) and
+//                      T(0:c0, L) = -T(0:c0,0:c0) S(0:c0, L) T_L, one CTA
 //     trailing update  P(c0:h, L+:) -= W_L T_L^T (W_L^T P(c0:h, L+:))  (3 GEMMs)
 // The leaf kernel is bound by L2 latency and the per-column barrier; the
 // GEMMs carry the O(h w^2) flops.  All reductions are fixed-order, so the
@@ -281,35 +281,78 @@ __global__ void extract_w_kernel(const double* __restrict__ P, i64 ldp, i64 h, i
 
 // T(c0:c0+w, c0:c0+w) from S = W^T W (same block) and tau: T_jj = tau_j,
 // T(0:j, j) = -tau_j T(0:j,0:j) S(0:j, j)   (dlarft, forward, columnwise).  One warp.
-__global__ void larft_leaf_kernel(const double* __restrict__ S, i64 lds, const double* __restrict__ tau, int w,
-                                  double* __restrict__ T, i64 ldt) {
+// The compact-WY factor of one leaf, in ONE kernel (replaces the larft warp
+// kernel, the two T-merge GEMMs and the fill, ~70 us of dependent launches per
+// leaf): with S = W^T W_L (column block L of W^T W, rows 0 .. c0+wl),
+//   T_LL          = dlarft recurrence on S_LL and tau (warp 0)
+//   M1            = S(0:c0, L) T_LL                      (thread per row)
+//   T(0:c0, L)    = -T(0:c0, 0:c0) M1                    (thread per row; T upper)
+//   T(L, L) = T_LL, T(L, 0:c0) = 0.
+// Dynamic shared memory: M1 (c0 x NB, ld c0; columns >= wl zero).
+__global__ void __launch_bounds__(256) t_block_kernel(const double* __restrict__ SL, i64 lds,
+                                                      const double* __restrict__ tau, int c0, int wl,
+                                                      double* __restrict__ T, i64 ldt) {
+  extern __shared__ double M1[];
   __shared__ double Ts[NB][NB + 1];
   __shared__ double Ss[NB][NB + 1];
-  const int lane = threadIdx.x;
-  for (int e = lane; e < w * w; e += 32) {
-    const int r = e % w, c = e / w;
-    Ss[r][c] = S[r + (i64)c * lds];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < NB * NB; e += blockDim.x) {
+    const int r = e % NB, c = e / NB;
+    Ss[r][c] = (r < wl && c < wl) ? SL[c0 + r + (i64)c * lds] : 0.0;
     Ts[r][c] = 0.0;
   }
-  __syncwarp();
-  for (int j = 0; j < w; ++j) {
-    const double tj = tau[j];
-    double v = 0.0;
-    if (lane < j && tj != 0.0) {
-      double s = 0.0;
-      for (int l = lane; l < j; ++l) s += Ts[lane][l] * Ss[l][j];
-      v = -tj * s;
+  __syncthreads();
+  if (warp == 0) {
+    for (int j = 0; j < wl; ++j) {
+      const double tj = tau[c0 + j];
+      double v = 0.0;
+      if (lane < j && tj != 0.0) {
+        double acc = 0.0;
+        for (int l = lane; l < j; ++l) acc += Ts[lane][l] * Ss[l][j];
+        v = -tj * acc;
+      }
+      __syncwarp();
+      if (lane < j) Ts[lane][j] = v;
+      if (lane == j) Ts[j][j] = tj;
+      __syncwarp();
     }
-    __syncwarp();
-    if (lane < j) Ts[lane][j] = v;
-    if (lane == j) Ts[j][j] = tj;
-    __syncwarp();
   }
-  for (int e = lane; e < w * w; e += 32) {
-    const int r = e % w, c = e / w;
-    T[r + (i64)c * ldt] = Ts[r][c];
+  __syncthreads();
+  // M1(i, :) = S(i, 0:wl) T_LL   (T_LL upper triangular)
+  for (int i = tid; i < c0; i += blockDim.x) {
+    double srow[NB];
+#pragma unroll
+    for (int l = 0; l < NB; ++l) srow[l] = l < wl ? SL[i + (i64)l * lds] : 0.0;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l <= j; ++l) acc = fma(srow[l], Ts[l][j], acc);
+      M1[i + j * c0] = j < wl ? acc : 0.0;  // all NB columns: the product below reads them
+    }
+  }
+  __syncthreads();
+  // T(i, c0 + j) = -sum_{l >= i} T(i, l) M1(l, j)
+  for (int i = tid; i < c0; i += blockDim.x) {
+    double acc[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[j] = 0.0;
+    for (int l = i; l < c0; ++l) {
+      const double til = T[i + (i64)l * ldt];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] = fma(til, M1[l + j * c0], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j < wl) T[i + (i64)(c0 + j) * ldt] = -acc[j];
+  }
+  // T(L, L) = T_LL, T(L, 0:c0) = 0
+  for (int e = tid; e < wl * (c0 + wl); e += blockDim.x) {
+    const int r = e % wl, c = e / wl;
+    T[c0 + r + (i64)c * ldt] = c < c0 ? 0.0 : Ts[r][c - c0];
   }
 }
+
 
 // Leaf grid: R rows per thread in registers when the slab fits (R = 1, 2),
 // otherwise rows in L2 (R = 0).  G depends on the panel height only, so the
@@ -376,18 +419,19 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
     double* SL = qw.S + c0 * w;  // S stored w x w, ld w
     RUTV_TRY(launch_dgemm(L, true, false, c0 + wl, wl, h - c0, 1.0, Wx + c0, ldw, Wx + c0 + c0 * ldw, ldw, 0.0,
                           SL, w, qw.gemm_ws, qw.gemm_ws_elems));
-    // ---- T_LL
-    larft_leaf_kernel<<<1, 32, 0, L.stream>>>(SL + c0, w, tau + c0, wl, Tf + c0 + c0 * ldtf, ldtf);
-    L.count();
-    RUTV_CHECK_LAUNCH("larft_leaf_kernel");
-    // ---- T(0:c0, L) = -T(0:c0,0:c0) S(0:c0,L) T_LL
-    if (c0 > 0) {
-      RUTV_TRY(launch_dgemm(L, false, false, c0, wl, c0, 1.0, Tf, ldtf, SL, w, 0.0, qw.tmp1, c0, nullptr, 0));
-      RUTV_TRY(launch_dgemm(L, false, false, c0, wl, wl, -1.0, qw.tmp1, c0, Tf + c0 + c0 * ldtf, ldtf, 0.0,
-                            Tf + c0 * ldtf, ldtf, nullptr, 0));
+    // ---- T(:, L): T_LL, T(0:c0, L) = -T(0:c0,0:c0) S(0:c0,L) T_LL, T(L, 0:c0) = 0
+    {
+      const size_t smem = (size_t)(c0 > 0 ? c0 : 1) * NB * sizeof(double);
+      static bool attr = false;
+      if (!attr) {  // up to c0 = 640 (b = 672) with the 17 KB of static shared memory
+        RUTV_CUDA(cudaFuncSetAttribute(t_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        attr = true;
+      }
+      if (smem > 160 * 1024) return -3;
+      t_block_kernel<<<1, 256, smem, L.stream>>>(SL, w, tau, (int)c0, wl, Tf, ldtf);
+      L.count();
+      RUTV_CHECK_LAUNCH("t_block_kernel");
     }
-    // ---- zero T(L, 0:c0) (strictly lower part of the w x w factor)
-    if (c0 > 0) RUTV_TRY(launch_fill(L, wl, c0, 0.0, Tf + c0, ldtf));
     // ---- trailing panel update C -= W_L T_LL^T (W_L^T C), C = P(c0:h, c0+wl:w)
     const i64 nrest = w - c0 - wl;
     if (nrest > 0) {
