@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--cache-gib", type=float, default=None,
                    help="device panel cache for --mode host (default: a quarter of A)")
     p.add_argument("--no-uv", action="store_true", help="T only (the paper's 'no orthonormal matrices')")
+    p.add_argument("--sharded", action="store_true",
+                   help="use the column-sharded NCCL path even on one GPU (exercises the N > 1 code path)")
     return p.parse_args()
 
 
@@ -172,19 +174,20 @@ def cpu_sample(cfg_name, A_host, seed):
             "seconds": dt, "flops": F}
 
 
-def config_dict(name, ws):
+def config_dict(name, ws, sharded=None):
     """The workload description shared by both arms."""
     from paper_2002_06960_b200.flops import randutv_flops
     from paper_2002_06960_b200.inputs import CONFIGS
     c = CONFIGS[name]
     m, n, b, q = c["m"], c["n"], c["b"], c["q"]
     k = c.get("k") if not c.get("full", True) else None
+    sharded = ws > 1 if sharded is None else sharded
     return {"workload": f"{name}: " + {
         "c1": "n=512 known spectrum", "c2": "n=4096 Gaussian", "c3": "n=16384 exp spectrum",
         "c4": "262144x8192 low-rank + noise", "c5": "n=65536 Gaussian"}[name]
         + f", b={b}, q={q}, " + (f"truncated rank-{k} randUTV (U_k, T_k, V)" if k else "full randUTV with U and V"),
         "m": m, "n": n, "b": b, "q": q, "flops_per_step": randutv_flops(m, n, b, q, build_uv=True, k=k),
-        "parallelism": f"column-sharded x{ws} (1-D block-cyclic, NCCL)" if ws > 1 else "single",
+        "parallelism": f"column-sharded x{ws} (1-D block-cyclic, NCCL)" if sharded else "single",
         "l2": "inputs larger than L2 (A is %.2f GB, L2 126 MB); no flush" % (8 * m * n / 1e9)
         if 8 * m * n > 126e6 else "input fits L2: not flushed"}
 
@@ -235,9 +238,14 @@ def run_ours(args):
     from paper_2002_06960_b200.randutv import Context, colmajor, randutv_factor
 
     ws, rank, local = dist_env()
-    if ws > 1:
+    sharded = ws > 1 or args.sharded
+    if sharded:
         import torch.distributed as dist
         torch.cuda.set_device(local)
+        if ws == 1 and "MASTER_ADDR" not in os.environ:
+            os.environ["MASTER_ADDR"] = "127.0.0.1"
+            os.environ["MASTER_PORT"] = os.environ.get("MASTER_PORT", "29531")
+            os.environ["RANK"], os.environ["WORLD_SIZE"] = "0", "1"
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
@@ -251,7 +259,7 @@ def run_ours(args):
     A = make_config_torch(args.config, device=f"cuda:{dev}")
     stream = torch.cuda.Stream()
     ctx = Context(dev, stream)
-    if ws > 1:
+    if sharded:
         # column-sharded path: block-cyclic columns of A, row
         # ranges of U and V; NCCL communicator bootstrapped over torch.distributed
         from paper_2002_06960_b200.randutv import dist_layout, local_columns
@@ -289,7 +297,7 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     def barrier():
-        if ws > 1:
+        if sharded:
             torch.distributed.barrier()
 
     clocks = ClockSampler(dev)
@@ -311,7 +319,7 @@ def run_ours(args):
     barrier()
     clocks.stop()
     ms = e0.elapsed_time(e1)
-    if ws > 1:
+    if sharded:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
@@ -323,7 +331,7 @@ def run_ours(args):
 
     # ---- e2e: the literal C-ABI entry on pinned host buffers, copies inside the timed region
     e2e = None
-    if not args.no_e2e and ws > 1:
+    if not args.no_e2e and sharded:
         # the sharded entry from pinned host memory: H2D of the rank's columns, the
         # collective factorisation, D2H of its T columns and U / V rows
         Ah = torch.empty((lay["ncols"], m), dtype=torch.float64, pin_memory=True)
@@ -384,7 +392,7 @@ def run_ours(args):
 
     # ---- CPU baseline: the oracle on a bounded sample, rank 0, N = 1 only
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not sharded and not args.no_cpu_baseline:
         sm_, sn_ = sample_shape(args.config)
         A_host = np.asfortranarray(A[:sm_, :sn_].cpu().numpy())
         cpu = cpu_sample(args.config, A_host, seed)
@@ -416,7 +424,7 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args.config, ws),
+            "config": config_dict(args.config, ws, sharded),
             "t_over_n3_x1e10": ms_step * 1e-3 / float(n) ** 3 * 1e10,
             "frac_of_fp64_peak": round(value / ws / 1e3 / peak, 4),   # of N x per-GPU peak
             "gpu_launches": stats["kernel_launches"],
@@ -428,7 +436,7 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     ctx.close()
-    if ws > 1:
+    if sharded:
         torch.distributed.destroy_process_group()
     return 0
 

@@ -57,7 +57,22 @@ __device__ __forceinline__ double warp_sum(double v) {
 // in every CTA, so every CTA obtains bitwise identical totals.
 __device__ __forceinline__ void reduce_partials(const double* __restrict__ pj, int G, double* stage, double* tot,
                                                 int tid, int lane, int warp) {
-  for (int e = tid; e < G * PSTRIDE; e += LEAF_THREADS) stage[e] = pj[e];
+  // all loads in flight at once (a loop of load -> shared store pairs left the
+  // G x 33 reads ~3 L2 round trips deep; tools/sync_micro.cu: write + grid.sync
+  // + read of 64 records 3.6 us vs grid.sync alone 1.2 us), and past L1: the
+  // same buffer was read two columns ago
+  constexpr int PER = (LEAF_MAX_CTAS * PSTRIDE + LEAF_THREADS - 1) / LEAF_THREADS;
+  double tmp[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = tid + q * LEAF_THREADS;
+    tmp[q] = e < G * PSTRIDE ? __ldcg(pj + e) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int e = tid + q * LEAF_THREADS;
+    if (e < G * PSTRIDE) stage[e] = tmp[q];
+  }
   __syncthreads();
   for (int e = warp; e < PSTRIDE; e += LEAF_THREADS / 32) {
     double s = 0.0;

@@ -157,3 +157,39 @@ def test_dist_loopback_truncated(ctx, m, n, k, b, q, P):
     assert np.max(np.abs(np.abs(Uk) - np.abs(o["Uk"]))) <= 1e-9
     assert spectral_orth_error(Uk) <= 1e-12 and spectral_orth_error(V) <= 1e-12
     assert abs(np.linalg.norm(A - Uk @ Tk @ V.T) - rho) <= 1e-12 * nA
+
+
+def test_nccl_single_rank_end_to_end(ctx):
+    """The NCCL back end itself (dlopen of torch's libnccl.so.2, ncclCommInitRank,
+    ncclCommSplit for the side communicator, AllReduce / AllGather / Broadcast /
+    AllReduce-min on the ctx streams) through randutv_factor_dist with one rank --
+    the only NCCL configuration a single GPU can run without co-scheduled ranks
+    waiting on each other."""
+    import torch
+    from paper_2002_06960_b200.randutv import Context, colmajor, nccl_unique_id
+    rng = np.random.default_rng(21)
+    m, n, b, q = 300, 260, 32, 1
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    c = Context()
+    try:
+        c.comm_init(nccl_unique_id(), 1, 0)
+        Ad = to_dev(A).clone(memory_format=torch.contiguous_format)
+        Al = colmajor(m, n)
+        Al.copy_(torch.from_numpy(np.ascontiguousarray(A)))
+        U, V = c.randutv_factor_dist(Al, m, n, b, q, 17, nranks=1, rank=0)
+        torch.cuda.synchronize()
+        T = to_np(Al)
+        U, V = to_np(U), to_np(V)
+        o = oracle_randutv(A, b, q, 17)
+        assert recon_error(A, U, T, V) <= 1e-12
+        assert spectral_orth_error(U) <= 1e-12 and spectral_orth_error(V) <= 1e-12
+        assert diag_parity(np.diag(T), np.diag(o["T"])) <= 1.0
+        assert np.max(np.abs(np.abs(T) - np.abs(o["T"]))) / np.linalg.norm(A) <= ELEM_TOL
+        # truncated sharded entry on the same communicator
+        Al.copy_(torch.from_numpy(np.ascontiguousarray(A)))
+        Uk, Vk, rho = c.randutv_factor_dist_rank(Al, m, n, 64, b, q, 17, nranks=1, rank=0)
+        to = oracle_randutv(A, b, q, 17, k=64, thin_u=True)
+        assert abs(rho - to["rho"]) <= 1e-9 * to["rho"]
+        assert np.max(np.abs(np.abs(to_np(Uk)) - np.abs(to["Uk"]))) <= 1e-9
+    finally:
+        c.close()
