@@ -41,7 +41,21 @@ namespace rutv {
 
 namespace {
 
-constexpr int BK = 16, PAD = 4;
+constexpr int BK = 16;
+// Shared-memory tile layout.  A tile is Lo rows of Lc doubles (Lc along the
+// operand's contiguous global dimension).  The 8-byte fragment loads of a
+// half-warp hit rows o..o+3 at the same column offsets, so a plain layout has
+// 4-way bank conflicts.  RUTV_GEMM_SWZ = 0 (default): rows padded to Lc + 4
+// doubles; 1: element (o, c) lives at o*Lc + (c ^ 4*(o & 3)) -- also
+// conflict-free, no padding (16 KB per 64x64x16 stage, so 4 stages fit 3
+// CTAs/SM), measured 1 % slower on B200 with 4 stages (profiles/gemm_tuning_r01.txt).
+#ifndef RUTV_GEMM_SWZ
+#define RUTV_GEMM_SWZ 0
+#endif
+constexpr int PAD = RUTV_GEMM_SWZ ? 0 : 4;
+__host__ __device__ constexpr int soff(int o, int c, int Lc) {
+  return RUTV_GEMM_SWZ ? o * Lc + (c ^ ((o & 3) << 2)) : o * (Lc + PAD) + c;
+}
 
 // Tile configuration: BM x BN CTA tile, WM x (NW/WM) warps, STAGES-deep ring,
 // MINB CTAs per SM.
@@ -57,7 +71,13 @@ struct Cfg {
 };
 //   Cfg< 64, 64,2,3,3,4>: 4 warps (2 x 2) of 32 x 32, 3 stages, 3 CTAs/SM (the CUTLASS
 //                       d884 64x64 shape cuBLAS picks on B200 at 98 % DMMA-pipe use)
-using CfgSmall = Cfg<64, 64, 2, 3, 3, 4>;
+#ifndef RUTV_GEMM_STAGES  // tuning overrides (tools/ab.sh); the defaults are the measured best
+#define RUTV_GEMM_STAGES 3
+#endif
+#ifndef RUTV_GEMM_MINB
+#define RUTV_GEMM_MINB 3
+#endif
+using CfgSmall = Cfg<64, 64, 2, RUTV_GEMM_STAGES, RUTV_GEMM_MINB, 4>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -82,7 +102,7 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 
 // Copy one Lc x Lo tile (Lc along the global contiguous dimension) into shared
-// memory rows of length Lc + PAD.  lim_c / lim_o: first invalid global index.
+// memory (layout soff).  lim_c / lim_o: first invalid global index.
 template <int Lc, int Lo, int VEC, int THREADS>
 __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__ g, i64 ld, i64 c0, i64 o0,
                                           i64 lim_c, i64 lim_o, int tid) {
@@ -99,7 +119,7 @@ __device__ __forceinline__ void load_tile(double* sm, const double* __restrict__
     nvalid = nvalid < 0 ? 0 : (nvalid > VEC ? VEC : nvalid);
     if (go >= lim_o) nvalid = 0;
     const double* src = nvalid > 0 ? g + gc + go * ld : g;
-    cp_async<VEC>(smem_u32(sm + o * (Lc + PAD) + ci), src, (int)(nvalid * 8));
+    cp_async<VEC>(smem_u32(sm + soff(o, ci, Lc)), src, (int)(nvalid * 8));
   }
 }
 
@@ -112,9 +132,8 @@ __device__ __forceinline__ void load_tile_fast(double* sm, const double* __restr
   constexpr int CPR = Lc / VEC, RPI = THREADS / CPR, NIT = CPR * Lo / THREADS;
   static_assert(THREADS % CPR == 0 && (CPR * Lo) % THREADS == 0, "tile/threads mismatch");
   const int o = tid / CPR, ci = (tid % CPR) * VEC;
-  double* d = sm + o * (Lc + PAD) + ci;
 #pragma unroll
-  for (int it = 0; it < NIT; ++it) cp_async<VEC>(smem_u32(d + it * RPI * (Lc + PAD)), g + it * gstep, VEC * 8);
+  for (int it = 0; it < NIT; ++it) cp_async<VEC>(smem_u32(sm + soff(o + it * RPI, ci, Lc)), g + it * gstep, VEC * 8);
 }
 
 // this thread's first chunk within an Lc x Lo tile whose origin is (c0, o0)
@@ -327,12 +346,12 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 #pragma unroll
     for (int mi = 0; mi < MI; ++mi) {
       const int row = wm * (MI * 8) + mi * 8 + g;
-      a[mi] = TA ? As[row * (BK + PAD) + k] : As[k * (BM + PAD) + row];
+      a[mi] = TA ? As[soff(row, k, BK)] : As[soff(k, row, BM)];
     }
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni) {
       const int col = wn * (NI * 8) + ni * 8 + g;
-      b[ni] = TB ? Bs[k * (BN + PAD) + col] : Bs[col * (BK + PAD) + k];
+      b[ni] = TB ? Bs[soff(k, col, BN)] : Bs[soff(col, k, BK)];
     }
   };
   // ---- main loop over the flattened (item, k-tile) sequence

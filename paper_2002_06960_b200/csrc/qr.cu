@@ -32,6 +32,8 @@
 // every rank of the multi-GPU layout).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -89,11 +91,15 @@ __device__ __forceinline__ void reduce_partials(const double* __restrict__ pj, i
 // thread keeps its R slab rows of the 32 leaf columns in registers for the whole
 // leaf (one read and one write of the slab); R == 0: rows stay in global memory
 // (L2) -- for panels taller than 128 x 256 x 2 rows.
-template <int R>
+// CLUSTER: the G (<= 16) CTAs form one thread-block cluster; the per-column
+// exchange is a cluster barrier + DSMEM reads of the other CTAs' records
+// (tools/sync_micro.cu: ~1.0 us for 16 CTAs) instead of a grid barrier + an L2
+// round trip through `partials` (~3.6 us for 64 CTAs).
+template <int R, bool CLUSTER>
 __global__ void __launch_bounds__(LEAF_THREADS, 1)
     qr_leaf_kernel(double* __restrict__ P, i64 h, i64 ldp, i64 c0, int nb, double* __restrict__ tau,
                    double* __restrict__ partials) {
-  cg::grid_group grid = cg::this_grid();
+  __shared__ double mine[2][PSTRIDE];  // CLUSTER: this CTA's record, by column parity
   __shared__ double TB[NB][NB + 1];  // TB[r][c]: top-block row r, leaf column c
   __shared__ double wred[LEAF_THREADS / 32][PSTRIDE];
   __shared__ double tot[PSTRIDE];
@@ -189,16 +195,42 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
       if (lane == 0) wred[warp][0] = nrm;
     }
     __syncthreads();
-    double* pj = partials + (size_t)(jj & 1) * G * PSTRIDE;
-    if (tid < PSTRIDE) {
-      double s2 = 0.0;
+    if constexpr (CLUSTER) {
+      cg::cluster_group cl = cg::this_cluster();
+      if (tid < PSTRIDE) {
+        double s2 = 0.0;
 #pragma unroll
-      for (int w = 0; w < LEAF_THREADS / 32; ++w) s2 += wred[w][tid];
-      pj[(size_t)cta * PSTRIDE + tid] = s2;
+        for (int w = 0; w < LEAF_THREADS / 32; ++w) s2 += wred[w][tid];
+        mine[jj & 1][tid] = s2;
+      }
+      // one cluster barrier per column: a CTA writes the other parity's record
+      // next, and cannot write this one again before every CTA has passed the
+      // next barrier, i.e. finished reading it
+      cl.sync();
+      for (int e = tid; e < G * PSTRIDE; e += LEAF_THREADS) {
+        const double* rr = cl.map_shared_rank(&mine[jj & 1][0], e / PSTRIDE);
+        stage[e] = rr[e % PSTRIDE];
+      }
+      __syncthreads();
+      for (int e = warp; e < PSTRIDE; e += LEAF_THREADS / 32) {
+        double s3 = 0.0;
+        for (int c = lane; c < G; c += 32) s3 += stage[c * PSTRIDE + e];
+        s3 = warp_sum(s3);
+        if (lane == 0) tot[e] = s3;
+      }
+      __syncthreads();
+    } else {
+      double* pj = partials + (size_t)(jj & 1) * G * PSTRIDE;
+      if (tid < PSTRIDE) {
+        double s2 = 0.0;
+#pragma unroll
+        for (int w = 0; w < LEAF_THREADS / 32; ++w) s2 += wred[w][tid];
+        pj[(size_t)cta * PSTRIDE + tid] = s2;
+      }
+      cg::this_grid().sync();
+      // ---------------- phase B: every CTA reduces the partials in the same order
+      reduce_partials(pj, G, stage, tot, tid, lane, warp);
     }
-    grid.sync();
-    // ---------------- phase B: every CTA reduces the partials in the same order
-    reduce_partials(pj, G, stage, tot, tid, lane, warp);
     if (tid == 0) {
       const double alpha = TB[jj][jj];
       const double xi = sqrt(tot[0]);
@@ -262,6 +294,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
     }
     __syncthreads();
   }
+  if constexpr (CLUSTER) cg::this_cluster().sync();  // no CTA exits while its record may still be read
   if constexpr (R > 0) {
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -390,6 +423,18 @@ void leaf_plan(i64 slab_rows, int* G, int* R) {
   *G = (int)g;
 }
 
+constexpr int kLeafClusterMax = 16;
+
+// RUTV_LEAF_CLUSTER=0 forces the cooperative-grid leaf (tuning only)
+bool leaf_cluster_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_LEAF_CLUSTER");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 }  // namespace
 
 i64 panel_qr_partials_elems(i64 h, i64 w) {
@@ -415,8 +460,31 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
       double* part = qw.partials;
       void* args[] = {&Pp, &hh, &ld, &cc, &nbv, &taup, &part};
       const size_t pe = L.pbegin();
-      void* fn = R == 1 ? (void*)qr_leaf_kernel<1> : (R == 2 ? (void*)qr_leaf_kernel<2> : (void*)qr_leaf_kernel<0>);
-      RUTV_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(LEAF_THREADS), args, 0, L.stream));
+      if (G <= kLeafClusterMax && R > 0 && leaf_cluster_on()) {
+        // one thread-block cluster of G CTAs (non-portable size up to 16)
+        void* fn = R == 1 ? (void*)qr_leaf_kernel<1, true> : (void*)qr_leaf_kernel<2, true>;
+        static bool attr[3] = {false, false, false};
+        if (!attr[R]) {
+          RUTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+          attr[R] = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(LEAF_THREADS);
+        cfg.stream = L.stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = G;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        RUTV_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+      } else {
+        void* fn = R == 1 ? (void*)qr_leaf_kernel<1, false>
+                          : (R == 2 ? (void*)qr_leaf_kernel<2, false> : (void*)qr_leaf_kernel<0, false>);
+        RUTV_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(LEAF_THREADS), args, 0, L.stream));
+      }
       L.count();
       // algorithmic: ~4 (h-c0) wl^2 flops (dlarfg + dlarf over the leaf); bytes: the leaf read + written once
       L.pend(PK_QR_LEAF, 4.0 * (double)(h - c0) * wl * wl, 16.0 * (double)(h - c0) * wl, pe);
