@@ -329,13 +329,17 @@ __global__ void extract_w_kernel(const double* __restrict__ P, i64 ldp, i64 h, i
 
 // T(c0:c0+w, c0:c0+w) from S = W^T W (same block) and tau: T_jj = tau_j,
 // T(0:j, j) = -tau_j T(0:j,0:j) S(0:j, j)   (dlarft, forward, columnwise).  One warp.
-// The compact-WY factor of one leaf, in ONE kernel (replaces the larft warp
-// kernel, the two T-merge GEMMs and the fill, ~70 us of dependent launches per
-// leaf): with S = W^T W_L (column block L of W^T W, rows 0 .. c0+wl),
-//   T_LL          = dlarft recurrence on S_LL and tau (warp 0)
-//   M1            = S(0:c0, L) T_LL                      (thread per row)
-//   T(0:c0, L)    = -T(0:c0, 0:c0) M1                    (thread per row; T upper)
-//   T(L, L) = T_LL, T(L, 0:c0) = 0.
+// The compact-WY factor of one leaf (replaces the larft warp kernel, the two
+// T-merge GEMMs and the fill): with S = W^T W_L (column block L of W^T W, rows
+// 0 .. c0+wl),
+//   T_LL  by recursive doubling: T = [T1, -T1 S12 T2; 0, T2] merges blocks of
+//         1, 2, 4, 8, 16 reflectors (the compact-WY product rule, exactly the
+//         dlarft recurrence in exact arithmetic; 5 parallel levels instead of 32
+//         sequential steps)
+//   M1    = S(0:c0, L) T_LL
+//   T(0:c0, L) = -T(0:c0, 0:c0) M1   (T upper triangular; CTA c takes rows
+//         32c .. 32c+32 so the grid is ceil(c0/32) CTAs)
+//   T(L, L) = T_LL, T(L, 0:c0) = 0   (CTA 0)
 // Dynamic shared memory: M1 (c0 x NB, ld c0; columns >= wl zero).
 __global__ void __launch_bounds__(256) t_block_kernel(const double* __restrict__ SL, i64 lds,
                                                       const double* __restrict__ tau, int c0, int wl,
@@ -343,31 +347,39 @@ __global__ void __launch_bounds__(256) t_block_kernel(const double* __restrict__
   extern __shared__ double M1[];
   __shared__ double Ts[NB][NB + 1];
   __shared__ double Ss[NB][NB + 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double Mm[NB][NB + 1];
+  const int tid = threadIdx.x;
   for (int e = tid; e < NB * NB; e += blockDim.x) {
     const int r = e % NB, c = e / NB;
     Ss[r][c] = (r < wl && c < wl) ? SL[c0 + r + (i64)c * lds] : 0.0;
-    Ts[r][c] = 0.0;
+    Ts[r][c] = (r == c && r < wl) ? tau[c0 + r] : 0.0;
   }
   __syncthreads();
-  if (warp == 0) {
-    for (int j = 0; j < wl; ++j) {
-      const double tj = tau[c0 + j];
-      double v = 0.0;
-      if (lane < j && tj != 0.0) {
-        double acc = 0.0;
-        for (int l = lane; l < j; ++l) acc += Ts[lane][l] * Ss[l][j];
-        v = -tj * acc;
-      }
-      __syncwarp();
-      if (lane < j) Ts[lane][j] = v;
-      if (lane == j) Ts[j][j] = tj;
-      __syncwarp();
+  // ---- T_LL by recursive doubling (blocks beyond wl stay zero)
+#pragma unroll
+  for (int sz = 1; sz < NB; sz *= 2) {
+    // Mm = S12 T22 for every pair (rows a.., cols a+sz..) ; T22 upper triangular
+    for (int e = tid; e < (NB / 2) * sz; e += blockDim.x) {
+      const int pair = e / (sz * sz), rem = e % (sz * sz);
+      const int a = pair * 2 * sz, r = a + rem % sz, c = a + sz + rem / sz;
+      double acc = 0.0;
+      for (int l = a + sz; l <= c; ++l) acc = fma(Ss[r][l], Ts[l][c], acc);
+      Mm[r][c] = acc;
     }
+    __syncthreads();
+    // T12 = -T11 Mm ; T11 upper triangular
+    for (int e = tid; e < (NB / 2) * sz; e += blockDim.x) {
+      const int pair = e / (sz * sz), rem = e % (sz * sz);
+      const int a = pair * 2 * sz, r = a + rem % sz, c = a + sz + rem / sz;
+      double acc = 0.0;
+      for (int l = r; l < a + sz; ++l) acc = fma(Ts[r][l], Mm[l][c], acc);
+      Ts[r][c] = -acc;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  // M1(i, :) = S(i, 0:wl) T_LL   (T_LL upper triangular)
-  for (int i = tid; i < c0; i += blockDim.x) {
+  // ---- M1(i, :) = S(i, 0:wl) T_LL for every row this CTA's product reads
+  const int i0 = blockIdx.x * NB;
+  for (int i = i0 + tid; i < c0; i += blockDim.x) {
     double srow[NB];
 #pragma unroll
     for (int l = 0; l < NB; ++l) srow[l] = l < wl ? SL[i + (i64)l * lds] : 0.0;
@@ -376,29 +388,32 @@ __global__ void __launch_bounds__(256) t_block_kernel(const double* __restrict__
       double acc = 0.0;
 #pragma unroll
       for (int l = 0; l <= j; ++l) acc = fma(srow[l], Ts[l][j], acc);
-      M1[i + j * c0] = j < wl ? acc : 0.0;  // all NB columns: the product below reads them
+      M1[i + j * c0] = acc;
     }
   }
   __syncthreads();
-  // T(i, c0 + j) = -sum_{l >= i} T(i, l) M1(l, j)
-  for (int i = tid; i < c0; i += blockDim.x) {
-    double acc[NB];
+  // ---- T(i, c0 + j) = -sum_{l >= i} T(i, l) M1(l, j): warp w takes columns 4w .. 4w+4
+  {
+    const int lane = tid & 31, w = tid >> 5;
+    const int i = i0 + lane;
+    if (i < c0) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int l = i; l < c0; ++l) {
+        const double til = T[i + (i64)l * ldt];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) acc[j] = 0.0;
-    for (int l = i; l < c0; ++l) {
-      const double til = T[i + (i64)l * ldt];
+        for (int q = 0; q < 4; ++q) acc[q] = fma(til, M1[l + (4 * w + q) * c0], acc[q]);
+      }
 #pragma unroll
-      for (int j = 0; j < NB; ++j) acc[j] = fma(til, M1[l + j * c0], acc[j]);
+      for (int q = 0; q < 4; ++q)
+        if (4 * w + q < wl) T[i + (i64)(c0 + 4 * w + q) * ldt] = -acc[q];
     }
-#pragma unroll
-    for (int j = 0; j < NB; ++j)
-      if (j < wl) T[i + (i64)(c0 + j) * ldt] = -acc[j];
   }
-  // T(L, L) = T_LL, T(L, 0:c0) = 0
-  for (int e = tid; e < wl * (c0 + wl); e += blockDim.x) {
-    const int r = e % wl, c = e / wl;
-    T[c0 + r + (i64)c * ldt] = c < c0 ? 0.0 : Ts[r][c - c0];
-  }
+  // ---- T(L, L) = T_LL, T(L, 0:c0) = 0
+  if (blockIdx.x == 0)
+    for (int e = tid; e < wl * (c0 + wl); e += blockDim.x) {
+      const int r = e % wl, c = e / wl;
+      T[c0 + r + (i64)c * ldt] = c < c0 ? 0.0 : Ts[r][c - c0];
+    }
 }
 
 
@@ -511,7 +526,8 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
         attr = true;
       }
       if (smem > 160 * 1024) return -3;
-      t_block_kernel<<<1, 256, smem, L.stream>>>(SL, w, tau, (int)c0, wl, Tf, ldtf);
+      const int tb = c0 > 0 ? (int)((c0 + NB - 1) / NB) : 1;
+      t_block_kernel<<<tb, 256, smem, L.stream>>>(SL, w, tau, (int)c0, wl, Tf, ldtf);
       L.count();
       RUTV_CHECK_LAUNCH("t_block_kernel");
     }
