@@ -36,7 +36,10 @@ namespace rutv {
 
 namespace {
 
-constexpr int JT = 256;  // threads per CTA
+#ifndef RUTV_JT
+#define RUTV_JT 512
+#endif
+constexpr int JT = RUTV_JT;  // threads per CTA
 constexpr int MAX_SWEEPS = 30;
 
 struct JacobiPlan {
