@@ -132,8 +132,15 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
   __syncthreads();
 
 #pragma unroll 1
+#ifdef RUTV_LEAF_PROF
+  long long tp[8];
+#define LEAF_T(i) tp[i] = clock64()
+#else
+#define LEAF_T(i)
+#endif
   for (int jj = 0; jj < NB; jj += 1) {
     if (jj >= nb) break;
+    LEAF_T(0);
     // ---------------- phase A: partial sums over this CTA's rows
     double acc[PSTRIDE];
 #pragma unroll
@@ -162,15 +169,6 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
           if (l > jj && l < nb) acc[1 + l] = fma(x, L0[r + (i64)l * ldp], acc[1 + l]);
       }
     }
-    if (cta == 0) {  // the top-block rows below the diagonal count once (CTA 0)
-      for (int r = jj + 1 + tid; r < nb; r += LEAF_THREADS) {
-        const double x = TB[r][jj];
-        acc[0] = fma(x, x, acc[0]);
-#pragma unroll
-        for (int l = 0; l < NB; ++l)
-          if (l > jj && l < nb) acc[1 + l] = fma(x, TB[r][l], acc[1 + l]);
-      }
-    }
 #pragma unroll
     {
       // warp reduction of the 32 dot products as a butterfly reduce-scatter:
@@ -190,11 +188,28 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
           v32[i] = keep + __shfl_xor_sync(0xffffffffu, send, st);
         }
       }
-      const double nrm = warp_sum(acc[0]);
+      double nrm = warp_sum(acc[0]);
+      if (cta == 0) {
+        // the top-block rows below the diagonal count once (CTA 0): warp w takes
+        // rows jj+1+4w .. +4 and lane L the column-L dot, added to the warp's
+        // butterfly result for value L (was one thread per row, 32 dependent
+        // shared loads on warp 0 of CTA 0 -- on every CTA's critical path)
+        double dl = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = jj + 1 + 4 * warp + i;
+          if (r < nb) dl = fma(TB[r][jj], TB[r][lane], dl);
+        }
+        const double dn = __shfl_sync(0xffffffffu, dl, jj);  // column jj itself: the norm part
+        if (lane > jj && lane < nb) v32[0] += dl;
+        nrm += dn;
+      }
       wred[warp][1 + lane] = v32[0];
       if (lane == 0) wred[warp][0] = nrm;
     }
+    LEAF_T(1);
     __syncthreads();
+    LEAF_T(2);
     if constexpr (CLUSTER) {
       cg::cluster_group cl = cg::this_cluster();
       if (tid < PSTRIDE) {
@@ -231,27 +246,29 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
       // ---------------- phase B: every CTA reduces the partials in the same order
       reduce_partials(pj, G, stage, tot, tid, lane, warp);
     }
-    if (tid == 0) {
+    LEAF_T(3);
+    if (warp == 0) {
+      // dlarfg (every lane, identical) and the w entries in one warp: one barrier
       const double alpha = TB[jj][jj];
       const double xi = sqrt(tot[0]);
-      if (xi == 0.0) {
-        sc[0] = 0.0;
-        sc[1] = 0.0;
-        sc[2] = alpha;
-        sc[3] = 0.0;
-      } else {
-        const double beta = -copysign(hypot(alpha, xi), alpha);
-        sc[0] = (beta - alpha) / beta;
-        sc[1] = 1.0 / (alpha - beta);
-        sc[2] = beta;
-        sc[3] = 1.0;
+      double t0 = 0.0, s0 = 0.0, b0 = alpha;
+      const bool act = xi != 0.0;
+      if (act) {
+        b0 = -copysign(hypot(alpha, xi), alpha);
+        t0 = (b0 - alpha) / b0;
+        s0 = 1.0 / (alpha - b0);
+      }
+      wv[lane] = (act && lane > jj && lane < nb) ? TB[jj][lane] + s0 * tot[1 + lane] : 0.0;
+      if (lane == 0) {
+        sc[0] = t0;
+        sc[1] = s0;
+        sc[2] = b0;
+        sc[3] = act ? 1.0 : 0.0;
       }
     }
     __syncthreads();
     const double t = sc[0], scal = sc[1];
     const bool active = sc[3] != 0.0;
-    if (tid < NB) wv[tid] = (active && tid > jj && tid < nb) ? TB[jj][tid] + scal * tot[1 + tid] : 0.0;
-    __syncthreads();
     if (active) {
       if constexpr (R > 0) {
 #pragma unroll
@@ -278,21 +295,31 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
             if (l > jj && l < nb) L0[r + (i64)l * ldp] = fma(-tv, wv[l], L0[r + (i64)l * ldp]);
         }
       }
-      // replicated top block: rows > j, then the pivot row j
-      for (int r = jj + 1 + tid; r < nb; r += LEAF_THREADS) {
-        const double vv = TB[r][jj] * scal;
-        TB[r][jj] = vv;
-        const double tv = t * vv;
-        for (int l = jj + 1; l < nb; ++l) TB[r][l] = fma(-tv, wv[l], TB[r][l]);
+      // replicated top block, element-parallel over (row r >= j, column l > j):
+      // the pivot row j has the implicit unit reflector entry; column j itself
+      // (read here) is scaled after the barrier
+      for (int e = tid; e < NB * NB; e += LEAF_THREADS) {
+        const int r = e / NB, l = e % NB;
+        if (r >= jj && r < nb && l > jj && l < nb) {
+          const double vv = (r == jj) ? 1.0 : TB[r][jj] * scal;
+          TB[r][l] = fma(-t * vv, wv[l], TB[r][l]);
+        }
       }
-      if (tid > jj && tid < nb) TB[jj][tid] -= t * wv[tid];
     }
     __syncthreads();
+    LEAF_T(4);
+    if (active && tid > jj && tid < nb) TB[tid][jj] *= scal;
     if (tid == 0) {
       TB[jj][jj] = sc[2];
       if (cta == 0) tau[c0 + jj] = t;
     }
     __syncthreads();
+    LEAF_T(5);
+#ifdef RUTV_LEAF_PROF
+    if (tid == 0 && cta == 0 && jj == 8 && c0 == 0)
+      printf("leafprof G=%d h=%lld: A %lld sync1 %lld exch %lld scal+update %lld tail %lld total %lld cycles\n", G,
+             (long long)h, tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[5] - tp[0]);
+#endif
   }
   if constexpr (CLUSTER) cg::this_cluster().sync();  // no CTA exits while its record may still be read
   if constexpr (R > 0) {
