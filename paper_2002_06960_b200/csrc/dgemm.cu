@@ -77,6 +77,9 @@ struct Cfg {
 #ifndef RUTV_GEMM_MINB
 #define RUTV_GEMM_MINB 3
 #endif
+#ifndef RUTV_SPLIT_FIXED_US  // fixed cost of a split-K reduction launch in the split model (us)
+#define RUTV_SPLIT_FIXED_US 12.0
+#endif
 #ifndef RUTV_RASTER_GROUP
 #define RUTV_RASTER_GROUP 64
 #endif
@@ -568,7 +571,7 @@ int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double a
       const i64 kch = ((K + sp - 1) / sp + BK - 1) / BK;
       const double waves = std::ceil((double)(tiles * sp) / (double)resident);
       double t = waves * (double)kch * t_kt;
-      if (sp > 1) t += (double)(sp + 2) * (double)M * (double)N * 8.0 / 5e12 + 3e-6;
+      if (sp > 1) t += (double)(sp + 2) * (double)M * (double)N * 8.0 / 5e12 + RUTV_SPLIT_FIXED_US * 1e-6;
       if (t < best * (1.0 - 1e-6)) {
         best = t;
         splits = sp;
