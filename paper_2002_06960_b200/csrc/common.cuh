@@ -55,6 +55,9 @@ struct Launch {
   // two device ints (tile counter, finished-CTA counter) private to this
   // stream: the persistent GEMM's dynamic tile scheduler (null: static tiles)
   int* sched = nullptr;
+  // one CTA per GEMM tile (no persistent grid): kernels on a concurrent stream,
+  // whose CTAs must retire tile by tile so other streams' kernels get SMs
+  bool oneshot = false;
   void count(int n = 1) const {
     if (counter) *counter += n;
   }

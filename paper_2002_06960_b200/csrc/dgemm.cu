@@ -588,7 +588,7 @@ int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double a
   const size_t pe = L.pbegin();
   // persistent grid: at most one wave of resident CTAs over all tiles x splits
   i64 ctas = tiles * splits;
-  if (persistent_on() && ctas > resident) ctas = resident;
+  if (persistent_on() && !L.oneshot && ctas > resident) ctas = resident;
   dim3 grid((unsigned)ctas, 1, 1);
   double* part = splits > 1 ? ws : nullptr;
   RUTV_TRY(launch_cfg<CF>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part));

@@ -23,12 +23,21 @@ struct randutv_ctx {
   // side stream (high priority) for the small SVD + folds, and its two events
   cudaStream_t side;
   cudaEvent_t eR, eF;
+  // V stream: the V update (S5 on V) of a step runs concurrently with the QR of
+  // the column block and the T updates (eWv: W_V ready; eV: V update done)
+  cudaStream_t vstr;
+  cudaEvent_t eWv, eV;
   // multi-GPU communicators (randutv_comm_init): main-stream and side-stream
   rutv::Comm* comm;
   rutv::Comm* comm_side;
   // GEMM tile-scheduler counters: [0..1] main stream, [2..3] side stream (zeroed once)
   int* sched;
   rutv::Launch launch() { return rutv::Launch{stream, &stats.kernel_launches, sms, &prof, sched}; }
+  rutv::Launch v_launch() {
+    rutv::Launch l{vstr, &stats.kernel_launches, sms, &prof, nullptr};
+    l.oneshot = true;
+    return l;
+  }
   rutv::Launch side_launch() { return rutv::Launch{side, &stats.kernel_launches, sms, &prof, sched ? sched + 2 : nullptr}; }
 };
 
@@ -65,6 +74,7 @@ struct Work {
   double* Zf;     // fold temporaries of the side stream (max(m,n) x b)
   double* Acat;   // fused S5/S7 update operands: [Z2(k:m) | W_U]  (m x 2b)
   double* Bt;     //                              [W2 | Y^T]       (n x 2b)
+  double *Zv, *Zv2, *gemm_ws_v;  // temporaries of the V stream (n x b each; split-K)
 };
 
 i64 gemm_ws_elems_for(i64 m, i64 n, i64 b);

@@ -121,6 +121,9 @@ size_t carve(Carver& c, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork) {
   w.Zf = c.take<double>(mx * b);
   w.Acat = c.take<double>(m * 2 * b);
   w.Bt = c.take<double>(n * 2 * b);
+  w.Zv = c.take<double>(n * b);
+  w.Zv2 = c.take<double>(n * b);
+  w.gemm_ws_v = c.take<double>(4 * n * b);
   w.Wv = c.take<double>(n * b);
   w.Wu = c.take<double>(m * b);
   w.TV = c.take<double>(b * b);
@@ -270,6 +273,18 @@ namespace {
 
 using namespace rutv;
 
+// RUTV_VSTREAM=0 keeps the V update on the main stream (comparison only)
+Launch vstream_launch(randutv_ctx* ctx) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_VSTREAM");
+    v = e ? atoi(e) : 1;
+  }
+  if (v != 0 && fuse_left()) return ctx->v_launch();
+  Launch l{nullptr, nullptr, 0, nullptr, nullptr};
+  return l;
+}
+
 struct Problem {
   i64 m, n, b;
   int q;
@@ -286,6 +301,8 @@ struct Problem {
   // eF = folds of step i done (side); S5 of step i+1 waits for eF.
   Launch side;
   cudaEvent_t eR, eF;
+  Launch vl;              // V stream (oneshot GEMMs); vl.stream == nullptr: V on the main stream
+  cudaEvent_t eWv, eV;
 };
 
 
@@ -339,10 +356,26 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
     RUTV_TRY(launch_dgemm(L, true, false, s, b, r, 1.0, At, P.ldt, w.Z, r, 0.0, w.Y, s, w.gemm_ws,
                           w.gemm_ws_elems));
   }
-  // S4
+  // S4 (overwrites W_V, T_V: the previous step's V update must have read them)
+  if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
   RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
-  // S5 for V(:, k:n) first: it does not touch T, so it needs no fold event
-  if (P.V) RUTV_TRY(apply_right(L, w, n, s, b, P.V + kk * P.ldv, P.ldv, w.Wv, s, w.TV, b));
+  // S5 for V(:, k:n): it does not touch T, so it needs no fold event; on the V
+  // stream it overlaps the QR of the column block and the T/U updates
+  if (P.V) {
+    if (P.vl.stream) {
+      RUTV_CUDA(cudaEventRecord(P.eWv, L.stream));
+      RUTV_CUDA(cudaStreamWaitEvent(P.vl.stream, P.eWv, 0));
+      Work wv = w;
+      wv.Z = w.Zv;
+      wv.Z2 = w.Zv2;
+      wv.gemm_ws = w.gemm_ws_v;
+      wv.gemm_ws_elems = 4 * n * b;
+      RUTV_TRY(apply_right(P.vl, wv, n, s, b, P.V + kk * P.ldv, P.ldv, w.Wv, s, w.TV, b));
+      RUTV_CUDA(cudaEventRecord(P.eV, P.vl.stream));
+    } else {
+      RUTV_TRY(apply_right(L, w, n, s, b, P.V + kk * P.ldv, P.ldv, w.Wv, s, w.TV, b));
+    }
+  }
   if (!fuse_left()) {
     // S5 for T: all m rows of T(:, k:n) (A2).  Row block i-1 of T(:, k:n) is
     // written by the side stream's U_s^T T12 fold of step i-1: wait for it
@@ -400,6 +433,7 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   // S8, S9 on the side stream, overlapping S1-S4 of step i+1
   RUTV_CUDA(cudaEventRecord(P.eR, L.stream));
   RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eR, 0));
+  if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eV, 0));
   RUTV_TRY(svd_and_fold(P.side, w, P, kk, b, (int)(i + 1)));
   if (P.record_lefts) RUTV_TRY(record_left_us(P.side, w, P, (int)i, b));
   RUTV_CUDA(cudaEventRecord(P.eF, P.side.stream));
@@ -414,6 +448,7 @@ int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   {
     const size_t pe = L.pbegin();
     RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));  // previous step's folds
+    if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
     L.pend(PK_OTHER, 0.0, 0.0, pe);
   }
   if (tall) {
@@ -436,6 +471,7 @@ int run_loop(const Launch& L, Work& w, const Problem& P, i64 nsteps, bool with_f
   for (i64 i = 0; i < nsteps; ++i) RUTV_TRY(sampled_step(L, w, P, i));
   if (with_final) RUTV_TRY(final_step(L, w, P, nsteps));
   RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
+  if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
   return 0;
 }
 
@@ -452,6 +488,9 @@ int begin_call(randutv_ctx* ctx) {
     RUTV_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi));
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eR, cudaEventDisableTiming));
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eF, cudaEventDisableTiming));
+    RUTV_CUDA(cudaStreamCreateWithPriority(&ctx->vstr, cudaStreamNonBlocking, lo));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eWv, cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eV, cudaEventDisableTiming));
   }
   return 0;
 }
@@ -531,6 +570,12 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
   rutv::comm_free(ctx->comm_side);
   rutv::comm_free(ctx->comm);
   ctx->comm = ctx->comm_side = nullptr;
+  if (ctx->vstr) {
+    cudaStreamSynchronize(ctx->vstr);
+    cudaEventDestroy(ctx->eWv);
+    cudaEventDestroy(ctx->eV);
+    cudaStreamDestroy(ctx->vstr);
+  }
   if (ctx->side) {
     cudaEventDestroy(ctx->eR);
     cudaEventDestroy(ctx->eF);
@@ -638,7 +683,7 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
     RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
   }
   Problem P{m, n, bb, q, seed, T, ldt, uv ? U : nullptr, ldu, uv ? V : nullptr, ldv, false,
-            ctx->side_launch(), ctx->eR, ctx->eF};
+            ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
   const i64 nsamp = sampled_steps(n, bb);
   RUTV_TRY(run_loop(L, w, P, nsamp, true));
   const int st = finish(ctx, w);
@@ -682,7 +727,7 @@ RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, cons
   RUTV_CUDA(cudaMemcpy2DAsync(w.Twork, m * 8, A, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
   if (uv) RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
   Problem P{m, n, bb, q, seed, w.Twork, m, nullptr, m, uv ? V : nullptr, ldv, uv,
-            ctx->side_launch(), ctx->eR, ctx->eF};
+            ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
   RUTV_TRY(run_loop(L, w, P, K, with_final));
   // rho = ||T(k:m, k:n)||_F
   RUTV_TRY(launch_sumsq(L, m - k, n - k, w.Twork + k + k * m, m, w.red, w.scal));
