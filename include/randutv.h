@@ -121,6 +121,20 @@ RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, cons
                                     double* Uk, int64_t ldu, double* Tk, int64_t ldt, double* V, int64_t ldv,
                                     double* resid_fro);
 
+/* Adaptive-rank variant (P:155-157 on why partial
+ * methods otherwise need k up front): sampled steps run until the trailing
+ * block meets ||T(k:m, k:n)||_F <= tol * ||A||_F, with k = (steps done) * b; if
+ * no sampled step meets it, the full factorisation runs and k = n (rho = 0).
+ * Each step adds one device-to-host norm readback.  Outputs as
+ * randutv_factor_rank for that k: caller sizes Uk (ldu >= m) and Tk (ldt >= n)
+ * for up to n columns / rows.  *k_out (host) receives k.
+ * Arguments: 1 ctx, 2 m, 3 n, 4 A, 5 lda, 6 tol (> 0), 7 b, 8 q, 9 seed,
+ * 10 flags, 11 Uk, 12 ldu, 13 Tk, 14 ldt, 15 V, 16 ldv, 17 k_out, 18 resid_fro. */
+RANDUTV_API int randutv_factor_tol(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, double tol,
+                                   int64_t b, int q, uint64_t seed, unsigned flags, double* Uk, int64_t ldu,
+                                   double* Tk, int64_t ldt, double* V, int64_t ldv, int64_t* k_out,
+                                   double* resid_fro);
+
 RANDUTV_API const char* randutv_status_string(int status);
 /* Last CUDA error message seen by any call of this thread ("" if none). */
 RANDUTV_API const char* randutv_last_error(void);

@@ -691,44 +691,69 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
   return st;
 }
 
-RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t k,
-                                    int64_t b, int q, uint64_t seed, unsigned flags, double* Uk, int64_t ldu,
-                                    double* Tk, int64_t ldt, double* V, int64_t ldv, double* resid_fro) {
-  RUTV_TRY(begin_call(ctx));
+}  // extern "C"
+
+namespace {
+
+// The truncated variant (fixed k) and the adaptive-rank variant (tol > 0: stop
+// after the first sampled step whose trailing block has ||T(k:m,k:n)||_F <=
+// tol ||A||_F; P:155-157 on why partial methods
+// otherwise need k up front).  Status, outputs and argument positions follow
+// randutv_factor_rank; *k_out receives the rank used.
+int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64 k, double tol, i64 b, int q,
+                   uint64_t seed, unsigned flags, double* Uk, i64 ldu, double* Tk, i64 ldt, double* V, i64 ldv,
+                   double* resid_fro, int64_t* k_out) {
+  const bool adaptive = tol > 0.0;
   const bool uv = !(flags & RANDUTV_NO_UV);
-  if (n < 1) return -3;
-  if (m < n) return -2;
-  if (!A) return -4;
-  if (lda < m) return -5;
-  if (k < 1 || k > n) return -6;
-  if (b < 1) return -7;
-  if (q < 0) return -8;
-  if (uv && !Uk) return -11;
-  if (uv && ldu < m) return -12;
-  if (!Tk) return -13;
-  if (ldt < k) return -14;
-  if (uv && !V) return -15;
-  if (uv && ldv < n) return -16;
-  if (!resid_fro) return -17;
   const i64 bb = b < n ? b : n;
   const i64 nsamp = sampled_steps(n, bb);
-  i64 K = (k + bb - 1) / bb;
-  bool with_final = false;
-  if (K > nsamp) {
+  i64 K = adaptive ? nsamp : (k + bb - 1) / bb;
+  bool with_final = adaptive;  // adaptive: the full factorisation if no step meets tol
+  if (!adaptive && K > nsamp) {
     K = nsamp;
     with_final = true;
   }
-  const i64 nrec = uv ? K + (with_final ? 1 : 0) : 0;
+  const i64 nrec_max = uv ? K + (with_final ? 1 : 0) : 0;
   Launch L = ctx->launch();
   Work w;
-  RUTV_TRY(prepare(ctx, w, m, n, bb, nrec, true));
+  RUTV_TRY(prepare(ctx, w, m, n, bb, nrec_max, true));
   if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
   RUTV_TRY(start_status(ctx, w));
   RUTV_CUDA(cudaMemcpy2DAsync(w.Twork, m * 8, A, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
   if (uv) RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
   Problem P{m, n, bb, q, seed, w.Twork, m, nullptr, m, uv ? V : nullptr, ldv, uv,
             ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
-  RUTV_TRY(run_loop(L, w, P, K, with_final));
+  if (!adaptive) {
+    RUTV_TRY(run_loop(L, w, P, K, with_final));
+  } else {
+    double a2 = 0.0;
+    RUTV_TRY(launch_sumsq(L, m, n, w.Twork, m, w.red, w.scal));
+    RUTV_CUDA(cudaMemcpyAsync(&a2, w.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double thr2 = tol * tol * a2;
+    i64 done = nsamp;
+    for (i64 i = 0; i < nsamp; ++i) {
+      RUTV_TRY(sampled_step(L, w, P, i));
+      // ||T(k':m, k':n)||^2, k' = (i+1) b: disjoint from the side stream's folds
+      // of step i (row and column block i)
+      const i64 kp = (i + 1) * bb;
+      double t2 = 0.0;
+      RUTV_TRY(launch_sumsq(L, m - kp, n - kp, w.Twork + kp + kp * m, m, w.red, w.scal));
+      RUTV_CUDA(cudaMemcpyAsync(&t2, w.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (t2 <= thr2) {
+        done = i + 1;
+        break;
+      }
+    }
+    K = done;
+    with_final = done == nsamp;
+    if (with_final) RUTV_TRY(final_step(L, w, P, nsamp));
+    RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
+    if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
+    k = with_final ? n : K * bb;
+  }
+  const i64 nrec = uv ? K + (with_final ? 1 : 0) : 0;
   // rho = ||T(k:m, k:n)||_F
   RUTV_TRY(launch_sumsq(L, m - k, n - k, w.Twork + k + k * m, m, w.red, w.scal));
   // Tk = T(0:k, :)
@@ -764,8 +789,59 @@ RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, cons
   RUTV_CUDA(cudaMemcpyAsync(&ss, w.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   const int st = finish(ctx, w);
   *resid_fro = std::sqrt(ss);
+  if (k_out) *k_out = k;
   if (st == 0) ctx->stats.factorizations++;
   return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t k,
+                                    int64_t b, int q, uint64_t seed, unsigned flags, double* Uk, int64_t ldu,
+                                    double* Tk, int64_t ldt, double* V, int64_t ldv, double* resid_fro) {
+  RUTV_TRY(begin_call(ctx));
+  const bool uv = !(flags & RANDUTV_NO_UV);
+  if (n < 1) return -3;
+  if (m < n) return -2;
+  if (!A) return -4;
+  if (lda < m) return -5;
+  if (k < 1 || k > n) return -6;
+  if (b < 1) return -7;
+  if (q < 0) return -8;
+  if (uv && !Uk) return -11;
+  if (uv && ldu < m) return -12;
+  if (!Tk) return -13;
+  if (ldt < k) return -14;
+  if (uv && !V) return -15;
+  if (uv && ldv < n) return -16;
+  if (!resid_fro) return -17;
+  return truncated_impl(ctx, m, n, A, lda, k, 0.0, b, q, seed, flags, Uk, ldu, Tk, ldt, V, ldv, resid_fro, nullptr);
+}
+
+RANDUTV_API int randutv_factor_tol(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, double tol,
+                                   int64_t b, int q, uint64_t seed, unsigned flags, double* Uk, int64_t ldu,
+                                   double* Tk, int64_t ldt, double* V, int64_t ldv, int64_t* k_out,
+                                   double* resid_fro) {
+  RUTV_TRY(begin_call(ctx));
+  const bool uv = !(flags & RANDUTV_NO_UV);
+  if (n < 1) return -3;
+  if (m < n) return -2;
+  if (!A) return -4;
+  if (lda < m) return -5;
+  if (!(tol > 0.0)) return -6;
+  if (b < 1) return -7;
+  if (q < 0) return -8;
+  if (uv && !Uk) return -11;
+  if (uv && ldu < m) return -12;
+  if (!Tk) return -13;
+  if (ldt < n) return -14;
+  if (uv && !V) return -15;
+  if (uv && ldv < n) return -16;
+  if (!k_out) return -17;
+  if (!resid_fro) return -18;
+  return truncated_impl(ctx, m, n, A, lda, 0, tol, b, q, seed, flags, Uk, ldu, Tk, ldt, V, ldv, resid_fro, k_out);
 }
 
 // ----------------------------------------------------------------- literal form

@@ -61,6 +61,8 @@ SIGNATURES = {
                                  _vp, _i64, _vp, _i64, _vp, _i64]),
     "randutv_factor_rank": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _int, _u64, _uint,
                                    _vp, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(_dbl)]),
+    "randutv_factor_tol": (_int, [_vp, _i64, _i64, _vp, _i64, _dbl, _i64, _int, _u64, _uint, _vp, _i64, _vp, _i64,
+                                  _vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_dbl)]),
     "randutv_status_string": (ctypes.c_char_p, [_int]),
     "randutv_last_error": (ctypes.c_char_p, []),
     "randutv_get_stats": (_int, [_vp, ctypes.POINTER(Stats)]),
@@ -232,6 +234,25 @@ class Context:
                                           ctypes.byref(rho))
         _check("randutv_factor_rank", st)
         return Uk, Tk, V, rho.value
+
+    def randutv_factor_tol(self, A, tol, b, q, seed, build_uv=True, flags=0):
+        """Adaptive-rank randUTV: returns (Uk, Tk, V, rho, k) for the first k = i*b whose
+        trailing block has ||T(k:m, k:n)||_F <= tol ||A||_F."""
+        m, n = A.shape
+        if not build_uv:
+            flags |= RANDUTV_NO_UV
+        Tf = colmajor(n, n, device=A.device)
+        Uf = colmajor(m, n, device=A.device) if build_uv else None
+        V = colmajor(n, n, device=A.device) if build_uv else None
+        rho = ctypes.c_double()
+        kk = ctypes.c_int64()
+        st = self.lib.randutv_factor_tol(self.h, m, n, _ptr(A), _ld(A), float(tol), int(b), int(q),
+                                         int(seed) & (2**64 - 1), flags, _ptr(Uf), _ld(Uf) if Uf is not None else 1,
+                                         _ptr(Tf), _ld(Tf), _ptr(V), _ld(V) if V is not None else 1,
+                                         ctypes.byref(kk), ctypes.byref(rho))
+        _check("randutv_factor_tol", st)
+        k = kk.value
+        return (Uf[:, :k] if Uf is not None else None), Tf[:k, :], V, rho.value, k
 
     # ---------------------------------------------------------------- step entries
     def randutv_gaussian(self, seed, it, rows, cols, G=None):

@@ -191,3 +191,28 @@ def test_error_codes(ctx):
     with pytest.raises(RandUTVError) as e:
         ctx.randutv_factor_ex(to_dev(Bn), 2, 1, 1, flags=RANDUTV_CHECK_FINITE)
     assert e.value.status == RANDUTV_ERR_NONFINITE
+
+
+def test_adaptive_rank(ctx):
+    """randutv_factor_tol stops at the first k = K b with ||T(k:, k:)||_F <= tol ||A||_F;
+    the oracle's truncated runs at K-1 and K bracket the tolerance, and the factors
+    match the oracle's truncated run at that k."""
+    A = make_numpy("powspec", 512, 512, cfg_index=1)
+    b, q, seed, tol = 64, 2, 2001, 1e-3
+    nA = np.linalg.norm(A)
+    Uk, Tk, V, rho, k = ctx.randutv_factor_tol(to_dev(A), tol, b, q, seed)
+    K = k // b
+    assert k % b == 0 and 1 <= K < 512 // b
+    o = oracle_randutv(A, b, q, seed, k=k, thin_u=True)
+    assert o["rho"] <= tol * nA
+    if K > 1:
+        assert oracle_randutv(A, b, q, seed, k=k - b, thin_u=True)["rho"] > tol * nA
+    assert abs(rho - o["rho"]) <= 1e-9 * o["rho"]
+    Uk, Tk, V = to_np(Uk), to_np(Tk), to_np(V)
+    assert np.max(np.abs(np.abs(Tk) - np.abs(o["Tk"]))) / nA <= ELEM_TOL
+    assert diag_parity(np.diag(Tk), np.diag(o["Tk"])) <= 1.0
+    assert spectral_orth_error(Uk) <= 1e-12 and spectral_orth_error(V) <= 1e-12
+    assert abs(np.linalg.norm(A - Uk @ Tk @ V.T) - rho) <= 1e-12 * nA
+    # a tolerance no sampled step meets: the full factorisation, k = n, rho = 0
+    _, Tk2, _, rho2, k2 = ctx.randutv_factor_tol(to_dev(A), 1e-300, b, q, seed)
+    assert k2 == 512 and rho2 == 0.0
