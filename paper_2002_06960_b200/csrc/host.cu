@@ -14,19 +14,20 @@
 // (cyclic sweeps larger than an LRU cache never hit).
 // Copies run on two copy streams (H2D prefetch of the next panel of the pass,
 // D2H write-back of victims) and overlap the DMMA work on the compute stream;
-// events order slot reuse.  Per sampled step i (k = i b), panels j >= i:
-//   pass 1   (RW)  pending U_s^T fold of row block i-1 (deferred from step
-//                  i-1, it commutes with everything before S5 of step i) and
-//                  Y_j = T_j(k:m)^T G                                   S1, S2
+// events order slot reuse.  Per sampled step i (k = i b), panels j >= i,
+// 2q + 2 passes over T (step 0: one more, its S2 pass):
 //   2q passes (R)  Z = sum_j T_j(k:m) Y_j ; Y_j = T_j(k:m)^T Z           S3
+//                  (rows k:m only: a panel fetched here loads rows k:m;
+//                  rows 0:k follow when a later pass needs them)
 //   QR(Y) on the device                                                  S4
 //   pass     (R)   Z = sum_j T_j W_j (all m rows)                        S5
-//   pass     (RW)  panel i: S5 update, QR of rows k:m (S6);
-//                  panels j > i: S5 update, then S7 left update          S5-S7
+//   panel i        S5 update, QR of rows k:m (S6), Jacobi SVD of the
+//                  diagonal block, T11 = diag d, A01 V_s                 S5, S6, S8, S9
+//   pass     (RW)  panels j > i: S5 update, S7 left update, U_s^T fold of
+//                  rows k:k+b, and the NEXT step's sample
+//                  Y'_j = T_j(k+b:m)^T G'  while the panel is resident   S5, S7, S9, S1+S2
 //   V, U           read pass (X W) + RW pass (X -= ...) over their trailing
-//                  panels                                                S5, S7
-//   panel i        Jacobi SVD of the diagonal block, T11 = diag d, A01 V_s;
-//                  U_i U_s, V_i V_s                                      S8, S9
+//                  panels, then U_i U_s, V_i V_s                          S5, S7, S9
 // The arithmetic is that of the in-HBM driver (same kernels, same reflector
 // conventions); only sums over panels are split (GEMM accumulation with
 // beta = 1), so results agree with randutv_factor_ex to rounding.
@@ -50,6 +51,7 @@ struct Slot {
   double* d = nullptr;
   int mat = -1;
   i64 panel = -1;
+  i64 lo = 0;  // rows [lo, rows) of the panel are resident (sample passes need only k..m)
   bool dirty = false;
   int pins = 0;
   uint64_t last = 0;
@@ -130,8 +132,8 @@ struct PanelCache {
     RUTV_CUDA(cudaStreamWaitEvent(d2h, s.idle, 0));
     size_t e0 = 0, e1 = 0;
     if (timer.on) RUTV_TRY(timer.mark(d2h, &e0));
-    RUTV_CUDA(cudaMemcpy2DAsync(M.h + s.panel * b * M.ld, M.ld * 8, s.d, M.rows * 8, M.rows * 8, w,
-                                cudaMemcpyDeviceToHost, d2h));
+    RUTV_CUDA(cudaMemcpy2DAsync(M.h + s.panel * b * M.ld + s.lo, M.ld * 8, s.d + s.lo, M.rows * 8,
+                                (M.rows - s.lo) * 8, w, cudaMemcpyDeviceToHost, d2h));
     if (timer.on) {
       RUTV_TRY(timer.mark(d2h, &e1));
       timer.d2h.push_back({e0, e1});
@@ -140,7 +142,7 @@ struct PanelCache {
     cudaEvent_t& we = wbev[s.mat][s.panel];
     if (!we) RUTV_CUDA(cudaEventCreateWithFlags(&we, cudaEventDisableTiming));
     RUTV_CUDA(cudaEventRecord(we, d2h));
-    rep->d2h_bytes += M.rows * w * 8;
+    rep->d2h_bytes += (M.rows - s.lo) * w * 8;
     s.dirty = false;
     return 0;
   }
@@ -160,11 +162,36 @@ struct PanelCache {
     return 0;
   }
 
-  // make (mat, panel) resident; `load` = false gives an uninitialised slot
-  // (the caller overwrites the whole panel, e.g. U := I)
-  int fetch(int mat, i64 panel, bool load, int* out) {
+  // H2D of rows [lo, hi) of (mat, panel) into slot v (after its earlier users)
+  int load_rows(Slot& v, int mat, i64 panel, i64 lo, i64 hi) {
+    const HostMat& M = mats[mat];
+    const i64 w = width(mat, panel);
+    if (wbev[mat][panel]) RUTV_CUDA(cudaStreamWaitEvent(h2d, wbev[mat][panel], 0));
+    size_t e0 = 0, e1 = 0;
+    if (timer.on) RUTV_TRY(timer.mark(h2d, &e0));
+    RUTV_CUDA(cudaMemcpy2DAsync(v.d + lo, M.rows * 8, M.h + panel * b * M.ld + lo, M.ld * 8, (hi - lo) * 8, w,
+                                cudaMemcpyHostToDevice, h2d));
+    if (timer.on) {
+      RUTV_TRY(timer.mark(h2d, &e1));
+      timer.h2d.push_back({e0, e1});
+    }
+    rep->h2d_bytes += (hi - lo) * w * 8;
+    return 0;
+  }
+
+  // make rows [lo, rows) of (mat, panel) resident; `load` = false gives an
+  // uninitialised slot (the caller overwrites the whole panel, e.g. U := I)
+  int fetch(int mat, i64 panel, bool load, int* out, i64 lo = 0) {
+    const HostMat& M = mats[mat];
     int s = where[mat][panel];
     if (s >= 0) {
+      Slot& v = slots[s];
+      if (load && lo < v.lo) {  // resident, but the rows above are needed now
+        RUTV_CUDA(cudaStreamWaitEvent(h2d, v.idle, 0));
+        RUTV_TRY(load_rows(v, mat, panel, lo, v.lo));
+        v.lo = lo;
+        RUTV_CUDA(cudaEventRecord(v.ready, h2d));
+      }
       ++rep->cache_hits;
       *out = s;
       return 0;
@@ -180,32 +207,20 @@ struct PanelCache {
     v.panel = panel;
     v.dirty = false;
     v.last = ++clock;
+    v.lo = load ? lo : 0;
     where[mat][panel] = s;
-    const HostMat& M = mats[mat];
-    const i64 w = width(mat, panel);
     RUTV_CUDA(cudaStreamWaitEvent(h2d, v.idle, 0));
     RUTV_CUDA(cudaStreamWaitEvent(h2d, v.clean, 0));
-    if (load) {
-      if (wbev[mat][panel]) RUTV_CUDA(cudaStreamWaitEvent(h2d, wbev[mat][panel], 0));
-      size_t e0 = 0, e1 = 0;
-      if (timer.on) RUTV_TRY(timer.mark(h2d, &e0));
-      RUTV_CUDA(cudaMemcpy2DAsync(v.d, M.rows * 8, M.h + panel * b * M.ld, M.ld * 8, M.rows * 8, w,
-                                  cudaMemcpyHostToDevice, h2d));
-      if (timer.on) {
-        RUTV_TRY(timer.mark(h2d, &e1));
-        timer.h2d.push_back({e0, e1});
-      }
-      rep->h2d_bytes += M.rows * w * 8;
-    }
+    if (load) RUTV_TRY(load_rows(v, mat, panel, lo, M.rows));
     RUTV_CUDA(cudaEventRecord(v.ready, h2d));
     *out = s;
     return 0;
   }
 
   // pin (mat, panel) for compute on `comp`; returns the device panel (ld = rows)
-  int get(int mat, i64 panel, double** d, bool load = true) {
+  int get(int mat, i64 panel, double** d, bool load = true, i64 lo = 0) {
     int s;
-    RUTV_TRY(fetch(mat, panel, load, &s));
+    RUTV_TRY(fetch(mat, panel, load, &s, lo));
     Slot& v = slots[s];
     v.pins++;
     v.last = ++clock;
@@ -220,10 +235,10 @@ struct PanelCache {
     RUTV_CUDA(cudaEventRecord(v.idle, comp));
     return 0;
   }
-  int prefetch(int mat, i64 panel) {
+  int prefetch(int mat, i64 panel, i64 lo = 0) {
     if (panel < 0 || panel >= mats[mat].npanels) return 0;
     int s;
-    return fetch(mat, panel, true, &s);
+    return fetch(mat, panel, true, &s, lo);
   }
   int flush() {
     for (Slot& s : slots)
@@ -242,32 +257,25 @@ struct HostRun {
   int q;
   uint64_t seed;
   bool dir = false;        // direction of the next pass (serpentine)
-  i64 fold_row = -1;       // pending U_s^T fold of row block [fold_row, fold_row + b) ...
-  i64 fold_from = 0;       // ... for panels >= fold_from
-  double* Usf = nullptr;   // its U_s (b x b)
+  bool y_ready = false;    // Y of the next step was taken by the previous step's fused pass
 };
 
 // Visit panels [p0, p1) of `mat` in the current serpentine direction with a
 // one-panel prefetch; f(panel, device ptr) enqueues the work on the compute stream.
 template <class F>
-int pass(HostRun& R, int mat, i64 p0, i64 p1, bool dirty, F&& f) {
+int pass(HostRun& R, int mat, i64 p0, i64 p1, bool dirty, F&& f, i64 lo = 0) {
   const bool fwd = R.dir;
   R.dir = !R.dir;
   const i64 cnt = p1 - p0;
   for (i64 t = 0; t < cnt; ++t) {
     const i64 j = fwd ? p0 + t : p1 - 1 - t;
     double* d;
-    RUTV_TRY(R.pc.get(mat, j, &d));
-    if (t + 1 < cnt) RUTV_TRY(R.pc.prefetch(mat, fwd ? j + 1 : j - 1));
+    RUTV_TRY(R.pc.get(mat, j, &d, true, lo));
+    if (t + 1 < cnt) RUTV_TRY(R.pc.prefetch(mat, fwd ? j + 1 : j - 1, lo));
     RUTV_TRY(f(j, d));
     RUTV_TRY(R.pc.put(mat, j, dirty));
   }
   return 0;
-}
-
-// X (rows x cols) := M^T X in place through Zt
-int fold_rows(HostRun& R, i64 bw, i64 cols, double* X, i64 ldx, const double* M) {
-  return left_mult_t_inplace(R.L, R.w.Zf, bw, cols, X, ldx, M, bw);
 }
 
 // right update of the trailing panels [p0, np) of matrix `mat` (rows x *):
@@ -292,16 +300,21 @@ int stream_apply_right(HostRun& R, int mat, i64 p0, i64 bw, const double* W, i64
   });
 }
 
-int host_svd_fold(HostRun& R, i64 i, i64 bw, bool defer_fold) {
+// S8 + the T part of S9 on panel i (width bw): T11 := diag(d), T(0:k, blk) := T(0:k, blk) V_s.
+// U_s^T T(k:k+b, k+b:n) is folded by the caller's pass over the trailing panels.
+int host_svd_T(HostRun& R, i64 i, i64 bw, double* X) {
   Work& w = R.w;
   const i64 k = i * R.b;
-  double* X;
-  RUTV_TRY(R.pc.get(R.mT, i, &X));
   double* T11 = X + k;
   RUTV_TRY(launch_jacobi_svd(R.L, bw, T11, R.m, w.Us, w.d, w.Vs, w.status, (int)(i + 1), w.jac, w.jac_elems));
   RUTV_TRY(launch_set_diag(R.L, bw, w.d, T11, R.m));
-  RUTV_TRY(right_mult_inplace(R.L, w.Zf, k, bw, X, R.m, w.Vs, bw));  // A01 V_s
-  RUTV_TRY(R.pc.put(R.mT, i, true));
+  return right_mult_inplace(R.L, w.Zf, k, bw, X, R.m, w.Vs, bw);  // A01 V_s
+}
+
+// the U and V parts of S9: U(:, blk) := U(:, blk) U_s, V(:, blk) := V(:, blk) V_s
+int host_fold_uv(HostRun& R, i64 i, i64 bw) {
+  Work& w = R.w;
+  double* X;
   if (R.mU >= 0) {
     RUTV_TRY(R.pc.get(R.mU, i, &X));
     RUTV_TRY(right_mult_inplace(R.L, w.Zf, R.m, bw, X, R.m, w.Us, bw));
@@ -312,43 +325,39 @@ int host_svd_fold(HostRun& R, i64 i, i64 bw, bool defer_fold) {
     RUTV_TRY(right_mult_inplace(R.L, w.Zf, R.n, bw, X, R.n, w.Vs, bw));
     RUTV_TRY(R.pc.put(R.mV, i, true));
   }
-  if (defer_fold) {
-    // U_s^T T(k:k+b, k+b:n) is applied by the next pass over the trailing panels
-    RUTV_TRY(launch_copy(R.L, bw, bw, w.Us, bw, R.Usf, bw));
-    R.fold_row = k;
-    R.fold_from = i + 1;
-  }
   return 0;
 }
 
-int apply_pending_fold(HostRun& R, i64 j, double* X) {
-  if (R.fold_row < 0 || j < R.fold_from) return 0;
-  return fold_rows(R, R.b, R.pc.width(R.mT, j), X + R.fold_row, R.m, R.Usf);
-}
-
+// One sampled step in 2q + 2 passes over the trailing panels of T (S12):
+// the 2q power passes, the S5 read pass (T W_V), and ONE read+write pass that
+// applies S5, S7 and the U_s^T fold to each panel and then already takes the
+// next step's sample Y' = T(k+b:m, j)^T G' (S1/S2 of step i+1) while the panel
+// is resident.  Only step 0 needs a separate S2 pass.
 int host_sampled_step(HostRun& R, i64 i) {
   Work& w = R.w;
   const i64 m = R.m, n = R.n, b = R.b, k = i * b, r = m - k, s = n - k;
   const i64 np = R.pc.mats[R.mT].npanels;
-  // S1; pass 1: pending fold + S2
-  RUTV_TRY(launch_gaussian(R.L, R.seed, i, r, b, w.G, r));
-  RUTV_TRY(pass(R, R.mT, i, np, R.fold_row >= 0, [&](i64 j, double* X) {
-    RUTV_TRY(apply_pending_fold(R, j, X));
-    return launch_dgemm(R.L, true, false, R.pc.width(R.mT, j), b, r, 1.0, X + k, m, w.G, r, 0.0,
-                        w.Y + (j - i) * b, s, w.gemm_ws, w.gemm_ws_elems);
-  }));
-  R.fold_row = -1;
+  const bool next_sampled = s - b > b;
+  // S1 + S2 (step 0 only)
+  if (!R.y_ready) {
+    RUTV_TRY(launch_gaussian(R.L, R.seed, i, r, b, w.G, r));
+    RUTV_TRY(pass(R, R.mT, i, np, false, [&](i64 j, double* X) {
+      return launch_dgemm(R.L, true, false, R.pc.width(R.mT, j), b, r, 1.0, X + k, m, w.G, r, 0.0,
+                          w.Y + (j - i) * b, s, w.gemm_ws, w.gemm_ws_elems);
+    }, k));  // rows above k are not read
+  }
+  R.y_ready = false;
   // S3
   for (int qq = 0; qq < R.q; ++qq) {
     RUTV_TRY(launch_fill(R.L, r, b, 0.0, w.Z, r));
     RUTV_TRY(pass(R, R.mT, i, np, false, [&](i64 j, double* X) {
       return launch_dgemm(R.L, false, false, r, b, R.pc.width(R.mT, j), 1.0, X + k, m, w.Y + (j - i) * b, s, 1.0,
                           w.Z, r, nullptr, 0);
-    }));
+    }, k));
     RUTV_TRY(pass(R, R.mT, i, np, false, [&](i64 j, double* X) {
       return launch_dgemm(R.L, true, false, R.pc.width(R.mT, j), b, r, 1.0, X + k, m, w.Z, r, 0.0,
                           w.Y + (j - i) * b, s, w.gemm_ws, w.gemm_ws_elems);
-    }));
+    }, k));
   }
   // S4
   RUTV_TRY(panel_qr(R.L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
@@ -359,7 +368,7 @@ int host_sampled_step(HostRun& R, i64 i) {
                         m, nullptr, 0);
   }));
   RUTV_TRY(launch_dgemm(R.L, false, false, m, b, b, 1.0, w.Z, m, w.TV, b, 0.0, w.Z2, m, nullptr, 0));
-  // S5 update + S6 on panel i
+  // panel i: S5 update, S6, S8 and the T part of S9
   {
     double* X;
     RUTV_TRY(R.pc.get(R.mT, i, &X));
@@ -367,21 +376,27 @@ int host_sampled_step(HostRun& R, i64 i) {
     RUTV_TRY(panel_qr(R.L, r, b, X + k, m, w.tauU, w.Wu, r, w.TU, b, w.qw));
     RUTV_TRY(launch_triu(R.L, b, b, X + k, m));
     RUTV_TRY(launch_fill(R.L, r - b, b, 0.0, X + k + b, m));
+    RUTV_TRY(host_svd_T(R, i, b, X));
     RUTV_TRY(R.pc.put(R.mT, i, true));
   }
-  // S5 update + S7 on panels > i (RW).  apply_left_t uses Z/Z2 as temporaries:
-  // keep Z2 (the S5 factor) in Zf meanwhile.
+  // panels > i (RW): S5 update, S7, U_s^T fold, next step's S2.  apply_left_t
+  // uses Z/Z2 as temporaries: keep Z2 (the S5 factor) in Zf meanwhile.
+  if (next_sampled) RUTV_TRY(launch_gaussian(R.L, R.seed, i + 1, r - b, b, w.G, r - b));
   RUTV_TRY(launch_copy(R.L, m, b, w.Z2, m, w.Zf, m));
   RUTV_TRY(pass(R, R.mT, i + 1, np, true, [&](i64 j, double* X) {
     const i64 wj = R.pc.width(R.mT, j);
     RUTV_TRY(launch_dgemm(R.L, false, true, m, wj, b, -1.0, w.Zf, m, w.Wv + (j - i) * b, s, 1.0, X, m, nullptr, 0));
-    return apply_left_t(R.L, w, r, wj, b, X + k, m, w.Wu, r, w.TU, b);
+    RUTV_TRY(apply_left_t(R.L, w, r, wj, b, X + k, m, w.Wu, r, w.TU, b));
+    RUTV_TRY(left_mult_t_inplace(R.L, w.Zv, b, wj, X + k, m, w.Us, b));
+    if (!next_sampled) return 0;
+    return launch_dgemm(R.L, true, false, wj, b, r - b, 1.0, X + k + b, m, w.G, r - b, 0.0,
+                        w.Y + (j - i - 1) * b, s - b, w.gemm_ws, w.gemm_ws_elems);
   }));
-  // V: right transform with W_V; U: right transform with W_U (columns k:m)
+  R.y_ready = next_sampled;
+  // V: right transform with W_V; U: right transform with W_U (columns k:m); then their S9 folds
   if (R.mV >= 0) RUTV_TRY(stream_apply_right(R, R.mV, i, b, w.Wv, s, w.TV, b));
   if (R.mU >= 0) RUTV_TRY(stream_apply_right(R, R.mU, i, b, w.Wu, r, w.TU, b));
-  // S8, S9
-  return host_svd_fold(R, i, b, true);
+  return host_fold_uv(R, i, b);
 }
 
 int host_final_step(HostRun& R, i64 i) {
@@ -390,17 +405,16 @@ int host_final_step(HostRun& R, i64 i) {
   if (s <= 0) return 0;
   double* X;
   RUTV_TRY(R.pc.get(R.mT, i, &X));
-  RUTV_TRY(apply_pending_fold(R, i, X));
-  R.fold_row = -1;
   const bool tall = r > s;
   if (tall) {
     RUTV_TRY(panel_qr(R.L, r, s, X + k, m, w.tauU, w.Wu, r, w.TU, R.b, w.qw));
     RUTV_TRY(launch_triu(R.L, s, s, X + k, m));
     RUTV_TRY(launch_fill(R.L, r - s, s, 0.0, X + k + s, m));
   }
+  RUTV_TRY(host_svd_T(R, i, s, X));
   RUTV_TRY(R.pc.put(R.mT, i, true));
   if (tall && R.mU >= 0) RUTV_TRY(stream_apply_right(R, R.mU, i, s, w.Wu, r, w.TU, R.b));
-  return host_svd_fold(R, i, s, false);
+  return host_fold_uv(R, i, s);
 }
 
 }  // namespace
@@ -444,7 +458,6 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
   // workspace: the in-HBM driver's buffers + U_s of the deferred fold + the slots
   Carver dry{nullptr, 0, 0, true};
   carve(dry, R.w, m, n, bb, 0, false);
-  dry.take<double>(bb * bb);
   const size_t fixed = dry.off;
   const size_t slot_bytes = (size_t)R.pc.slot_elems * 8;
   size_t budget = device_cache_bytes;
@@ -460,7 +473,6 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
   RUTV_TRY(ensure_ws(ctx, fixed + (size_t)nslots * slot_bytes + kAlign));
   Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
   carve(real, R.w, m, n, bb, 0, false);
-  R.Usf = real.take<double>(bb * bb);
   double* slots = real.take<double>(nslots * R.pc.slot_elems);
   rep.cache_slots = nslots;
   rep.slot_bytes = (int64_t)slot_bytes;

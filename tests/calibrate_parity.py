@@ -7,7 +7,9 @@ oracle by this much; the tolerances in test_gpu_randutv.py sit >= 30x above it
 (DESIGN.md "Parity tolerances").
 """
 import numpy as np, sys, time
-import os\nsys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))\nsys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from oracle.randutv import randutv
 from paper_2002_06960_b200.inputs import make_numpy
 from gpu_util import diag_parity
@@ -25,3 +27,8 @@ for (m,n,b,q) in [(200,200,32,2),(333,333,64,1),(300,170,40,2)]:
     A = np.asfortranarray(np.random.default_rng(m * 1000 + n + b + q).standard_normal((m, n)))
     o1 = randutv(A,b,q,99); o8 = randutv(pert(A),b,q,99)
     print(m,n,b,q,"diag", diag_parity(np.diag(o1["T"]), np.diag(o8["T"])), "T", np.max(np.abs(np.abs(o1["T"])-np.abs(o8["T"])))/np.linalg.norm(A), "U", np.max(np.abs(np.abs(o1["U"])-np.abs(o8["U"]))))
+# host-streamed cases (tests/test_gpu_host.py): (520, 520, 64, 2) is the ill-conditioned one
+for (m,n,b,q) in [(520,520,64,2),(300,300,32,1),(400,250,40,2)]:
+    A = np.asfortranarray(np.random.default_rng(3 * m + n + b).standard_normal((m, n)))
+    o1 = randutv(A,b,q,41); o8 = randutv(pert(A),b,q,41)
+    print("host", m,n,b,q,"T", np.max(np.abs(np.abs(o1["T"])-np.abs(o8["T"])))/np.linalg.norm(A), "U", np.max(np.abs(np.abs(o1["U"])-np.abs(o8["U"]))), "V", np.max(np.abs(np.abs(o1["V"])-np.abs(o8["V"]))))

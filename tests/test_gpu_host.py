@@ -1,8 +1,8 @@
 """Host-streamed randUTV (the GPU analogue of the
 paper's out-of-core cache + overlap runtime) against the CPU
 oracle and the in-HBM path.  A tiny device cache (3 panels) forces every pass
-to stream, so the serpentine LRU, the write-back ordering and the deferred
-U_s^T fold are all exercised; a cache that holds everything must move each
+to stream, so the serpentine LRU, the write-back ordering, the partial (rows k:m)
+panel loads and the fused update/fold/next-sample pass are all exercised; a cache that holds everything must move each
 matrix exactly once in and once out."""
 import numpy as np
 import pytest
@@ -36,10 +36,18 @@ def _run_host(ctx, A, b, q, seed, cache_panels, pinned=True, build_uv=True):
     return (np.array(U) if U is not None else None), np.array(Ah), (np.array(V) if V is not None else None), rep
 
 
+# U, V elementwise bound per case: 1e-11, except (520, 520, 64, 2), whose
+# tail singular vectors are ill-conditioned -- the oracle on A vs on
+# A(1 + 2^-52 N(0,1)) already differs by 7.2e-12 in |V| (tests/calibrate_parity.py,
+# bounds sit >= 30x above the calibrated noise).
+UV_TOL = {(520, 520, 64, 2): 3e-10}
+
+
 @pytest.mark.parametrize("m,n,b,q", [(300, 300, 32, 1), (400, 250, 40, 2), (129, 129, 128, 0), (64, 40, 64, 1),
                                      (60, 60, 4, 1), (520, 520, 64, 2)])
 @pytest.mark.parametrize("cache_panels", [3, 1000])
 def test_host_streamed_parity(ctx, m, n, b, q, cache_panels):
+    uv_tol = UV_TOL.get((m, n, b, q), ELEM_TOL)
     rng = np.random.default_rng(3 * m + n + b)
     A = np.asfortranarray(rng.standard_normal((m, n)))
     U, T, V, rep = _run_host(ctx, A, b, q, 41, cache_panels)
@@ -50,8 +58,8 @@ def test_host_streamed_parity(ctx, m, n, b, q, cache_panels):
     assert np.all(np.tril(T, -1) == 0.0)
     assert diag_parity(np.diag(T), np.diag(o["T"])) <= 1.0
     assert np.max(np.abs(np.abs(T) - np.abs(o["T"]))) / nA <= ELEM_TOL
-    assert np.max(np.abs(np.abs(U) - np.abs(o["U"]))) <= ELEM_TOL
-    assert np.max(np.abs(np.abs(V) - np.abs(o["V"]))) <= ELEM_TOL
+    assert np.max(np.abs(np.abs(U) - np.abs(o["U"]))) <= uv_tol
+    assert np.max(np.abs(np.abs(V) - np.abs(o["V"]))) <= uv_tol
     Ug, Tg, Vg, _ = ctx.randutv_factor_ex(to_dev(A), b, q, 41)
     assert np.max(np.abs(np.abs(T) - np.abs(to_np(Tg)))) / nA <= ELEM_TOL
     if cache_panels >= 1000:
