@@ -235,6 +235,30 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
                                     int64_t ldu, double* V_host, int64_t ldv, randutv_host_report* report);
 
 /* ---------------------------------------------------------------------------
+ * HQRRP: the paper's other factorisation, the blocked
+ * randomized column-pivoted QR  A P = Q R  (Sec. 2).
+ *
+ * Step i (k = i b, w = min(b, n - k)): sketch Y = G^(i) R22 (b x (n-k),
+ * P:330-335; G^(i) is the transpose of randUTV's Gaussian draw of (seed, i)),
+ * w steps of Businger-Golub column-pivoted QR of Y pick the pivots (
+ * norms recomputed each step, exact ties to the lower column), the columns
+ * k:n of R (all rows) and jpvt are permuted by LAPACK dgeqp3's swap
+ * convention, then the unpivoted Householder QR of the w pivoted
+ * columns and its compact-WY application to the trailing columns and to Q
+ * (P:372-390).  All device pointers, column-major FP64, m >= n, 1 <= b.
+ *   A     (m x n, lda >= m) in: the matrix; out: R (upper trapezoidal,
+ *         exact zeros below the diagonal)
+ *   b     block size; min(b, n) must be <= 512 (else -6)
+ *   jpvt  (n int64) out: A(:, jpvt[j]) is column j of A P (0-based)
+ *   Q     (m x m, ldq >= m) out: the orthogonal factor; not touched (may be
+ *         NULL) with flags & RANDUTV_NO_UV
+ * Returns 0, a negative argument index (-2 m < n, -3 n, -4 A, -5 lda, -6 b,
+ * -8 jpvt, -9 Q, -10 ldq) or RANDUTV_ERR_*.  Synchronous on the ctx stream.
+ * ------------------------------------------------------------------------- */
+RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, int64_t b,
+                              uint64_t seed, unsigned flags, int64_t* jpvt, double* Q, int64_t ldq);
+
+/* ---------------------------------------------------------------------------
  * Multi-GPU: the column-sharded randUTV.
  *
  * The paper's method is sequential over column blocks (each sample depends on

@@ -77,6 +77,7 @@ def hqrrp(A, b, seed, build_q=True, record=None):
         raise ValueError("hqrrp expects m >= n")
     if b < 1:
         raise ValueError("b >= 1")
+    b = min(b, n)                                         # 1 <= b <= n
     R = np.array(A, order="F", copy=True)
     Q = np.eye(m, order="F") if build_q else None
     jpvt = np.arange(n)
@@ -114,6 +115,7 @@ def hqrrp_flops(m, n, b, build_q=True):
     4 r (s - w) w and the Q update 4 m r w (the CPQR of the b x s sketch,
     ~ 2 b^2 s, is counted too)."""
     fl = 0.0
+    b = min(b, n)
     for k in range(0, n, b):
         r, s = m - k, n - k
         w = min(b, s)

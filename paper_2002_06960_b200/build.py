@@ -13,7 +13,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-SOURCES = ["philox.cu", "dgemm.cu", "qr.cu", "jacobi.cu", "misc.cu", "randutv.cu", "dist.cu", "host.cu"]
+SOURCES = ["philox.cu", "dgemm.cu", "qr.cu", "jacobi.cu", "misc.cu", "randutv.cu", "dist.cu", "host.cu", "hqrrp.cu"]
 
 
 def nccl_dir():

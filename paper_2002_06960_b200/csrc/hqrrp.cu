@@ -1,0 +1,386 @@
+// HQRRP: blocked randomized column-pivoted Householder QR, A P = Q R
+// (Sec. 2 of the paper).  Step i (k = i b,
+// r = m - k, s = n - k, w = min(b, s)):
+//   H1/H2  Y = G^T R(k:m, k:n)            (b x s; G = randUTV's draw of step i)
+//   H3     w steps of Businger-Golub CPQR of Y      -> pivot columns (cpqr_sketch_kernel)
+//   H4     the swap-convention permutation of columns k:n of R (all m rows) and
+//          of jpvt -- only the <= 2w columns that move are copied
+//   H5     unpivoted Householder QR of R(k:m, k:k+w)  (the randUTV panel QR)
+//   H6     R(k:m, k+w:n) := Q22^T R(k:m, k+w:n);  Q(:, k:m) := Q(:, k:m) Q22
+// H2, H5 and H6 are the DMMA GEMM / panel-QR kernels of the randUTV path; the
+// sketch CPQR is the one new kernel.
+#include <algorithm>
+#include <climits>
+#include <cooperative_groups.h>
+
+#include "driver.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rutv {
+namespace {
+
+constexpr int CP_THREADS = 256;
+constexpr int CP_WARPS = CP_THREADS / 32;
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// (a, ca) beats (b, cb): larger squared norm, ties -> lower column (oracle A27)
+__device__ __forceinline__ bool beats(double a, int ca, double b, int cb) { return a > b || (a == b && ca < cb); }
+
+__device__ __forceinline__ void warp_argmax(double& v, int& c) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oc = __shfl_xor_sync(0xffffffffu, c, o);
+    if (beats(ov, oc, v, c)) {
+      v = ov;
+      c = oc;
+    }
+  }
+}
+
+// H3: `steps` steps of CPQR of Y (rows x s, column-major, ld ldy), rows <= 32 RPL.
+// Warp gw owns the columns c with c % NW == gw and keeps no state but its
+// running argmax; lanes hold rows lane + 32 t of one column at a time.  One
+// grid barrier per step: the CTA argmax partials are exchanged through
+// part_* (double-buffered by step parity), then every CTA recomputes the
+// pivot's reflector (dlarfg, P:337-339 / oracle.hqrrp.cpqr_sketch) from the
+// pivot column in global memory and applies it to its own columns, whose
+// squared norms of rows j+1: give the next step's candidates.  Columns are
+// never moved: piv[j] is the Y column chosen at step j; the swap-convention
+// permutation is built afterwards (hq_swap_kernel).
+template <int RPL>
+__global__ void __launch_bounds__(CP_THREADS) cpqr_sketch_kernel(int rows, int s, int steps, double* __restrict__ Y,
+                                                                 i64 ldy, double* part_val, int* part_col,
+                                                                 int* __restrict__ piv,
+                                                                 unsigned char* __restrict__ done) {
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = gridDim.x;
+  const int NW = G * CP_WARPS, gw = blockIdx.x * CP_WARPS + warp;
+  __shared__ double v[32 * RPL];
+  __shared__ double s_tau;
+  __shared__ int s_p;
+  __shared__ double wv[CP_WARPS];
+  __shared__ int wc[CP_WARPS];
+
+  double best = -1.0;
+  int bestc = INT_MAX;
+  for (int c = gw; c < s; c += NW) {
+    const double* y = Y + (i64)c * ldy;
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int r = lane + 32 * t;
+      if (r < rows) {
+        const double x = y[r];
+        acc += x * x;
+      }
+    }
+    acc = warp_sum_d(acc);
+    if (beats(acc, c, best, bestc)) {
+      best = acc;
+      bestc = c;
+    }
+  }
+
+  for (int j = 0; j < steps; ++j) {
+    if (lane == 0) {
+      wv[warp] = best;
+      wc[warp] = bestc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bv = wv[0];
+      int bc = wc[0];
+      for (int q = 1; q < CP_WARPS; ++q)
+        if (beats(wv[q], wc[q], bv, bc)) {
+          bv = wv[q];
+          bc = wc[q];
+        }
+      part_val[(j & 1) * G + blockIdx.x] = bv;
+      part_col[(j & 1) * G + blockIdx.x] = bc;
+    }
+    grid.sync();
+    if (warp == 0) {
+      double bv = -1.0;
+      int bc = INT_MAX;
+      for (int g = lane; g < G; g += 32) {
+        const double pv = __ldcg(part_val + (j & 1) * G + g);
+        const int pc = __ldcg(part_col + (j & 1) * G + g);
+        if (beats(pv, pc, bv, bc)) {
+          bv = pv;
+          bc = pc;
+        }
+      }
+      warp_argmax(bv, bc);
+      const int p = bc;
+      // dlarfg of the pivot column's rows j:rows (oracle.householder.dlarfg)
+      const double* y = Y + (i64)p * ldy;
+      double x[RPL];
+      double xn = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int r = lane + 32 * t;
+        x[t] = (r > j && r < rows) ? __ldcg(y + r) : 0.0;
+        xn += x[t] * x[t];
+      }
+      xn = warp_sum_d(xn);
+      const double alpha = __ldcg(y + j);
+      double tau = 0.0, den = 1.0;
+      if (xn != 0.0) {
+        const double beta = -copysign(hypot(alpha, sqrt(xn)), alpha);
+        tau = (beta - alpha) / beta;
+        den = alpha - beta;
+      }
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int r = lane + 32 * t;
+        v[r] = (r == j) ? 1.0 : ((r > j && r < rows) ? x[t] / den : 0.0);
+      }
+      if (lane == 0) {
+        s_tau = tau;
+        s_p = p;
+        if (blockIdx.x == 0) piv[j] = p;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    const double tau = s_tau;
+    if (p % NW == gw && lane == 0) done[p] = 1;
+    __syncwarp();
+    best = -1.0;
+    bestc = INT_MAX;
+    if (j + 1 == steps) break;  // the last pivot needs no update
+    for (int c = gw; c < s; c += NW) {
+      if (c == p || done[c]) continue;
+      double* y = Y + (i64)c * ldy;
+      double yr[RPL];
+      double dot = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int r = lane + 32 * t;
+        yr[t] = (r >= j && r < rows) ? y[r] : 0.0;
+        dot += v[r] * yr[t];
+      }
+      dot = warp_sum_d(dot);
+      double nn = 0.0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) {
+        const int r = lane + 32 * t;
+        if (r >= j && r < rows) {
+          if (tau != 0.0) {
+            yr[t] -= tau * (v[r] * dot);
+            y[r] = yr[t];
+          }
+          if (r > j) nn += yr[t] * yr[t];
+        }
+      }
+      nn = warp_sum_d(nn);
+      if (beats(nn, c, best, bestc)) {
+        best = nn;
+        bestc = c;
+      }
+    }
+  }
+}
+
+template <int RPL>
+int launch_cpqr_t(const Launch& L, int rows, int s, int steps, double* Y, i64 ldy, double* part_val, int* part_col,
+                  int* piv, unsigned char* done, int gmax) {
+  static int occ = -1;
+  if (occ < 0) {
+    RUTV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cpqr_sketch_kernel<RPL>, CP_THREADS, 0));
+    if (occ < 1) occ = 1;
+  }
+  int G = (s + CP_WARPS * 2 - 1) / (CP_WARPS * 2);  // >= 2 columns per warp
+  G = G < 1 ? 1 : G;
+  G = G > occ * L.device_sms ? occ * L.device_sms : G;
+  G = G > gmax ? gmax : G;
+  void* args[] = {&rows, &s, &steps, &Y, &ldy, &part_val, &part_col, &piv, &done};
+  const size_t pe = L.pbegin();
+  RUTV_CUDA(cudaLaunchCooperativeKernel((void*)cpqr_sketch_kernel<RPL>, dim3(G), dim3(CP_THREADS), args, 0,
+                                        L.stream));
+  L.count();
+  // algorithmic: the b x s sketch read + written once per step (rows j:b)
+  L.pend(PK_OTHER, 4.0 * rows * (double)s * steps, 8.0 * 2.0 * rows * (double)s * steps / 2.0, pe);
+  return 0;
+}
+
+// H4 helpers: perm (position -> Y column) and inv start as the identity; the
+// w recorded pivots are replayed as swaps (LAPACK dgeqp3's convention).
+__global__ void hq_iota_kernel(int s, int* perm, int* inv, int* cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s; i += gridDim.x * blockDim.x) {
+    perm[i] = i;
+    inv[i] = i;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cnt = 0;
+}
+
+__global__ void hq_swap_kernel(int steps, const int* __restrict__ piv, int* perm, int* inv) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  for (int j = 0; j < steps; ++j) {
+    const int p = piv[j];
+    const int pp = inv[p];
+    if (pp != j) {
+      const int cj = perm[j];
+      perm[j] = p;
+      perm[pp] = cj;
+      inv[p] = j;
+      inv[cj] = pp;
+    }
+  }
+}
+
+__global__ void hq_collect_kernel(int s, const int* __restrict__ perm, int* cnt, int* moved) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < s; i += gridDim.x * blockDim.x)
+    if (perm[i] != i) moved[atomicAdd(cnt, 1)] = i;
+}
+
+// tmp(:, t) := X(:, perm[moved[t]]) for t < *cnt (and the jpvt entries)
+__global__ void hq_gather_kernel(i64 m, const double* __restrict__ X, i64 ldx, const int* __restrict__ perm,
+                                 const int* __restrict__ cnt, const int* __restrict__ moved, double* __restrict__ tmp,
+                                 const int64_t* __restrict__ jp, int64_t* __restrict__ jtmp) {
+  const int t = blockIdx.y;
+  if (t >= *cnt) return;
+  const int src = perm[moved[t]];
+  const double* x = X + (i64)src * ldx;
+  double* d = tmp + (i64)t * m;
+  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (i64)gridDim.x * blockDim.x) d[r] = x[r];
+  if (blockIdx.x == 0 && threadIdx.x == 0) jtmp[t] = jp[src];
+}
+
+__global__ void hq_scatter_kernel(i64 m, double* __restrict__ X, i64 ldx, const int* __restrict__ cnt,
+                                  const int* __restrict__ moved, const double* __restrict__ tmp,
+                                  int64_t* __restrict__ jp, const int64_t* __restrict__ jtmp) {
+  const int t = blockIdx.y;
+  if (t >= *cnt) return;
+  const int dst = moved[t];
+  double* x = X + (i64)dst * ldx;
+  const double* sp = tmp + (i64)t * m;
+  for (i64 r = (i64)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (i64)gridDim.x * blockDim.x) x[r] = sp[r];
+  if (blockIdx.x == 0 && threadIdx.x == 0) jp[dst] = jtmp[t];
+}
+
+__global__ void hq_jpvt_init_kernel(i64 n, int64_t* jp) {
+  for (i64 i = (i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) jp[i] = i;
+}
+
+struct HqWork {
+  double* part_val;
+  int* part_col;
+  int* piv;
+  int* perm;
+  int* inv;
+  int* cnt;
+  int* moved;
+  unsigned char* done;
+  int64_t* jtmp;
+  int gmax;
+};
+
+void carve_hq(Carver& c, HqWork& h, i64 n, i64 b) {
+  h.gmax = 8 * 148;
+  h.part_val = c.take<double>(2 * h.gmax);
+  h.part_col = c.take<int>(2 * h.gmax);
+  h.piv = c.take<int>(b);
+  h.perm = c.take<int>(n);
+  h.inv = c.take<int>(n);
+  h.cnt = c.take<int>(4);
+  h.moved = c.take<int>(2 * b);
+  h.done = c.take<unsigned char>(n);
+  h.jtmp = c.take<int64_t>(2 * b);
+}
+
+int launch_cpqr(const Launch& L, int rows, int s, int steps, double* Y, i64 ldy, const HqWork& h) {
+  const int rpl = (rows + 31) / 32;
+  if (rpl <= 1) return launch_cpqr_t<1>(L, rows, s, steps, Y, ldy, h.part_val, h.part_col, h.piv, h.done, h.gmax);
+  if (rpl <= 2) return launch_cpqr_t<2>(L, rows, s, steps, Y, ldy, h.part_val, h.part_col, h.piv, h.done, h.gmax);
+  if (rpl <= 4) return launch_cpqr_t<4>(L, rows, s, steps, Y, ldy, h.part_val, h.part_col, h.piv, h.done, h.gmax);
+  if (rpl <= 8) return launch_cpqr_t<8>(L, rows, s, steps, Y, ldy, h.part_val, h.part_col, h.piv, h.done, h.gmax);
+  return launch_cpqr_t<16>(L, rows, s, steps, Y, ldy, h.part_val, h.part_col, h.piv, h.done, h.gmax);
+}
+
+// H4: permute the columns k:n of R (m rows) and jpvt(k:n) by the CPQR pivots
+int permute_columns(const Launch& L, i64 m, i64 s, int steps, double* Rk, i64 ldr, int64_t* jpk, double* tmp,
+                    const HqWork& h) {
+  const unsigned gb = (unsigned)std::min<i64>((s + 255) / 256, 4 * 148);
+  hq_iota_kernel<<<gb, 256, 0, L.stream>>>((int)s, h.perm, h.inv, h.cnt);
+  hq_swap_kernel<<<1, 32, 0, L.stream>>>(steps, h.piv, h.perm, h.inv);
+  hq_collect_kernel<<<gb, 256, 0, L.stream>>>((int)s, h.perm, h.cnt, h.moved);
+  const dim3 grid((unsigned)std::min<i64>((m + 255) / 256, 64), (unsigned)(2 * steps));
+  hq_gather_kernel<<<grid, 256, 0, L.stream>>>(m, Rk, ldr, h.perm, h.cnt, h.moved, tmp, jpk, h.jtmp);
+  hq_scatter_kernel<<<grid, 256, 0, L.stream>>>(m, Rk, ldr, h.cnt, h.moved, tmp, jpk, h.jtmp);
+  L.count(5);
+  RUTV_CHECK_LAUNCH("hqrrp permute");
+  return 0;
+}
+
+}  // namespace
+}  // namespace rutv
+
+using namespace rutv;
+
+extern "C" {
+
+RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, int64_t b,
+                              uint64_t seed, unsigned flags, int64_t* jpvt, double* Q, int64_t ldq) {
+  RUTV_TRY(begin_call(ctx));
+  const bool bq = !(flags & RANDUTV_NO_UV);
+  if (n < 1) return -3;
+  if (m < n) return -2;
+  if (!A) return -4;
+  if (lda < m) return -5;
+  if (b < 1) return -6;
+  if (!jpvt) return -8;
+  if (bq && !Q) return -9;
+  if (bq && ldq < m) return -10;
+  const i64 bb = b < n ? b : n;
+  if (bb > 512) return -6;  // the sketch CPQR keeps <= 512 rows per column in registers
+  Launch L = ctx->launch();
+  Work w;
+  HqWork h;
+  Carver dry{nullptr, 0, 0, true};
+  carve(dry, w, m, n, bb, 0, false);
+  carve_hq(dry, h, n, bb);
+  RUTV_TRY(ensure_ws(ctx, dry.off));
+  Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
+  carve(real, w, m, n, bb, 0, false);
+  carve_hq(real, h, n, bb);
+  if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
+  RUTV_TRY(start_status(ctx, w));
+  hq_jpvt_init_kernel<<<(unsigned)std::min<i64>((n + 255) / 256, 1024), 256, 0, L.stream>>>(n, jpvt);
+  L.count();
+  if (bq) RUTV_TRY(launch_set_identity(L, m, m, Q, ldq));
+  i64 i = 0;
+  for (i64 k = 0; k < n; k += bb, ++i) {
+    const i64 r = m - k, s = n - k, wd = bb < s ? bb : s;
+    double* Rk = A + k * lda;  // columns k:n, all rows
+    // H1, H2: Y (bb x s, ld bb) = G^T R(k:m, k:n)
+    RUTV_TRY(launch_gaussian(L, seed, i, r, bb, w.G, r));
+    RUTV_TRY(launch_dgemm(L, true, false, bb, s, r, 1.0, w.G, r, Rk + k, lda, 0.0, w.Y, bb, w.gemm_ws,
+                          w.gemm_ws_elems));
+    // H3
+    RUTV_CUDA(cudaMemsetAsync(h.done, 0, (size_t)s, L.stream));
+    RUTV_TRY(launch_cpqr(L, (int)bb, (int)s, (int)wd, w.Y, bb, h));
+    // H4
+    RUTV_TRY(permute_columns(L, m, s, (int)wd, Rk, lda, jpvt + k, w.Acat, h));
+    // H5
+    RUTV_TRY(panel_qr(L, r, wd, Rk + k, lda, w.tauU, w.Wu, r, w.TU, bb, w.qw));
+    RUTV_TRY(launch_triu(L, wd, wd, Rk + k, lda));
+    RUTV_TRY(launch_fill(L, r - wd, wd, 0.0, Rk + k + wd, lda));
+    // H6
+    if (s > wd) RUTV_TRY(apply_left_t(L, w, r, s - wd, wd, Rk + k + wd * lda, lda, w.Wu, r, w.TU, bb));
+    if (bq) RUTV_TRY(apply_right(L, w, m, r, wd, Q + k * ldq, ldq, w.Wu, r, w.TU, bb));
+  }
+  const int st = finish(ctx, w);
+  if (st == 0) ctx->stats.factorizations++;
+  return st;
+}
+
+}  // extern "C"

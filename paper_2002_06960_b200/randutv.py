@@ -63,6 +63,7 @@ SIGNATURES = {
                                    _vp, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(_dbl)]),
     "randutv_factor_tol": (_int, [_vp, _i64, _i64, _vp, _i64, _dbl, _i64, _int, _u64, _uint, _vp, _i64, _vp, _i64,
                                   _vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_dbl)]),
+    "randutv_hqrrp": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _u64, _uint, _vp, _vp, _i64]),
     "randutv_status_string": (ctypes.c_char_p, [_int]),
     "randutv_last_error": (ctypes.c_char_p, []),
     "randutv_get_stats": (_int, [_vp, ctypes.POINTER(Stats)]),
@@ -253,6 +254,20 @@ class Context:
         _check("randutv_factor_tol", st)
         k = kk.value
         return (Uf[:, :k] if Uf is not None else None), Tf[:k, :], V, rho.value, k
+
+    def randutv_hqrrp(self, A, b, seed, build_q=True, flags=0):
+        """HQRRP (column-pivoted QR, A P = Q R) of the column-major device matrix A,
+        overwritten by R: returns (Q, jpvt) with jpvt an int64 device tensor."""
+        import torch
+        m, n = A.shape
+        if not build_q:
+            flags |= RANDUTV_NO_UV
+        jpvt = torch.empty(n, dtype=torch.int64, device=A.device)
+        Q = colmajor(m, m, device=A.device) if build_q else None
+        st = self.lib.randutv_hqrrp(self.h, m, n, _ptr(A), _ld(A), int(b), int(seed) & (2**64 - 1), flags,
+                                    _ptr(jpvt), _ptr(Q), _ld(Q) if Q is not None else 1)
+        _check("randutv_hqrrp", st)
+        return Q, jpvt
 
     # ---------------------------------------------------------------- step entries
     def randutv_gaussian(self, seed, it, rows, cols, G=None):
