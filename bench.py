@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--cache-gib", type=float, default=None,
                    help="device panel cache for --mode host (default: a quarter of A)")
     p.add_argument("--no-uv", action="store_true", help="T only (the paper's 'no orthonormal matrices')")
+    p.add_argument("--algo", default="randutv", choices=["randutv", "hqrrp"],
+                   help="hqrrp: the paper's column-pivoted QR (Sec. 2, SURVEY §8(f) NEXT-3) on the config's matrix")
     p.add_argument("--sharded", action="store_true",
                    help="use the column-sharded NCCL path even on one GPU (exercises the N > 1 code path)")
     return p.parse_args()
@@ -511,10 +513,66 @@ def run_host_streamed(args):
     return 0
 
 
+def run_hqrrp(args):
+    """HQRRP (A P = Q R, Sec. 2 of the paper) of the config's matrix with the
+    config's b, Q built unless --no-uv; device-timed like the randUTV line.
+    A separate workload, not the BASELINE metric."""
+    import torch
+
+    from paper_2002_06960_b200.flops import hqrrp_flops
+    from paper_2002_06960_b200.inputs import CONFIGS, make_config_torch
+    from paper_2002_06960_b200.randutv import Context, colmajor
+
+    torch.cuda.set_device(0)
+    cfg = CONFIGS[args.config]
+    m, n, b = cfg["m"], cfg["n"], cfg["b"]
+    seed = 2000 + int(args.config[1:])
+    bq = not args.no_uv
+    F = hqrrp_flops(m, n, b, build_q=bq)
+    A = make_config_torch(args.config)
+    R = colmajor(m, n)
+    stream = torch.cuda.Stream()
+    ctx = Context(0, stream)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            R.copy_(A)
+            ctx.randutv_hqrrp(R, b, seed, build_q=bq)
+        torch.cuda.synchronize()
+        tot = 0.0
+        for it in range(args.steps):
+            R.copy_(A)
+            if it == args.steps - 1 and not args.no_profile:
+                ctx.set_profiling(True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctx.randutv_hqrrp(R, b, seed, build_q=bq)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        prof = ctx.profile() if not args.no_profile else {}
+    ms = tot / args.steps
+    # PK_OTHER (the "fold_wait" slot of randUTV) holds the sketch CPQR here
+    names = {"fold_wait": "cpqr_sketch"}
+    kernels = {names.get(k, k): {"launches": v["launches"], "ms": round(v["ms"], 3)}
+               for k, v in prof.items() if v["launches"]}
+    line = {"metric": "HQRRP FP64 GFLOP/s", "value": round(F / (ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} matrix (m={m}, n={n}), HQRRP b={b}" + (", Q built" if bq else ", R only"),
+                       "m": m, "n": n, "b": b, "flops_per_step": F, "algo": "hqrrp",
+                       "l2": "inputs larger than L2; no flush" if 8 * m * n > 126e6 else "input fits in L2; no flush"},
+            "kernels_last_step": kernels}
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.algo == "hqrrp":
+        return run_hqrrp(args)
     if args.mode == "host":
         return run_host_streamed(args)
     return run_ours(args)

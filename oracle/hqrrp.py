@@ -108,18 +108,3 @@ def hqrrp(A, b, seed, build_q=True, record=None):
         i += 1
     return Q, R, jpvt
 
-
-def hqrrp_flops(m, n, b, build_q=True):
-    """Algorithmic flop model of hqrrp (bench.py's GFLOP/s): per step the
-    sketch 2 b r s, the panel QR 2 r w^2 - 2 w^3 / 3, the left update
-    4 r (s - w) w and the Q update 4 m r w (the CPQR of the b x s sketch,
-    ~ 2 b^2 s, is counted too)."""
-    fl = 0.0
-    b = min(b, n)
-    for k in range(0, n, b):
-        r, s = m - k, n - k
-        w = min(b, s)
-        fl += 2.0 * b * r * s + 2.0 * b * b * s + 2.0 * r * w * w - 2.0 * w ** 3 / 3 + 4.0 * r * (s - w) * w
-        if build_q:
-            fl += 4.0 * m * r * w
-    return fl

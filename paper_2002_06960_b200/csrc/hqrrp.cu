@@ -20,6 +20,9 @@ namespace cg = cooperative_groups;
 namespace rutv {
 namespace {
 
+#ifndef RUTV_CP_COLS
+#define RUTV_CP_COLS 2
+#endif
 constexpr int CP_THREADS = 256;
 constexpr int CP_WARPS = CP_THREADS / 32;
 
@@ -198,7 +201,7 @@ int launch_cpqr_t(const Launch& L, int rows, int s, int steps, double* Y, i64 ld
     RUTV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cpqr_sketch_kernel<RPL>, CP_THREADS, 0));
     if (occ < 1) occ = 1;
   }
-  int G = (s + CP_WARPS * 2 - 1) / (CP_WARPS * 2);  // >= 2 columns per warp
+  int G = (s + CP_WARPS * RUTV_CP_COLS - 1) / (CP_WARPS * RUTV_CP_COLS);  // >= RUTV_CP_COLS columns per warp
   G = G < 1 ? 1 : G;
   G = G > occ * L.device_sms ? occ * L.device_sms : G;
   G = G > gmax ? gmax : G;

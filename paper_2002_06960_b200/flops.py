@@ -62,3 +62,19 @@ def randutv_flops(m, n, b, q, build_uv=True, k=None):
             if build_uv:
                 F += 2 * s * s * (m + n)
     return float(F)
+
+
+def hqrrp_flops(m, n, b, build_q=True):
+    """Algorithmic flop model of HQRRP (Sec. 2) per step (k = i b,
+    r = m - k, s = n - k, w = min(b, s)): sketch 2 b r s, sketch CPQR
+    ~ 2 b^2 s, panel QR 2 r w^2 - 2 w^3 / 3, left update 4 r (s - w) w, and the
+    Q update 4 m r w when Q is built."""
+    b = min(b, n)
+    F = 0.0
+    for k in range(0, n, b):
+        r, s = m - k, n - k
+        w = min(b, s)
+        F += 2.0 * b * r * s + 2.0 * b * b * s + 2.0 * r * w * w - 2.0 * w ** 3 / 3 + 4.0 * r * (s - w) * w
+        if build_q:
+            F += 4.0 * m * r * w
+    return F

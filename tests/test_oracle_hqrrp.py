@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import scipy.linalg as sl
 
-from oracle.hqrrp import cpqr_sketch, hqrrp, hqrrp_flops
+from oracle.hqrrp import cpqr_sketch, hqrrp
 from oracle.philox import gaussian_block
 
 
@@ -87,6 +87,7 @@ def test_hqrrp_first_block_pivots_are_dgeqp3_of_the_sketch():
 
 def test_hqrrp_flops_model():
     # square, b = n: sketch + CPQR + Householder QR of n columns + Q
+    from paper_2002_06960_b200.flops import hqrrp_flops
     m = n = b = 64
     fl = hqrrp_flops(m, n, b)
     assert fl == pytest.approx(2 * b * m * n + 2 * b * b * n + 2 * m * n * n - 2 * n ** 3 / 3 + 4 * m * m * n)
