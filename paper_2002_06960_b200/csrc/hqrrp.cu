@@ -203,7 +203,13 @@ int launch_cpqr_t(const Launch& L, int rows, int s, int steps, double* Y, i64 ld
   }
   int G = (s + CP_WARPS * RUTV_CP_COLS - 1) / (CP_WARPS * RUTV_CP_COLS);  // >= RUTV_CP_COLS columns per warp
   G = G < 1 ? 1 : G;
-  G = G > occ * L.device_sms ? occ * L.device_sms : G;
+  static int occ_cap = -1;
+  if (occ_cap < 0) {
+    const char* e = getenv("RUTV_HQ_CPQR_OCC");
+    occ_cap = e ? atoi(e) : 0;
+  }
+  const int oc = (occ_cap > 0 && occ_cap < occ) ? occ_cap : occ;
+  G = G > oc * L.device_sms ? oc * L.device_sms : G;
   G = G > gmax ? gmax : G;
   void* args[] = {&rows, &s, &steps, &Y, &ldy, &part_val, &part_col, &piv, &done};
   const size_t pe = L.pbegin();
@@ -285,6 +291,9 @@ struct HqWork {
   unsigned char* done;
   int64_t* jtmp;
   int gmax;
+  // Q stream (the Q update of step i overlaps step i+1): second (W, T) buffer
+  // and the stream's own GEMM temporaries
+  double *Wu2, *TU2, *Zq, *Zq2, *gq;
 };
 
 void carve_hq(Carver& c, HqWork& h, i64 n, i64 b) {
@@ -298,6 +307,23 @@ void carve_hq(Carver& c, HqWork& h, i64 n, i64 b) {
   h.moved = c.take<int>(2 * b);
   h.done = c.take<unsigned char>(n);
   h.jtmp = c.take<int64_t>(2 * b);
+}
+
+void carve_hq_q(Carver& c, HqWork& h, i64 m, i64 b) {
+  h.Wu2 = c.take<double>(m * b);
+  h.TU2 = c.take<double>(b * b);
+  h.Zq = c.take<double>(m * b);
+  h.Zq2 = c.take<double>(m * b);
+  h.gq = c.take<double>(4 * m * b);
+}
+
+bool hq_qstream_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_HQ_QSTREAM");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
 }
 
 int launch_cpqr(const Launch& L, int rows, int s, int steps, double* Y, i64 ldy, const HqWork& h) {
@@ -348,40 +374,82 @@ RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A,
   Launch L = ctx->launch();
   Work w;
   HqWork h;
+  const bool qs = bq && hq_qstream_on();
   Carver dry{nullptr, 0, 0, true};
   carve(dry, w, m, n, bb, 0, false);
   carve_hq(dry, h, n, bb);
+  if (qs) carve_hq_q(dry, h, m, bb);
   RUTV_TRY(ensure_ws(ctx, dry.off));
   Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
   carve(real, w, m, n, bb, 0, false);
   carve_hq(real, h, n, bb);
+  if (qs) carve_hq_q(real, h, m, bb);
   if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
   RUTV_TRY(start_status(ctx, w));
   hq_jpvt_init_kernel<<<(unsigned)std::min<i64>((n + 255) / 256, 1024), 256, 0, L.stream>>>(n, jpvt);
   L.count();
   if (bq) RUTV_TRY(launch_set_identity(L, m, m, Q, ldq));
-  i64 i = 0;
-  for (i64 k = 0; k < n; k += bb, ++i) {
-    const i64 r = m - k, s = n - k, wd = bb < s ? bb : s;
-    double* Rk = A + k * lda;  // columns k:n, all rows
-    // H1, H2: Y (bb x s, ld bb) = G^T R(k:m, k:n)
-    RUTV_TRY(launch_gaussian(L, seed, i, r, bb, w.G, r));
-    RUTV_TRY(launch_dgemm(L, true, false, bb, s, r, 1.0, w.G, r, Rk + k, lda, 0.0, w.Y, bb, w.gemm_ws,
-                          w.gemm_ws_elems));
-    // H3
-    RUTV_CUDA(cudaMemsetAsync(h.done, 0, (size_t)s, L.stream));
-    RUTV_TRY(launch_cpqr(L, (int)bb, (int)s, (int)wd, w.Y, bb, h));
-    // H4
-    RUTV_TRY(permute_columns(L, m, s, (int)wd, Rk, lda, jpvt + k, w.Acat, h));
-    // H5
-    RUTV_TRY(panel_qr(L, r, wd, Rk + k, lda, w.tauU, w.Wu, r, w.TU, bb, w.qw));
-    RUTV_TRY(launch_triu(L, wd, wd, Rk + k, lda));
-    RUTV_TRY(launch_fill(L, r - wd, wd, 0.0, Rk + k + wd, lda));
-    // H6
-    if (s > wd) RUTV_TRY(apply_left_t(L, w, r, s - wd, wd, Rk + k + wd * lda, lda, w.Wu, r, w.TU, bb));
-    if (bq) RUTV_TRY(apply_right(L, w, m, r, wd, Q + k * ldq, ldq, w.Wu, r, w.TU, bb));
+  // Q stream: H6's Q update of step i runs on ctx->vstr (one-shot GEMM tiles)
+  // behind step i+1's sketch, CPQR and permutation; (W, T) alternate between
+  // two buffers, and step i+2's panel QR waits for the Q update of step i.
+  Launch LQ = ctx->v_launch();
+  Work wq = w;
+  cudaEvent_t eQ[2] = {nullptr, nullptr};
+  if (qs) {
+    wq.Z = h.Zq;
+    wq.Z2 = h.Zq2;
+    wq.gemm_ws = h.gq;
+    wq.gemm_ws_elems = 4 * m * bb;
+    for (auto& e : eQ) RUTV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  const int st = finish(ctx, w);
+  int st = 0;
+  i64 i = 0;
+  for (i64 k = 0; k < n && st == 0; k += bb, ++i) {
+    const i64 r = m - k, s = n - k, wd = bb < s ? bb : s;
+    const int sel = (int)(i & 1);
+    double* Wu = (qs && sel) ? h.Wu2 : w.Wu;
+    double* TU = (qs && sel) ? h.TU2 : w.TU;
+    double* Rk = A + k * lda;  // columns k:n, all rows
+    auto step = [&]() -> int {
+      // H1, H2: Y (bb x s, ld bb) = G^T R(k:m, k:n)
+      RUTV_TRY(launch_gaussian(L, seed, i, r, bb, w.G, r));
+      RUTV_TRY(launch_dgemm(L, true, false, bb, s, r, 1.0, w.G, r, Rk + k, lda, 0.0, w.Y, bb, w.gemm_ws,
+                            w.gemm_ws_elems));
+      // H3
+      RUTV_CUDA(cudaMemsetAsync(h.done, 0, (size_t)s, L.stream));
+      RUTV_TRY(launch_cpqr(L, (int)bb, (int)s, (int)wd, w.Y, bb, h));
+      // H4
+      RUTV_TRY(permute_columns(L, m, s, (int)wd, Rk, lda, jpvt + k, w.Acat, h));
+      // H5 (the (W, T) buffer is free once the Q update of step i-2 is done)
+      if (qs && i >= 2) RUTV_CUDA(cudaStreamWaitEvent(L.stream, eQ[sel], 0));
+      RUTV_TRY(panel_qr(L, r, wd, Rk + k, lda, w.tauU, Wu, r, TU, bb, w.qw));
+      RUTV_TRY(launch_triu(L, wd, wd, Rk + k, lda));
+      RUTV_TRY(launch_fill(L, r - wd, wd, 0.0, Rk + k + wd, lda));
+      // H6
+      if (qs) {
+        RUTV_CUDA(cudaEventRecord(ctx->eWv, L.stream));
+        RUTV_CUDA(cudaStreamWaitEvent(LQ.stream, ctx->eWv, 0));
+        RUTV_TRY(apply_right(LQ, wq, m, r, wd, Q + k * ldq, ldq, Wu, r, TU, bb));
+        RUTV_CUDA(cudaEventRecord(eQ[sel], LQ.stream));
+      }
+      if (s > wd) RUTV_TRY(apply_left_t(L, w, r, s - wd, wd, Rk + k + wd * lda, lda, Wu, r, TU, bb));
+      if (bq && !qs) RUTV_TRY(apply_right(L, w, m, r, wd, Q + k * ldq, ldq, Wu, r, TU, bb));
+      return 0;
+    };
+    st = step();
+  }
+  if (qs) {
+    // the main stream (and so the caller) must not run ahead of the Q stream
+    if (cudaEventRecord(ctx->eV, LQ.stream) != cudaSuccess || cudaStreamWaitEvent(L.stream, ctx->eV, 0) != cudaSuccess)
+      st = st ? st : RANDUTV_ERR_CUDA;
+    for (auto& e : eQ)
+      if (e) cudaEventDestroy(e);
+  }
+  if (st != 0) {
+    cudaStreamSynchronize(L.stream);
+    return st;
+  }
+  st = finish(ctx, w);
   if (st == 0) ctx->stats.factorizations++;
   return st;
 }
