@@ -49,7 +49,7 @@ def sampled_steps(n, b):
     return max(0, -(-(n - b) // b)) if n > b else 0
 
 
-def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None):
+def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reorth=False):
     """Oracle randUTV of A (m x n, m >= n).
 
     Parameters
@@ -61,6 +61,8 @@ def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None):
                  run and truncated)
     thin_u     : form U by backward accumulation (economy m x n, or m x k truncated)
     record     : optional dict; receives per-step diagnostics (Y, tau, d, ...)
+    reorth     : re-orthonormalise the sample between power steps (SURVEY §8(f)
+                 NEXT-4, the alternative to reading A8; see _sample)
 
     Returns dict with keys U, T, V (full) or Uk, Tk, V, rho (truncated).
     """
@@ -96,7 +98,7 @@ def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None):
         if s > b:
             if i >= K:
                 break
-            _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin_u and build_uv, record)
+            _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin_u and build_uv, record, reorth)
         else:
             if truncated and not truncated_full:
                 break
@@ -116,21 +118,43 @@ def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None):
     return out
 
 
-def _sample(At, G, q):
-    """O2: Y = (A_t^T A_t)^q A_t^T G, evaluated literally right to left."""
+def _orth(X):
+    """The first w columns of the Householder Q of X (h x w, h >= w):
+    Q(:, 0:w) = (I - W T W^T) E = E - W (T W_1^T), E = [I_w; 0], W_1 = W[0:w, :]
+    (dlarfg convention, oracle.householder)."""
+    F, tau = householder_qr(X)
+    W = unit_lower(F)
+    Tq = larft(W, tau)
+    w = X.shape[1]
+    E = np.zeros_like(W)
+    E[np.arange(w), np.arange(w)] = 1.0
+    return np.asfortranarray(E - W @ (Tq @ W[:w, :].T))
+
+
+def _sample(At, G, q, reorth=False):
+    """O2: Y = (A_t^T A_t)^q A_t^T G, evaluated literally right to left (A8).
+    reorth (NEXT-4): Y and Z are replaced by the orthonormal bases _orth(Y),
+    _orth(Z) before each product -- the same column span in exact arithmetic
+    (each _orth is a right multiplication by an invertible triangular factor),
+    but directions below eps^(1/(2q+1)) of the top one survive (the standard
+    power scheme of the randomized-SVD literature the paper cites)."""
     Y = At.T @ G
     for _ in range(q):
+        if reorth:
+            Y = _orth(Y)
         Z = At @ Y
+        if reorth:
+            Z = _orth(Z)
         Y = At.T @ Z
     return Y
 
 
-def _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin, record):
+def _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin, record, reorth=False):
     m, n = T.shape
     r = m - kk
     # O1, O2
     G = gaussian_block(seed, i, r, b)
-    Y = _sample(T[kk:, kk:], G, q)
+    Y = _sample(T[kk:, kk:], G, q, reorth)
     # O3, O4 on Y
     FY, tauV = householder_qr(Y)
     WV = unit_lower(FY)

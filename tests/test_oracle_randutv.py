@@ -161,3 +161,42 @@ def test_invalid_arguments():
         randutv(np.zeros((3, 5)), 2, 1, 0)
     with pytest.raises(ValueError):
         randutv(np.zeros((5, 5)), 0, 1, 0)
+
+
+# ---------------------------------------------------------------- NEXT-4: re-orthonormalised power steps
+def test_orth_matches_lapack_q():
+    """_orth is the explicit Householder Q: identical (signs included, same
+    dlarfg convention) to LAPACK dgeqrf + dorgqr via numpy."""
+    from oracle.randutv import _orth
+    X = np.random.default_rng(8).standard_normal((200, 24))
+    Q = _orth(X)
+    Qn, _ = np.linalg.qr(X)
+    assert np.max(np.abs(Q - Qn)) <= 1e-14
+    assert np.allclose(np.tril(Q.T @ X, -1), 0.0, atol=1e-13)
+
+
+def test_reorth_same_span_on_well_conditioned():
+    # exact arithmetic: the same span, hence the same T up to rounding
+    A = np.asfortranarray(np.random.default_rng(5).standard_normal((300, 200)))
+    o1 = randutv(A, 32, 2, 5)
+    o2 = randutv(A, 32, 2, 5, reorth=True)
+    d1, d2 = np.abs(np.diag(o1["T"])), np.abs(np.diag(o2["T"]))
+    assert np.max(np.abs(d1 - d2) / d1) <= 1e-12
+    assert np.linalg.norm(A - o2["U"] @ o2["T"] @ o2["V"].T) <= 1e-13 * np.linalg.norm(A)
+
+
+def test_reorth_resolves_graded_spectrum():
+    """sigma_j = 10^(-j/8), q = 3: the literal products (A8) push directions
+    below eps^(1/7) of a block's top singular value under rounding, and
+    |T_jj| / sigma_j strays by more than 10x; re-orthonormalised power steps
+    keep it within [0.5, 2] down to sigma = 1e-16."""
+    rng = np.random.default_rng(0)
+    n = 256
+    U0, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    V0, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = 10.0 ** (-np.arange(n) / 8)
+    A = np.asfortranarray((U0 * sig) @ V0.T)
+    lit = np.abs(np.diag(randutv(A, 32, 3, 5, build_uv=False)["T"]))[:n // 2] / sig[:n // 2]
+    ro = np.abs(np.diag(randutv(A, 32, 3, 5, build_uv=False, reorth=True)["T"]))[:n // 2] / sig[:n // 2]
+    assert ro.min() >= 0.5 and ro.max() <= 2.0
+    assert lit.min() < 0.1 or lit.max() > 10.0
