@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--cache-gib", type=float, default=None,
                    help="device panel cache for --mode host (default: a quarter of A)")
     p.add_argument("--no-uv", action="store_true", help="T only (the paper's 'no orthonormal matrices')")
+    p.add_argument("--reorth", action="store_true",
+                   help="RANDUTV_REORTH: re-orthonormalised power steps (NEXT-4; extra QRs not in the flop model)")
     p.add_argument("--algo", default="randutv", choices=["randutv", "hqrrp"],
                    help="hqrrp: the paper's column-pivoted QR (Sec. 2, SURVEY §8(f) NEXT-3) on the config's matrix")
     p.add_argument("--sharded", action="store_true",
@@ -290,8 +292,10 @@ def run_ours(args):
         U = colmajor(m, m)
         V = colmajor(n, n)
 
+        fl = 4 if args.reorth else 0  # RANDUTV_REORTH
+
         def step():
-            ctx.randutv_factor_ex(A, b, q, seed, U=U, T=T, V=V)
+            ctx.randutv_factor_ex(A, b, q, seed, U=U, T=T, V=V, flags=fl)
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -426,7 +430,9 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args.config, ws, sharded),
+            "config": dict(config_dict(args.config, ws, sharded),
+                           **({"reorth": True, "note": "re-orthonormalised power steps; their QRs are not in flops_per_step"}
+                              if args.reorth else {})),
             "t_over_n3_x1e10": ms_step * 1e-3 / float(n) ** 3 * 1e10,
             "frac_of_fp64_peak": round(value / ws / 1e3 / peak, 4),   # of N x per-GPU peak
             "gpu_launches": stats["kernel_launches"],

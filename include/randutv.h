@@ -59,6 +59,14 @@ extern "C" {
 /* flags */
 #define RANDUTV_NO_UV         1u    /* do not build U and V ("no orthonormal matrices") */
 #define RANDUTV_CHECK_FINITE  2u    /* pre-scan A for NaN/Inf and fail with RANDUTV_ERR_NONFINITE    */
+/* Re-orthonormalise the sample between power steps:
+ * Y := Q(Y) before Z = A_t Y and Z := Q(Z) before Y = A_t^T Z, Q(X) the first
+ * columns of X's Householder Q.  Same span as the literal products (reading
+ * A8) in exact arithmetic; resolves directions below eps^(1/(2q+1)) of a
+ * block's top singular value.  Costs 2q extra panel QRs per step.  Honoured by
+ * randutv_factor_ex, randutv_factor_rank and randutv_factor_tol; the
+ * host-streamed and sharded entries reject it (-9). */
+#define RANDUTV_REORTH        4u
 
 typedef struct randutv_ctx randutv_ctx;
 

@@ -686,6 +686,7 @@ int dist_run(DistRun& R, i64 K, i64 k, double* resid_fro) {
 int dist_check(const Layout& lay, const double* A, i64 lda, int q, unsigned flags, const double* U, i64 ldu,
                const double* V, i64 ldv) {
   const bool uv = !(flags & RANDUTV_NO_UV);
+  if (flags & RANDUTV_REORTH) return -9;  // not implemented on the sharded path
   if (lay.n < 1) return -3;
   if (lay.m < lay.n) return -2;
   const i64 nc = lay.ncols(lay.p);

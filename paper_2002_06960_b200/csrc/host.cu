@@ -430,6 +430,7 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
                                     int64_t ldu, double* V_host, int64_t ldv, randutv_host_report* report) {
   RUTV_TRY(begin_call(ctx));
   const bool uv = !(flags & RANDUTV_NO_UV);
+  if (flags & RANDUTV_REORTH) return -9;  // not implemented on the host-streamed path
   if (n < 1) return -3;
   if (m < n) return -2;
   if (!A_host) return -4;

@@ -303,6 +303,7 @@ struct Problem {
   cudaEvent_t eR, eF;
   Launch vl;              // V stream (oneshot GEMMs); vl.stream == nullptr: V on the main stream
   cudaEvent_t eWv, eV;
+  bool reorth = false;    // RANDUTV_REORTH: orthonormal Y, Z between power steps (NEXT-4)
 };
 
 
@@ -344,6 +345,16 @@ bool fuse_left() {
   return v != 0;
 }
 
+// X (h x b, ld h) := the first b columns of its Householder Q, E - W (T W_1^T)
+// (oracle.randutv._orth).  Uses the S6 buffers W_U, T_U, tau_U (free until the
+// column-block QR of this step) and the panel-QR scratch S for T W_1^T.
+int orthonormalize(const Launch& L, Work& w, i64 h, i64 b, double* X) {
+  RUTV_TRY(panel_qr(L, h, b, X, h, w.tauU, w.Wu, h, w.TU, b, w.qw));
+  RUTV_TRY(launch_dgemm(L, false, true, b, b, b, 1.0, w.TU, b, w.Wu, h, 0.0, w.qw.S, b, nullptr, 0));
+  RUTV_TRY(launch_set_identity(L, h, b, X, h));
+  return launch_dgemm(L, false, false, h, b, b, -1.0, w.Wu, h, w.qw.S, b, 1.0, X, h, nullptr, 0);
+}
+
 int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   const i64 m = P.m, n = P.n, b = P.b, kk = i * b, r = m - kk, s = n - kk;
   double* At = P.T + kk + kk * P.ldt;
@@ -351,8 +362,10 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   RUTV_TRY(launch_gaussian(L, P.seed, i, r, b, w.G, r));
   RUTV_TRY(launch_dgemm(L, true, false, s, b, r, 1.0, At, P.ldt, w.G, r, 0.0, w.Y, s, w.gemm_ws, w.gemm_ws_elems));
   for (int qq = 0; qq < P.q; ++qq) {
+    if (P.reorth) RUTV_TRY(orthonormalize(L, w, s, b, w.Y));
     RUTV_TRY(launch_dgemm(L, false, false, r, b, s, 1.0, At, P.ldt, w.Y, s, 0.0, w.Z, r, w.gemm_ws,
                           w.gemm_ws_elems));
+    if (P.reorth) RUTV_TRY(orthonormalize(L, w, r, b, w.Z));
     RUTV_TRY(launch_dgemm(L, true, false, s, b, r, 1.0, At, P.ldt, w.Z, r, 0.0, w.Y, s, w.gemm_ws,
                           w.gemm_ws_elems));
   }
@@ -684,6 +697,7 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
   }
   Problem P{m, n, bb, q, seed, T, ldt, uv ? U : nullptr, ldu, uv ? V : nullptr, ldv, false,
             ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
+  P.reorth = (flags & RANDUTV_REORTH) != 0;
   const i64 nsamp = sampled_steps(n, bb);
   RUTV_TRY(run_loop(L, w, P, nsamp, true));
   const int st = finish(ctx, w);
@@ -723,6 +737,7 @@ int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64
   if (uv) RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
   Problem P{m, n, bb, q, seed, w.Twork, m, nullptr, m, uv ? V : nullptr, ldv, uv,
             ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
+  P.reorth = (flags & RANDUTV_REORTH) != 0;
   if (!adaptive) {
     RUTV_TRY(run_loop(L, w, P, K, with_final));
   } else {

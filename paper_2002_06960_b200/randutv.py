@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("RUTV_LIB", os.path.join(_HERE, "librandutv.so"))  # R
 
 RANDUTV_NO_UV = 1
 RANDUTV_CHECK_FINITE = 2
+RANDUTV_REORTH = 4
 RANDUTV_ERR_CUDA = 1000
 RANDUTV_ERR_ALLOC = 1001
 RANDUTV_ERR_NONFINITE = 1002

@@ -216,3 +216,48 @@ def test_adaptive_rank(ctx):
     # a tolerance no sampled step meets: the full factorisation, k = n, rho = 0
     _, Tk2, _, rho2, k2 = ctx.randutv_factor_tol(to_dev(A), 1e-300, b, q, seed)
     assert k2 == 512 and rho2 == 0.0
+
+
+# ---------------------------------------------------------------- NEXT-4: RANDUTV_REORTH
+@pytest.mark.parametrize("m,n,b,q", [(200, 200, 32, 2), (300, 170, 40, 1), (333, 333, 64, 3)])
+def test_reorth_parity(ctx, m, n, b, q):
+    from paper_2002_06960_b200.randutv import RANDUTV_REORTH
+    A = np.asfortranarray(np.random.default_rng(m + n + q).standard_normal((m, n)))
+    U, T, V, st = ctx.randutv_factor_ex(to_dev(A), b, q, 19, flags=RANDUTV_REORTH)
+    o = oracle_randutv(A, b, q, 19, reorth=True)
+    _check_full(A, to_np(U), to_np(T), to_np(V), o)
+
+
+def test_reorth_graded_spectrum_and_truncated(ctx):
+    """sigma_j = 10^(-j/8), q = 3 (tests/test_oracle_randutv.py's pin): with
+    RANDUTV_REORTH the GPU's |T_jj| / sigma_j stays in [0.5, 2] and matches the
+    oracle's reorth run; the truncated entry honours the flag too."""
+    from paper_2002_06960_b200.randutv import RANDUTV_REORTH
+    rng = np.random.default_rng(0)
+    n = 256
+    U0, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    V0, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = 10.0 ** (-np.arange(n) / 8)
+    A = np.asfortranarray((U0 * sig) @ V0.T)
+    _, T, _, _ = ctx.randutv_factor_ex(to_dev(A), 32, 3, 5, build_uv=False, flags=RANDUTV_REORTH)
+    d = np.abs(np.diag(to_np(T)))
+    ratio = d[:n // 2] / sig[:n // 2]
+    assert ratio.min() >= 0.5 and ratio.max() <= 2.0
+    o = oracle_randutv(A, 32, 3, 5, build_uv=False, reorth=True)
+    assert diag_parity(d, np.diag(o["T"])) <= 1.0
+    Uk, Tk, Vk, rho = ctx.randutv_factor_rank(to_dev(A), 64, 32, 3, 5, flags=RANDUTV_REORTH)
+    ot = oracle_randutv(A, 32, 3, 5, k=64, thin_u=True, reorth=True)
+    assert abs(rho - ot["rho"]) <= 1e-9 * ot["rho"]
+
+
+def test_reorth_rejected_by_host_and_dist(ctx):
+    import ctypes
+    from paper_2002_06960_b200.randutv import RANDUTV_REORTH, colmajor
+    A = colmajor(8, 8)
+    st = ctx.lib.randutv_factor_dist(ctx.h, 8, 8, ctypes.c_void_p(A.data_ptr()), 8, 4, 1, 1, RANDUTV_REORTH,
+                                     None, 1, None, 1)
+    assert st in (-9, 1005)   # the flag is checked after the communicator (NOCOMM) or before
+    Ah = np.zeros((8, 8), order="F")
+    st = ctx.lib.randutv_factor_host(ctx.h, 8, 8, Ah.ctypes.data, 8, 4, 1, 1, RANDUTV_REORTH | 1, 0,
+                                     None, 8, None, 8, None)
+    assert st == -9
