@@ -23,6 +23,13 @@ namespace {
 #ifndef RUTV_CP_COLS
 #define RUTV_CP_COLS 2
 #endif
+#ifndef RUTV_CP_NB
+#define RUTV_CP_NB 2
+#endif
+#ifndef RUTV_CP_MINB
+#define RUTV_CP_MINB 1
+#endif
+constexpr int CP_NB = RUTV_CP_NB;
 constexpr int CP_THREADS = 256;
 constexpr int CP_WARPS = CP_THREADS / 32;
 
@@ -58,7 +65,7 @@ __device__ __forceinline__ void warp_argmax(double& v, int& c) {
 // never moved: piv[j] is the Y column chosen at step j; the swap-convention
 // permutation is built afterwards (hq_swap_kernel).
 template <int RPL>
-__global__ void __launch_bounds__(CP_THREADS) cpqr_sketch_kernel(int rows, int s, int steps, double* __restrict__ Y,
+__global__ void __launch_bounds__(CP_THREADS, RUTV_CP_MINB) cpqr_sketch_kernel(int rows, int s, int steps, double* __restrict__ Y,
                                                                  i64 ldy, double* part_val, int* part_col,
                                                                  int* __restrict__ piv,
                                                                  unsigned char* __restrict__ done) {
@@ -92,6 +99,12 @@ __global__ void __launch_bounds__(CP_THREADS) cpqr_sketch_kernel(int rows, int s
     }
   }
 
+#ifdef RUTV_CP_PROF
+  long long pc[4] = {0, 0, 0, 0}, t0 = clock64(), t1;
+#define CP_MARK(i) do { t1 = clock64(); pc[i] += t1 - t0; t0 = t1; } while (0)
+#else
+#define CP_MARK(i) do { } while (0)
+#endif
   for (int j = 0; j < steps; ++j) {
     if (lane == 0) {
       wv[warp] = best;
@@ -109,11 +122,16 @@ __global__ void __launch_bounds__(CP_THREADS) cpqr_sketch_kernel(int rows, int s
       part_val[(j & 1) * G + blockIdx.x] = bv;
       part_col[(j & 1) * G + blockIdx.x] = bc;
     }
+    CP_MARK(0);
     grid.sync();
-    if (warp == 0) {
+    CP_MARK(1);
+    // global argmax: every thread reads <= ceil(G / CP_THREADS) partials (one
+    // L2 round trip), then warp and CTA reductions
+    {
       double bv = -1.0;
       int bc = INT_MAX;
-      for (int g = lane; g < G; g += 32) {
+#pragma unroll 4
+      for (int g = threadIdx.x; g < G; g += CP_THREADS) {
         const double pv = __ldcg(part_val + (j & 1) * G + g);
         const int pc = __ldcg(part_col + (j & 1) * G + g);
         if (beats(pv, pc, bv, bc)) {
@@ -121,6 +139,17 @@ __global__ void __launch_bounds__(CP_THREADS) cpqr_sketch_kernel(int rows, int s
           bc = pc;
         }
       }
+      warp_argmax(bv, bc);
+      // (wv / wc of the partial-write phase were consumed before grid.sync)
+      if (lane == 0) {
+        wv[warp] = bv;
+        wc[warp] = bc;
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      double bv = lane < CP_WARPS ? wv[lane] : -1.0;
+      int bc = lane < CP_WARPS ? wc[lane] : INT_MAX;
       warp_argmax(bv, bc);
       const int p = bc;
       // dlarfg of the pivot column's rows j:rows (oracle.householder.dlarfg)
@@ -153,6 +182,7 @@ __global__ void __launch_bounds__(CP_THREADS) cpqr_sketch_kernel(int rows, int s
       }
     }
     __syncthreads();
+    CP_MARK(2);
     const int p = s_p;
     const double tau = s_tau;
     if (p % NW == gw && lane == 0) done[p] = 1;
@@ -160,37 +190,68 @@ __global__ void __launch_bounds__(CP_THREADS) cpqr_sketch_kernel(int rows, int s
     best = -1.0;
     bestc = INT_MAX;
     if (j + 1 == steps) break;  // the last pivot needs no update
-    for (int c = gw; c < s; c += NW) {
-      if (c == p || done[c]) continue;
-      double* y = Y + (i64)c * ldy;
-      double yr[RPL];
-      double dot = 0.0;
+    // CP_NB columns per batch: their done flags and rows are loaded together
+    // (done columns are loaded too and then ignored), one L2 round trip per batch
+    for (int c0 = gw; c0 < s; c0 += CP_NB * NW) {
+      double yr[CP_NB][RPL];
+      bool act[CP_NB];
 #pragma unroll
-      for (int t = 0; t < RPL; ++t) {
-        const int r = lane + 32 * t;
-        yr[t] = (r >= j && r < rows) ? y[r] : 0.0;
-        dot += v[r] * yr[t];
-      }
-      dot = warp_sum_d(dot);
-      double nn = 0.0;
+      for (int u = 0; u < CP_NB; ++u) {
+        const int c = c0 + u * NW;
+        const bool in = c < s;
+        act[u] = in && c != p && !done[in ? c : 0];
+        const double* y = Y + (i64)(in ? c : 0) * ldy;
 #pragma unroll
-      for (int t = 0; t < RPL; ++t) {
-        const int r = lane + 32 * t;
-        if (r >= j && r < rows) {
-          if (tau != 0.0) {
-            yr[t] -= tau * (v[r] * dot);
-            y[r] = yr[t];
-          }
-          if (r > j) nn += yr[t] * yr[t];
+        for (int t = 0; t < RPL; ++t) {
+          const int r = lane + 32 * t;
+          yr[u][t] = (in && r >= j && r < rows) ? y[r] : 0.0;
         }
       }
-      nn = warp_sum_d(nn);
-      if (beats(nn, c, best, bestc)) {
-        best = nn;
-        bestc = c;
+      double dot[CP_NB];
+#pragma unroll
+      for (int u = 0; u < CP_NB; ++u) {
+        dot[u] = 0.0;
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) dot[u] += v[lane + 32 * t] * yr[u][t];
+      }
+#pragma unroll
+      for (int u = 0; u < CP_NB; ++u) dot[u] = warp_sum_d(dot[u]);
+      double nn[CP_NB];
+#pragma unroll
+      for (int u = 0; u < CP_NB; ++u) {
+        nn[u] = 0.0;
+        const int c = c0 + u * NW;
+        double* y = Y + (i64)(c < s ? c : 0) * ldy;
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+          const int r = lane + 32 * t;
+          if (act[u] && r >= j && r < rows) {
+            if (tau != 0.0) {
+              yr[u][t] -= tau * (v[r] * dot[u]);
+              y[r] = yr[u][t];
+            }
+            if (r > j) nn[u] += yr[u][t] * yr[u][t];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < CP_NB; ++u) nn[u] = warp_sum_d(nn[u]);
+#pragma unroll
+      for (int u = 0; u < CP_NB; ++u) {
+        const int c = c0 + u * NW;
+        if (act[u] && beats(nn[u], c, best, bestc)) {
+          best = nn[u];
+          bestc = c;
+        }
       }
     }
+    CP_MARK(3);
   }
+#ifdef RUTV_CP_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("cpqr_prof G=%d s=%d steps=%d reduce %.0f sync %.0f pivot %.0f update %.0f cycles/step\n", G, s, steps,
+           (double)pc[0] / steps, (double)pc[1] / steps, (double)pc[2] / steps, (double)pc[3] / steps);
+#endif
 }
 
 template <int RPL>
