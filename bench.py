@@ -533,6 +533,8 @@ def run_hqrrp(args):
     cfg = CONFIGS[args.config]
     m, n, b = cfg["m"], cfg["n"], cfg["b"]
     seed = 2000 + int(args.config[1:])
+    if args.mode == "host":
+        return run_hqrrp_host(args, m, n, b, seed)
     bq = not args.no_uv
     F = hqrrp_flops(m, n, b, build_q=bq)
     A = make_config_torch(args.config)
@@ -568,6 +570,59 @@ def run_hqrrp(args):
                        "m": m, "n": n, "b": b, "flops_per_step": F, "algo": "hqrrp",
                        "l2": "inputs larger than L2; no flush" if 8 * m * n > 126e6 else "input fits in L2; no flush"},
             "kernels_last_step": kernels}
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
+
+
+def run_hqrrp_host(args, m, n, b, seed):
+    """HQRRP_left from pinned host memory (Sec. 2.3), Table-1 style:
+    compute time = the in-HBM right-looking HQRRP (R only) of the same matrix."""
+    import numpy as np
+    import torch
+
+    from paper_2002_06960_b200.flops import hqrrp_flops
+    from paper_2002_06960_b200.inputs import make_config_torch
+    from paper_2002_06960_b200.randutv import Context, colmajor, pinned_colmajor
+
+    A = make_config_torch(args.config)
+    A0 = pinned_colmajor(m, n)
+    torch.from_numpy(A0.T).copy_(A.t())
+    stream = torch.cuda.Stream()
+    ctx = Context(0, stream)
+    with torch.cuda.stream(stream):
+        R = colmajor(m, n)
+        R.copy_(A)
+        ctx.randutv_hqrrp(R, b, seed, build_q=False)
+        R.copy_(A)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.randutv_hqrrp(R, b, seed, build_q=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        comp_ms = e0.elapsed_time(e1)
+    del A, R
+    torch.cuda.empty_cache()
+    Ah = pinned_colmajor(m, n)
+    reps = []
+    for it in range(max(args.warmup, 0) + args.steps):
+        np.copyto(Ah, A0)
+        _, _, rep = ctx.randutv_hqrrp_host(Ah, b, seed)
+        if it >= args.warmup:
+            reps.append(rep)
+    real = sum(r["wall_ms"] for r in reps) / len(reps)
+    io = sum(r["h2d_ms"] for r in reps) / len(reps)
+    r0 = reps[-1]
+    F = hqrrp_flops(m, n, b, build_q=False)
+    line = {"metric": "HQRRP FP64 GFLOP/s", "value": round(F / (real * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(real, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} matrix (m={m}, n={n}), HQRRP_left from pinned host memory, b={b}",
+                       "m": m, "n": n, "b": b, "flops_per_step": F, "algo": "hqrrp", "mode": "host-streamed (left-looking)"},
+            "table1": {"computational_time_s": comp_ms * 1e-3, "io_time_s": io * 1e-3, "real_time_s": real * 1e-3,
+                       "real_over_comp": real / comp_ms, "h2d_bytes": r0["h2d_bytes"], "d2h_bytes": r0["d2h_bytes"],
+                       "h2d_GBps": r0["h2d_bytes"] / (r0["h2d_ms"] * 1e-3) / 1e9 if r0["h2d_ms"] > 0 else None}}
     print(json.dumps(line), flush=True)
     ctx.close()
     return 0

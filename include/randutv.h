@@ -266,6 +266,27 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
 RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, int64_t b,
                               uint64_t seed, unsigned flags, int64_t* jpvt, double* Q, int64_t ldq);
 
+/* HQRRP_left, host-streamed (Sec. 2.3): the left-looking HQRRP for
+ * a matrix that stays in HOST memory.  Per block: the sketch Gaussian is
+ * pushed through the stored reflectors (Q [0; G]), Y = (Q [0; G])^T A(:, k:n)
+ * is taken over the still-unmodified remaining columns (the "repeated
+ * arithmetic" of P:508-514), the CPQR of Y picks the pivots, the <= 2w host
+ * columns the permutation moves are swapped, and only the current block is
+ * updated (Q^* applied from the stored reflectors), factored and written back.
+ *   A_host (m x n, lda >= m, host; pinned, else registered for the call)
+ *          in: A; out: R on/above the diagonal and the Householder tails below
+ *          it (LAPACK dgeqp3 layout: Q = H_0 H_1 ... with H_j = I - tau_j v_j v_j^T)
+ *   jpvt_host (n int64, host) out: column j of A P is A(:, jpvt[j])
+ *   tau_host  (n doubles, host) out: the reflector scalars
+ *   report    (host, may be NULL) traffic and time (cache_slots = 2 staging slots)
+ * The pivots and R equal randutv_hqrrp's up to rounding (the sketch is formed
+ * in a different order).  flags must be 0 (else -8); min(b, n) <= 512.
+ * Arguments: 1 ctx, 2 m, 3 n, 4 A_host, 5 lda, 6 b, 7 seed, 8 flags, 9 jpvt_host,
+ * 10 tau_host, 11 report.  Synchronous. */
+RANDUTV_API int randutv_hqrrp_host(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b,
+                                   uint64_t seed, unsigned flags, int64_t* jpvt_host, double* tau_host,
+                                   randutv_host_report* report);
+
 /* ---------------------------------------------------------------------------
  * Multi-GPU: the column-sharded randUTV.
  *

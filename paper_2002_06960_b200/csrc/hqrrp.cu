@@ -11,6 +11,8 @@
 // sketch CPQR is the one new kernel.
 #include <algorithm>
 #include <climits>
+#include <cstring>
+#include <vector>
 #include <cooperative_groups.h>
 
 #include "driver.cuh"
@@ -511,6 +513,312 @@ RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A,
     return st;
   }
   st = finish(ctx, w);
+  if (st == 0) ctx->stats.factorizations++;
+  return st;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// HQRRP_left, host-streamed (Sec. 2.3 of the paper): A stays in
+// (pinned) host memory and is overwritten by R with the Householder tails
+// below the diagonal (LAPACK dgeqp3 layout); only the current
+// column block is ever written back.  Iteration i (k = i b, w = min(b, n-k)):
+//   L1  Gt = [0; G^(i)] (m x b);  Gt := Q Gt = H_0 (... (H_{i-1} Gt))
+//       -- a pass over the stored reflector blocks i-1 .. 0 (rows k_j:m)
+//   L2  Y = Gt^T A(:, k:n)  (b x s) -- a pass over the UNMODIFIED remaining
+//       columns: Y = G (Q^* A P)(k:m, k:n) = G R22 of the right-looking
+//       algorithm ("repeat some of the arithmetic")
+//   L3  CPQR of Y (cpqr_sketch_kernel) -> pivots; the <= 2w host columns the
+//       swap-convention permutation moves are copied through the device
+//   L4  X = A(:, k:k+w);  X := Q^* X  -- a pass over reflector blocks 0 .. i-1
+//   L5  Householder QR of X(k:m) (tau, T_i kept on the device); X -> host.
+// Panels stream H2D through a two-slot ring (one-panel prefetch on a copy
+// stream); the T factors of all blocks stay in HBM (n b doubles).
+namespace rutv {
+namespace {
+
+__global__ void unit_lower_kernel(i64 rows, i64 cols, const double* __restrict__ P, i64 ldp, double* __restrict__ W,
+                                  i64 ldw) {
+  const i64 total = rows * cols;
+  for (i64 e = (i64)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (i64)gridDim.x * blockDim.x) {
+    const i64 r = e % rows, c = e / rows;
+    W[r + c * ldw] = r > c ? P[r + c * ldp] : (r == c ? 1.0 : 0.0);
+  }
+}
+
+int launch_unit_lower(const Launch& L, i64 rows, i64 cols, const double* P, i64 ldp, double* W, i64 ldw) {
+  if (rows <= 0 || cols <= 0) return 0;
+  const unsigned g = (unsigned)std::min<i64>((rows * cols + 255) / 256, 4 * 148);
+  unit_lower_kernel<<<g, 256, 0, L.stream>>>(rows, cols, P, ldp, W, ldw);
+  L.count();
+  RUTV_CHECK_LAUNCH("unit_lower_kernel");
+  return 0;
+}
+
+struct HostLeft {
+  Launch L;
+  cudaStream_t h2d = nullptr;
+  double* A = nullptr;
+  i64 m = 0, n = 0, lda = 0, b = 0;
+  double* slot[2] = {nullptr, nullptr};
+  cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr}, compdone = nullptr;
+  randutv_host_report* rep = nullptr;
+  std::vector<cudaEvent_t> pool;  // H2D copy timing (start, end) pairs
+  size_t used = 0;
+  std::vector<std::pair<size_t, size_t>> spans;
+  int mark(cudaStream_t s, size_t* idx) {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      RUTV_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    RUTV_CUDA(cudaEventRecord(pool[used], s));
+    *idx = used++;
+    return 0;
+  }
+  ~HostLeft() {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    for (int s = 0; s < 2; ++s) {
+      if (ready[s]) cudaEventDestroy(ready[s]);
+      if (freed[s]) cudaEventDestroy(freed[s]);
+    }
+    if (compdone) cudaEventDestroy(compdone);
+    if (h2d) cudaStreamDestroy(h2d);
+  }
+};
+
+struct PanelItem {
+  i64 col0, r0, w;  // columns col0 .. col0+w, rows r0 .. m
+};
+
+// stream the items H2D through the two slots; f(t, device ptr (ld = m - r0))
+template <class F>
+int left_pass(HostLeft& H, const std::vector<PanelItem>& items, F&& f) {
+  const int N = (int)items.size();
+  if (N == 0) return 0;
+  // everything the compute stream wrote to host so far lands before the pass reads
+  RUTV_CUDA(cudaEventRecord(H.compdone, H.L.stream));
+  RUTV_CUDA(cudaStreamWaitEvent(H.h2d, H.compdone, 0));
+  auto issue = [&](int t) -> int {
+    const int s = t & 1;
+    const PanelItem& it = items[t];
+    const i64 rows = H.m - it.r0;
+    RUTV_CUDA(cudaStreamWaitEvent(H.h2d, H.freed[s], 0));
+    size_t e0 = 0, e1 = 0;
+    RUTV_TRY(H.mark(H.h2d, &e0));
+    RUTV_CUDA(cudaMemcpy2DAsync(H.slot[s], rows * 8, H.A + it.col0 * H.lda + it.r0, H.lda * 8, rows * 8, it.w,
+                                cudaMemcpyHostToDevice, H.h2d));
+    RUTV_TRY(H.mark(H.h2d, &e1));
+    H.spans.push_back({e0, e1});
+    RUTV_CUDA(cudaEventRecord(H.ready[s], H.h2d));
+    H.rep->h2d_bytes += rows * it.w * 8;
+    return 0;
+  };
+  RUTV_TRY(issue(0));
+  for (int t = 0; t < N; ++t) {
+    if (t + 1 < N) RUTV_TRY(issue(t + 1));
+    const int s = t & 1;
+    RUTV_CUDA(cudaStreamWaitEvent(H.L.stream, H.ready[s], 0));
+    RUTV_TRY(f(t, H.slot[s]));
+    RUTV_CUDA(cudaEventRecord(H.freed[s], H.L.stream));
+  }
+  return 0;
+}
+
+}  // namespace
+}  // namespace rutv
+
+extern "C" {
+
+RANDUTV_API int randutv_hqrrp_host(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b,
+                                   uint64_t seed, unsigned flags, int64_t* jpvt_host, double* tau_host,
+                                   randutv_host_report* report) {
+  RUTV_TRY(begin_call(ctx));
+  if (n < 1) return -3;
+  if (m < n) return -2;
+  if (!A_host) return -4;
+  if (lda < m) return -5;
+  if (b < 1) return -6;
+  if (flags != 0) return -8;
+  if (!jpvt_host) return -9;
+  if (!tau_host) return -10;
+  const i64 bb = b < n ? b : n;
+  if (bb > 512) return -6;
+  const i64 nblk = (n + bb - 1) / bb;
+  randutv_host_report rep;
+  memset(&rep, 0, sizeof(rep));
+  Launch L = ctx->launch();
+  Work w;
+  HqWork h;
+  double *slots = nullptr, *Tall = nullptr, *tauall = nullptr, *gath = nullptr;
+  auto carve_all = [&](Carver& c) {
+    carve(c, w, m, n, bb, 0, false);
+    carve_hq(c, h, n, bb);
+    slots = c.take<double>(2 * m * bb);
+    Tall = c.take<double>(nblk * bb * bb);
+    tauall = c.take<double>(n);
+    gath = c.take<double>(2 * bb * m);
+  };
+  Carver dry{nullptr, 0, 0, true};
+  carve_all(dry);
+  RUTV_TRY(ensure_ws(ctx, dry.off));
+  Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
+  carve_all(real);
+  double* Gt = w.G;   // m x b
+  double* Y = w.Y;    // b x s, ld b
+  double* X = w.Zf;   // m x b: the current block
+  double* Wb = w.Wu;  // explicit unit-lower W of a streamed reflector block
+  double* Wx = w.Acat;  // panel_qr's explicit W (unused here)
+
+  bool registered = false;
+  {
+    cudaPointerAttributes a;
+    if (!(cudaPointerGetAttributes(&a, A_host) == cudaSuccess && a.type == cudaMemoryTypeHost)) {
+      cudaGetLastError();
+      RUTV_CUDA(cudaHostRegister(A_host, (size_t)lda * n * 8, cudaHostRegisterDefault));
+      registered = true;
+    }
+  }
+  int st = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  {
+    HostLeft H;
+    H.L = L;
+    H.A = A_host;
+    H.m = m;
+    H.n = n;
+    H.lda = lda;
+    H.b = bb;
+    H.rep = &rep;
+    H.slot[0] = slots;
+    H.slot[1] = slots + m * bb;
+    auto init = [&]() -> int {
+      RUTV_CUDA(cudaStreamCreateWithFlags(&H.h2d, cudaStreamNonBlocking));
+      for (int s = 0; s < 2; ++s) {
+        RUTV_CUDA(cudaEventCreateWithFlags(&H.ready[s], cudaEventDisableTiming));
+        RUTV_CUDA(cudaEventCreateWithFlags(&H.freed[s], cudaEventDisableTiming));
+        RUTV_CUDA(cudaEventRecord(H.freed[s], L.stream));
+      }
+      RUTV_CUDA(cudaEventCreateWithFlags(&H.compdone, cudaEventDisableTiming));
+      RUTV_CUDA(cudaEventCreate(&t0));
+      RUTV_CUDA(cudaEventCreate(&t1));
+      RUTV_CUDA(cudaEventRecord(t0, L.stream));
+      return start_status(ctx, w);
+    };
+    st = init();
+    std::vector<int> piv((size_t)bb), perm, inv;
+    std::vector<int64_t> jp((size_t)n);
+    for (i64 c = 0; c < n; ++c) jp[c] = c;
+    i64 i = 0;
+    for (i64 k = 0; k < n && st == 0; k += bb, ++i) {
+      const i64 r = m - k, s = n - k, wd = bb < s ? bb : s;
+      auto iteration = [&]() -> int {
+        // L1: Gt = Q [0; G]
+        RUTV_TRY(launch_fill(L, k, bb, 0.0, Gt, m));
+        RUTV_TRY(launch_gaussian(L, seed, i, r, bb, Gt + k, m));
+        std::vector<PanelItem> back, fwd, rest;
+        for (i64 j = i - 1; j >= 0; --j) back.push_back({j * bb, j * bb, std::min(bb, n - j * bb)});
+        for (i64 j = 0; j < i; ++j) fwd.push_back({j * bb, j * bb, std::min(bb, n - j * bb)});
+        for (i64 p = i; p < nblk; ++p) rest.push_back({p * bb, 0, std::min(bb, n - p * bb)});
+        RUTV_TRY(left_pass(H, back, [&](int t, double* P) -> int {
+          const PanelItem& it = back[t];
+          const i64 rj = m - it.r0;
+          RUTV_TRY(launch_unit_lower(L, rj, it.w, P, rj, Wb, rj));
+          const double* Tj = Tall + (it.col0 / bb) * bb * bb;
+          RUTV_TRY(launch_dgemm(L, true, false, it.w, bb, rj, 1.0, Wb, rj, Gt + it.r0, m, 0.0, w.Z, it.w, w.gemm_ws,
+                                w.gemm_ws_elems));
+          RUTV_TRY(launch_dgemm(L, false, false, it.w, bb, it.w, 1.0, Tj, bb, w.Z, it.w, 0.0, w.Z2, it.w, nullptr, 0));
+          return launch_dgemm(L, false, false, rj, bb, it.w, -1.0, Wb, rj, w.Z2, it.w, 1.0, Gt + it.r0, m, nullptr, 0);
+        }));
+        // L2: Y = Gt^T A(:, k:n)
+        RUTV_TRY(left_pass(H, rest, [&](int t, double* P) -> int {
+          const PanelItem& it = rest[t];
+          return launch_dgemm(L, true, false, bb, it.w, m, 1.0, Gt, m, P, m, 0.0, Y + (it.col0 - k) * bb, bb,
+                              w.gemm_ws, w.gemm_ws_elems);
+        }));
+        // L3: pivots, then the swap-convention permutation of the host columns k:n
+        RUTV_CUDA(cudaMemsetAsync(h.done, 0, (size_t)s, L.stream));
+        RUTV_TRY(launch_cpqr(L, (int)bb, (int)s, (int)wd, Y, bb, h));
+        RUTV_CUDA(cudaMemcpyAsync(piv.data(), h.piv, wd * sizeof(int), cudaMemcpyDeviceToHost, L.stream));
+        RUTV_CUDA(cudaStreamSynchronize(L.stream));
+        perm.resize((size_t)s);
+        inv.resize((size_t)s);
+        for (i64 c = 0; c < s; ++c) perm[c] = inv[c] = (int)c;
+        for (i64 j = 0; j < wd; ++j) {
+          const int p = piv[j], pp = inv[p];
+          if (pp != j) {
+            const int cj = perm[j];
+            perm[j] = p;
+            perm[pp] = cj;
+            inv[p] = (int)j;
+            inv[cj] = pp;
+          }
+        }
+        std::vector<i64> moved;
+        for (i64 c = 0; c < s; ++c)
+          if (perm[c] != c) moved.push_back(c);
+        for (size_t t = 0; t < moved.size(); ++t) {
+          RUTV_CUDA(cudaMemcpyAsync(gath + t * m, A_host + (k + perm[moved[t]]) * lda, m * 8, cudaMemcpyHostToDevice,
+                                    L.stream));
+          rep.h2d_bytes += m * 8;
+        }
+        for (size_t t = 0; t < moved.size(); ++t) {
+          RUTV_CUDA(cudaMemcpyAsync(A_host + (k + moved[t]) * lda, gath + t * m, m * 8, cudaMemcpyDeviceToHost,
+                                    L.stream));
+          rep.d2h_bytes += m * 8;
+        }
+        {
+          std::vector<int64_t> old(jp.begin() + k, jp.end());
+          for (i64 c : moved) jp[k + c] = old[perm[c]];
+        }
+        // L4: X = Q^* A(:, k:k+w)
+        RUTV_CUDA(cudaMemcpy2DAsync(X, m * 8, A_host + k * lda, lda * 8, m * 8, wd, cudaMemcpyHostToDevice, L.stream));
+        rep.h2d_bytes += m * wd * 8;
+        RUTV_TRY(left_pass(H, fwd, [&](int t, double* P) -> int {
+          const PanelItem& it = fwd[t];
+          const i64 rj = m - it.r0;
+          RUTV_TRY(launch_unit_lower(L, rj, it.w, P, rj, Wb, rj));
+          const double* Tj = Tall + (it.col0 / bb) * bb * bb;
+          return apply_left_t(L, w, rj, wd, it.w, X + it.r0, m, Wb, rj, Tj, bb);
+        }));
+        // L5: QR of the block, write back
+        RUTV_TRY(panel_qr(L, r, wd, X + k, m, tauall + k, Wx, r, Tall + i * bb * bb, bb, w.qw));
+        RUTV_CUDA(cudaMemcpy2DAsync(A_host + k * lda, lda * 8, X, m * 8, m * 8, wd, cudaMemcpyDeviceToHost, L.stream));
+        rep.d2h_bytes += m * wd * 8;
+        return 0;
+      };
+      st = iteration();
+    }
+    if (st == 0) {
+      cudaEventRecord(t1, L.stream);
+      if (cudaMemcpyAsync(tau_host, tauall, n * 8, cudaMemcpyDeviceToHost, L.stream) != cudaSuccess) st = RANDUTV_ERR_CUDA;
+      rep.d2h_bytes += n * 8;
+    }
+    if (st == 0) st = finish(ctx, w);
+    if (st == 0) {
+      memcpy(jpvt_host, jp.data(), n * sizeof(int64_t));
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, t0, t1) == cudaSuccess) rep.wall_ms = ms;
+      double tot = 0.0;
+      for (auto& pr : H.spans) {
+        float x = 0.f;
+        if (cudaEventElapsedTime(&x, H.pool[pr.first], H.pool[pr.second]) == cudaSuccess) tot += x;
+      }
+      rep.h2d_ms = tot;
+      rep.cache_slots = 2;
+      rep.slot_bytes = (int64_t)(m * bb * 8);
+    }
+    cudaStreamSynchronize(L.stream);
+    if (H.h2d) cudaStreamSynchronize(H.h2d);
+  }
+  if (t0) cudaEventDestroy(t0);
+  if (t1) cudaEventDestroy(t1);
+  if (registered) cudaHostUnregister(A_host);
+  cudaGetLastError();
+  ctx->stats.h2d_bytes += rep.h2d_bytes;
+  ctx->stats.d2h_bytes += rep.d2h_bytes;
+  if (report) *report = rep;
   if (st == 0) ctx->stats.factorizations++;
   return st;
 }

@@ -65,6 +65,7 @@ SIGNATURES = {
     "randutv_factor_tol": (_int, [_vp, _i64, _i64, _vp, _i64, _dbl, _i64, _int, _u64, _uint, _vp, _i64, _vp, _i64,
                                   _vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_dbl)]),
     "randutv_hqrrp": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _u64, _uint, _vp, _vp, _i64]),
+    "randutv_hqrrp_host": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _u64, _uint, _vp, _vp, ctypes.POINTER(HostReport)]),
     "randutv_status_string": (ctypes.c_char_p, [_int]),
     "randutv_last_error": (ctypes.c_char_p, []),
     "randutv_get_stats": (_int, [_vp, ctypes.POINTER(Stats)]),
@@ -269,6 +270,20 @@ class Context:
                                     _ptr(jpvt), _ptr(Q), _ld(Q) if Q is not None else 1)
         _check("randutv_hqrrp", st)
         return Q, jpvt
+
+    def randutv_hqrrp_host(self, A_host, b, seed):
+        """HQRRP_left of the column-major host (numpy, Fortran-order) matrix A_host,
+        overwritten by R + Householder tails: returns (jpvt, tau, report)."""
+        import numpy as np
+        m, n = A_host.shape
+        assert A_host.flags.f_contiguous and A_host.dtype == np.float64
+        jpvt = np.zeros(n, dtype=np.int64)
+        tau = np.zeros(n)
+        rep = HostReport()
+        st = self.lib.randutv_hqrrp_host(self.h, m, n, A_host.ctypes.data, m, int(b), int(seed) & (2**64 - 1), 0,
+                                         jpvt.ctypes.data, tau.ctypes.data, ctypes.byref(rep))
+        _check("randutv_hqrrp_host", st)
+        return jpvt, tau, {k: getattr(rep, k) for k, _ in HostReport._fields_}
 
     # ---------------------------------------------------------------- step entries
     def randutv_gaussian(self, seed, it, rows, cols, G=None):

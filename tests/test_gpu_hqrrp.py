@@ -112,3 +112,42 @@ def test_hqrrp_errors(ctx):
     st = ctx.lib.randutv_hqrrp(ctx.h, 10, 10, None, 10, 4, 1, 0, None, None, 10)
     assert st == -4
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("m,n,b", [(300, 200, 32), (200, 200, 64), (129, 129, 128), (64, 40, 64), (257, 100, 24),
+                                   (520, 520, 64), (1000, 300, 100)])
+def test_hqrrp_host_left_parity(ctx, m, n, b):
+    """HQRRP_left from host memory against the right-looking oracle:
+    same pivots, same R, and the stored Householder tails + tau form the
+    oracle's Q (LAPACK dorgqr)."""
+    import scipy.linalg.lapack as lp
+    from paper_2002_06960_b200.randutv import pinned_colmajor
+    A = np.asfortranarray(np.random.default_rng(m + 7 * n + b).standard_normal((m, n)))
+    Ah = pinned_colmajor(m, n)
+    Ah[:] = A
+    jp, tau, rep = ctx.randutv_hqrrp_host(Ah, b, 77)
+    Qo, Ro, jpo = oracle_hqrrp(A, b, 77)
+    nA = np.linalg.norm(A)
+    assert np.array_equal(jp, jpo)
+    R = np.triu(Ah)
+    assert np.max(np.abs(R - Ro)) / nA <= ELEM_TOL
+    Q, _, info = lp.dorgqr(np.array(Ah, order="F"), tau)
+    assert info == 0
+    assert np.max(np.abs(Q - Qo[:, :n])) <= ELEM_TOL
+    assert np.linalg.norm(A[:, jp] - Q @ R[:n, :]) <= 1e-12 * nA
+    # left-looking: the host matrix is written once per block plus the moved columns
+    assert rep["d2h_bytes"] <= 8 * m * n + 8 * n + 8 * m * 2 * b * (-(-n // b))
+    assert rep["h2d_bytes"] >= 8 * m * n
+
+
+def test_hqrrp_host_unpinned_and_errors(ctx):
+    from paper_2002_06960_b200.randutv import RandUTVError
+    A = np.asfortranarray(np.random.default_rng(5).standard_normal((150, 90)))
+    Ah = A.copy(order="F")                   # pageable: registered for the call
+    jp, tau, _ = ctx.randutv_hqrrp_host(Ah, 16, 3)
+    _, Ro, jpo = oracle_hqrrp(A, 16, 3, build_q=False)
+    assert np.array_equal(jp, jpo)
+    assert np.max(np.abs(np.triu(Ah) - Ro)) <= 1e-11 * np.linalg.norm(A)
+    with pytest.raises(RandUTVError) as e:
+        ctx.randutv_hqrrp_host(np.zeros((10, 20), order="F"), 4, 1)
+    assert e.value.status == -2
