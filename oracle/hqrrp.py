@@ -65,12 +65,17 @@ def cpqr_sketch(Y, steps):
     return perm, F
 
 
-def hqrrp(A, b, seed, build_q=True, record=None):
+def hqrrp(A, b, seed, build_q=True, record=None, k=None):
     """Oracle HQRRP of A (m x n, m >= n): returns (Q, R, jpvt) with
     A[:, jpvt] = Q R, Q (m x m) orthogonal (None if not build_q), R upper
     trapezoidal, jpvt a permutation of 0..n-1.  `record`, if a list, receives
     per step the dict {k, w, perm} (perm: positions k:n after H4, as indices
-    into the columns k:n before it)."""
+    into the columns k:n before it).
+
+    k (partial factorisation, the section's "partial rank-revealing QR",
+    P:252-262): stop after K = ceil(k / b) blocks; then A[:, jpvt] = Q R still
+    holds with R(K b:m, K b:n) the unreduced trailing block, and the rank-k
+    truncation error is rho = ||R(k:m, k:n)||_F, returned as a 4th value."""
     A = np.asarray(A, dtype=np.float64)
     m, n = A.shape
     if m < n:
@@ -82,7 +87,11 @@ def hqrrp(A, b, seed, build_q=True, record=None):
     Q = np.eye(m, order="F") if build_q else None
     jpvt = np.arange(n)
     i = 0
-    for k in range(0, n, b):
+    kstop = n if k is None else min(n, -(-int(k) // b) * b)
+    if k is not None and not (1 <= k <= n):
+        raise ValueError("need 1 <= k <= n")
+    ktrunc = k
+    for k in range(0, kstop, b):
         r, s = m - k, n - k
         w = min(b, s)
         # H1, H2
@@ -106,5 +115,7 @@ def hqrrp(A, b, seed, build_q=True, record=None):
         if build_q:
             Q[:, k:] -= ((Q[:, k:] @ W) @ Tq) @ W.T
         i += 1
+    if ktrunc is not None:
+        return Q, R, jpvt, float(np.linalg.norm(R[ktrunc:, ktrunc:]))
     return Q, R, jpvt
 

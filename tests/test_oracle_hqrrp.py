@@ -91,3 +91,21 @@ def test_hqrrp_flops_model():
     m = n = b = 64
     fl = hqrrp_flops(m, n, b)
     assert fl == pytest.approx(2 * b * m * n + 2 * b * b * n + 2 * m * n * n - 2 * n ** 3 / 3 + 4 * m * m * n)
+
+
+def test_hqrrp_partial_is_a_prefix_of_the_full_run():
+    """The partial run (K = ceil(k/b) blocks) computes exactly the first K
+    steps of the full run; A P = Q R holds with the unreduced trailing block,
+    and rho = ||R(k:, k:)||_F is the exact error of the rank-k truncation
+    A P ~ Q(:, :k) R(:k, :)."""
+    A = np.random.default_rng(21).standard_normal((200, 150))
+    Qf, Rf, jf = hqrrp(A, 32, 4)
+    for k in (32, 50, 150):
+        Q, R, jp, rho = hqrrp(A, 32, 4, k=k)
+        K = -(-k // 32) * 32
+        assert np.array_equal(jp[:K], jf[:K])
+        assert np.array_equal(R[:K, :K], Rf[:K, :K])
+        assert np.linalg.norm(A[:, jp] - Q @ R) <= 1e-13 * np.linalg.norm(A)
+        assert np.all(R[K:, :K] == 0.0)
+        err = np.linalg.norm(A[:, jp] - Q[:, :k] @ R[:k, :])
+        assert abs(err - rho) <= 1e-12 * np.linalg.norm(A)
