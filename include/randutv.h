@@ -261,10 +261,22 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
  *   Q     (m x m, ldq >= m) out: the orthogonal factor; not touched (may be
  *         NULL) with flags & RANDUTV_NO_UV
  * Returns 0, a negative argument index (-2 m < n, -3 n, -4 A, -5 lda, -6 b,
- * -8 jpvt, -9 Q, -10 ldq) or RANDUTV_ERR_*.  Synchronous on the ctx stream.
+ * -9 jpvt, -10 Q, -11 ldq) or RANDUTV_ERR_*.  Synchronous on the ctx stream.
  * ------------------------------------------------------------------------- */
 RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, int64_t b,
                               uint64_t seed, unsigned flags, int64_t* jpvt, double* Q, int64_t ldq);
+
+/* Partial HQRRP ("partial rank-revealing QR factorization"): only
+ * the first K = ceil(k / b) blocks.  A is overwritten by R whose rows 0:K b
+ * are final and whose trailing block R(K b:m, K b:n) is the updated,
+ * unreduced remainder, so A(:, jpvt) = Q R still holds;
+ * *resid_fro = ||R(k:m, k:n)||_F = ||A P - Q(:, 0:k) R(0:k, :)||_F.  Arguments
+ * as randutv_hqrrp with k inserted after lda; errors are the argument
+ * positions (-6 k, -7 b, -10 jpvt, -11 Q, -12 ldq).  resid_fro (host, may be
+ * NULL). */
+RANDUTV_API int randutv_hqrrp_rank(randutv_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, int64_t k,
+                                   int64_t b, uint64_t seed, unsigned flags, int64_t* jpvt, double* Q, int64_t ldq,
+                                   double* resid_fro);
 
 /* HQRRP_left, host-streamed (Sec. 2.3): the left-looking HQRRP for
  * a matrix that stays in HOST memory.  Per block: the sketch Gaussian is

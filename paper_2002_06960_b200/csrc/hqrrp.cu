@@ -420,8 +420,33 @@ using namespace rutv;
 
 extern "C" {
 
+static int hqrrp_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, int64_t ktr, int64_t b,
+                      uint64_t seed, unsigned flags, int64_t* jpvt, double* Q, int64_t ldq, double* resid_fro);
+
 RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, int64_t b,
                               uint64_t seed, unsigned flags, int64_t* jpvt, double* Q, int64_t ldq) {
+  return hqrrp_impl(ctx, m, n, A, lda, -1, b, seed, flags, jpvt, Q, ldq, nullptr);
+}
+
+RANDUTV_API int randutv_hqrrp_rank(randutv_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, int64_t k,
+                                   int64_t b, uint64_t seed, unsigned flags, int64_t* jpvt, double* Q, int64_t ldq,
+                                   double* resid_fro) {
+  RUTV_TRY(begin_call(ctx));
+  const bool bq = !(flags & RANDUTV_NO_UV);
+  if (n < 1) return -3;
+  if (m < n) return -2;
+  if (!A) return -4;
+  if (lda < m) return -5;
+  if (k < 1 || k > n) return -6;
+  if (b < 1 || (b < n ? b : n) > 512) return -7;
+  if (!jpvt) return -10;
+  if (bq && !Q) return -11;
+  if (bq && ldq < m) return -12;
+  return hqrrp_impl(ctx, m, n, A, lda, k, b, seed, flags, jpvt, Q, ldq, resid_fro);
+}
+
+static int hqrrp_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A, int64_t lda, int64_t ktr, int64_t b,
+                      uint64_t seed, unsigned flags, int64_t* jpvt, double* Q, int64_t ldq, double* resid_fro) {
   RUTV_TRY(begin_call(ctx));
   const bool bq = !(flags & RANDUTV_NO_UV);
   if (n < 1) return -3;
@@ -429,9 +454,9 @@ RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A,
   if (!A) return -4;
   if (lda < m) return -5;
   if (b < 1) return -6;
-  if (!jpvt) return -8;
-  if (bq && !Q) return -9;
-  if (bq && ldq < m) return -10;
+  if (!jpvt) return -9;
+  if (bq && !Q) return -10;
+  if (bq && ldq < m) return -11;
   const i64 bb = b < n ? b : n;
   if (bb > 512) return -6;  // the sketch CPQR keeps <= 512 rows per column in registers
   Launch L = ctx->launch();
@@ -467,7 +492,8 @@ RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A,
   }
   int st = 0;
   i64 i = 0;
-  for (i64 k = 0; k < n && st == 0; k += bb, ++i) {
+  const i64 kstop = ktr < 0 ? n : std::min<i64>(n, (ktr + bb - 1) / bb * bb);
+  for (i64 k = 0; k < kstop && st == 0; k += bb, ++i) {
     const i64 r = m - k, s = n - k, wd = bb < s ? bb : s;
     const int sel = (int)(i & 1);
     double* Wu = (qs && sel) ? h.Wu2 : w.Wu;
@@ -512,7 +538,16 @@ RANDUTV_API int randutv_hqrrp(randutv_ctx* ctx, int64_t m, int64_t n, double* A,
     cudaStreamSynchronize(L.stream);
     return st;
   }
-  st = finish(ctx, w);
+  if (ktr > 0 && resid_fro) {
+    // rho = ||R(k:m, k:n)||_F: the error of the rank-k truncation
+    RUTV_TRY(launch_sumsq(L, m - ktr, n - ktr, A + ktr + ktr * lda, lda, w.red, w.scal));
+    double ss = 0.0;
+    RUTV_CUDA(cudaMemcpyAsync(&ss, w.scal, sizeof(double), cudaMemcpyDeviceToHost, L.stream));
+    st = finish(ctx, w);
+    *resid_fro = sqrt(ss);
+  } else {
+    st = finish(ctx, w);
+  }
   if (st == 0) ctx->stats.factorizations++;
   return st;
 }

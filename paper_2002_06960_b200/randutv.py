@@ -65,6 +65,8 @@ SIGNATURES = {
     "randutv_factor_tol": (_int, [_vp, _i64, _i64, _vp, _i64, _dbl, _i64, _int, _u64, _uint, _vp, _i64, _vp, _i64,
                                   _vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_dbl)]),
     "randutv_hqrrp": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _u64, _uint, _vp, _vp, _i64]),
+    "randutv_hqrrp_rank": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _u64, _uint, _vp, _vp, _i64,
+                                  ctypes.POINTER(_dbl)]),
     "randutv_hqrrp_host": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _u64, _uint, _vp, _vp, ctypes.POINTER(HostReport)]),
     "randutv_status_string": (ctypes.c_char_p, [_int]),
     "randutv_last_error": (ctypes.c_char_p, []),
@@ -270,6 +272,22 @@ class Context:
                                     _ptr(jpvt), _ptr(Q), _ld(Q) if Q is not None else 1)
         _check("randutv_hqrrp", st)
         return Q, jpvt
+
+    def randutv_hqrrp_rank(self, A, k, b, seed, build_q=True, flags=0):
+        """Partial HQRRP (K = ceil(k/b) blocks) of the device matrix A, overwritten by
+        R: returns (Q, jpvt, rho) with rho = ||R(k:, k:)||_F."""
+        import torch
+        m, n = A.shape
+        if not build_q:
+            flags |= RANDUTV_NO_UV
+        jpvt = torch.empty(n, dtype=torch.int64, device=A.device)
+        Q = colmajor(m, m, device=A.device) if build_q else None
+        rho = ctypes.c_double()
+        st = self.lib.randutv_hqrrp_rank(self.h, m, n, _ptr(A), _ld(A), int(k), int(b), int(seed) & (2**64 - 1),
+                                         flags, _ptr(jpvt), _ptr(Q), _ld(Q) if Q is not None else 1,
+                                         ctypes.byref(rho))
+        _check("randutv_hqrrp_rank", st)
+        return Q, jpvt, rho.value
 
     def randutv_hqrrp_host(self, A_host, b, seed):
         """HQRRP_left of the column-major host (numpy, Fortran-order) matrix A_host,

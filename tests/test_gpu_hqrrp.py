@@ -151,3 +151,18 @@ def test_hqrrp_host_unpinned_and_errors(ctx):
     with pytest.raises(RandUTVError) as e:
         ctx.randutv_hqrrp_host(np.zeros((10, 20), order="F"), 4, 1)
     assert e.value.status == -2
+
+
+@pytest.mark.parametrize("m,n,k,b", [(300, 200, 64, 32), (300, 200, 50, 32), (520, 520, 200, 64), (129, 129, 129, 128)])
+def test_hqrrp_partial_parity(ctx, m, n, k, b):
+    A = np.asfortranarray(np.random.default_rng(m + n + k).standard_normal((m, n)))
+    Ad = to_dev(A)
+    Q, jp, rho = ctx.randutv_hqrrp_rank(Ad, k, b, 13)
+    Q, R, jp = to_np(Q), to_np(Ad), jp.cpu().numpy()
+    Qo, Ro, jpo, rho_o = oracle_hqrrp(A, b, 13, k=k)
+    nA = np.linalg.norm(A)
+    assert np.array_equal(jp, jpo)
+    assert abs(rho - rho_o) <= 1e-9 * rho_o + 1e-14 * nA
+    assert np.max(np.abs(R - Ro)) / nA <= ELEM_TOL
+    assert np.max(np.abs(Q - Qo)) <= ELEM_TOL
+    assert np.linalg.norm(A[:, jp] - Q @ R) <= 1e-12 * nA
