@@ -153,3 +153,38 @@ def test_c5_fullsize(ctx):
     assert abs(float(torch.linalg.norm(T)) - nA) <= 1e-12 * nA
     d = torch.diagonal(T).abs()
     assert abs(float(torch.log(d).sum()) - lad) <= 1e-4
+
+
+def test_c3_fullsize_hqrrp(ctx):
+    """HQRRP on c3's full matrix: A P = Q R, Q orthogonal,
+    R exactly upper triangular; the first block's pivots (a sketch CPQR over
+    all 16384 columns) and the partial run's rho against the oracle on the
+    same bytes."""
+    import torch
+    from oracle.hqrrp import hqrrp as oracle_hqrrp
+    from paper_2002_06960_b200.inputs import CONFIGS, make_config_torch
+    from paper_2002_06960_b200.randutv import colmajor
+    c = CONFIGS["c3"]
+    b, seed = c["b"], 2003
+    A = make_config_torch("c3")
+    nA = float(torch.linalg.norm(A))
+    R = colmajor(*A.shape)
+    R.copy_(A)
+    Q, jp = ctx.randutv_hqrrp(R, b, seed)
+    torch.cuda.synchronize()
+    assert bool((torch.sort(jp).values == torch.arange(A.shape[1], device=jp.device)).all())
+    E = A.index_select(1, jp) - Q @ R
+    assert float(torch.linalg.norm(E)) / nA <= 1e-12
+    del E
+    assert _orth_err_exact(Q) <= 1e-12
+    assert bool((torch.tril(R, -1) == 0).all())
+    del Q
+    # the first block against the oracle (partial run, k = b)
+    R.copy_(A)
+    _, jpk, rho = ctx.randutv_hqrrp_rank(R, b, b, seed, build_q=False)
+    Ah = np.asfortranarray(A.cpu().numpy())
+    _, Ro, jpo, rho_o = oracle_hqrrp(Ah, b, seed, build_q=False, k=b)
+    assert np.array_equal(jp[:b].cpu().numpy(), jpo[:b])
+    assert np.array_equal(jpk.cpu().numpy(), jpo)
+    assert abs(rho - rho_o) <= 1e-9 * rho_o
+    assert np.max(np.abs(R[:b, :].cpu().numpy() - Ro[:b, :])) / nA <= 1e-11
