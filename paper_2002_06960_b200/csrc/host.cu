@@ -32,6 +32,7 @@
 // conventions); only sums over panels are split (GEMM accumulation with
 // beta = 1), so results agree with randutv_factor_ex to rounding.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -258,6 +259,21 @@ struct HostRun {
   uint64_t seed;
   bool dir = false;        // direction of the next pass (serpentine)
   bool y_ready = false;    // Y of the next step was taken by the previous step's fused pass
+  // Deferred U / V accumulation: up to G steps' (W, T, S) of one matrix are
+  // merged into ONE compact-WY transform and applied in one read + one RW pass
+  // (see flush_uv).  G <= 1: per-step application.
+  struct Batch {
+    int mat = -1;
+    i64 rows = 0;             // U: m, V: n (the matrix's column-index space)
+    double* W = nullptr;      // rows x G b: block l = [0 (rows < k_l); W_l]
+    double* T = nullptr;      // G blocks of b x b: T_l
+    double* S = nullptr;      // G blocks of b x b: the S9 fold factor (U_s or V_s)
+    double* Tc = nullptr;     // G b x G b: the merged T
+    std::vector<i64> k;       // first column of each pending step
+  };
+  int G = 1;
+  Batch bu, bv;
+  double *Zb = nullptr, *Zb2 = nullptr;  // max(m, n) x G b temporaries of the merged apply
 };
 
 // Visit panels [p0, p1) of `mat` in the current serpentine direction with a
@@ -280,10 +296,15 @@ int pass(HostRun& R, int mat, i64 p0, i64 p1, bool dirty, F&& f, i64 lo = 0) {
 
 // right update of the trailing panels [p0, np) of matrix `mat` (rows x *):
 // X -= ((X W) Tf) W^T with W (ld ldw) rows aligned to panel p0's first column
-int stream_apply_right(HostRun& R, int mat, i64 p0, i64 bw, const double* W, i64 ldw, const double* Tf, i64 ldtf) {
+int stream_apply_right(HostRun& R, int mat, i64 p0, i64 bw, const double* W, i64 ldw, const double* Tf, i64 ldtf,
+                       double* Z = nullptr, double* Z2 = nullptr) {
   const HostMat& M = R.pc.mats[mat];
   const i64 rows = M.rows;
-  Work& w = R.w;
+  Work w = R.w;
+  if (Z) {
+    w.Z = Z;
+    w.Z2 = Z2;
+  }
   // Z = sum_j X_j W_j   (fixed panel order inside a pass is not needed for
   // correctness; the GEMM accumulation is beta = 1)
   RUTV_TRY(launch_fill(R.L, rows, bw, 0.0, w.Z, rows));
@@ -325,6 +346,59 @@ int host_fold_uv(HostRun& R, i64 i, i64 bw) {
     RUTV_TRY(right_mult_inplace(R.L, w.Zf, R.n, bw, X, R.n, w.Vs, bw));
     RUTV_TRY(R.pc.put(R.mV, i, true));
   }
+  return 0;
+}
+
+// Deferred U / V updates.  Step l of a batch applies X := X H_l D_l with
+// H_l = I - W_l T_l W_l^T (columns k_l:) and D_l = diag(I, S_l, I) (the S9
+// fold of block l).  Since H D = D (D^T H D) and every D_j acts on its own
+// column block, the batch equals X D_0 ... D_{L-1} (I - W^f T_c W^f^T) with
+// W^f = D^T [W_0 .. W_{L-1}] (block row j of W multiplied by S_j^T) and T_c
+// the merged forward T (T_c(0:lb, lb:(l+1)b) = -T_c(0:lb, 0:lb) W^f_{0:l}^T W^f_l T_l).
+int flush_uv(HostRun& R, HostRun::Batch& B) {
+  const i64 L = (i64)B.k.size();
+  if (L == 0) return 0;
+  Work& w = R.w;
+  const i64 b = R.b, k0 = B.k[0], rows = B.rows, ldc = R.G * b, h = rows - k0;
+  double* Wf = B.W + k0;  // rows k0:rows of the batch's W, ld rows
+  // D: the folds of the L blocks
+  for (i64 l = 0; l < L; ++l) {
+    double* X;
+    RUTV_TRY(R.pc.get(B.mat, B.k[l] / b, &X));
+    RUTV_TRY(right_mult_inplace(R.L, w.Zf, rows, b, X, rows, B.S + l * b * b, b));
+    RUTV_TRY(R.pc.put(B.mat, B.k[l] / b, true));
+  }
+  // W^f = D^T W: block row j (rows k_j:k_j+b) of the blocks l <= j
+  for (i64 j = 0; j < L; ++j)
+    RUTV_TRY(left_mult_t_inplace(R.L, w.Zf, b, (j + 1) * b, B.W + B.k[j], rows, B.S + j * b * b, b));
+  // T_c
+  RUTV_TRY(launch_fill(R.L, L * b, L * b, 0.0, B.Tc, ldc));
+  for (i64 l = 0; l < L; ++l) {
+    RUTV_TRY(launch_copy(R.L, b, b, B.T + l * b * b, b, B.Tc + l * b * (ldc + 1), ldc));
+    if (l == 0) continue;
+    const i64 lb = l * b;
+    RUTV_TRY(launch_dgemm(R.L, true, false, lb, b, h, 1.0, Wf, rows, Wf + lb * rows, rows, 0.0, w.Z, lb, w.gemm_ws,
+                          w.gemm_ws_elems));
+    RUTV_TRY(launch_dgemm(R.L, false, false, lb, b, lb, 1.0, B.Tc, ldc, w.Z, lb, 0.0, w.Z2, lb, nullptr, 0));
+    RUTV_TRY(launch_dgemm(R.L, false, false, lb, b, b, -1.0, w.Z2, lb, B.T + l * b * b, b, 0.0, B.Tc + lb * ldc, ldc,
+                          nullptr, 0));
+  }
+  RUTV_TRY(stream_apply_right(R, B.mat, k0 / b, L * b, Wf, rows, B.Tc, ldc, R.Zb, R.Zb2));
+  B.k.clear();
+  return 0;
+}
+
+// queue step k's (W (h x b, ld ldw, rows k:), T, S) of one matrix; flush at G
+int defer_uv(HostRun& R, HostRun::Batch& B, i64 k, const double* W, i64 ldw, const double* T, const double* S) {
+  const i64 b = R.b, l = (i64)B.k.size();
+  const i64 k0 = l == 0 ? k : B.k[0];
+  double* Wl = B.W + l * b * B.rows;
+  if (k > k0) RUTV_TRY(launch_fill(R.L, k - k0, b, 0.0, Wl + k0, B.rows));
+  RUTV_TRY(launch_copy(R.L, B.rows - k, b, W, ldw, Wl + k, B.rows));
+  RUTV_TRY(launch_copy(R.L, b, b, T, b, B.T + l * b * b, b));
+  RUTV_TRY(launch_copy(R.L, b, b, S, b, B.S + l * b * b, b));
+  B.k.push_back(k);
+  if ((i64)B.k.size() == R.G) RUTV_TRY(flush_uv(R, B));
   return 0;
 }
 
@@ -393,6 +467,12 @@ int host_sampled_step(HostRun& R, i64 i) {
                         w.Y + (j - i - 1) * b, s - b, w.gemm_ws, w.gemm_ws_elems);
   }));
   R.y_ready = next_sampled;
+  if (R.G > 1) {
+    // deferred: merged with the next steps' transforms (flush_uv)
+    if (R.mV >= 0) RUTV_TRY(defer_uv(R, R.bv, k, w.Wv, s, w.TV, w.Vs));
+    if (R.mU >= 0) RUTV_TRY(defer_uv(R, R.bu, k, w.Wu, r, w.TU, w.Us));
+    return 0;
+  }
   // V: right transform with W_V; U: right transform with W_U (columns k:m); then their S9 folds
   if (R.mV >= 0) RUTV_TRY(stream_apply_right(R, R.mV, i, b, w.Wv, s, w.TV, b));
   if (R.mU >= 0) RUTV_TRY(stream_apply_right(R, R.mU, i, b, w.Wu, r, w.TU, b));
@@ -402,6 +482,8 @@ int host_sampled_step(HostRun& R, i64 i) {
 int host_final_step(HostRun& R, i64 i) {
   Work& w = R.w;
   const i64 m = R.m, n = R.n, k = i * R.b, r = m - k, s = n - k;
+  RUTV_TRY(flush_uv(R, R.bv));
+  RUTV_TRY(flush_uv(R, R.bu));
   if (s <= 0) return 0;
   double* X;
   RUTV_TRY(R.pc.get(R.mT, i, &X));
@@ -458,7 +540,26 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
   R.pc.slot_elems = ((std::max(m, n) * bb + 31) / 32) * 32;
   // workspace: the in-HBM driver's buffers + U_s of the deferred fold + the slots
   Carver dry{nullptr, 0, 0, true};
+  {
+    const char* e = getenv("RUTV_HOST_UV_BATCH");
+    R.G = uv ? (e ? atoi(e) : 8) : 1;
+    if (R.G < 1) R.G = 1;
+  }
+  const i64 Gb = R.G * bb, mx = std::max(m, n);
+  auto carve_batch = [&](Carver& c) {
+    if (R.G <= 1) return;
+    R.bu.W = c.take<double>(m * Gb);
+    R.bv.W = c.take<double>(n * Gb);
+    for (HostRun::Batch* B : {&R.bu, &R.bv}) {
+      B->T = c.take<double>(Gb * bb);
+      B->S = c.take<double>(Gb * bb);
+      B->Tc = c.take<double>(Gb * Gb);
+    }
+    R.Zb = c.take<double>(mx * Gb);
+    R.Zb2 = c.take<double>(mx * Gb);
+  };
   carve(dry, R.w, m, n, bb, 0, false);
+  carve_batch(dry);
   const size_t fixed = dry.off;
   const size_t slot_bytes = (size_t)R.pc.slot_elems * 8;
   size_t budget = device_cache_bytes;
@@ -474,6 +575,7 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
   RUTV_TRY(ensure_ws(ctx, fixed + (size_t)nslots * slot_bytes + kAlign));
   Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
   carve(real, R.w, m, n, bb, 0, false);
+  carve_batch(real);
   double* slots = real.take<double>(nslots * R.pc.slot_elems);
   rep.cache_slots = nslots;
   rep.slot_bytes = (int64_t)slot_bytes;
@@ -510,6 +612,10 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
     if (uv) {
       R.mU = R.pc.add_mat(U_host, m, m, ldu);
       R.mV = R.pc.add_mat(V_host, n, n, ldv);
+      R.bu.mat = R.mU;
+      R.bu.rows = m;
+      R.bv.mat = R.mV;
+      R.bv.rows = n;
     }
     cudaEventRecord(t0, ctx->stream);
     st = start_status(ctx, R.w);
