@@ -166,3 +166,24 @@ def test_hqrrp_partial_parity(ctx, m, n, k, b):
     assert np.max(np.abs(R - Ro)) / nA <= ELEM_TOL
     assert np.max(np.abs(Q - Qo)) <= ELEM_TOL
     assert np.linalg.norm(A[:, jp] - Q @ R) <= 1e-12 * nA
+
+
+@pytest.mark.parametrize("m,n,b", [(1, 1, 1), (5, 1, 4), (7, 3, 1), (33, 33, 33), (40, 2, 64)])
+def test_hqrrp_degenerate_shapes(ctx, m, n, b):
+    """Single column / single row / b = 1 / b > n: in-HBM, partial and host-streamed entries."""
+    from paper_2002_06960_b200.randutv import pinned_colmajor
+    A = np.asfortranarray(np.random.default_rng(m * 31 + n).standard_normal((m, n)))
+    Q, R, jp = _gpu(ctx, A, b, 4)
+    Qo, Ro, jpo = oracle_hqrrp(A, b, 4)
+    nA = np.linalg.norm(A)
+    assert np.array_equal(jp, jpo)
+    assert np.max(np.abs(R - Ro)) <= 1e-12 * nA and np.max(np.abs(Q - Qo)) <= 1e-12
+    Ad = to_dev(A)
+    _, jpk, rho = ctx.randutv_hqrrp_rank(Ad, 1, b, 4, build_q=False)
+    _, _, jpko, rho_o = oracle_hqrrp(A, b, 4, build_q=False, k=1)
+    assert np.array_equal(jpk.cpu().numpy(), jpko) and abs(rho - rho_o) <= 1e-12 * nA
+    Ah = pinned_colmajor(m, n)
+    Ah[:] = A
+    jph, tau, _ = ctx.randutv_hqrrp_host(Ah, b, 4)
+    assert np.array_equal(jph, jpo)
+    assert np.max(np.abs(np.triu(Ah) - Ro)) <= 1e-12 * nA
