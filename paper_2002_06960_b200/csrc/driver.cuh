@@ -27,6 +27,8 @@ struct randutv_ctx {
   // the column block and the T updates (eWv: W_V ready; eV: V update done)
   cudaStream_t vstr;
   cudaEvent_t eWv, eV;
+  // U update of step i on the V stream (eWu: W_U ready; eU: U update done)
+  cudaEvent_t eWu, eU;
   // multi-GPU communicators (randutv_comm_init): main-stream and side-stream
   rutv::Comm* comm;
   rutv::Comm* comm_side;

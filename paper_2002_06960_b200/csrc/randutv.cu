@@ -121,9 +121,9 @@ size_t carve(Carver& c, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork) {
   w.Zf = c.take<double>(mx * b);
   w.Acat = c.take<double>(m * 2 * b);
   w.Bt = c.take<double>(n * 2 * b);
-  w.Zv = c.take<double>(n * b);
-  w.Zv2 = c.take<double>(n * b);
-  w.gemm_ws_v = c.take<double>(4 * n * b);
+  w.Zv = c.take<double>(mx * b);   // V stream: the V update (n rows) and the U update (m rows)
+  w.Zv2 = c.take<double>(mx * b);
+  w.gemm_ws_v = c.take<double>(4 * mx * b);
   w.Wv = c.take<double>(n * b);
   w.Wu = c.take<double>(m * b);
   w.TV = c.take<double>(b * b);
@@ -257,6 +257,16 @@ int fused_right_left(const Launch& L, Work& w, i64 m, i64 r, i64 b, i64 kk, i64 
   return launch_dgemm(L, false, true, r, c, 2 * b, -1.0, w.Acat, r, w.Bt, c, 1.0, X + kk, ldx, nullptr, 0);
 }
 
+// RUTV_USTREAM=0 keeps the U update on the main stream (comparison only)
+bool ustream_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_USTREAM");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 // RUTV_FUSE_LEFT=0 restores the separate S5 / S7 passes over T (comparison only)
 bool fuse_left() {
   static int v = -1;
@@ -304,6 +314,11 @@ struct Problem {
   Launch vl;              // V stream (oneshot GEMMs); vl.stream == nullptr: V on the main stream
   cudaEvent_t eWv, eV;
   bool reorth = false;    // RANDUTV_REORTH: orthonormal Y, Z between power steps (NEXT-4)
+  // U update on the V stream (after the V update of the same step): it overlaps
+  // the next step's sampling, S4 QR and S5; the next S6 (overwrites W_U, T_U),
+  // the side stream's U fold and the final step wait for eU
+  bool ustream = false;
+  cudaEvent_t eWu = nullptr, eU = nullptr;
 };
 
 
@@ -361,6 +376,7 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   // S1, S2, S3
   RUTV_TRY(launch_gaussian(L, P.seed, i, r, b, w.G, r));
   RUTV_TRY(launch_dgemm(L, true, false, s, b, r, 1.0, At, P.ldt, w.G, r, 0.0, w.Y, s, w.gemm_ws, w.gemm_ws_elems));
+  if (P.reorth && P.ustream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eU, 0));  // W_U, T_U are reused below
   for (int qq = 0; qq < P.q; ++qq) {
     if (P.reorth) RUTV_TRY(orthonormalize(L, w, s, b, w.Y));
     RUTV_TRY(launch_dgemm(L, false, false, r, b, s, 1.0, At, P.ldt, w.Y, s, 0.0, w.Z, r, w.gemm_ws,
@@ -423,12 +439,25 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
     RUTV_TRY(launch_dgemm(L, false, false, r, b, b, 1.0, w.Z + kk, m, w.TV, b, 0.0, w.Z2 + kk, m, nullptr, 0));
     if (pk > 0) RUTV_TRY(launch_dgemm(L, false, true, pk, b, b, -1.0, w.Z2, m, w.Wv, s, 1.0, Tk, P.ldt, nullptr, 0));
     RUTV_TRY(launch_dgemm(L, false, true, r, b, b, -1.0, w.Z2 + kk, m, w.Wv, s, 1.0, Tk + kk, P.ldt, nullptr, 0));
+    if (P.ustream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eU, 0));  // the previous U update read W_U, T_U
     RUTV_TRY(panel_qr(L, r, b, At, P.ldt, w.tauU, w.Wu, r, w.TU, b, w.qw));
     RUTV_TRY(launch_triu(L, b, b, At, P.ldt));
     RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, P.ldt));
     RUTV_TRY(fused_right_left(L, w, m, r, b, kk, s - b, P.T + (kk + b) * P.ldt, P.ldt, w.Wv + b, s, w.Z2, m, w.Wu, r,
                               w.TU, b, pk));
-    if (P.U) RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
+    if (P.U && P.ustream) {
+      RUTV_CUDA(cudaEventRecord(P.eWu, L.stream));
+      RUTV_CUDA(cudaStreamWaitEvent(P.vl.stream, P.eWu, 0));
+      Work wu = w;
+      wu.Z = w.Zv;
+      wu.Z2 = w.Zv2;
+      wu.gemm_ws = w.gemm_ws_v;
+      wu.gemm_ws_elems = 4 * (m > n ? m : n) * b;
+      RUTV_TRY(apply_right(P.vl, wu, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
+      RUTV_CUDA(cudaEventRecord(P.eU, P.vl.stream));
+    } else if (P.U) {
+      RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
+    }
     {
       const size_t pe = L.pbegin();
       RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
@@ -447,6 +476,7 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   RUTV_CUDA(cudaEventRecord(P.eR, L.stream));
   RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eR, 0));
   if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eV, 0));
+  if (P.ustream) RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eU, 0));
   RUTV_TRY(svd_and_fold(P.side, w, P, kk, b, (int)(i + 1)));
   if (P.record_lefts) RUTV_TRY(record_left_us(P.side, w, P, (int)i, b));
   RUTV_CUDA(cudaEventRecord(P.eF, P.side.stream));
@@ -462,6 +492,7 @@ int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
     const size_t pe = L.pbegin();
     RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));  // previous step's folds
     if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
+    if (P.ustream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eU, 0));
     L.pend(PK_OTHER, 0.0, 0.0, pe);
   }
   if (tall) {
@@ -485,6 +516,7 @@ int run_loop(const Launch& L, Work& w, const Problem& P, i64 nsteps, bool with_f
   if (with_final) RUTV_TRY(final_step(L, w, P, nsteps));
   RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
   if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
+  if (P.ustream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eU, 0));
   return 0;
 }
 
@@ -504,6 +536,8 @@ int begin_call(randutv_ctx* ctx) {
     RUTV_CUDA(cudaStreamCreateWithPriority(&ctx->vstr, cudaStreamNonBlocking, lo));
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eWv, cudaEventDisableTiming));
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eV, cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eWu, cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eU, cudaEventDisableTiming));
   }
   return 0;
 }
@@ -587,6 +621,8 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
     cudaStreamSynchronize(ctx->vstr);
     cudaEventDestroy(ctx->eWv);
     cudaEventDestroy(ctx->eV);
+    cudaEventDestroy(ctx->eWu);
+    cudaEventDestroy(ctx->eU);
     cudaStreamDestroy(ctx->vstr);
   }
   if (ctx->side) {
@@ -698,6 +734,9 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
   Problem P{m, n, bb, q, seed, T, ldt, uv ? U : nullptr, ldu, uv ? V : nullptr, ldv, false,
             ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
   P.reorth = (flags & RANDUTV_REORTH) != 0;
+  P.ustream = P.U && P.vl.stream && ustream_on();
+  P.eWu = ctx->eWu;
+  P.eU = ctx->eU;
   const i64 nsamp = sampled_steps(n, bb);
   RUTV_TRY(run_loop(L, w, P, nsamp, true));
   const int st = finish(ctx, w);
