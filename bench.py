@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--cache-gib", type=float, default=None,
                    help="device panel cache for --mode host (default: a quarter of A)")
     p.add_argument("--no-uv", action="store_true", help="T only (the paper's 'no orthonormal matrices')")
+    p.add_argument("--no-graph", dest="graph", action="store_false",
+                   help="time eager calls instead of replays of one captured RANDUTV_ASYNC factorisation "
+                        "(CUDA graph; the default for full single-GPU factorisations)")
     p.add_argument("--reorth", action="store_true",
                    help="RANDUTV_REORTH: re-orthonormalised power steps (NEXT-4; extra QRs not in the flop model)")
     p.add_argument("--algo", default="randutv", choices=["randutv", "hqrrp"],
@@ -301,6 +304,34 @@ def run_ours(args):
         for _ in range(args.warmup):
             step()
     torch.cuda.synchronize()
+    graph_launches = None
+    if args.graph and (sharded or trunc_k is not None):
+        args.graph = False  # graphs are captured for the full single-GPU factorisation only
+    if args.graph:
+        # the whole factorisation (main, side and V streams) as one CUDA graph
+        g = torch.cuda.CUDAGraph()
+        ctx.reset_stats()
+        if not args.no_profile:
+            # the per-launch events are captured too: every replay re-records them
+            # and randutv_wait collects the last replay's (one step's) durations
+            ctx.set_profiling(True)
+        try:
+            with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+                ctx.randutv_factor_ex(A, b, q, seed, U=U, T=T, V=V, flags=fl | 8)  # RANDUTV_ASYNC
+            graph_launches = ctx.stats()["kernel_launches"]
+            with torch.cuda.stream(stream):
+                g.replay()
+            torch.cuda.synchronize()
+
+            def step():
+                g.replay()
+        except Exception as ex:  # keep the run: eager calls instead
+            print(f"bench: CUDA-graph capture failed ({ex}); timing eager calls", file=sys.stderr)
+            torch.cuda.synchronize()
+            ctx.close()
+            ctx = Context(dev, stream)
+            args.graph = False
+            graph_launches = None
 
     def barrier():
         if sharded:
@@ -308,7 +339,7 @@ def run_ours(args):
 
     clocks = ClockSampler(dev)
     ctx.reset_stats()
-    if not args.no_profile:
+    if not args.no_profile and not args.graph:
         ctx.set_profiling(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -330,7 +361,10 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     stats = ctx.stats()
+    if args.graph and not args.no_profile:
+        ctx.wait()  # collects the captured events of the last replay
     prof = ctx.profile() if not args.no_profile else None
+    psteps = 1 if args.graph else args.steps  # steps the profile covers
     ctx.set_profiling(False)
     ms_step = ms / args.steps
     value = F * args.steps / (ms * 1e-3) / 1e9   # one factorisation per step, whole job
@@ -409,7 +443,11 @@ def run_ours(args):
         roof = None
         if prof and prof["dgemm"]["ms"] > 0:
             g = prof["dgemm"]
-            ach = g["flops"] / (g["ms"] * 1e-3) / 1e12
+            # DGEMM launches of the main, V (and side) streams overlap: the time
+            # the kernel ran is the UNION of their event spans (busy_ms); the
+            # summed spans (ms) count concurrent launches twice
+            busy = g.get("busy_ms") or g["ms"]
+            ach = g["flops"] / (busy * 1e-3) / 1e12
             traffic = None
             try:
                 tr = json.load(open(NCU_TRAFFIC_FILE))
@@ -420,11 +458,14 @@ def run_ours(args):
             roof = {"bound": "tensor", "achieved": round(ach, 3), "peak": peak, "unit": "TFLOP/s",
                     "frac": round(ach / peak, 4), "traffic": traffic,
                     "kernel": "dgemm_kernel (mma.sync.m8n8k4.f64 / DMMA)",
-                    "launches": g["launches"], "kernel_ms_per_step": g["ms"] / args.steps,
-                    "kernel_share_of_step": round(g["ms"] / ms, 4),
+                    "launches": g["launches"], "kernel_ms_per_step": round(busy / psteps, 3),
+                    "kernel_share_of_step": round(busy / psteps / ms_step, 4),
+                    "summed_launch_spans_ms_per_step": round(g["ms"] / psteps, 3),
+                    "timing": "CUDA events around every launch inside the timed region; achieved = sum 2MNK / "
+                              "union of the launch spans across streams",
                     "peak_source": peak_src,
                     "algorithmic": "2*M*N*K flops per GEMM launch (SURVEY.md §8(d) M3 terms)"}
-            roof["other_kernels"] = {k: {"ms_per_step": v["ms"] / args.steps, "launches": v["launches"]}
+            roof["other_kernels"] = {k: {"ms_per_step": v["ms"] / psteps, "launches": v["launches"]}
                                      for k, v in prof.items() if k != "dgemm"}
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
@@ -432,11 +473,14 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(config_dict(args.config, ws, sharded),
                            **({"reorth": True, "note": "re-orthonormalised power steps; their QRs are not in flops_per_step"}
-                              if args.reorth else {})),
+                              if args.reorth else {}),
+                           **({"cuda_graph": "one captured RANDUTV_ASYNC factorisation replayed per step"}
+                              if args.graph else {})),
             "t_over_n3_x1e10": ms_step * 1e-3 / float(n) ** 3 * 1e10,
             "frac_of_fp64_peak": round(value / ws / 1e3 / peak, 4),   # of N x per-GPU peak
-            "gpu_launches": stats["kernel_launches"],
-            "gpu_launches_per_step": stats["kernel_launches"] / args.steps,
+            "gpu_launches": stats["kernel_launches"] if graph_launches is None else graph_launches * args.steps,
+            "gpu_launches_per_step": (stats["kernel_launches"] / args.steps) if graph_launches is None
+            else graph_launches,
             "clocks": clocks.summary(),
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -67,6 +67,13 @@ extern "C" {
  * randutv_factor_ex, randutv_factor_rank and randutv_factor_tol; the
  * host-streamed and sharded entries reject it (-9). */
 #define RANDUTV_REORTH        4u
+/* randutv_factor_ex only: enqueue the whole factorisation on the ctx stream
+ * (and the ctx's side / V streams, joined back into it) and return without
+ * synchronising; randutv_wait gives the status.  The call then contains no
+ * host synchronisation, so after one warm-up call (which sizes the
+ * workspace) it can be captured into a CUDA graph on the ctx stream and
+ * replayed.  Not combinable with RANDUTV_CHECK_FINITE (-9). */
+#define RANDUTV_ASYNC         8u
 
 typedef struct randutv_ctx randutv_ctx;
 
@@ -143,6 +150,10 @@ RANDUTV_API int randutv_factor_tol(randutv_ctx* ctx, int64_t m, int64_t n, const
                                    double* Tk, int64_t ldt, double* V, int64_t ldv, int64_t* k_out,
                                    double* resid_fro);
 
+/* Synchronise the ctx stream and return the status of the last RANDUTV_ASYNC
+ * factorisation (0, or the 1-based block of a non-converged SVD). */
+RANDUTV_API int randutv_wait(randutv_ctx* ctx);
+
 RANDUTV_API const char* randutv_status_string(int status);
 /* Last CUDA error message seen by any call of this thread ("" if none). */
 RANDUTV_API const char* randutv_last_error(void);
@@ -164,6 +175,9 @@ typedef struct randutv_profile {
   double ms;         /* summed event-to-event device time                    */
   double flops;      /* summed algorithmic flops of those launches           */
   double bytes;      /* summed compulsory bytes (operands read + C written)  */
+  double busy_ms;    /* union of the launches' event spans: time during which at
+                        least one launch of this kind ran (launches on the main,
+                        side and V streams overlap, so busy_ms <= ms)             */
 } randutv_profile;
 RANDUTV_API int randutv_set_profiling(randutv_ctx* ctx, int enable);
 RANDUTV_API int randutv_get_profile(randutv_ctx* ctx, int kind, randutv_profile* out);

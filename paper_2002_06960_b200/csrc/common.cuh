@@ -40,6 +40,7 @@ struct Profiler {
   double ms[PK_COUNT] = {0};
   double flops[PK_COUNT] = {0};
   double bytes[PK_COUNT] = {0};
+  double busy_ms[PK_COUNT] = {0};  // union of the launch spans per kind
   size_t begin(cudaStream_t s);
   void end(cudaStream_t s, int kind, double fl, double by, size_t e0, int64_t m = 0, int64_t n = 0, int64_t k = 0);
   void collect();  // after the stream is synchronised

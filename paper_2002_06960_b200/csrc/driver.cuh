@@ -32,6 +32,8 @@ struct randutv_ctx {
   // multi-GPU communicators (randutv_comm_init): main-stream and side-stream
   rutv::Comm* comm;
   rutv::Comm* comm_side;
+  // device status word of the last RANDUTV_ASYNC call (randutv_wait)
+  int* async_status;
   // GEMM tile-scheduler counters: [0..1] main stream, [2..3] side stream (zeroed once)
   int* sched;
   rutv::Launch launch() { return rutv::Launch{stream, &stats.kernel_launches, sms, &prof, sched}; }

@@ -1,3 +1,4 @@
+#include <algorithm>
 // randUTV driver and C ABI (include/randutv.h).
 //
 // The host side of the hot path: one right-looking loop over column blocks of
@@ -53,7 +54,13 @@ size_t Profiler::begin(cudaStream_t s) {
     }
     pool.push_back(e);
   }
-  cudaEventRecord(pool[used], s);
+  // inside a CUDA-graph capture a plain record only orders streams; an
+  // external record becomes an event-record node that every replay re-records
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(pool[used], s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(pool[used], s);
   return used++;
 }
 
@@ -67,12 +74,16 @@ void Profiler::collect() {
   // RUTV_PROF_DUMP=<file>: append one line per recorded launch (tuning only)
   static const char* dump = getenv("RUTV_PROF_DUMP");
   FILE* f = dump ? fopen(dump, "a") : nullptr;
+  // spans relative to the first record's start, for the union per kind
+  std::vector<std::pair<double, double>> spans[PK_COUNT];
   for (const Rec& r : recs) {
-    float t = 0.f;
-    if (cudaEventElapsedTime(&t, pool[r.e0], pool[r.e1]) != cudaSuccess) {
+    float t = 0.f, t0 = 0.f;
+    if (cudaEventElapsedTime(&t, pool[r.e0], pool[r.e1]) != cudaSuccess ||
+        cudaEventElapsedTime(&t0, pool[recs[0].e0], pool[r.e0]) != cudaSuccess) {
       cudaGetLastError();
       continue;
     }
+    spans[r.kind].push_back({(double)t0, (double)t0 + t});
     if (f) fprintf(f, "%d %lld %lld %lld %.6f %.6e\n", r.kind, (long long)r.shape[0], (long long)r.shape[1],
                    (long long)r.shape[2], t, r.flops);
     launches[r.kind] += 1;
@@ -81,6 +92,22 @@ void Profiler::collect() {
     bytes[r.kind] += r.bytes;
   }
   if (f) fclose(f);
+  for (int k = 0; k < PK_COUNT; ++k) {
+    auto& v = spans[k];
+    std::sort(v.begin(), v.end());
+    double busy = 0.0, lo = 0.0, hi = -1.0;
+    for (auto& iv : v) {
+      if (iv.first > hi) {
+        if (hi > lo) busy += hi - lo;
+        lo = iv.first;
+        hi = iv.second;
+      } else if (iv.second > hi) {
+        hi = iv.second;
+      }
+    }
+    if (hi > lo) busy += hi - lo;
+    busy_ms[k] += busy;
+  }
   recs.clear();
   used = 0;
 }
@@ -90,7 +117,7 @@ void Profiler::reset() {
   used = 0;
   for (int k = 0; k < PK_COUNT; ++k) {
     launches[k] = 0;
-    ms[k] = flops[k] = bytes[k] = 0.0;
+    ms[k] = flops[k] = bytes[k] = busy_ms[k] = 0.0;
   }
 }
 
@@ -319,7 +346,15 @@ struct Problem {
   // the side stream's U fold and the final step wait for eU
   bool ustream = false;
   cudaEvent_t eWu = nullptr, eU = nullptr;
+  // events recorded during THIS call: waits on the others are skipped (a wait
+  // on an event recorded before a CUDA-graph capture began is not capturable)
+  mutable bool rec_f = false, rec_v = false, rec_u = false;
 };
+
+int wait_if(cudaStream_t s, cudaEvent_t e, bool recorded) {
+  if (recorded) RUTV_CUDA(cudaStreamWaitEvent(s, e, 0));
+  return 0;
+}
 
 
 // S8 + S9 for a bw x bw diagonal block at (kk, kk).  `B` is the block to
@@ -376,7 +411,7 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   // S1, S2, S3
   RUTV_TRY(launch_gaussian(L, P.seed, i, r, b, w.G, r));
   RUTV_TRY(launch_dgemm(L, true, false, s, b, r, 1.0, At, P.ldt, w.G, r, 0.0, w.Y, s, w.gemm_ws, w.gemm_ws_elems));
-  if (P.reorth && P.ustream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eU, 0));  // W_U, T_U are reused below
+  if (P.reorth && P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));  // W_U, T_U are reused below
   for (int qq = 0; qq < P.q; ++qq) {
     if (P.reorth) RUTV_TRY(orthonormalize(L, w, s, b, w.Y));
     RUTV_TRY(launch_dgemm(L, false, false, r, b, s, 1.0, At, P.ldt, w.Y, s, 0.0, w.Z, r, w.gemm_ws,
@@ -386,7 +421,7 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
                           w.gemm_ws_elems));
   }
   // S4 (overwrites W_V, T_V: the previous step's V update must have read them)
-  if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
+  if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
   RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
   // S5 for V(:, k:n): it does not touch T, so it needs no fold event; on the V
   // stream it overlaps the QR of the column block and the T/U updates
@@ -401,6 +436,7 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
       wv.gemm_ws_elems = 4 * n * b;
       RUTV_TRY(apply_right(P.vl, wv, n, s, b, P.V + kk * P.ldv, P.ldv, w.Wv, s, w.TV, b));
       RUTV_CUDA(cudaEventRecord(P.eV, P.vl.stream));
+      P.rec_v = true;
     } else {
       RUTV_TRY(apply_right(L, w, n, s, b, P.V + kk * P.ldv, P.ldv, w.Wv, s, w.TV, b));
     }
@@ -410,7 +446,7 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
     // written by the side stream's U_s^T T12 fold of step i-1: wait for it
     // (the stall is recorded as profile kind PK_OTHER, "fold wait").
     const size_t pe = L.pbegin();
-    RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
+    RUTV_TRY(wait_if(L.stream, P.eF, P.rec_f));
     L.pend(PK_OTHER, 0.0, 0.0, pe);
     RUTV_TRY(apply_right(L, w, m, s, b, P.T + kk * P.ldt, P.ldt, w.Wv, s, w.TV, b));
     // S6: QR of the column block in place; keep R, zero below
@@ -439,7 +475,7 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
     RUTV_TRY(launch_dgemm(L, false, false, r, b, b, 1.0, w.Z + kk, m, w.TV, b, 0.0, w.Z2 + kk, m, nullptr, 0));
     if (pk > 0) RUTV_TRY(launch_dgemm(L, false, true, pk, b, b, -1.0, w.Z2, m, w.Wv, s, 1.0, Tk, P.ldt, nullptr, 0));
     RUTV_TRY(launch_dgemm(L, false, true, r, b, b, -1.0, w.Z2 + kk, m, w.Wv, s, 1.0, Tk + kk, P.ldt, nullptr, 0));
-    if (P.ustream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eU, 0));  // the previous U update read W_U, T_U
+    if (P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));  // the previous U update read W_U, T_U
     RUTV_TRY(panel_qr(L, r, b, At, P.ldt, w.tauU, w.Wu, r, w.TU, b, w.qw));
     RUTV_TRY(launch_triu(L, b, b, At, P.ldt));
     RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, P.ldt));
@@ -455,12 +491,13 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
       wu.gemm_ws_elems = 4 * (m > n ? m : n) * b;
       RUTV_TRY(apply_right(P.vl, wu, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
       RUTV_CUDA(cudaEventRecord(P.eU, P.vl.stream));
+      P.rec_u = true;
     } else if (P.U) {
       RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
     }
     {
       const size_t pe = L.pbegin();
-      RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
+      RUTV_TRY(wait_if(L.stream, P.eF, P.rec_f));
       L.pend(PK_OTHER, 0.0, 0.0, pe);
     }
     if (pb > 0) {
@@ -475,11 +512,12 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   // S8, S9 on the side stream, overlapping S1-S4 of step i+1
   RUTV_CUDA(cudaEventRecord(P.eR, L.stream));
   RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eR, 0));
-  if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eV, 0));
-  if (P.ustream) RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eU, 0));
+  if (P.V && P.vl.stream) RUTV_TRY(wait_if(P.side.stream, P.eV, P.rec_v));
+  if (P.ustream) RUTV_TRY(wait_if(P.side.stream, P.eU, P.rec_u));
   RUTV_TRY(svd_and_fold(P.side, w, P, kk, b, (int)(i + 1)));
   if (P.record_lefts) RUTV_TRY(record_left_us(P.side, w, P, (int)i, b));
   RUTV_CUDA(cudaEventRecord(P.eF, P.side.stream));
+  P.rec_f = true;
   return 0;
 }
 
@@ -490,9 +528,9 @@ int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   const bool tall = r > s;
   {
     const size_t pe = L.pbegin();
-    RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));  // previous step's folds
-    if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
-    if (P.ustream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eU, 0));
+    RUTV_TRY(wait_if(L.stream, P.eF, P.rec_f));  // previous step's folds
+    if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
+    if (P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));
     L.pend(PK_OTHER, 0.0, 0.0, pe);
   }
   if (tall) {
@@ -514,9 +552,9 @@ int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
 int run_loop(const Launch& L, Work& w, const Problem& P, i64 nsteps, bool with_final) {
   for (i64 i = 0; i < nsteps; ++i) RUTV_TRY(sampled_step(L, w, P, i));
   if (with_final) RUTV_TRY(final_step(L, w, P, nsteps));
-  RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
-  if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
-  if (P.ustream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eU, 0));
+  RUTV_TRY(wait_if(L.stream, P.eF, P.rec_f));
+  if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
+  if (P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));
   return 0;
 }
 
@@ -673,6 +711,7 @@ RANDUTV_API int randutv_get_profile(randutv_ctx* ctx, int kind, randutv_profile*
   out->ms = ctx->prof.ms[kind];
   out->flops = ctx->prof.flops[kind];
   out->bytes = ctx->prof.bytes[kind];
+  out->busy_ms = ctx->prof.busy_ms[kind];
   return 0;
 }
 
@@ -717,6 +756,7 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
   if (ldt < m) return -13;
   if (uv && !V) return -14;
   if (uv && ldv < n) return -15;
+  if ((flags & RANDUTV_ASYNC) && (flags & RANDUTV_CHECK_FINITE)) return -9;  // the scan synchronises
   const bool alias = (T == A);
   if (alias && ldt != lda) return -13;
   if (!alias && overlaps(A, (size_t)lda * n * 8, T, (size_t)ldt * n * 8)) return -12;
@@ -739,9 +779,28 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
   P.eU = ctx->eU;
   const i64 nsamp = sampled_steps(n, bb);
   RUTV_TRY(run_loop(L, w, P, nsamp, true));
+  if (flags & RANDUTV_ASYNC) {
+    // enqueued only: the status word stays on the device (randutv_wait)
+    ctx->async_status = w.status;
+    ctx->stats.factorizations++;
+    return 0;
+  }
   const int st = finish(ctx, w);
   if (st == 0) ctx->stats.factorizations++;
   return st;
+}
+
+RANDUTV_API int randutv_wait(randutv_ctx* ctx) {
+  if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
+  RUTV_CUDA(cudaSetDevice(ctx->device));
+  RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
+  // per-kernel events of the async call (or of the last replay of a graph
+  // captured with profiling on)
+  if (ctx->prof.on) ctx->prof.collect();
+  if (!ctx->async_status) return 0;
+  int status = 0x7f7f7f7f;
+  RUTV_CUDA(cudaMemcpy(&status, ctx->async_status, sizeof(int), cudaMemcpyDeviceToHost));
+  return status == 0x7f7f7f7f ? 0 : status;
 }
 
 }  // extern "C"
@@ -803,8 +862,8 @@ int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64
     K = done;
     with_final = done == nsamp;
     if (with_final) RUTV_TRY(final_step(L, w, P, nsamp));
-    RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eF, 0));
-    if (P.V && P.vl.stream) RUTV_CUDA(cudaStreamWaitEvent(L.stream, P.eV, 0));
+    RUTV_TRY(wait_if(L.stream, P.eF, P.rec_f));
+    if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
     k = with_final ? n : K * bb;
   }
   const i64 nrec = uv ? K + (with_final ? 1 : 0) : 0;

@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("RUTV_LIB", os.path.join(_HERE, "librandutv.so"))  # R
 RANDUTV_NO_UV = 1
 RANDUTV_CHECK_FINITE = 2
 RANDUTV_REORTH = 4
+RANDUTV_ASYNC = 8
 RANDUTV_ERR_CUDA = 1000
 RANDUTV_ERR_ALLOC = 1001
 RANDUTV_ERR_NONFINITE = 1002
@@ -41,7 +42,7 @@ class Stats(ctypes.Structure):
 
 class Profile(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64), ("ms", ctypes.c_double), ("flops", ctypes.c_double),
-                ("bytes", ctypes.c_double)]
+                ("bytes", ctypes.c_double), ("busy_ms", ctypes.c_double)]
 
 
 class HostReport(ctypes.Structure):
@@ -68,6 +69,7 @@ SIGNATURES = {
     "randutv_hqrrp_rank": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _u64, _uint, _vp, _vp, _i64,
                                   ctypes.POINTER(_dbl)]),
     "randutv_hqrrp_host": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _u64, _uint, _vp, _vp, ctypes.POINTER(HostReport)]),
+    "randutv_wait": (_int, [_vp]),
     "randutv_status_string": (ctypes.c_char_p, [_int]),
     "randutv_last_error": (ctypes.c_char_p, []),
     "randutv_get_stats": (_int, [_vp, ctypes.POINTER(Stats)]),
@@ -223,6 +225,12 @@ class Context:
                                         _ptr(V), _ld(V) if V is not None else 1)
         _check("randutv_factor_ex", st, allow_positive=allow_nonconvergence)
         return U, T, V, st
+
+    def wait(self):
+        """Synchronise; the status of the last RANDUTV_ASYNC factorisation."""
+        st = self.lib.randutv_wait(self.h)
+        _check("randutv_wait", st, allow_positive=True)
+        return st
 
     def randutv_factor_rank(self, A, k, b, q, seed, build_uv=True, flags=0):
         """Truncated randUTV: returns (Uk, Tk, V, rho)."""

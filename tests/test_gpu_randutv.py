@@ -261,3 +261,44 @@ def test_reorth_rejected_by_host_and_dist(ctx):
     st = ctx.lib.randutv_factor_host(ctx.h, 8, 8, Ah.ctypes.data, 8, 4, 1, 1, RANDUTV_REORTH | 1, 0,
                                      None, 8, None, 8, None)
     assert st == -9
+
+
+def test_async_and_cuda_graph_replay():
+    """RANDUTV_ASYNC enqueues without a host sync (randutv_wait gives the status);
+    the call captured into a CUDA graph on the ctx stream replays to the same
+    bits, also on new contents of A."""
+    import torch
+    from paper_2002_06960_b200.randutv import RANDUTV_ASYNC, Context, colmajor
+    s = torch.cuda.Stream()
+    c = Context(0, s)
+    try:
+        m, n, b, q = 300, 260, 32, 1
+        rng = np.random.default_rng(44)
+        A1 = np.asfortranarray(rng.standard_normal((m, n)))
+        A2 = np.asfortranarray(rng.standard_normal((m, n)))
+        A = to_dev(A1)
+        U, T, V = colmajor(m, m), colmajor(m, n), colmajor(n, n)
+        U0, T0, V0, _ = c.randutv_factor_ex(A, b, q, 7)
+        with torch.cuda.stream(s):
+            c.randutv_factor_ex(A, b, q, 7, U=U, T=T, V=V, flags=RANDUTV_ASYNC)
+        assert c.wait() == 0
+        assert torch.equal(T, T0) and torch.equal(U, U0) and torch.equal(V, V0)
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
+            c.randutv_factor_ex(A, b, q, 7, U=U, T=T, V=V, flags=RANDUTV_ASYNC)
+        for X in (U, T, V):
+            X.zero_()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(T, T0) and torch.equal(U, U0) and torch.equal(V, V0)
+        A.copy_(to_dev(A2))
+        g.replay()
+        torch.cuda.synchronize()
+        U2, T2, V2, _ = c.randutv_factor_ex(to_dev(A2), b, q, 7)
+        assert torch.equal(T, T2) and torch.equal(U, U2) and torch.equal(V, V2)
+        o = oracle_randutv(A2, b, q, 7)
+        _check_full(A2, to_np(U), to_np(T), to_np(V), o)
+    finally:
+        c.close()
