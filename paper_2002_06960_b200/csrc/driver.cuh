@@ -32,6 +32,9 @@ struct randutv_ctx {
   // multi-GPU communicators (randutv_comm_init): main-stream and side-stream
   rutv::Comm* comm;
   rutv::Comm* comm_side;
+  // copy stream of the literal host-pointer entry (column blocks drain to the
+  // host while the factorisation runs)
+  cudaStream_t cps;
   // device status word of the last RANDUTV_ASYNC call (randutv_wait)
   int* async_status;
   // GEMM tile-scheduler counters: [0..1] main stream, [2..3] side stream (zeroed once)

@@ -349,6 +349,12 @@ struct Problem {
   // events recorded during THIS call: waits on the others are skipped (a wait
   // on an event recorded before a CUDA-graph capture began is not capturable)
   mutable bool rec_f = false, rec_v = false, rec_u = false;
+  // literal host-pointer entry: column block i of T, U and V is final once the
+  // folds of step i are done (later steps only touch columns >= k + b), so it
+  // is copied to the (pinned) host buffers on `cps` while the next steps run
+  double *hT = nullptr, *hU = nullptr, *hV = nullptr;
+  cudaStream_t cps = nullptr;
+  mutable i64 drained = 0;  // columns of T, U, V already copied
 };
 
 int wait_if(cudaStream_t s, cudaEvent_t e, bool recorded) {
@@ -518,6 +524,18 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   if (P.record_lefts) RUTV_TRY(record_left_us(P.side, w, P, (int)i, b));
   RUTV_CUDA(cudaEventRecord(P.eF, P.side.stream));
   P.rec_f = true;
+  if (P.cps) {
+    RUTV_CUDA(cudaStreamWaitEvent(P.cps, P.eF, 0));
+    RUTV_CUDA(cudaMemcpy2DAsync(P.hT + kk * m, m * 8, P.T + kk * P.ldt, P.ldt * 8, m * 8, b, cudaMemcpyDeviceToHost,
+                                P.cps));
+    if (P.hU)
+      RUTV_CUDA(cudaMemcpy2DAsync(P.hU + kk * m, m * 8, P.U + kk * P.ldu, P.ldu * 8, m * 8, b, cudaMemcpyDeviceToHost,
+                                  P.cps));
+    if (P.hV)
+      RUTV_CUDA(cudaMemcpy2DAsync(P.hV + kk * n, n * 8, P.V + kk * P.ldv, P.ldv * 8, n * 8, b, cudaMemcpyDeviceToHost,
+                                  P.cps));
+    P.drained = kk + b;
+  }
   return 0;
 }
 
@@ -663,6 +681,10 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
     cudaEventDestroy(ctx->eU);
     cudaStreamDestroy(ctx->vstr);
   }
+  if (ctx->cps) {
+    cudaStreamSynchronize(ctx->cps);
+    cudaStreamDestroy(ctx->cps);
+  }
   if (ctx->side) {
     cudaEventDestroy(ctx->eR);
     cudaEventDestroy(ctx->eF);
@@ -739,9 +761,24 @@ RANDUTV_API int randutv_workspace_bytes(int64_t m, int64_t n, int64_t b, int q, 
   return 0;
 }
 
+struct Drain {
+  double *hT, *hU, *hV;  // pinned host T (m x n), U (m x m), V (n x n), ld = rows
+  i64 drained;           // out: columns already copied
+};
+
+static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int q,
+                          uint64_t seed, unsigned flags, double* U, int64_t ldu, double* T, int64_t ldt, double* V,
+                          int64_t ldv, Drain* dr);
+
 RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b,
                                   int q, uint64_t seed, unsigned flags, double* U, int64_t ldu, double* T,
                                   int64_t ldt, double* V, int64_t ldv) {
+  return factor_ex_impl(ctx, m, n, A, lda, b, q, seed, flags, U, ldu, T, ldt, V, ldv, nullptr);
+}
+
+static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int q,
+                          uint64_t seed, unsigned flags, double* U, int64_t ldu, double* T, int64_t ldt, double* V,
+                          int64_t ldv, Drain* dr) {
   RUTV_TRY(begin_call(ctx));
   const bool uv = !(flags & RANDUTV_NO_UV);
   if (n < 1) return -3;
@@ -777,8 +814,21 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
   P.ustream = P.U && P.vl.stream && ustream_on();
   P.eWu = ctx->eWu;
   P.eU = ctx->eU;
+  if (dr && uv) {
+    if (!ctx->cps) RUTV_CUDA(cudaStreamCreateWithFlags(&ctx->cps, cudaStreamNonBlocking));
+    P.cps = ctx->cps;
+    P.hT = dr->hT;
+    P.hU = dr->hU;
+    P.hV = dr->hV;
+  }
   const i64 nsamp = sampled_steps(n, bb);
   RUTV_TRY(run_loop(L, w, P, nsamp, true));
+  if (P.cps) {
+    // the main stream (and so finish) waits for the drained copies too
+    RUTV_CUDA(cudaEventRecord(ctx->eWu, P.cps));
+    RUTV_CUDA(cudaStreamWaitEvent(L.stream, ctx->eWu, 0));
+    dr->drained = P.drained;
+  }
   if (flags & RANDUTV_ASYNC) {
     // enqueued only: the status word stays on the device (randutv_wait)
     ctx->async_status = w.status;
@@ -1016,11 +1066,21 @@ RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t ld
   double* dV = dU + (size_t)m * m;
   RUTV_CUDA(cudaMemcpy2DAsync(dT, m * 8, A, lda * 8, m * 8, n, cudaMemcpyHostToDevice, ctx->stream));
   ctx->stats.h2d_bytes += (int64_t)m * n * 8;
-  int st = randutv_factor_ex(ctx, m, n, dT, m, b, q, seed, 0u, dU, m, dT, m, dV, n);
+  // pinned outputs: column blocks drain to the host during the factorisation
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes a;
+    const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  Drain dr{T, U, V, 0};
+  const bool drain = pinned(T) && pinned(U) && pinned(V);
+  int st = factor_ex_impl(ctx, m, n, dT, m, b, q, seed, 0u, dU, m, dT, m, dV, n, drain ? &dr : nullptr);
   if (st < 0 || st >= 1000) return st;
-  RUTV_CUDA(cudaMemcpyAsync(T, dT, (size_t)m * n * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  RUTV_CUDA(cudaMemcpyAsync(U, dU, (size_t)m * m * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  RUTV_CUDA(cudaMemcpyAsync(V, dV, (size_t)n * n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  const i64 c0 = drain ? dr.drained : 0;  // columns still on the device
+  RUTV_CUDA(cudaMemcpyAsync(T + c0 * m, dT + c0 * m, (size_t)m * (n - c0) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RUTV_CUDA(cudaMemcpyAsync(U + c0 * m, dU + c0 * m, (size_t)m * (m - c0) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  RUTV_CUDA(cudaMemcpyAsync(V + c0 * n, dV + c0 * n, (size_t)n * (n - c0) * 8, cudaMemcpyDeviceToHost, ctx->stream));
   RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->stats.d2h_bytes += (int64_t)((size_t)m * n + (size_t)m * m + (size_t)n * n) * 8;
   return st;

@@ -165,6 +165,13 @@ def test_literal_entry_host_and_device(ctx):
     assert np.array_equal(Th, to_np(Td)) and np.array_equal(Uh, to_np(Ud)) and np.array_equal(Vh, to_np(Vd))
     o = oracle_randutv(A, 32, 1, 77)
     _check_full(A, Uh, Th, Vh, o)
+    # pinned outputs: finished column blocks drain to the host during the run
+    from paper_2002_06960_b200.randutv import pinned_colmajor
+    Up, Tp, Vp = pinned_colmajor(m, m), pinned_colmajor(m, n), pinned_colmajor(n, n)
+    for X in (Up, Tp, Vp):
+        X[:] = np.nan
+    randutv_factor(m, n, A, m, 32, 1, 77, Up, Tp, Vp)
+    assert np.array_equal(Tp, Th) and np.array_equal(Up, Uh) and np.array_equal(Vp, Vh)
 
 
 def test_in_place_alias_and_no_uv(ctx):
