@@ -1,3 +1,4 @@
+#include <cstdlib>
 // K7 -- S8 of SURVEY.md §8(a): SVD of the b x b diagonal block.
 //
 // Paper: "Compute the SVD of (U22(:,1:b))* T22 V22(:,1:b) = U_SVD D V_SVD*"
@@ -51,7 +52,15 @@ struct JacobiPlan {
 
 JacobiPlan plan_for(i64 w) {
   JacobiPlan p;
-  p.nb = w <= 256 ? 16 : 8;
+  p.nb = 8;  // 16 for w <= 256 was measured 15-20 % slower (more CTAs per block round win)
+  {
+    static int env_nb = -1;  // RUTV_JNB: block width override (tuning only)
+    if (env_nb < 0) {
+      const char* e = getenv("RUTV_JNB");
+      env_nb = e ? atoi(e) : 0;
+    }
+    if (env_nb > 0 && 2 * (i64)env_nb * ((w < 1 ? 1 : w) + w + 2 * env_nb) * 8 <= 200 * 1024) p.nb = env_nb;
+  }
   const i64 ww = w < 1 ? 1 : w;
   p.nc = (int)((ww + 2 * p.nb - 1) / (2 * p.nb) * (2 * p.nb));
   p.P = p.nc / p.nb / 2;
