@@ -24,4 +24,6 @@ randutv     O2, O5-O7, O9-O11 the blocked loop and the truncated variant
             (P:549-649, P:651-688, P:1311-1373, P:103-110)
 bruteforce  explicit-matrix mini-oracle for tiny n (forms every H_j, every
             orthogonal factor, and multiplies literally)
+hqrrp       H1-H6 the paper's first method, HQRRP (randomized blocked
+            column-pivoted QR) and its partial variant
 """
