@@ -58,7 +58,7 @@ __device__ __forceinline__ void warp_argmax(double& v, int& c) {
 
 // H3: `steps` steps of CPQR of Y (rows x s, column-major, ld ldy), rows <= 32 RPL.
 // Warp gw owns the columns c with c % NW == gw and keeps no state but its
-// running argmax; lanes hold rows lane + 32 t of one column at a time.  One
+// running argmax; lanes hold rows lane + 32 t of CP_NB columns at a time.  One
 // grid barrier per step: the CTA argmax partials are exchanged through
 // part_* (double-buffered by step parity), then every CTA recomputes the
 // pivot's reflector (dlarfg, P:337-339 / oracle.hqrrp.cpqr_sketch) from the
