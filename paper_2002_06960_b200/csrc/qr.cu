@@ -449,8 +449,16 @@ __global__ void __launch_bounds__(256) t_block_kernel(const double* __restrict__
 // factorisation is bitwise reproducible.
 void leaf_plan(i64 slab_rows, int* G, int* R) {
   const i64 cap1 = (i64)LEAF_MAX_CTAS * LEAF_THREADS;
+  static i64 r2_from = -2;  // RUTV_LEAF_R2_FROM: use 2 rows per thread from this slab height (tuning only)
+  if (r2_from == -2) {
+    const char* e = getenv("RUTV_LEAF_R2_FROM");
+    r2_from = e ? atoll(e) : -1;
+  }
   i64 g;
-  if (slab_rows <= cap1) {
+  if (r2_from > 0 && slab_rows >= r2_from && slab_rows <= 2 * cap1) {
+    *R = 2;
+    g = (slab_rows + 2 * LEAF_THREADS - 1) / (2 * LEAF_THREADS);
+  } else if (slab_rows <= cap1) {
     *R = 1;
     g = (slab_rows + LEAF_THREADS - 1) / LEAF_THREADS;
   } else if (slab_rows <= 2 * cap1) {
