@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--cache-gib", type=float, default=None,
                    help="device panel cache for --mode host (default: a quarter of A)")
     p.add_argument("--no-uv", action="store_true", help="T only (the paper's 'no orthonormal matrices')")
+    p.add_argument("--q", type=int, default=None,
+                   help="--mode host only: override the config's power steps (the paper's Table 1 runs use q = 0)")
     p.add_argument("--no-graph", dest="graph", action="store_false",
                    help="time eager calls instead of replays of one captured RANDUTV_ASYNC factorisation "
                         "(CUDA graph; the default for full single-GPU factorisations)")
@@ -519,6 +521,8 @@ def run_host_streamed(args):
     torch.cuda.set_device(0)
     cfg = CONFIGS[args.config]
     m, n, b, q = cfg["m"], cfg["n"], cfg["b"], cfg["q"]
+    if args.q is not None:
+        q = args.q
     seed = 2000 + int(args.config[1:])
     uv = not args.no_uv
     F = randutv_flops(m, n, b, q, build_uv=uv)
@@ -555,13 +559,17 @@ def run_host_streamed(args):
     real = sum(r["wall_ms"] for r in reps) / len(reps)
     io = sum(r["h2d_ms"] + r["d2h_ms"] for r in reps) / len(reps)
     r0 = reps[-1]
+    cfgd = config_dict(args.config, 1)
     if not uv:
-        cfgd = config_dict(args.config, 1)
         cfgd["workload"] = cfgd["workload"].replace("with U and V", "T only (no orthonormal matrices)")
+    if args.q is not None and args.q != cfg["q"]:
+        cfgd["workload"] = cfgd["workload"].replace(f"q={cfg['q']}", f"q={q}")
+        cfgd["q"] = q
+        cfgd["flops_per_step"] = F
     line = {"metric": METRIC, "value": round(F / (real * 1e-3) / 1e9, 2), "unit": "GFLOP/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(real, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(config_dict(args.config, 1) if uv else cfgd, mode="host-streamed", build_uv=uv, flops_per_step=F,
+            "config": dict(cfgd, mode="host-streamed", build_uv=uv, flops_per_step=F,
                            device_cache_bytes=cache, cache_slots=r0["cache_slots"]),
             "table1": {"computational_time_s": comp_ms * 1e-3, "io_time_s": io * 1e-3, "real_time_s": real * 1e-3,
                        "real_over_comp": real / comp_ms, "comp_over_io": comp_ms / io if io > 0 else None,
