@@ -58,7 +58,12 @@ def householder_qr(P):
         if t != 0.0 and j + 1 < w:
             vf = np.concatenate(([1.0], v))
             wrow = vf @ F[j:, j + 1:]
-            F[j:, j + 1:] -= t * np.outer(vf, wrow)
+            # F[j:, j+1:] -= t * outer(vf, wrow), the outer product built in the
+            # panel's (Fortran) order so the subtraction streams both operands
+            O = np.empty((h - j, w - j - 1), order="F")
+            np.multiply(vf[:, None], wrow[None, :], out=O)
+            O *= t
+            F[j:, j + 1:] -= O
     return F, tau
 
 

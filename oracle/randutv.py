@@ -49,7 +49,7 @@ def sampled_steps(n, b):
     return max(0, -(-(n - b) // b)) if n > b else 0
 
 
-def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reorth=False):
+def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reorth=False, overwrite_a=False):
     """Oracle randUTV of A (m x n, m >= n).
 
     Parameters
@@ -63,6 +63,9 @@ def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reo
     record     : optional dict; receives per-step diagnostics (Y, tau, d, ...)
     reorth     : re-orthonormalise the sample between power steps (SURVEY §8(f)
                  NEXT-4, the alternative to reading A8; see _sample)
+    overwrite_a: T is A itself (A must be a Fortran-ordered float64 array) -- the
+                 paper's in-place factorisation ("T := A"); saves one
+                 copy of A for the full-size parity tests (17-34 GB)
 
     Returns dict with keys U, T, V (full) or Uk, Tk, V, rho (truncated).
     """
@@ -72,7 +75,12 @@ def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reo
         raise ValueError("randUTV assumes m >= n (P:532)")
     if b < 1 or q < 0:
         raise ValueError("need b >= 1, q >= 0")
-    T = np.array(A, order="F", copy=True)
+    if overwrite_a:
+        if not (A.flags.f_contiguous and A.dtype == np.float64):
+            raise ValueError("overwrite_a needs a Fortran-ordered float64 A")
+        T = A
+    else:
+        T = np.array(A, order="F", copy=True)
     forward_u = build_uv and not thin_u
     U = np.eye(m, order="F") if forward_u else None
     V = np.eye(n, order="F") if build_uv else None
@@ -160,11 +168,13 @@ def _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin, record, reorth=False)
     WV = unit_lower(FY)
     TV = larft(WV, tauV)
     # O5: right transform, all m rows of columns kk:n (A2); V likewise
+    # (X -= ... is X := X - ... elementwise; in place only to hold one m x s
+    # temporary at the full sizes)
     X = T[:, kk:]
-    T[:, kk:] = X - ((X @ WV) @ TV) @ WV.T
+    X -= ((X @ WV) @ TV) @ WV.T
     if V is not None:
         XV = V[:, kk:]
-        V[:, kk:] = XV - ((XV @ WV) @ TV) @ WV.T
+        XV -= ((XV @ WV) @ TV) @ WV.T
     # O6: left QR of the leading column block
     FU, tauU = householder_qr(T[kk:, kk:kk + b])
     WU = unit_lower(FU)
@@ -174,10 +184,10 @@ def _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin, record, reorth=False)
     T[kk + b:, kk:kk + b] = 0.0
     # O7: left transform of the trailing columns (A3) and U
     Xl = T[kk:, kk + b:]
-    T[kk:, kk + b:] = Xl - WU @ (TU.T @ (WU.T @ Xl))
+    Xl -= WU @ (TU.T @ (WU.T @ Xl))
     if U is not None:
         XU = U[:, kk:]
-        U[:, kk:] = XU - ((XU @ WU) @ TU) @ WU.T
+        XU -= ((XU @ WU) @ TU) @ WU.T
     # O8, O9
     Us, d, Vs, sweeps = svd_block(R)
     _fold(T, U, V, kk, b, Us, d, Vs)
