@@ -30,9 +30,13 @@
  *   - Status codes (LAPACK "info" style):
  *        0            success
  *       -i            argument i (1-based, in the C signature) is invalid
- *       +j            the Jacobi SVD of diagonal block j (1-based) did not
- *                     converge in 30 sweeps; outputs are undefined
- *       RANDUTV_ERR_* >= 1000: CUDA / allocation / non-finite-input failures
+ *       +j            the Jacobi SVD of diagonal block j (1-based, j < 2^30)
+ *                     did not converge in 30 sweeps; outputs are undefined
+ *       RANDUTV_ERR_* >= RANDUTV_ERR_BASE (2^30): CUDA / allocation /
+ *                     non-finite-input / communicator failures
+ *   - Threads: a ctx is used by one host thread at a time (its workspace,
+ *     streams and events are shared by every call on it); use one ctx per
+ *     thread.  The literal randutv_factor serialises its calls per device.
  *   - No CPU fallback exists: without a CUDA device every compute entry point
  *     returns RANDUTV_ERR_CUDA.
  */
@@ -48,13 +52,18 @@ extern "C" {
 
 #define RANDUTV_API __attribute__((visibility("default")))
 
-/* status codes >= 1000 */
-#define RANDUTV_ERR_CUDA      1000  /* a CUDA runtime call failed (message: randutv_last_error) */
-#define RANDUTV_ERR_ALLOC     1001  /* device workspace allocation failed                      */
-#define RANDUTV_ERR_NONFINITE 1002  /* A holds a NaN/Inf (only with RANDUTV_CHECK_FINITE)       */
-#define RANDUTV_ERR_CTX       1003  /* NULL or destroyed context                                */
-#define RANDUTV_ERR_NCCL      1004  /* NCCL missing or a collective failed (randutv_last_error)   */
-#define RANDUTV_ERR_NOCOMM    1005  /* randutv_factor_dist before randutv_comm_init              */
+/* status codes >= RANDUTV_ERR_BASE (2^30): far above any Jacobi block index
+ * +j (a factorisation has at most n / b <= 2^30 blocks), so the two never
+ * collide */
+#define RANDUTV_ERR_BASE      0x40000000
+#define RANDUTV_ERR_CUDA      (RANDUTV_ERR_BASE + 0)  /* a CUDA runtime call failed (message: randutv_last_error) */
+#define RANDUTV_ERR_ALLOC     (RANDUTV_ERR_BASE + 1)  /* device workspace allocation failed                      */
+#define RANDUTV_ERR_NONFINITE (RANDUTV_ERR_BASE + 2)  /* A holds a NaN/Inf (only with RANDUTV_CHECK_FINITE)       */
+#define RANDUTV_ERR_CTX       (RANDUTV_ERR_BASE + 3)  /* NULL or destroyed context                                */
+#define RANDUTV_ERR_NCCL      (RANDUTV_ERR_BASE + 4)  /* NCCL missing, a collective failed or timed out           */
+#define RANDUTV_ERR_NOCOMM    (RANDUTV_ERR_BASE + 5)  /* randutv_factor_dist before randutv_comm_init              */
+#define RANDUTV_ERR_PEER      (RANDUTV_ERR_BASE + 6)  /* sharded call: another rank failed its argument /
+                                                          workspace checks (agreed before any collective)     */
 
 /* flags */
 #define RANDUTV_NO_UV         1u    /* do not build U and V ("no orthonormal matrices") */
@@ -72,8 +81,19 @@ extern "C" {
  * synchronising; randutv_wait gives the status.  The call then contains no
  * host synchronisation, so after one warm-up call (which sizes the
  * workspace) it can be captured into a CUDA graph on the ctx stream and
- * replayed.  Not combinable with RANDUTV_CHECK_FINITE (-9). */
+ * replayed.  A workspace an ASYNC call has used is never freed before
+ * randutv_destroy: a later call that needs more allocates a new one and the
+ * old one stays valid for graphs captured over it (randutv_destroy
+ * invalidates them).  Not combinable with RANDUTV_CHECK_FINITE (-9). */
 #define RANDUTV_ASYNC         8u
+/* randutv_factor_ex only, m > n: U is the economy m x n factor U(:, 0:n)
+ * (ldu >= m), formed by backward accumulation of the left transforms
+ * (reading A12) -- the paper's m x m U of a tall A is
+ * often too large to hold (c4: 550 GB); A = U T(0:n, :) V^T still holds since
+ * rows n..m-1 of T are zero.  Ignored for m == n.  Costs a record of the
+ * reflectors (~m n doubles of workspace); not combinable with the literal
+ * host-pointer entry. */
+#define RANDUTV_ECON_U        16u
 
 typedef struct randutv_ctx randutv_ctx;
 
@@ -91,6 +111,13 @@ typedef struct randutv_stats {
  * workspace only; destroy it with randutv_destroy. */
 RANDUTV_API int randutv_create(randutv_ctx** ctx, int device, void* stream);
 RANDUTV_API int randutv_destroy(randutv_ctx* ctx);
+/* Per-ctx options.  RANDUTV_OPT_JACOBI_SWEEPS: the Jacobi SVD sweep cap, 1..30
+ * (0 = the default 30 of reading A10); lowering it makes blocks fail to
+ * converge, which is how the +j status path is tested.  Returns 0, -2 (unknown
+ * option) or -3 (value out of range). */
+#define RANDUTV_OPT_JACOBI_SWEEPS 1
+RANDUTV_API int randutv_set_option(randutv_ctx* ctx, int option, int64_t value);
+
 /* Re-bind the ctx to another stream of the same device. */
 RANDUTV_API int randutv_set_stream(randutv_ctx* ctx, void* stream);
 
@@ -113,8 +140,8 @@ RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t ld
 /* Full form on device pointers.
  *   T: m x n (ldt >= m) receives the triangular factor; T may alias A exactly
  *   (T == A and ldt == lda): A is then overwritten; any other overlap is -12.
- *   U: m x m (ldu >= m) and V: n x n (ldv >= n); ignored (may be NULL) with
- *   RANDUTV_NO_UV.
+ *   U: m x m (ldu >= m), or m x n with RANDUTV_ECON_U; V: n x n (ldv >= n);
+ *   both ignored (may be NULL) with RANDUTV_NO_UV.
  * Arguments: 1 ctx, 2 m, 3 n, 4 A, 5 lda, 6 b, 7 q, 8 seed, 9 flags, 10 U, 11 ldu,
  * 12 T, 13 ldt, 14 V, 15 ldv. */
 RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda,
@@ -128,13 +155,20 @@ RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const 
  *   Tk: k x n (ldt >= k) = T(0:k, :)
  *   V : n x n (ldv >= n)
  *   *resid_fro (host) = ||T(k:m, k:n)||_F = ||A - Uk Tk V^T||_F
+ *   *resid_2 (host, may be NULL = not computed) = ||A - Uk Tk V^T||_2 =
+ *       sigma_1 of T(k:m, k:n) (SURVEY.md §8(c) reading A11): exact (QR +
+ *       Jacobi SVD) when n - k <= 512; otherwise the Rayleigh-Ritz value of a
+ *       512-column block Krylov space (block 32) -- a lower bound whose error
+ *       decays with the gap sigma_1 / sigma_33 of the trailing block.  -1 if
+ *       the small SVD did not converge.  Costs 32 pairs of skinny products
+ *       with the trailing block.
  * Uk and V may be NULL with RANDUTV_NO_UV.  A is read only.
  * Arguments: 1 ctx, 2 m, 3 n, 4 A, 5 lda, 6 k, 7 b, 8 q, 9 seed, 10 flags, 11 Uk,
- * 12 ldu, 13 Tk, 14 ldt, 15 V, 16 ldv, 17 resid_fro. */
+ * 12 ldu, 13 Tk, 14 ldt, 15 V, 16 ldv, 17 resid_fro, 18 resid_2. */
 RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda,
                                     int64_t k, int64_t b, int q, uint64_t seed, unsigned flags,
                                     double* Uk, int64_t ldu, double* Tk, int64_t ldt, double* V, int64_t ldv,
-                                    double* resid_fro);
+                                    double* resid_fro, double* resid_2);
 
 /* Adaptive-rank variant (P:155-157 on why partial
  * methods otherwise need k up front): sampled steps run until the trailing

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
 #include <vector>
 
@@ -59,6 +60,9 @@ struct Launch {
   // one CTA per GEMM tile (no persistent grid): kernels on a concurrent stream,
   // whose CTAs must retire tile by tile so other streams' kernels get SMs
   bool oneshot = false;
+  // Jacobi SVD sweep cap (randutv_set_option RANDUTV_OPT_JACOBI_SWEEPS; 30 =
+  // reading A10); lower it only to exercise the non-convergence status
+  int jacobi_max_sweeps = 30;
   void count(int n = 1) const {
     if (counter) *counter += n;
   }
@@ -84,6 +88,22 @@ struct Launch {
       ::rutv::set_last_error(where, e__);                       \
       return RANDUTV_ERR_CUDA;                                  \
     }                                                           \
+  } while (0)
+
+// Kernel function attributes (dynamic shared memory opt-in, cluster sizes)
+// belong to a device context: `stmt` runs once per (call site, device), so a
+// process driving several GPUs opts in on each; concurrent first calls may
+// both run it (idempotent).  Devices >= 64 run it every time.
+#define RUTV_ONCE_PER_DEVICE(stmt)                                              \
+  do {                                                                          \
+    static std::atomic<uint64_t> once__{0};                                     \
+    int d__ = 0;                                                                \
+    RUTV_CUDA(cudaGetDevice(&d__));                                             \
+    const uint64_t bit__ = (d__ >= 0 && d__ < 64) ? (1ull << d__) : 0ull;       \
+    if (!bit__ || !(once__.load(std::memory_order_acquire) & bit__)) {          \
+      stmt;                                                                     \
+      if (bit__) once__.fetch_or(bit__, std::memory_order_acq_rel);            \
+    }                                                                           \
   } while (0)
 
 #define RUTV_TRY(expr)                                          \

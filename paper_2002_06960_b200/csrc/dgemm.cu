@@ -483,12 +483,8 @@ template <class CF, bool TA, bool TB, int VA, int VB, bool CPF>
 int launch_t(const Launch& L, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
              i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
   const int splits = (int)((K + kchunk - 1) / (kchunk > 0 ? kchunk : 1));
-  static bool attr_set = false;  // per instantiation; first call from any ctx
-  if (!attr_set) {
-    RUTV_CUDA(cudaFuncSetAttribute(dgemm_kernel<CF, TA, TB, VA, VB, CPF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)CF::SMEM_BYTES));
-    attr_set = true;
-  }
+  RUTV_ONCE_PER_DEVICE(RUTV_CUDA(cudaFuncSetAttribute(
+      dgemm_kernel<CF, TA, TB, VA, VB, CPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM_BYTES)));
   dgemm_kernel<CF, TA, TB, VA, VB, CPF><<<grid, CF::THREADS, CF::SMEM_BYTES, L.stream>>>(M, N, K, alpha, A, lda, B, ldb,
                                                                                beta, C, ldc, kchunk, splits < 1 ? 1 : splits, part,
                                                                                use_sched(L) ? L.sched : nullptr);

@@ -40,6 +40,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -87,7 +88,17 @@ struct Layout {
 
 struct Comm {
   int rank = 0, nranks = 1;
-  virtual ~Comm() {}
+  int* dflag = nullptr;  // one device int for the pre-collective agreement (agree())
+  virtual ~Comm() {
+    if (dflag) cudaFree(dflag);
+  }
+  // wait for stream `s`, whose work includes this communicator's collectives:
+  // NCCL polls the communicator's asynchronous error state and aborts it on
+  // an error or after the timeout instead of blocking forever on a dead peer
+  virtual int sync(cudaStream_t s) {
+    RUTV_CUDA(cudaStreamSynchronize(s));
+    return 0;
+  }
   virtual int allreduce_sum(double* buf, i64 count, cudaStream_t s) = 0;
   // recv holds nranks * count doubles, rank q's block at q * count
   virtual int allgather(const double* send, double* recv, i64 count, cudaStream_t s) = 0;
@@ -109,6 +120,8 @@ struct NcclApi {
   decltype(&ncclAllGather) AllGather;
   decltype(&ncclBroadcast) Broadcast;
   decltype(&ncclGetErrorString) GetErrorString;
+  decltype(&ncclCommGetAsyncError) GetAsyncError;
+  decltype(&ncclCommAbort) CommAbort;
 };
 
 static std::mutex g_nccl_mu;
@@ -139,6 +152,8 @@ const NcclApi* nccl_api() {
   RUTV_SYM(AllGather, "ncclAllGather");
   RUTV_SYM(Broadcast, "ncclBroadcast");
   RUTV_SYM(GetErrorString, "ncclGetErrorString");
+  RUTV_SYM(GetAsyncError, "ncclCommGetAsyncError");
+  RUTV_SYM(CommAbort, "ncclCommAbort");
 #undef RUTV_SYM
   g_nccl.ok = true;
   return &g_nccl;
@@ -154,29 +169,86 @@ const NcclApi* nccl_api() {
     }                                                                                        \
   } while (0)
 
+// RUTV_NCCL_TIMEOUT_S: seconds a sharded call may wait on its collectives
+// before aborting the communicator (default 1800; <= 0 waits forever)
+static double nccl_timeout_s() {
+  static double t = -1.0;
+  if (t < 0.0) {
+    const char* e = getenv("RUTV_NCCL_TIMEOUT_S");
+    t = e ? atof(e) : 1800.0;
+    if (t < 0.0) t = 0.0;
+  }
+  return t;
+}
+
 struct NcclComm : Comm {
   const NcclApi* api;
   ncclComm_t comm = nullptr;
+  NcclComm* partner = nullptr;  // the side-stream communicator split from this one
   ~NcclComm() override {
     if (comm) api->CommDestroy(comm);
   }
+  // abort this communicator and its partner: a collective of either may be
+  // the one stuck on a dead peer
+  void abort_all() {
+    if (comm) api->CommAbort(comm);
+    comm = nullptr;
+    if (partner && partner->comm) {
+      api->CommAbort(partner->comm);
+      partner->comm = nullptr;
+    }
+  }
+  int sync(cudaStream_t s) override {
+    const double limit = nccl_timeout_s();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q == cudaSuccess) return 0;
+      if (q != cudaErrorNotReady) {
+        ::rutv::set_last_error("cudaStreamQuery (sharded call)", q);
+        return RANDUTV_ERR_CUDA;
+      }
+      ncclResult_t ae = ncclSuccess;
+      if (api->GetAsyncError(comm, &ae) != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress)) {
+        snprintf(g_nccl_err, sizeof(g_nccl_err), "NCCL asynchronous error: %s (communicator aborted)",
+                 api->GetErrorString(ae));
+        ::rutv::set_last_error(g_nccl_err, cudaErrorUnknown);
+        abort_all();
+        return RANDUTV_ERR_NCCL;
+      }
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (limit > 0.0 && el > limit) {
+        snprintf(g_nccl_err, sizeof(g_nccl_err),
+                 "sharded call still waiting on its collectives after %.0f s (RUTV_NCCL_TIMEOUT_S): "
+                 "communicator aborted", el);
+        ::rutv::set_last_error(g_nccl_err, cudaErrorUnknown);
+        abort_all();
+        return RANDUTV_ERR_NCCL;
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(el < 0.01 ? 20 : 500));
+    }
+  }
   int allreduce_sum(double* buf, i64 count, cudaStream_t s) override {
     if (count <= 0) return 0;
+    if (!comm) return RANDUTV_ERR_NCCL;
     RUTV_NCCL(api->AllReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, comm, s));
     return 0;
   }
   int allgather(const double* send, double* recv, i64 count, cudaStream_t s) override {
     if (count <= 0) return 0;
+    if (!comm) return RANDUTV_ERR_NCCL;
     RUTV_NCCL(api->AllGather(send, recv, (size_t)count, ncclFloat64, comm, s));
     return 0;
   }
   int bcast(double* buf, i64 count, int root, cudaStream_t s) override {
     if (count <= 0) return 0;
+    if (!comm) return RANDUTV_ERR_NCCL;
     RUTV_NCCL(api->Broadcast(buf, buf, (size_t)count, ncclFloat64, root, comm, s));
     return 0;
   }
   int allreduce_min_int(int* buf, i64 count, cudaStream_t s) override {
     if (count <= 0) return 0;
+    if (!comm) return RANDUTV_ERR_NCCL;
     RUTV_NCCL(api->AllReduce(buf, buf, (size_t)count, ncclInt32, ncclMin, comm, s));
     return 0;
   }
@@ -418,6 +490,7 @@ struct DistProblem {
   double* V;  // rows [v0, v0 + nv) of V (n x n), ld ldv; may be null
   i64 ldv, v0, nv;
   bool record;  // truncated with U_k: keep (W_U, T_U, U_s) of every step
+  bool uv;      // U and V requested (rank-uniform; U / V above are null on ranks without rows)
 };
 
 struct DistRun {
@@ -580,10 +653,9 @@ int dist_final_step(DistRun& R, i64 i) {
       RUTV_TRY(launch_triu(L, s, s, At, R.P.lda));
       RUTV_TRY(launch_fill(L, r - s, s, 0.0, At + s, R.P.lda));
     }
-    if (R.P.U) {
-      RUTV_TRY(R.comm->bcast(R.d.wbuf, r * s + s * s, o, st));
-      RUTV_TRY(apply_right(L, w, R.P.mu, r, s, R.P.U + k * R.P.ldu, R.P.ldu, Wu, r, TU, s));
-    }
+    // participation in the broadcast depends on rank-uniform values only
+    if (R.P.uv) RUTV_TRY(R.comm->bcast(R.d.wbuf, r * s + s * s, o, st));
+    if (R.P.U) RUTV_TRY(apply_right(L, w, R.P.mu, r, s, R.P.U + k * R.P.ldu, R.P.ldu, Wu, r, TU, s));
   }
   return dist_svd_and_fold(R, L, R.comm, i, s, r == s);
 }
@@ -630,6 +702,33 @@ int dist_backward_uk(DistRun& R, i64 K, i64 k) {
   return 0;
 }
 
+// finish() of the sharded path: the wait goes through the communicator
+// (asynchronous-error polling and timeout, NcclComm::sync)
+int dist_finish(DistRun& R) {
+  randutv_ctx* ctx = R.ctx;
+  int status = 0x7f7f7f7f;
+  RUTV_CUDA(cudaMemcpyAsync(&status, R.d.w.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  RUTV_TRY(R.comm->sync(ctx->stream));
+  RUTV_CUDA(cudaGetLastError());
+  if (ctx->prof.on) ctx->prof.collect();
+  return status != 0x7f7f7f7f ? status : 0;
+}
+
+// Agreement before the first collective of a sharded call: every rank
+// contributes whether its own checks passed (argument checks, workspace,
+// finiteness scan); the minimum decides for all, so either every rank enters
+// the collectives or none does.  Returns 1 if every rank is ready.
+int agree(Comm* comm, cudaStream_t s, bool ready, int* all_ready) {
+  if (!comm->dflag) RUTV_CUDA(cudaMalloc(&comm->dflag, sizeof(int)));
+  int h = ready ? 1 : 0;
+  RUTV_CUDA(cudaMemcpyAsync(comm->dflag, &h, sizeof(int), cudaMemcpyHostToDevice, s));
+  RUTV_TRY(comm->allreduce_min_int(comm->dflag, 1, s));
+  RUTV_CUDA(cudaMemcpyAsync(&h, comm->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  RUTV_TRY(comm->sync(s));
+  *all_ready = h;
+  return 0;
+}
+
 // K = -1: full factorisation; K >= 1: truncated after K sampled steps (rank k)
 int dist_run(DistRun& R, i64 K, i64 k, double* resid_fro) {
   const Layout& lay = R.P.lay;
@@ -672,13 +771,13 @@ int dist_run(DistRun& R, i64 K, i64 k, double* resid_fro) {
     double ss = 0.0;
     RUTV_CUDA(cudaMemcpyAsync(&ss, R.d.colss + nl, sizeof(double), cudaMemcpyDeviceToHost, L.stream));
     RUTV_TRY(R.comm->allreduce_min_int(w.status, 1, L.stream));
-    const int st = finish(ctx, w);
+    const int st = dist_finish(R);
     *resid_fro = std::sqrt(ss);
     return st;
   }
   // every rank returns the first non-converged block (status word: min)
   RUTV_TRY(R.comm->allreduce_min_int(w.status, 1, L.stream));
-  return finish(ctx, w);
+  return dist_finish(R);
 }
 
 // argument checks shared by the NCCL and loopback entries; returns 0 or -i
@@ -707,16 +806,17 @@ int dist_check(const Layout& lay, const double* A, i64 lda, int q, unsigned flag
 // rank-k (U_local: rows of U_k, m x k; *resid_fro = ||T(k:m, k:n)||_F)
 int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, double* A, i64 lda, i64 b, int q,
                 uint64_t seed, unsigned flags, double* U, i64 ldu, double* V, i64 ldv, i64 k, double* resid_fro) {
-  Layout lay{m, n, std::min(b, n), comm->nranks, comm->rank, 0};
-  if (b < 1) return -6;
+  Layout lay{m, n, std::max<i64>(1, std::min(b, n)), comm->nranks, comm->rank, 0};
   lay.nblocks = (n + lay.b - 1) / lay.b;
-  RUTV_TRY(dist_check(lay, A, lda, q, flags, U, ldu, V, ldv));
+  // local checks first; no rank returns before the agreement, so a rank whose
+  // arguments or workspace fail never leaves its peers blocked in a collective
+  int local = b < 1 ? -6 : dist_check(lay, A, lda, q, flags, U, ldu, V, ldv);
   const bool uv = !(flags & RANDUTV_NO_UV);
   i64 K = -1;
-  if (k != 0) {
+  if (local == 0 && k != 0) {
     K = (k + lay.b - 1) / lay.b;
-    if (k < 0 || K > sampled_steps(n, lay.b)) return -14;  // truncation needs k <= b * (sampled steps)
-    if (!resid_fro) return -15;
+    if (k < 0 || K > sampled_steps(n, lay.b)) local = -14;  // truncation needs k <= b * (sampled steps)
+    else if (!resid_fro) local = -15;
   }
   DistRun R;
   R.ctx = ctx;
@@ -724,28 +824,33 @@ int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, dou
   R.side_comm = side_comm;
   R.L = ctx->launch();
   R.S = ctx->side_launch();
-  Carver dry{nullptr, 0, 0, true};
-  const size_t need = carve_dist(dry, R.d, lay, K > 0 ? K : 0, k);
-  RUTV_TRY(ensure_ws(ctx, need));
+  if (local == 0) {
+    Carver dry{nullptr, 0, 0, true};
+    const size_t need = carve_dist(dry, R.d, lay, K > 0 ? K : 0, k);
+    local = ensure_ws(ctx, need);
+  }
+  {
+    int all = 0;
+    RUTV_TRY(agree(comm, ctx->stream, local == 0, &all));
+    if (local != 0) return local;
+    if (!all) return RANDUTV_ERR_PEER;
+  }
   Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
   carve_dist(real, R.d, lay, K > 0 ? K : 0, k);
   const i64 u0 = Layout::row0(m, lay.P, lay.p), u1 = Layout::row0(m, lay.P, lay.p + 1);
   const i64 v0 = Layout::row0(n, lay.P, lay.p), v1 = Layout::row0(n, lay.P, lay.p + 1);
   R.P = DistProblem{lay, q, seed, A, lda, uv ? U : nullptr, ldu, u0, u1 - u0, uv ? V : nullptr, ldv, v0, v1 - v0,
-                    uv && K > 0};
+                    uv && K > 0, uv};
   if (R.P.U && R.P.mu == 0) R.P.U = nullptr;
   if (R.P.V && R.P.nv == 0) R.P.V = nullptr;
   if (flags & RANDUTV_CHECK_FINITE) {
     int bad = 0;
     if (lay.ncols(lay.p) > 0) bad = check_finite(ctx, R.L, R.d.w, m, lay.ncols(lay.p), A, lda);
+    // agree on the verdict (a CUDA failure of the scan counts as "not clean")
+    int all = 0;
+    RUTV_TRY(agree(comm, ctx->stream, bad == 0, &all));
     if (bad != 0 && bad != RANDUTV_ERR_NONFINITE) return bad;
-    // agree on the verdict: min over ranks of (0 = bad, 1 = good)
-    int h = bad ? 0 : 1;
-    RUTV_CUDA(cudaMemcpyAsync(R.d.w.flag, &h, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-    RUTV_TRY(comm->allreduce_min_int(R.d.w.flag, 1, ctx->stream));
-    RUTV_CUDA(cudaMemcpyAsync(&h, R.d.w.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (!h) return RANDUTV_ERR_NONFINITE;
+    if (!all) return RANDUTV_ERR_NONFINITE;
   }
   const int st = dist_run(R, K, k, resid_fro);
   if (st == 0) ctx->stats.factorizations++;
@@ -824,6 +929,8 @@ RANDUTV_API int randutv_comm_init(randutv_ctx* ctx, const void* unique_id, int n
     delete c;
     return RANDUTV_ERR_NCCL;
   }
+  c->partner = cs;
+  cs->partner = c;
   ctx->comm = c;
   ctx->comm_side = cs;
   return 0;

@@ -15,6 +15,11 @@ struct randutv_ctx {
   int sms;
   void* ws;
   size_t ws_bytes;
+  // ws was used by a RANDUTV_ASYNC call (maybe captured into a graph): a
+  // growth retires it to `retired` (freed by randutv_destroy) instead of
+  // freeing it under the graph
+  bool ws_captured;
+  std::vector<void*> retired;
   randutv_stats stats;
   // host-staging buffers of the literal (host pointer) entry
   double* stage;
@@ -39,13 +44,20 @@ struct randutv_ctx {
   int* async_status;
   // GEMM tile-scheduler counters: [0..1] main stream, [2..3] side stream (zeroed once)
   int* sched;
-  rutv::Launch launch() { return rutv::Launch{stream, &stats.kernel_launches, sms, &prof, sched}; }
+  int jacobi_max_sweeps;  // 0 = the default 30 (randutv_set_option)
+  rutv::Launch with_opts(rutv::Launch l) const {
+    if (jacobi_max_sweeps > 0) l.jacobi_max_sweeps = jacobi_max_sweeps;
+    return l;
+  }
+  rutv::Launch launch() { return with_opts(rutv::Launch{stream, &stats.kernel_launches, sms, &prof, sched}); }
   rutv::Launch v_launch() {
     rutv::Launch l{vstr, &stats.kernel_launches, sms, &prof, nullptr};
     l.oneshot = true;
-    return l;
+    return with_opts(l);
   }
-  rutv::Launch side_launch() { return rutv::Launch{side, &stats.kernel_launches, sms, &prof, sched ? sched + 2 : nullptr}; }
+  rutv::Launch side_launch() {
+    return with_opts(rutv::Launch{side, &stats.kernel_launches, sms, &prof, sched ? sched + 2 : nullptr});
+  }
 };
 
 namespace rutv {

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(JT)
     jacobi_block_kernel(int w, const double* __restrict__ B, i64 ldb, double* __restrict__ Us, double* __restrict__ d,
                         double* __restrict__ Vs, int* status, int block_id, int nb, int nc, double* __restrict__ Xg,
                         double* __restrict__ Wg, double* __restrict__ red, int* __restrict__ flags, double tol,
-                        int* zero_flag) {
+                        int* zero_flag, int max_sweeps) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   __shared__ double wred[JT / 32];
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(JT)
   int sweeps = 0;
   bool converged = (w <= 1);
   while (!converged) {
-    if (sweeps >= MAX_SWEEPS) break;
+    if (sweeps >= max_sweeps) break;
     int rotated = 0;
     for (int r = 0; r < nblk - 1; ++r) {
       const int I = rr(cta, r, nblk), J = rr(nblk - 1 - cta, r, nblk);
@@ -350,18 +350,17 @@ int launch_jacobi_svd(const Launch& L, i64 w, const double* B, i64 ldb, double* 
   int* iflags = reinterpret_cast<int*>(ctmp + w);  // [0] zero flag, [1..] sweep flags
   int* zero_flag = iflags;
   int* flags = iflags + 1;
-  static bool attr_done = false;
-  if (!attr_done) {
-    RUTV_CUDA(cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr_done = true;
-  }
+  RUTV_ONCE_PER_DEVICE(
+      RUTV_CUDA(cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)));
   RUTV_CUDA(cudaMemsetAsync(iflags, 0, sizeof(int) * (MAX_SWEEPS + 2), L.stream));
   const size_t pe = L.pbegin();
   int wi = (int)w, bid = block_id, nbv = p.nb, ncv = p.nc;
   i64 ldbv = ldb;
   double tol = sqrt((double)w) * 0x1p-53;
   const double* Bv = B;
-  void* args[] = {&wi, &Bv, &ldbv, &Us, &d, &Vs, &status, &bid, &nbv, &ncv, &Xg, &Wg, &red, &flags, &tol, &zero_flag};
+  int msw = L.jacobi_max_sweeps < 1 ? 1 : (L.jacobi_max_sweeps > MAX_SWEEPS ? MAX_SWEEPS : L.jacobi_max_sweeps);
+  void* args[] = {&wi, &Bv, &ldbv, &Us, &d, &Vs, &status, &bid, &nbv, &ncv, &Xg, &Wg, &red, &flags, &tol, &zero_flag,
+                  &msw};
   RUTV_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_block_kernel, dim3(p.P), dim3(JT), args, p.smem, L.stream));
   L.count();
   jacobi_complete_kernel<<<1, 256, 0, L.stream>>>((int)w, Vs, d, zero_flag, ctmp);

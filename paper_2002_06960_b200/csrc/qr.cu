@@ -513,11 +513,10 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
       if (G <= kLeafClusterMax && R > 0 && leaf_cluster_on()) {
         // one thread-block cluster of G CTAs (non-portable size up to 16)
         void* fn = R == 1 ? (void*)qr_leaf_kernel<1, true> : (void*)qr_leaf_kernel<2, true>;
-        static bool attr[3] = {false, false, false};
-        if (!attr[R]) {
-          RUTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-          attr[R] = true;
-        }
+        if (R == 1)
+          RUTV_ONCE_PER_DEVICE(RUTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)));
+        else
+          RUTV_ONCE_PER_DEVICE(RUTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(G);
         cfg.blockDim = dim3(LEAF_THREADS);
@@ -555,11 +554,9 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
     // ---- T(:, L): T_LL, T(0:c0, L) = -T(0:c0,0:c0) S(0:c0,L) T_LL, T(L, 0:c0) = 0
     {
       const size_t smem = (size_t)(c0 > 0 ? c0 : 1) * NB * sizeof(double);
-      static bool attr = false;
-      if (!attr) {  // up to c0 = 640 (b = 672) with the 17 KB of static shared memory
-        RUTV_CUDA(cudaFuncSetAttribute(t_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        attr = true;
-      }
+      // up to c0 = 640 (b = 672) with the 17 KB of static shared memory
+      RUTV_ONCE_PER_DEVICE(
+          RUTV_CUDA(cudaFuncSetAttribute(t_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024)));
       if (smem > 160 * 1024) return -3;
       const int tb = c0 > 0 ? (int)((c0 + NB - 1) / NB) : 1;
       t_block_kernel<<<tb, 256, smem, L.stream>>>(SL, w, tau, (int)c0, wl, Tf, ldtf);

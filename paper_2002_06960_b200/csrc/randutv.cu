@@ -185,8 +185,15 @@ size_t carve(Carver& c, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork) {
 int ensure_ws(randutv_ctx* ctx, size_t bytes) {
   if (ctx->ws_bytes >= bytes) return 0;
   if (ctx->ws) {
-    cudaStreamSynchronize(ctx->stream);
-    cudaFree(ctx->ws);
+    if (ctx->ws_captured) {
+      // an ASYNC call (possibly captured into a CUDA graph) used it: keep it
+      // alive until randutv_destroy so replays stay valid
+      ctx->retired.push_back(ctx->ws);
+      ctx->ws_captured = false;
+    } else {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->ws);
+    }
     ctx->ws = nullptr;
     ctx->ws_bytes = 0;
   }
@@ -211,6 +218,105 @@ int prepare(randutv_ctx* ctx, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool tw
 }
 
 i64 sampled_steps(i64 n, i64 b) { return n > b ? (n - b + b - 1) / b : 0; }
+
+// ---------------------------------------------------------------- resid_2
+// ||A - A_k||_2 = sigma_1 of the trailing block X = T(k:m, k:n) (r x s, r >= s;
+// reading A11).  s <= kSpecM: exact -- Householder QR of a copy of X and the
+// Jacobi SVD of its R.  s > kSpecM: block Krylov with Rayleigh-Ritz -- Q_0 =
+// orth(Omega) (s x p, a Philox Gaussian), Y_j = X^T X Q_j, Q_{j+1} = orth(Y_j
+// with Q_0..Q_j projected out twice), M = kSpecM columns in all; then
+// sigma_1 ~ sqrt(lambda_max(Q^T X^T X Q)), the Gram H = Q^T [Y_0 .. Y_{J-1}]
+// (M x M) by the Jacobi SVD.  The Ritz value is a lower bound that converges
+// at the block-Krylov rate set by the gap sigma_1 / sigma_{p+1}.
+constexpr i64 kSpecP = 32, kSpecM = 512;
+
+struct SpecWork {
+  double *Q, *Yall, *Z, *C, *H, *Us, *Vs, *d, *jac, *gemm_ws, *tau, *Wx, *Tf, *Xc;
+  i64 jac_elems, gemm_ws_elems;
+  QrWork qw;
+  int* status;
+};
+
+size_t carve_spec(Carver& c, SpecWork& sw, i64 r, i64 s) {
+  const i64 M = kSpecM, p = kSpecP;
+  const bool exact = s <= M;
+  const i64 w = exact ? (s > 0 ? s : 1) : M;  // Jacobi / QR width
+  sw.Q = exact ? nullptr : c.take<double>(s * M);
+  sw.Yall = exact ? nullptr : c.take<double>(s * M);
+  sw.Z = exact ? nullptr : c.take<double>(r * p);
+  sw.C = exact ? nullptr : c.take<double>(M * p);
+  sw.H = c.take<double>(w * w);
+  sw.Us = c.take<double>(w * w);
+  sw.Vs = c.take<double>(w * w);
+  sw.d = c.take<double>(w);
+  sw.jac_elems = jacobi_scratch_elems(w);
+  sw.jac = c.take<double>(sw.jac_elems);
+  sw.gemm_ws_elems = std::max<i64>(4 * std::max(r, s) * std::max(p, exact ? w : p), 1 << 20);
+  sw.gemm_ws = c.take<double>(sw.gemm_ws_elems);
+  const i64 qh = exact ? r : s, qw_ = exact ? w : p;  // panels factored
+  sw.tau = c.take<double>(qw_);
+  sw.Wx = c.take<double>(qh * qw_);
+  sw.Tf = c.take<double>(qw_ * qw_);
+  sw.Xc = exact ? c.take<double>(r * w) : nullptr;
+  sw.qw.S = c.take<double>(qw_ * qw_);
+  sw.qw.tmp1 = c.take<double>(qw_ * 32);
+  sw.qw.tmp2 = c.take<double>(32 * qw_);
+  sw.qw.tmp3 = c.take<double>(32 * qw_);
+  sw.qw.partials_elems = panel_qr_partials_elems(qh, qw_);
+  sw.qw.partials = c.take<double>(sw.qw.partials_elems);
+  sw.qw.gemm_ws = sw.gemm_ws;
+  sw.qw.gemm_ws_elems = sw.gemm_ws_elems;
+  sw.status = c.take<int>(4);
+  return c.off;
+}
+
+// X (h x p, ld h) := the first p columns of its Householder Q (as orthonormalize)
+int spec_orth(const Launch& L, SpecWork& sw, i64 h, i64 p, double* X) {
+  RUTV_TRY(panel_qr(L, h, p, X, h, sw.tau, sw.Wx, h, sw.Tf, p, sw.qw));
+  RUTV_TRY(launch_dgemm(L, false, true, p, p, p, 1.0, sw.Tf, p, sw.Wx, h, 0.0, sw.qw.S, p, nullptr, 0));
+  RUTV_TRY(launch_set_identity(L, h, p, X, h));
+  return launch_dgemm(L, false, false, h, p, p, -1.0, sw.Wx, h, sw.qw.S, p, 1.0, X, h, nullptr, 0);
+}
+
+// Enqueues the estimate; *sigma2_dev (device) receives sigma_1^2 (exact case:
+// sigma_1 itself, flagged by *squared = false).
+int spectral_norm(const Launch& L, SpecWork& sw, i64 r, i64 s, const double* X, i64 ldx, uint64_t seed,
+                  bool* squared) {
+  RUTV_CUDA(cudaMemsetAsync(sw.status, 0x7f, sizeof(int), L.stream));
+  if (s <= kSpecM) {
+    *squared = false;
+    RUTV_TRY(launch_copy(L, r, s, X, ldx, sw.Xc, r));
+    RUTV_TRY(panel_qr(L, r, s, sw.Xc, r, sw.tau, sw.Wx, r, sw.Tf, s, sw.qw));
+    RUTV_TRY(launch_copy(L, s, s, sw.Xc, r, sw.H, s));
+    RUTV_TRY(launch_triu(L, s, s, sw.H, s));
+    return launch_jacobi_svd(L, s, sw.H, s, sw.Us, sw.d, sw.Vs, sw.status, 1, sw.jac, sw.jac_elems);
+  }
+  *squared = true;
+  const i64 p = kSpecP, J = kSpecM / kSpecP;
+  // Omega: the Philox Gaussian of a stream no factorisation step uses
+  RUTV_TRY(launch_gaussian(L, seed ^ 0x5eC7A1u, 0x7fffffff, s, p, sw.Q, s));
+  RUTV_TRY(spec_orth(L, sw, s, p, sw.Q));
+  for (i64 j = 0; j < J; ++j) {
+    double* Qj = sw.Q + j * p * s;
+    double* Yj = sw.Yall + j * p * s;
+    RUTV_TRY(launch_dgemm(L, false, false, r, p, s, 1.0, X, ldx, Qj, s, 0.0, sw.Z, r, sw.gemm_ws, sw.gemm_ws_elems));
+    RUTV_TRY(launch_dgemm(L, true, false, s, p, r, 1.0, X, ldx, sw.Z, r, 0.0, Yj, s, sw.gemm_ws, sw.gemm_ws_elems));
+    if (j + 1 == J) break;
+    double* Qn = Qj + p * s;
+    RUTV_TRY(launch_copy(L, s, p, Yj, s, Qn, s));
+    const i64 cols = (j + 1) * p;
+    for (int pass = 0; pass < 2; ++pass) {  // block classical Gram-Schmidt, twice
+      RUTV_TRY(launch_dgemm(L, true, false, cols, p, s, 1.0, sw.Q, s, Qn, s, 0.0, sw.C, cols, sw.gemm_ws,
+                            sw.gemm_ws_elems));
+      RUTV_TRY(launch_dgemm(L, false, false, s, p, cols, -1.0, sw.Q, s, sw.C, cols, 1.0, Qn, s, nullptr, 0));
+    }
+    RUTV_TRY(spec_orth(L, sw, s, p, Qn));
+  }
+  // H = Q^T (X^T X Q), symmetrised by the Jacobi SVD's own arithmetic (PSD: d = eigenvalues)
+  RUTV_TRY(launch_dgemm(L, true, false, kSpecM, kSpecM, s, 1.0, sw.Q, s, sw.Yall, s, 0.0, sw.H, kSpecM, sw.gemm_ws,
+                        sw.gemm_ws_elems));
+  return launch_jacobi_svd(L, kSpecM, sw.H, kSpecM, sw.Us, sw.d, sw.Vs, sw.status, 1, sw.jac, sw.jac_elems);
+}
 
 // X(rows x s, ldx) -= ((X W) Tf) W^T : the right application of Q = I - W Tf W^T
 int apply_right(const Launch& L, Work& w, i64 rows, i64 s, i64 bw, double* X, i64 ldx, const double* W, i64 ldw,
@@ -668,6 +774,8 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   if (ctx->side) cudaStreamSynchronize(ctx->side);
   if (ctx->ws) cudaFree(ctx->ws);
+  for (void* p : ctx->retired) cudaFree(p);
+  ctx->retired.clear();
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->sched) cudaFree(ctx->sched);
   rutv::comm_free(ctx->comm_side);
@@ -693,6 +801,16 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
   ctx->magic = 0;
   delete ctx;
   return 0;
+}
+
+RANDUTV_API int randutv_set_option(randutv_ctx* ctx, int option, int64_t value) {
+  if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
+  if (option == RANDUTV_OPT_JACOBI_SWEEPS) {
+    if (value < 0 || value > 30) return -3;
+    ctx->jacobi_max_sweeps = (int)value;
+    return 0;
+  }
+  return -2;
 }
 
 RANDUTV_API int randutv_set_stream(randutv_ctx* ctx, void* stream) {
@@ -744,6 +862,10 @@ RANDUTV_API const char* randutv_status_string(int s) {
   if (s == RANDUTV_ERR_ALLOC) return "device workspace allocation failed";
   if (s == RANDUTV_ERR_NONFINITE) return "input matrix holds NaN or Inf";
   if (s == RANDUTV_ERR_CTX) return "invalid or destroyed context";
+  if (s == RANDUTV_ERR_NCCL) return "NCCL missing, or a collective failed or timed out (randutv_last_error)";
+  if (s == RANDUTV_ERR_NOCOMM) return "sharded entry called before randutv_comm_init";
+  if (s == RANDUTV_ERR_PEER) return "another rank of the sharded call rejected its arguments or workspace";
+  if (s >= RANDUTV_ERR_BASE) return "unknown error";
   return "Jacobi SVD of a diagonal block did not converge (status = 1-based block index)";
 }
 
@@ -759,6 +881,11 @@ RANDUTV_API int randutv_workspace_bytes(int64_t m, int64_t n, int64_t b, int q, 
   Carver dry{nullptr, 0, 0, true};
   *bytes = carve(dry, w, m, n, bb, 0, false);
   return 0;
+}
+
+namespace {
+int backward_uk(const rutv::Launch& L, rutv::Work& w, rutv::i64 m, rutv::i64 n, rutv::i64 bb, rutv::i64 nrec,
+                bool with_final, rutv::i64 k, double* Uk, rutv::i64 ldu);
 }
 
 struct Drain {
@@ -794,21 +921,27 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
   if (uv && !V) return -14;
   if (uv && ldv < n) return -15;
   if ((flags & RANDUTV_ASYNC) && (flags & RANDUTV_CHECK_FINITE)) return -9;  // the scan synchronises
+  // economy U (m x n) by backward accumulation (reading A12); for m == n it is
+  // the full U and the forward accumulation is kept
+  const bool econ = uv && (flags & RANDUTV_ECON_U) && m > n;
+  if (econ && dr) return -9;
   const bool alias = (T == A);
   if (alias && ldt != lda) return -13;
   if (!alias && overlaps(A, (size_t)lda * n * 8, T, (size_t)ldt * n * 8)) return -12;
   const i64 bb = b < n ? b : n;
+  const i64 nsamp = sampled_steps(n, bb);
+  const i64 nrec = econ ? nsamp + 1 : 0;
   Launch L = ctx->launch();
   Work w;
-  RUTV_TRY(prepare(ctx, w, m, n, bb, 0, false));
+  RUTV_TRY(prepare(ctx, w, m, n, bb, nrec, false));
   if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
   RUTV_TRY(start_status(ctx, w));
   if (!alias) RUTV_CUDA(cudaMemcpy2DAsync(T, ldt * 8, A, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
   if (uv) {
-    RUTV_TRY(launch_set_identity(L, m, m, U, ldu));
+    if (!econ) RUTV_TRY(launch_set_identity(L, m, m, U, ldu));
     RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
   }
-  Problem P{m, n, bb, q, seed, T, ldt, uv ? U : nullptr, ldu, uv ? V : nullptr, ldv, false,
+  Problem P{m, n, bb, q, seed, T, ldt, (uv && !econ) ? U : nullptr, ldu, uv ? V : nullptr, ldv, econ,
             ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
   P.reorth = (flags & RANDUTV_REORTH) != 0;
   P.ustream = P.U && P.vl.stream && ustream_on();
@@ -821,8 +954,8 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
     P.hU = dr->hU;
     P.hV = dr->hV;
   }
-  const i64 nsamp = sampled_steps(n, bb);
   RUTV_TRY(run_loop(L, w, P, nsamp, true));
+  if (econ) RUTV_TRY(backward_uk(L, w, m, n, bb, nrec, true, n, U, ldu));
   if (P.cps) {
     // the main stream (and so finish) waits for the drained copies too
     RUTV_CUDA(cudaEventRecord(ctx->eWu, P.cps));
@@ -832,6 +965,7 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
   if (flags & RANDUTV_ASYNC) {
     // enqueued only: the status word stays on the device (randutv_wait)
     ctx->async_status = w.status;
+    ctx->ws_captured = true;
     ctx->stats.factorizations++;
     return 0;
   }
@@ -857,6 +991,40 @@ RANDUTV_API int randutv_wait(randutv_ctx* ctx) {
 
 namespace {
 
+// U_k = U^(1) ... U^(p) [I_k; 0] = U(:, 0:k) by backward accumulation of the
+// recorded left transforms (reading A12): X := [I_k; 0]; for j = nrec-1 .. 0:
+// X(k_j:k_j+w_j, :) := U_s^(j) X(...); X(k_j:m, :) -= W_j (T_j (W_j^T X(k_j:m, :))).
+// The last record is the final step's when `with_final` (width n - k_j; no
+// reflectors if that block was square).
+int backward_uk(const Launch& L, Work& w, i64 m, i64 n, i64 bb, i64 nrec, bool with_final, i64 k, double* Uk,
+                i64 ldu) {
+  RUTV_TRY(launch_set_identity(L, m, k, Uk, ldu));
+  for (i64 j = nrec - 1; j >= 0; --j) {
+    const i64 kj = j * bb;
+    if (kj >= k) continue;
+    const bool fin = with_final && j == nrec - 1;
+    const i64 wj = fin ? n - kj : bb;
+    const i64 rj = m - kj;
+    const bool has_w = !fin || rj > wj;
+    const double* rec = w.lefts + j * (m * bb + 2 * bb * bb);
+    const i64 cols = k - kj;
+    double* X = Uk + kj + kj * ldu;  // rows kj.., cols kj..k
+    // X(0:wj, :) = U_s X(0:wj, :)
+    RUTV_TRY(launch_dgemm(L, false, false, wj, cols, wj, 1.0, rec + m * bb + bb * bb, wj, X, ldu, 0.0, w.Z, wj,
+                          nullptr, 0));
+    RUTV_TRY(launch_copy(L, wj, cols, w.Z, wj, X, ldu));
+    if (has_w) {
+      // X(kj:m) -= W (T (W^T X))
+      RUTV_TRY(launch_dgemm(L, true, false, wj, cols, rj, 1.0, rec, rj, X, ldu, 0.0, w.Z, wj, w.gemm_ws,
+                            w.gemm_ws_elems));
+      RUTV_TRY(launch_dgemm(L, false, false, wj, cols, wj, 1.0, rec + m * bb, wj, w.Z, wj, 0.0, w.Z2, wj, nullptr,
+                            0));
+      RUTV_TRY(launch_dgemm(L, false, false, rj, cols, wj, -1.0, rec, rj, w.Z2, wj, 1.0, X, ldu, nullptr, 0));
+    }
+  }
+  return 0;
+}
+
 // The truncated variant (fixed k) and the adaptive-rank variant (tol > 0: stop
 // after the first sampled step whose trailing block has ||T(k:m,k:n)||_F <=
 // tol ||A||_F; P:155-157 on why partial methods
@@ -864,7 +1032,7 @@ namespace {
 // randutv_factor_rank; *k_out receives the rank used.
 int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64 k, double tol, i64 b, int q,
                    uint64_t seed, unsigned flags, double* Uk, i64 ldu, double* Tk, i64 ldt, double* V, i64 ldv,
-                   double* resid_fro, int64_t* k_out) {
+                   double* resid_fro, int64_t* k_out, double* resid_2 = nullptr) {
   const bool adaptive = tol > 0.0;
   const bool uv = !(flags & RANDUTV_NO_UV);
   const i64 bb = b < n ? b : n;
@@ -878,7 +1046,19 @@ int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64
   const i64 nrec_max = uv ? K + (with_final ? 1 : 0) : 0;
   Launch L = ctx->launch();
   Work w;
-  RUTV_TRY(prepare(ctx, w, m, n, bb, nrec_max, true));
+  SpecWork sw{};
+  if (resid_2) {
+    // the main workspace followed by the resid_2 region (fixed k: the
+    // trailing block is (m - k) x (n - k))
+    Carver dry{nullptr, 0, 0, true};
+    carve(dry, w, m, n, bb, nrec_max, true);
+    carve_spec(dry, sw, m - k, n - k);
+    RUTV_TRY(ensure_ws(ctx, dry.off));
+    Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
+    carve(real, w, m, n, bb, nrec_max, true);
+  } else {
+    RUTV_TRY(prepare(ctx, w, m, n, bb, nrec_max, true));
+  }
   if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
   RUTV_TRY(start_status(ctx, w));
   RUTV_CUDA(cudaMemcpy2DAsync(w.Twork, m * 8, A, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -921,37 +1101,28 @@ int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64
   RUTV_TRY(launch_sumsq(L, m - k, n - k, w.Twork + k + k * m, m, w.red, w.scal));
   // Tk = T(0:k, :)
   RUTV_CUDA(cudaMemcpy2DAsync(Tk, ldt * 8, w.Twork, m * 8, k * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
-  if (uv) {
-    // U_k = U^(1) ... U^(p) [I_k; 0], backward (A12)
-    RUTV_TRY(launch_set_identity(L, m, k, Uk, ldu));
-    for (i64 j = nrec - 1; j >= 0; --j) {
-      const i64 kj = j * bb;
-      if (kj >= k) continue;
-      const bool fin = with_final && j == nrec - 1;
-      const i64 wj = fin ? n - kj : bb;
-      const i64 rj = m - kj;
-      const bool has_w = !fin || rj > wj;
-      const double* rec = w.lefts + j * (m * bb + 2 * bb * bb);
-      const i64 cols = k - kj;
-      double* X = Uk + kj + kj * ldu;  // rows kj.., cols kj..k
-      // X(0:wj, :) = U_s X(0:wj, :)
-      RUTV_TRY(launch_dgemm(L, false, false, wj, cols, wj, 1.0, rec + m * bb + bb * bb, wj, X, ldu, 0.0, w.Z, wj,
-                            nullptr, 0));
-      RUTV_TRY(launch_copy(L, wj, cols, w.Z, wj, X, ldu));
-      if (has_w) {
-        // X(kj:m) -= W (T (W^T X))
-        RUTV_TRY(launch_dgemm(L, true, false, wj, cols, rj, 1.0, rec, rj, X, ldu, 0.0, w.Z, wj, w.gemm_ws,
-                              w.gemm_ws_elems));
-        RUTV_TRY(launch_dgemm(L, false, false, wj, cols, wj, 1.0, rec + m * bb, wj, w.Z, wj, 0.0, w.Z2, wj,
-                              nullptr, 0));
-        RUTV_TRY(launch_dgemm(L, false, false, rj, cols, wj, -1.0, rec, rj, w.Z2, wj, 1.0, X, ldu, nullptr, 0));
-      }
-    }
-  }
+  if (uv) RUTV_TRY(backward_uk(L, w, m, n, bb, nrec, with_final, k, Uk, ldu));
   double ss = 0.0;
   RUTV_CUDA(cudaMemcpyAsync(&ss, w.scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  double s2 = 0.0;
+  bool squared = false;
+  int spec_st = 0x7f7f7f7f;
+  if (resid_2 && k < n) {
+    Carver rc{(char*)ctx->ws, 0, ctx->ws_bytes, false};
+    Work wdummy;
+    carve(rc, wdummy, m, n, bb, nrec_max, true);
+    carve_spec(rc, sw, m - k, n - k);
+    RUTV_TRY(spectral_norm(L, sw, m - k, n - k, w.Twork + k + k * m, m, seed, &squared));
+    RUTV_CUDA(cudaMemcpyAsync(&s2, sw.d, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    RUTV_CUDA(cudaMemcpyAsync(&spec_st, sw.status, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  }
   const int st = finish(ctx, w);
   *resid_fro = std::sqrt(ss);
+  if (resid_2) {
+    *resid_2 = k < n ? (squared ? std::sqrt(s2 > 0.0 ? s2 : 0.0) : s2) : 0.0;
+    // a non-converged Jacobi SVD of the Rayleigh-Ritz problem: no estimate
+    if (spec_st != 0x7f7f7f7f) *resid_2 = -1.0;
+  }
   if (k_out) *k_out = k;
   if (st == 0) ctx->stats.factorizations++;
   return st;
@@ -963,7 +1134,8 @@ extern "C" {
 
 RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t k,
                                     int64_t b, int q, uint64_t seed, unsigned flags, double* Uk, int64_t ldu,
-                                    double* Tk, int64_t ldt, double* V, int64_t ldv, double* resid_fro) {
+                                    double* Tk, int64_t ldt, double* V, int64_t ldv, double* resid_fro,
+                                    double* resid_2) {
   RUTV_TRY(begin_call(ctx));
   const bool uv = !(flags & RANDUTV_NO_UV);
   if (n < 1) return -3;
@@ -980,7 +1152,8 @@ RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, cons
   if (uv && !V) return -15;
   if (uv && ldv < n) return -16;
   if (!resid_fro) return -17;
-  return truncated_impl(ctx, m, n, A, lda, k, 0.0, b, q, seed, flags, Uk, ldu, Tk, ldt, V, ldv, resid_fro, nullptr);
+  return truncated_impl(ctx, m, n, A, lda, k, 0.0, b, q, seed, flags, Uk, ldu, Tk, ldt, V, ldv, resid_fro, nullptr,
+                        resid_2);
 }
 
 RANDUTV_API int randutv_factor_tol(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, double tol,
@@ -1011,6 +1184,9 @@ RANDUTV_API int randutv_factor_tol(randutv_ctx* ctx, int64_t m, int64_t n, const
 
 static std::mutex g_lit_mu;
 static randutv_ctx* g_lit_ctx[64];
+// one literal call per device at a time: the internal ctx's workspace, staging
+// buffers and streams are shared by every caller on that device
+static std::mutex g_lit_call_mu[64];
 
 static int literal_ctx(randutv_ctx** out) {
   int dev = 0;
@@ -1044,6 +1220,7 @@ RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t ld
   if (!V) return -10;
   randutv_ctx* ctx = nullptr;
   RUTV_TRY(literal_ctx(&ctx));
+  std::lock_guard<std::mutex> call_lock(g_lit_call_mu[ctx->device]);
   const bool dev = is_device_ptr(A);
   if (dev != is_device_ptr(T) || dev != is_device_ptr(U) || dev != is_device_ptr(V)) return -9;
   if (dev) return randutv_factor_ex(ctx, m, n, A, lda, b, q, seed, 0u, U, m, T, m, V, n);
@@ -1076,7 +1253,14 @@ RANDUTV_API int randutv_factor(int64_t m, int64_t n, const double* A, int64_t ld
   Drain dr{T, U, V, 0};
   const bool drain = pinned(T) && pinned(U) && pinned(V);
   int st = factor_ex_impl(ctx, m, n, dT, m, b, q, seed, 0u, dU, m, dT, m, dV, n, drain ? &dr : nullptr);
-  if (st < 0 || st >= 1000) return st;
+  if (st < 0 || st >= RANDUTV_ERR_BASE) {
+    // no drain copy may still be writing the caller's buffers after return
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->cps) cudaStreamSynchronize(ctx->cps);
+    if (ctx->side) cudaStreamSynchronize(ctx->side);
+    if (ctx->vstr) cudaStreamSynchronize(ctx->vstr);
+    return st;
+  }
   const i64 c0 = drain ? dr.drained : 0;  // columns still on the device
   RUTV_CUDA(cudaMemcpyAsync(T + c0 * m, dT + c0 * m, (size_t)m * (n - c0) * 8, cudaMemcpyDeviceToHost, ctx->stream));
   RUTV_CUDA(cudaMemcpyAsync(U + c0 * m, dU + c0 * m, (size_t)m * (m - c0) * 8, cudaMemcpyDeviceToHost, ctx->stream));

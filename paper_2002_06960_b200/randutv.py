@@ -21,12 +21,16 @@ RANDUTV_NO_UV = 1
 RANDUTV_CHECK_FINITE = 2
 RANDUTV_REORTH = 4
 RANDUTV_ASYNC = 8
-RANDUTV_ERR_CUDA = 1000
-RANDUTV_ERR_ALLOC = 1001
-RANDUTV_ERR_NONFINITE = 1002
-RANDUTV_ERR_CTX = 1003
-RANDUTV_ERR_NCCL = 1004
-RANDUTV_ERR_NOCOMM = 1005
+RANDUTV_ECON_U = 16
+RANDUTV_OPT_JACOBI_SWEEPS = 1
+RANDUTV_ERR_BASE = 0x40000000
+RANDUTV_ERR_CUDA = RANDUTV_ERR_BASE + 0
+RANDUTV_ERR_ALLOC = RANDUTV_ERR_BASE + 1
+RANDUTV_ERR_NONFINITE = RANDUTV_ERR_BASE + 2
+RANDUTV_ERR_CTX = RANDUTV_ERR_BASE + 3
+RANDUTV_ERR_NCCL = RANDUTV_ERR_BASE + 4
+RANDUTV_ERR_NOCOMM = RANDUTV_ERR_BASE + 5
+RANDUTV_ERR_PEER = RANDUTV_ERR_BASE + 6
 RANDUTV_UNIQUE_ID_BYTES = 128
 
 # name -> (restype, argtypes) ; mirrors include/randutv.h
@@ -57,12 +61,13 @@ SIGNATURES = {
     "randutv_create": (_int, [ctypes.POINTER(_vp), _int, _vp]),
     "randutv_destroy": (_int, [_vp]),
     "randutv_set_stream": (_int, [_vp, _vp]),
+    "randutv_set_option": (_int, [_vp, _int, _i64]),
     "randutv_workspace_bytes": (_int, [_i64, _i64, _i64, _int, _uint, ctypes.POINTER(ctypes.c_size_t)]),
     "randutv_factor": (_int, [_i64, _i64, _vp, _i64, _i64, _int, _u64, _vp, _vp, _vp]),
     "randutv_factor_ex": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint,
                                  _vp, _i64, _vp, _i64, _vp, _i64]),
     "randutv_factor_rank": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _i64, _int, _u64, _uint,
-                                   _vp, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(_dbl)]),
+                                   _vp, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
     "randutv_factor_tol": (_int, [_vp, _i64, _i64, _vp, _i64, _dbl, _i64, _int, _u64, _uint, _vp, _i64, _vp, _i64,
                                   _vp, _i64, ctypes.POINTER(_i64), ctypes.POINTER(_dbl)]),
     "randutv_hqrrp": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _u64, _uint, _vp, _vp, _i64]),
@@ -124,7 +129,7 @@ class RandUTVError(RuntimeError):
 
 
 def _check(fn, status, allow_positive=False):
-    if status != 0 and not (allow_positive and 0 < status < 1000):
+    if status != 0 and not (allow_positive and 0 < status < RANDUTV_ERR_BASE):
         raise RandUTVError(fn, status)
     return status
 
@@ -189,6 +194,9 @@ class Context:
         except Exception:
             pass
 
+    def set_option(self, option, value):
+        _check("randutv_set_option", self.lib.randutv_set_option(self.h, int(option), int(value)))
+
     def stats(self):
         s = Stats()
         _check("randutv_get_stats", self.lib.randutv_get_stats(self.h, ctypes.byref(s)))
@@ -210,15 +218,18 @@ class Context:
 
     # ---------------------------------------------------------------- factorisations
     def randutv_factor_ex(self, A, b, q, seed, build_uv=True, U=None, T=None, V=None, flags=0,
-                          allow_nonconvergence=False):
-        """Full randUTV of the column-major device matrix A: returns (U, T, V, status)."""
+                          allow_nonconvergence=False, econ_u=False):
+        """Full randUTV of the column-major device matrix A: returns (U, T, V, status).
+        econ_u: U is the economy m x n factor (RANDUTV_ECON_U)."""
         m, n = A.shape
         if not build_uv:
             flags |= RANDUTV_NO_UV
+        if econ_u:
+            flags |= RANDUTV_ECON_U
         if T is None:
             T = colmajor(m, n, device=A.device)
         if build_uv:
-            U = colmajor(m, m, device=A.device) if U is None else U
+            U = colmajor(m, n if econ_u else m, device=A.device) if U is None else U
             V = colmajor(n, n, device=A.device) if V is None else V
         st = self.lib.randutv_factor_ex(self.h, m, n, _ptr(A), _ld(A), int(b), int(q), int(seed) & (2**64 - 1),
                                         flags, _ptr(U), _ld(U) if U is not None else 1, _ptr(T), _ld(T),
@@ -232,8 +243,9 @@ class Context:
         _check("randutv_wait", st, allow_positive=True)
         return st
 
-    def randutv_factor_rank(self, A, k, b, q, seed, build_uv=True, flags=0):
-        """Truncated randUTV: returns (Uk, Tk, V, rho)."""
+    def randutv_factor_rank(self, A, k, b, q, seed, build_uv=True, flags=0, resid_2=False):
+        """Truncated randUTV: returns (Uk, Tk, V, rho), or (Uk, Tk, V, rho, rho_2) with
+        resid_2 (the spectral-norm residual, reading A11)."""
         m, n = A.shape
         if not build_uv:
             flags |= RANDUTV_NO_UV
@@ -241,11 +253,14 @@ class Context:
         Uk = colmajor(m, k, device=A.device) if build_uv else None
         V = colmajor(n, n, device=A.device) if build_uv else None
         rho = ctypes.c_double()
+        rho2 = ctypes.c_double()
         st = self.lib.randutv_factor_rank(self.h, m, n, _ptr(A), _ld(A), int(k), int(b), int(q),
                                           int(seed) & (2**64 - 1), flags, _ptr(Uk), _ld(Uk) if Uk is not None else 1,
                                           _ptr(Tk), _ld(Tk), _ptr(V), _ld(V) if V is not None else 1,
-                                          ctypes.byref(rho))
+                                          ctypes.byref(rho), ctypes.byref(rho2) if resid_2 else None)
         _check("randutv_factor_rank", st)
+        if resid_2:
+            return Uk, Tk, V, rho.value, rho2.value
         return Uk, Tk, V, rho.value
 
     def randutv_factor_tol(self, A, tol, b, q, seed, build_uv=True, flags=0):

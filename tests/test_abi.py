@@ -56,4 +56,18 @@ def test_host_only_entries(lib):
     assert lib.randutv_workspace_bytes(10, 20, 4, 1, 0, ctypes.byref(out)) == -1
     assert lib.randutv_workspace_bytes(10, 10, 0, 1, 0, ctypes.byref(out)) == -3
     assert b"success" in lib.randutv_status_string(0)
-    assert lib.randutv_destroy(None) == 1003
+    assert lib.randutv_destroy(None) == 0x40000003
+
+
+def test_status_codes_do_not_collide(lib):
+    """Jacobi block indices (+j, up to n / b) and the error codes
+    (>= 2^30) are disjoint -- a factorisation with >= 1000 blocks reports its
+    non-converged block, not a CUDA error."""
+    from paper_2002_06960_b200 import randutv as r
+    for code in (r.RANDUTV_ERR_CUDA, r.RANDUTV_ERR_ALLOC, r.RANDUTV_ERR_NONFINITE, r.RANDUTV_ERR_CTX,
+                 r.RANDUTV_ERR_NCCL, r.RANDUTV_ERR_NOCOMM, r.RANDUTV_ERR_PEER):
+        assert code >= 2 ** 30
+        assert b"Jacobi" not in lib.randutv_status_string(code)
+    for j in (1, 999, 1000, 1005, 65536, 2 ** 30 - 1):
+        assert b"Jacobi" in lib.randutv_status_string(j)
+    assert lib.randutv_set_option(None, 1, 5) == r.RANDUTV_ERR_CTX

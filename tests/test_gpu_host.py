@@ -38,7 +38,7 @@ def _run_host(ctx, A, b, q, seed, cache_panels, pinned=True, build_uv=True):
 
 # U, V elementwise bound per case: 1e-11, except (520, 520, 64, 2), whose
 # tail singular vectors are ill-conditioned -- the oracle on A vs on
-# A(1 + 2^-52 N(0,1)) already differs by 7.2e-12 in |V| (tests/calibrate_parity.py,
+# A(1 + 2^-52 N(0,1)) already differs by 7.2e-12 in |V| (tests/test_parity_calibration.py,
 # bounds sit >= 30x above the calibrated noise).
 UV_TOL = {(520, 520, 64, 2): 3e-10}
 

@@ -79,7 +79,7 @@ def test_c1_full_parity(c1_pair):
     A, (U, T, V), o = c1_pair
     # |U|, |V| are not compared elementwise on c1: its singular values 1e-8..1 are only
     # ~3.6% apart, so the singular vectors of the tail are conditioned ~u/gap ~ 1e-7 and
-    # two valid FP64 runs differ by ~3e-9 there (tests/calibrate_parity.py); the
+    # two valid FP64 runs differ by ~3e-9 there (tests/test_parity_calibration.py); the
     # invariants and |diag T| pin them instead.
     _check_full(A, U, T, V, o, elementwise=("T",))
     # closed form: sum log10 |T_kk| = sum log10 sigma_k = -2048 (tests/golden/small_cases.txt)
@@ -286,7 +286,7 @@ def test_reorth_rejected_by_host_and_dist(ctx):
     A = colmajor(8, 8)
     st = ctx.lib.randutv_factor_dist(ctx.h, 8, 8, ctypes.c_void_p(A.data_ptr()), 8, 4, 1, 1, RANDUTV_REORTH,
                                      None, 1, None, 1)
-    assert st in (-9, 1005)   # the flag is checked after the communicator (NOCOMM) or before
+    assert st in (-9, 0x40000005)   # the flag is checked after the communicator (NOCOMM) or before
     Ah = np.zeros((8, 8), order="F")
     st = ctx.lib.randutv_factor_host(ctx.h, 8, 8, Ah.ctypes.data, 8, 4, 1, 1, RANDUTV_REORTH | 1, 0,
                                      None, 8, None, 8, None)
@@ -330,5 +330,87 @@ def test_async_and_cuda_graph_replay():
         assert torch.equal(T, T2) and torch.equal(U, U2) and torch.equal(V, V2)
         o = oracle_randutv(A2, b, q, 7)
         _check_full(A2, to_np(U), to_np(T), to_np(V), o)
+    finally:
+        c.close()
+
+
+# ---------------------------------------------------------------- economy U (RANDUTV_ECON_U, reading A12)
+@pytest.mark.parametrize("m,n,b,q", [(300, 170, 40, 2), (80, 50, 100, 1), (1000, 256, 64, 1), (64, 64, 16, 1)])
+def test_economy_u(ctx, m, n, b, q):
+    """U (m x n) by backward accumulation equals the oracle's thin U and the
+    forward run's U(:, 0:n); A = U T(0:n, :) V^T."""
+    rng = np.random.default_rng(m + 7 * n + b)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    Ue, Te, Ve, st = ctx.randutv_factor_ex(to_dev(A), b, q, 23, econ_u=True)
+    assert st == 0 and tuple(Ue.shape) == (m, n)
+    Ue, Te, Ve = to_np(Ue), to_np(Te), to_np(Ve)
+    Uf, Tf, Vf = _gpu_full(ctx, A, b, q, 23)
+    o = oracle_randutv(A, b, q, 23, thin_u=True)
+    assert np.array_equal(Te, Tf) and np.array_equal(Ve, Vf)   # T, V do not depend on how U is formed
+    assert np.max(np.abs(np.abs(Ue) - np.abs(o["U"]))) <= ELEM_TOL
+    assert np.max(np.abs(Ue - Uf[:, :n])) <= 1e-13
+    assert recon_error(A, Ue, Te[:n], Ve) <= 1e-12
+    assert spectral_orth_error(Ue) <= 1e-12
+
+
+# ---------------------------------------------------------------- resid_2 (reading A11)
+@pytest.mark.parametrize("case", ["c1_k64", "c1_k128", "tall_k256", "gauss_k128"])
+def test_resid_2(ctx, case):
+    """randutv_factor_rank's spectral-norm residual ||A - A_k||_2 against the exact
+    sigma_1 of the oracle's trailing block T(k:m, k:n) (LAPACK SVD).  n - k <= 512:
+    the exact path (QR + Jacobi SVD), north-star 1e-9; n - k > 512: the block-Krylov
+    Rayleigh-Ritz value, a lower bound."""
+    if case.startswith("c1"):
+        A = make_numpy("powspec", 512, 512, cfg_index=1)
+        k, b, q, seed = int(case[4:]), 64, 2, 2001
+    elif case == "tall_k256":
+        A = make_numpy("lowrank", 4096, 1024, cfg_index=4, rank=200)
+        k, b, q, seed = 256, 64, 2, 2004
+    else:
+        A = make_numpy("gauss", 1536, 1024, cfg_index=2)
+        k, b, q, seed = 128, 64, 1, 2002
+    Uk, Tk, V, rho, rho2 = ctx.randutv_factor_rank(to_dev(A), k, b, q, seed, resid_2=True)
+    o = oracle_randutv(A, b, q, seed, k=k, thin_u=True)
+    exact = np.linalg.norm(o["T"][k:, k:], 2)
+    Ak = to_np(Uk) @ to_np(Tk) @ to_np(V).T
+    gpu_exact = np.linalg.norm(A - Ak, 2)
+    rel = abs(rho2 - exact) / exact
+    print(case, "resid_2", rho2, "oracle sigma_1", exact, "rel", rel, "vs own A_k", abs(rho2 - gpu_exact) / gpu_exact)
+    assert abs(rho - o["rho"]) <= 1e-9 * o["rho"]
+    assert rho2 <= gpu_exact * (1 + 1e-12)
+    if A.shape[1] - k <= 512:
+        assert rel <= 1e-9
+    else:
+        assert rel <= 1e-3
+
+
+def test_jacobi_nonconvergence_status():
+    """The +j status path (SURVEY §8(b) conventions): with the sweep cap lowered
+    to 1 (randutv_set_option), the Jacobi SVD of the first diagonal block cannot
+    converge, and every entry reports the 1-based index of the FIRST such block;
+    restoring the cap restores status 0."""
+    import torch
+    from paper_2002_06960_b200.randutv import RANDUTV_OPT_JACOBI_SWEEPS, Context, RandUTVError
+    c = Context()
+    try:
+        rng = np.random.default_rng(31)
+        A = np.asfortranarray(rng.standard_normal((256, 256)))
+        c.set_option(RANDUTV_OPT_JACOBI_SWEEPS, 1)
+        _, _, _, st = c.randutv_factor_ex(to_dev(A), 64, 1, 3, allow_nonconvergence=True)
+        assert st == 1
+        with pytest.raises(RandUTVError) as e:
+            c.randutv_factor_ex(to_dev(A), 64, 1, 3)
+        assert e.value.status == 1
+        _, _, _, st = c.randutv_small_svd(to_dev(np.linalg.qr(A[:64, :64])[1]), allow_nonconvergence=True)
+        assert st == 1
+        with pytest.raises(RandUTVError) as e:
+            c.randutv_factor_rank(to_dev(A), 128, 64, 1, 3)
+        assert e.value.status == 1
+        with pytest.raises(RandUTVError):
+            c.set_option(RANDUTV_OPT_JACOBI_SWEEPS, 31)
+        c.set_option(RANDUTV_OPT_JACOBI_SWEEPS, 0)
+        _, _, _, st = c.randutv_factor_ex(to_dev(A), 64, 1, 3)
+        assert st == 0
+        torch.cuda.synchronize()
     finally:
         c.close()
