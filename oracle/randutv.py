@@ -49,7 +49,8 @@ def sampled_steps(n, b):
     return max(0, -(-(n - b) // b)) if n > b else 0
 
 
-def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reorth=False, overwrite_a=False):
+def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reorth=False, overwrite_a=False,
+            oversample=0):
     """Oracle randUTV of A (m x n, m >= n).
 
     Parameters
@@ -63,6 +64,8 @@ def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reo
     record     : optional dict; receives per-step diagnostics (Y, tau, d, ...)
     reorth     : re-orthonormalise the sample between power steps (SURVEY §8(f)
                  NEXT-4, the alternative to reading A8; see _sample)
+    oversample : p >= 0 extra sample columns with Rayleigh-Ritz selection of the
+                 b directions (reading A28; see _select)
     overwrite_a: T is A itself (A must be a Fortran-ordered float64 array) -- the
                  paper's in-place factorisation ("T := A"); saves one
                  copy of A for the full-size parity tests (17-34 GB)
@@ -73,8 +76,8 @@ def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reo
     m, n = A.shape
     if m < n:
         raise ValueError("randUTV assumes m >= n (P:532)")
-    if b < 1 or q < 0:
-        raise ValueError("need b >= 1, q >= 0")
+    if b < 1 or q < 0 or oversample < 0:
+        raise ValueError("need b >= 1, q >= 0, oversample >= 0")
     if overwrite_a:
         if not (A.flags.f_contiguous and A.dtype == np.float64):
             raise ValueError("overwrite_a needs a Fortran-ordered float64 A")
@@ -106,7 +109,7 @@ def randutv(A, b, q, seed, build_uv=True, k=None, thin_u=False, record=None, reo
         if s > b:
             if i >= K:
                 break
-            _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin_u and build_uv, record, reorth)
+            _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin_u and build_uv, record, reorth, oversample)
         else:
             if truncated and not truncated_full:
                 break
@@ -157,12 +160,31 @@ def _sample(At, G, q, reorth=False):
     return Y
 
 
-def _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin, record, reorth=False):
+def _select(At, Y, b):
+    """Reading A28 (oversampling, NEXT-4): the sample Y has b + p columns
+    (p <= s - b); keep
+    the b directions of span(Y) along which A_t is largest -- the Rayleigh-Ritz
+    choice of the randomized range finder the paper's construction comes from
+    (P:651-656): Q_Y = _orth(Y); R_B = the R factor of B = A_t Q_Y (Householder,
+    oracle.householder); R_B = U_R diag(d) V_R^T (oracle.jacobi.svd_block, d
+    descending); return Y_hat = Q_Y V_R[:, 0:b], whose Householder QR then
+    defines V_hat as without oversampling."""
+    QY = _orth(Y)
+    FB, _ = householder_qr(At @ QY)
+    _, _, VR, _ = svd_block(upper_r(FB))
+    return np.asfortranarray(QY @ VR[:, :b])
+
+
+def _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin, record, reorth=False, oversample=0):
     m, n = T.shape
     r = m - kk
-    # O1, O2
-    G = gaussian_block(seed, i, r, b)
+    # O1, O2 (with oversampling: b + p columns, the first b the same draws;
+    # p capped at s - b, beyond which span(Y) cannot grow)
+    p = min(oversample, (n - kk) - b)
+    G = gaussian_block(seed, i, r, b + p)
     Y = _sample(T[kk:, kk:], G, q, reorth)
+    if p > 0:
+        Y = _select(T[kk:, kk:], Y, b)
     # O3, O4 on Y
     FY, tauV = householder_qr(Y)
     WV = unit_lower(FY)

@@ -80,6 +80,16 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// RUTV_JACOBI_CLUSTER=0 forces the L2-staged cooperative kernel for w <= 256 (A/B only)
+bool jacobi_cluster_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_JACOBI_CLUSTER");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 // round-robin tournament over `n` (even) slots: slot 0 fixed, others rotate
 __device__ __forceinline__ int rr(int pos, int round, int n) {
   return pos == 0 ? 0 : 1 + (pos - 1 + round) % (n - 1);
@@ -329,6 +339,187 @@ __global__ void jacobi_complete_kernel(int w, double* __restrict__ Us, const dou
   if (tid == 0) *zero_flag = 0;
 }
 
+// ---------------------------------------------------------------------------
+// w <= 256: the same block Jacobi with the data RESIDENT in one thread-block
+// cluster (P = nc / 16 <= 16 CTAs, non-portable size).  CTA c keeps the X and
+// W columns of the two blocks at tournament positions c and 2P-1-c in its own
+// shared memory for the whole SVD; after every block round the blocks move one
+// position (slot 0 fixed, the others rotate -- the round-robin schedule of
+// rr()), each CTA copying its two incoming blocks from the neighbours'
+// shared memory over DSMEM into its second buffer.  One cluster barrier per
+// block round, no L2 round trips, no grid barrier.  Same pair order and
+// arithmetic as jacobi_block_kernel.
+constexpr int JCT = 256;  // threads per cluster CTA: one warp per pair (nb = 8)
+
+__global__ void __launch_bounds__(JCT, 1)
+    jacobi_cluster_kernel(int w, const double* __restrict__ B, i64 ldb, double* __restrict__ Us,
+                          double* __restrict__ d, double* __restrict__ Vs, int* status, int block_id, int nb, int nc,
+                          double tol, int* zero_flag, int max_sweeps) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double wred[JCT / 32];
+  __shared__ double part;       // this CTA's sum of squares of B
+  __shared__ int rotf[2];       // rotations in the sweep, by sweep parity
+  __shared__ double dn[2 * 8];  // this CTA's column norms (2 nb <= 16)
+  __shared__ double dall[256];  // every column norm (global column order)
+  __shared__ int srot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = JCT / 32;
+  const int cta = (int)cl.block_rank(), P = (int)cl.num_blocks();
+  const int nblk = 2 * P;
+  const int sx = nb * w, sw = nb * nc, slot = sx + sw;  // one block: X (nb x w) then W (nb x nc)
+  double* buf[2] = {sm, sm + 2 * slot};
+
+  // ---- X = B^T, W = I for the blocks at positions cta (slot 0) and nblk-1-cta (slot 1)
+  double ss = 0.0;
+  for (int sl = 0; sl < 2; ++sl) {
+    const int blk = sl == 0 ? cta : nblk - 1 - cta;
+    double* X = buf[0] + sl * slot;
+    double* W = X + sx;
+    for (int e = tid; e < sx; e += JCT) {
+      const int cl_ = e / w, r = e % w, col = blk * nb + cl_;
+      const double x = col < w ? B[col + (i64)r * ldb] : 0.0;
+      X[e] = x;
+      ss = fma(x, x, ss);
+    }
+    for (int e = tid; e < sw; e += JCT) {
+      const int cl_ = e / nc, r = e % nc, col = blk * nb + cl_;
+      W[e] = (r == col) ? 1.0 : 0.0;
+    }
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) wred[warp] = ss;
+  if (tid < 2) rotf[tid] = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int k = 0; k < nwarps; ++k) t += wred[k];
+    part = t;
+  }
+  cl.sync();
+  double fro2 = 0.0;
+  for (int c = 0; c < P; ++c) fro2 += *cl.map_shared_rank(&part, c);  // same order in every CTA
+  const double nu = (double)w * 0x1p-53 * sqrt(fro2);
+  const double nu2 = nu * nu;
+
+  // sources of the two incoming blocks after a round (positions move p -> p-1,
+  // 1 -> nblk-1, 0 fixed): slot 0 <- position cta+1, slot 1 <- position nblk-cta
+  int src0_rank = cta, src0_slot = 0, src1_rank = 0, src1_slot = 0;
+  if (cta > 0) {
+    if (cta + 1 <= P - 1) src0_rank = cta + 1, src0_slot = 0;
+    else src0_rank = P - 1, src0_slot = 1;  // position P = nblk-1-(P-1)
+  }
+  if (cta == 0) src1_rank = P > 1 ? 1 : 0, src1_slot = 0;  // position nblk-1 <- position 1
+  else src1_rank = cta - 1, src1_slot = 1;
+
+  int cur = 0, sweeps = 0;
+  bool converged = (w <= 1);
+  while (!converged) {
+    if (sweeps >= max_sweeps) break;
+    int rotated = 0;
+    for (int r = 0; r < nblk - 1; ++r) {
+      double* Xs = buf[cur];          // slot 0 X at Xs, slot 1 X at Xs + slot
+      double* X0 = Xs;
+      double* X1 = Xs + slot;
+      double* W0 = X0 + sx;
+      double* W1 = X1 + sx;
+      if (r == 0) {
+        // intra-block pairs of both blocks: nb-1 inner rounds, nb/2 pairs per block
+        for (int t = 0; t < nb - 1; ++t) {
+          for (int pi = warp; pi < nb; pi += nwarps) {
+            const int blk = pi / (nb / 2), k = pi % (nb / 2);
+            const int p = rr(k, t, nb), q = rr(nb - 1 - k, t, nb);
+            double* Xb = blk == 0 ? X0 : X1;
+            double* Wb = blk == 0 ? W0 : W1;
+            rotated |= jacobi_pair(Xb + (size_t)p * w, Xb + (size_t)q * w, Wb + (size_t)p * nc, Wb + (size_t)q * nc,
+                                   w, nc, tol, nu2, lane);
+          }
+          __syncthreads();
+        }
+      }
+      // cross pairs (a in slot 0, (a + t) mod nb in slot 1): nb inner rounds of nb disjoint pairs
+      for (int t = 0; t < nb; ++t) {
+        for (int a = warp; a < nb; a += nwarps) {
+          const int q = (a + t) % nb;
+          rotated |= jacobi_pair(X0 + (size_t)a * w, X1 + (size_t)q * w, W0 + (size_t)a * nc, W1 + (size_t)q * nc, w,
+                                 nc, tol, nu2, lane);
+        }
+        __syncthreads();
+      }
+      if (nblk > 2) {
+        // rotate the tournament: fetch the two incoming blocks into the other buffer
+        cl.sync();
+        double* dst = buf[cur ^ 1];
+        const double* s0 = cl.map_shared_rank(buf[cur] + src0_slot * slot, src0_rank);
+        const double* s1 = cl.map_shared_rank(buf[cur] + src1_slot * slot, src1_rank);
+        for (int e = tid; e < slot; e += JCT) {
+          dst[e] = s0[e];
+          dst[slot + e] = s1[e];
+        }
+        __syncthreads();
+        cur ^= 1;
+      }
+    }
+    // sweep verdict: any rotation in any CTA
+    if (tid == 0) srot = 0;
+    __syncthreads();
+    if (rotated) atomicOr(&srot, 1);
+    __syncthreads();
+    if (tid == 0) rotf[sweeps & 1] = srot;
+    cl.sync();
+    int any = 0;
+    for (int c = 0; c < P; ++c) any |= *cl.map_shared_rank(&rotf[sweeps & 1], c);
+    converged = any == 0;
+    ++sweeps;
+  }
+  if (!converged && cta == 0 && tid == 0) atomicMin(status, block_id);
+
+  // ---- column norms, global ranks (stable descending), outputs
+  double* Xc = buf[cur];
+  for (int cl_ = warp; cl_ < 2 * nb; cl_ += nwarps) {
+    const double* xc = Xc + (cl_ / nb) * slot + (size_t)(cl_ % nb) * w;
+    double s2 = 0.0;
+    for (int e = lane; e < w; e += 32) s2 = fma(xc[e], xc[e], s2);
+    s2 = warp_sum(s2);
+    if (lane == 0) dn[cl_] = (s2 <= nu2) ? 0.0 : sqrt(s2);
+  }
+  cl.sync();
+  for (int col = tid; col < nc; col += JCT) {
+    const int blk = col / nb, i = col % nb;
+    const int owner = blk < P ? blk : nblk - 1 - blk, sl = blk < P ? 0 : 1;
+    dall[col] = *cl.map_shared_rank(&dn[sl * nb + i], owner);
+  }
+  __syncthreads();
+  int anyzero = 0;
+  for (int cl_ = 0; cl_ < 2 * nb; ++cl_) {
+    const int blk = cl_ < nb ? cta : nblk - 1 - cta;
+    const int col = blk * nb + cl_ % nb;
+    if (col >= w) continue;
+    const double dj = dall[col];
+    int rk = 0;
+    for (int i = tid; i < nc; i += JCT) {
+      const double di = dall[i];
+      rk += (di > dj) || (di == dj && i < col);
+    }
+    rk = __reduce_add_sync(0xffffffffu, rk);
+    if (lane == 0) wred[warp] = (double)rk;
+    __syncthreads();
+    int rank = 0;
+    for (int k = 0; k < nwarps; ++k) rank += (int)wred[k];
+    __syncthreads();
+    if (tid == 0) d[rank] = dj;
+    anyzero |= (dj == 0.0);
+    const double inv = dj != 0.0 ? 1.0 / dj : 0.0;
+    const double* xc = Xc + (cl_ / nb) * slot + (size_t)(cl_ % nb) * w;
+    const double* wc = Xc + (cl_ / nb) * slot + sx + (size_t)(cl_ % nb) * nc;
+    for (int e = tid; e < w; e += JCT) {
+      Vs[e + (i64)rank * w] = dj != 0.0 ? xc[e] * inv : 0.0;  // V_SVD = Q = X / d
+      Us[e + (i64)rank * w] = wc[e];                         // U_SVD = W
+    }
+  }
+  if (anyzero && tid == 0) atomicExch(zero_flag, 1);
+  cl.sync();  // no CTA exits while its shared memory may still be read
+}
+
 }  // namespace
 
 i64 jacobi_scratch_elems(i64 w) {
@@ -354,6 +545,37 @@ int launch_jacobi_svd(const Launch& L, i64 w, const double* B, i64 ldb, double* 
       RUTV_CUDA(cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)));
   RUTV_CUDA(cudaMemsetAsync(iflags, 0, sizeof(int) * (MAX_SWEEPS + 2), L.stream));
   const size_t pe = L.pbegin();
+  const int msw0 = L.jacobi_max_sweeps < 1 ? 1 : (L.jacobi_max_sweeps > MAX_SWEEPS ? MAX_SWEEPS : L.jacobi_max_sweeps);
+  if (w <= 256 && jacobi_cluster_on()) {
+    // data-resident cluster variant: nb = 8, P = nc / 16 CTAs (<= 16)
+    const int nb = 8, nc = (int)((w + 15) / 16 * 16), P = nc / 16;
+    const size_t smem = (size_t)4 * nb * ((size_t)w + nc) * sizeof(double);
+    RUTV_ONCE_PER_DEVICE({
+      RUTV_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      RUTV_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     4 * 8 * 512 * 8));
+    });
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P);
+    cfg.blockDim = dim3(JCT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = L.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = P;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RUTV_CUDA(cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, (int)w, B, (i64)ldb, Us, d, Vs, status, block_id, nb, nc,
+                                 sqrt((double)w) * 0x1p-53, zero_flag, msw0));
+    L.count();
+    jacobi_complete_kernel<<<1, 256, 0, L.stream>>>((int)w, Vs, d, zero_flag, ctmp);
+    L.count();
+    RUTV_CHECK_LAUNCH("jacobi_complete_kernel");
+    L.pend(PK_JACOBI, 0.0, 8.0 * 4.0 * (double)w * w, pe);
+    return 0;
+  }
   int wi = (int)w, bid = block_id, nbv = p.nb, ncv = p.nc;
   i64 ldbv = ldb;
   double tol = sqrt((double)w) * 0x1p-53;

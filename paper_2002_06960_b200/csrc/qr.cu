@@ -21,7 +21,8 @@
 //                      updates its own rows, so no second barrier is needed.
 //                      The NB x NB top block is replicated in every CTA's
 //                      shared memory and updated identically by all of them.
-//     extract_w        explicit W columns (unit diagonal, zeros above)
+//                      It also writes the leaf's explicit W columns (unit
+//                      diagonal, zeros above) -- no separate extraction pass.
 //     S = W^T W_L      DMMA GEMM (K = h - c0, split-K)
 //     t_block          T_L from S_LL and tau (dlarft recurrence, one warp) and
 //                      T(0:c0, L) = -T(0:c0,0:c0) S(0:c0, L) T_L, one CTA
@@ -95,17 +96,25 @@ __device__ __forceinline__ void reduce_partials(const double* __restrict__ pj, i
 // exchange is a cluster barrier + DSMEM reads of the other CTAs' records
 // (tools/sync_micro.cu: ~1.0 us for 16 CTAs) instead of a grid barrier + an L2
 // round trip through `partials` (~3.6 us for 64 CTAs).
-template <int R, bool CLUSTER>
+// S > 0 (cluster leaves only): each thread also keeps S more rows of the slab
+// in shared memory (dynamic, column-major with ld S*256 so a warp's row
+// accesses are consecutive), so one 16-CTA cluster holds panels of up to
+// 16 * 256 * (R + S) rows and the per-column exchange stays a cluster barrier
+// + DSMEM instead of a grid barrier + L2 round trips (c3's 16384-row panels:
+// R = 2, S = 2).
+template <int R, bool CLUSTER, int S = 0>
 __global__ void __launch_bounds__(LEAF_THREADS, 1)
     qr_leaf_kernel(double* __restrict__ P, i64 h, i64 ldp, i64 c0, int nb, double* __restrict__ tau,
-                   double* __restrict__ partials) {
+                   double* __restrict__ partials, double* __restrict__ Wx, i64 ldw) {
   __shared__ double mine[2][PSTRIDE];  // CLUSTER: this CTA's record, by column parity
   __shared__ double TB[NB][NB + 1];  // TB[r][c]: top-block row r, leaf column c
   __shared__ double wred[LEAF_THREADS / 32][PSTRIDE];
   __shared__ double tot[PSTRIDE];
   __shared__ double wv[NB];
   __shared__ double sc[4];  // tau, scal, beta, flag
-  __shared__ double stage[LEAF_MAX_CTAS * PSTRIDE];
+  __shared__ double stage[(CLUSTER ? 16 : LEAF_MAX_CTAS) * PSTRIDE];
+  extern __shared__ double slab_s[];  // S * LEAF_THREADS rows x NB columns
+  constexpr int SLD = S * LEAF_THREADS;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, cta = blockIdx.x;
@@ -123,6 +132,15 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
       const i64 r = rb + tid + (i64)k * LEAF_THREADS;
 #pragma unroll
       for (int l = 0; l < NB; ++l) v[k][l] = (r < re && l < nb) ? L0[r + (i64)l * ldp] : 0.0;
+    }
+  }
+  if constexpr (S > 0) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const int sr = k * LEAF_THREADS + tid;
+      const i64 r = rb + (i64)(R + k) * LEAF_THREADS + tid;
+#pragma unroll 8
+      for (int l = 0; l < NB; ++l) slab_s[sr + l * SLD] = (r < re && l < nb) ? L0[r + (i64)l * ldp] : 0.0;
     }
   }
   for (int e = tid; e < NB * NB; e += LEAF_THREADS) {
@@ -167,6 +185,18 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
 #pragma unroll
         for (int l = 0; l < NB; ++l)
           if (l > jj && l < nb) acc[1 + l] = fma(x, L0[r + (i64)l * ldp], acc[1 + l]);
+      }
+    }
+    if constexpr (S > 0) {
+      // shared-memory rows (zero beyond the slab: no bounds test)
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const int sr = k * LEAF_THREADS + tid;
+        const double x = slab_s[sr + jj * SLD];
+        acc[0] = fma(x, x, acc[0]);
+#pragma unroll
+        for (int l = 0; l < NB; ++l)
+          if (l > jj) acc[1 + l] = fma(x, slab_s[sr + l * SLD], acc[1 + l]);
       }
     }
 #pragma unroll
@@ -295,6 +325,18 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
             if (l > jj && l < nb) L0[r + (i64)l * ldp] = fma(-tv, wv[l], L0[r + (i64)l * ldp]);
         }
       }
+      if constexpr (S > 0) {
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+          const int sr = k * LEAF_THREADS + tid;
+          const double vv = slab_s[sr + jj * SLD] * scal;
+          slab_s[sr + jj * SLD] = vv;
+          const double tv = t * vv;
+#pragma unroll
+          for (int l = 0; l < NB; ++l)
+            if (l > jj) slab_s[sr + l * SLD] = fma(-tv, wv[l], slab_s[sr + l * SLD]);
+        }
+      }
       // replicated top block, element-parallel over (row r >= j, column l > j):
       // the pivot row j has the implicit unit reflector entry; column j itself
       // (read here) is scaled after the barrier
@@ -322,6 +364,9 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
 #endif
   }
   if constexpr (CLUSTER) cg::this_cluster().sync();  // no CTA exits while its record may still be read
+  // the factored leaf into P and its explicit reflectors W (unit diagonal,
+  // zeros above) into Wx(0:h, c0:c0+nb): the slab rows are the same values
+  double* W0 = Wx + c0 + c0 * ldw;
   if constexpr (R > 0) {
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -329,29 +374,44 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
       if (r < re) {
 #pragma unroll
         for (int l = 0; l < NB; ++l)
-          if (l < nb) L0[r + (i64)l * ldp] = v[k][l];
+          if (l < nb) {
+            L0[r + (i64)l * ldp] = v[k][l];
+            W0[r + (i64)l * ldw] = v[k][l];
+          }
       }
     }
+  }
+  if constexpr (S > 0) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const int sr = k * LEAF_THREADS + tid;
+      const i64 r = rb + (i64)(R + k) * LEAF_THREADS + tid;
+      if (r < re) {
+#pragma unroll 8
+        for (int l = 0; l < NB; ++l)
+          if (l < nb) {
+            const double x = slab_s[sr + l * SLD];
+            L0[r + (i64)l * ldp] = x;
+            W0[r + (i64)l * ldw] = x;
+          }
+      }
+    }
+  }
+  if constexpr (R == 0) {
+    // rows in L2: already in P; copy them to W
+    for (i64 r = rb + tid; r < re; r += LEAF_THREADS)
+      for (int l = 0; l < nb; ++l) W0[r + (i64)l * ldw] = L0[r + (i64)l * ldp];
   }
   if (cta == 0) {
     for (int e = tid; e < nb * nb; e += LEAF_THREADS) {
       const int r = e % nb, c = e / nb;
       L0[r + (i64)c * ldp] = TB[r][c];
+      W0[r + (i64)c * ldw] = r > c ? TB[r][c] : (r == c ? 1.0 : 0.0);
     }
   }
-}
-
-// Wx(0:h, c0:c0+w) := explicit reflectors of the factored columns (unit diag, 0 above).
-__global__ void extract_w_kernel(const double* __restrict__ P, i64 ldp, i64 h, i64 c0, i64 w,
-                                 double* __restrict__ Wx, i64 ldw) {
-  const i64 total = h * w;
-  for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
-    const i64 r = idx % h, cl = idx / h, c = c0 + cl;
-    double v;
-    if (r > c) v = P[r + c * ldp];
-    else v = (r == c) ? 1.0 : 0.0;
-    Wx[r + c * ldw] = v;
-  }
+  // rows 0 .. c0 of W's leaf columns are zero
+  for (i64 e = (i64)cta * LEAF_THREADS + tid; e < c0 * nb; e += (i64)G * LEAF_THREADS)
+    Wx[e % c0 + (c0 + e / c0) * ldw] = 0.0;
 }
 
 // T(c0:c0+w, c0:c0+w) from S = W^T W (same block) and tau: T_jj = tau_j,
@@ -444,10 +504,40 @@ __global__ void __launch_bounds__(256) t_block_kernel(const double* __restrict__
 }
 
 
-// Leaf grid: R rows per thread in registers when the slab fits (R = 1, 2),
-// otherwise rows in L2 (R = 0).  G depends on the panel height only, so the
-// factorisation is bitwise reproducible.
-void leaf_plan(i64 slab_rows, int* G, int* R) {
+constexpr int kLeafClusterMax = 16;
+
+// RUTV_LEAF_CLUSTER=0 forces the cooperative-grid leaf (tuning only)
+bool leaf_cluster_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_LEAF_CLUSTER");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+// Leaf grid: one thread-block cluster of <= 16 CTAs whenever the slab fits in
+// its registers + shared memory (R rows per thread in registers, S in shared
+// memory: up to 16 * 256 * 5 = 20480 rows); else a cooperative grid with R
+// rows per thread in registers (R = 1, 2) or rows in L2 (R = 0).  G, R, S
+// depend on the panel height only, so the factorisation is bitwise
+// reproducible.
+void leaf_plan(i64 slab_rows, int* G, int* R, int* S) {
+  *S = 0;
+  if (leaf_cluster_on()) {
+    const i64 per_cta_rows = (i64)kLeafClusterMax * LEAF_THREADS;  // rows per (R + S) unit over 16 CTAs
+    for (int units = 1; units <= 5; ++units) {
+      if (slab_rows <= per_cta_rows * units) {
+        const int r = units >= 2 ? 2 : 1;
+        *R = r;
+        *S = units - r;
+        const i64 rows_per_cta = (i64)units * LEAF_THREADS;
+        i64 g = (slab_rows + rows_per_cta - 1) / rows_per_cta;
+        *G = (int)(g < 1 ? 1 : g);
+        return;
+      }
+    }
+  }
   const i64 cap1 = (i64)LEAF_MAX_CTAS * LEAF_THREADS;
   static i64 r2_from = -2;  // RUTV_LEAF_R2_FROM: use 2 rows per thread from this slab height (tuning only)
   if (r2_from == -2) {
@@ -473,16 +563,28 @@ void leaf_plan(i64 slab_rows, int* G, int* R) {
   *G = (int)g;
 }
 
-constexpr int kLeafClusterMax = 16;
-
-// RUTV_LEAF_CLUSTER=0 forces the cooperative-grid leaf (tuning only)
-bool leaf_cluster_on() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("RUTV_LEAF_CLUSTER");
-    v = e ? atoi(e) : 1;
-  }
-  return v != 0;
+template <int R, int S>
+int launch_leaf_cluster(const Launch& L, int G, void** args) {
+  void* fn = (void*)qr_leaf_kernel<R, true, S>;
+  const size_t smem = (size_t)S * LEAF_THREADS * NB * sizeof(double);
+  RUTV_ONCE_PER_DEVICE({
+    RUTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RUTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  });
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(LEAF_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = L.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RUTV_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+  return 0;
 }
 
 }  // namespace
@@ -501,34 +603,25 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
     const int wl = (int)((w - c0) < NB ? (w - c0) : NB);
     // ---- leaf factorisation (cooperative grid)
     {
-      int G = 1, R = 1;
-      leaf_plan(h - c0 - wl, &G, &R);
+      int G = 1, R = 1, S = 0;
+      leaf_plan(h - c0 - wl, &G, &R, &S);
       double* Pp = P;
       i64 hh = h, ld = ldp, cc = c0;
       int nbv = wl;
       double* taup = tau;
       double* part = qw.partials;
-      void* args[] = {&Pp, &hh, &ld, &cc, &nbv, &taup, &part};
+      double* wxp = Wx;
+      i64 ldwv = ldw;
+      void* args[] = {&Pp, &hh, &ld, &cc, &nbv, &taup, &part, &wxp, &ldwv};
       const size_t pe = L.pbegin();
       if (G <= kLeafClusterMax && R > 0 && leaf_cluster_on()) {
         // one thread-block cluster of G CTAs (non-portable size up to 16)
-        void* fn = R == 1 ? (void*)qr_leaf_kernel<1, true> : (void*)qr_leaf_kernel<2, true>;
-        if (R == 1)
-          RUTV_ONCE_PER_DEVICE(RUTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)));
-        else
-          RUTV_ONCE_PER_DEVICE(RUTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)));
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(G);
-        cfg.blockDim = dim3(LEAF_THREADS);
-        cfg.stream = L.stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = G;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        RUTV_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+        const int units = R + S;
+        if (units == 1) RUTV_TRY((launch_leaf_cluster<1, 0>(L, G, args)));
+        else if (units == 2) RUTV_TRY((launch_leaf_cluster<2, 0>(L, G, args)));
+        else if (units == 3) RUTV_TRY((launch_leaf_cluster<2, 1>(L, G, args)));
+        else if (units == 4) RUTV_TRY((launch_leaf_cluster<2, 2>(L, G, args)));
+        else RUTV_TRY((launch_leaf_cluster<2, 3>(L, G, args)));
       } else {
         void* fn = R == 1 ? (void*)qr_leaf_kernel<1, false>
                           : (R == 2 ? (void*)qr_leaf_kernel<2, false> : (void*)qr_leaf_kernel<0, false>);
@@ -538,15 +631,7 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
       // algorithmic: ~4 (h-c0) wl^2 flops (dlarfg + dlarf over the leaf); bytes: the leaf read + written once
       L.pend(PK_QR_LEAF, 4.0 * (double)(h - c0) * wl * wl, 16.0 * (double)(h - c0) * wl, pe);
     }
-    // ---- explicit W for this leaf
-    {
-      const i64 total = h * wl;
-      i64 blocks = (total + 255) / 256;
-      if (blocks > (i64)L.device_sms * 8) blocks = (i64)L.device_sms * 8;
-      extract_w_kernel<<<(unsigned)blocks, 256, 0, L.stream>>>(P, ldp, h, c0, wl, Wx, ldw);
-      L.count();
-      RUTV_CHECK_LAUNCH("extract_w_kernel");
-    }
+    // (the leaf kernel wrote the explicit W of this leaf)
     // ---- S(0:c0+wl, L) = W(c0:h, 0:c0+wl)^T W(c0:h, L)
     double* SL = qw.S + c0 * w;  // S stored w x w, ld w
     RUTV_TRY(launch_dgemm(L, true, false, c0 + wl, wl, h - c0, 1.0, Wx + c0, ldw, Wx + c0 + c0 * ldw, ldw, 0.0,

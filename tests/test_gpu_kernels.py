@@ -87,7 +87,10 @@ def test_dgemm_beta_zero_ignores_nan(ctx):
 
 
 # ------------------------------------------------------------------------- S4/S6 QR
-@pytest.mark.parametrize("h,w", [(1000, 64), (777, 45), (300, 300), (5000, 128), (40, 1), (33, 32), (4096, 256)])
+# (cluster leaf variants of qr.cu's leaf_plan: slab <= 4096 rows R=1; <= 8192 R=2;
+#  <= 12288, 16384, 20480 R=2 plus 1, 2, 3 rows per thread in shared memory)
+@pytest.mark.parametrize("h,w", [(1000, 64), (777, 45), (300, 300), (5000, 128), (40, 1), (33, 32), (4096, 256),
+                                 (10000, 64), (16384, 96), (20000, 64), (20513, 40)])
 def test_panel_qr_matches_oracle(ctx, h, w):
     rng = np.random.default_rng(h * 7 + w)
     P = rng.standard_normal((h, w))

@@ -200,3 +200,62 @@ def test_reorth_resolves_graded_spectrum():
     ro = np.abs(np.diag(randutv(A, 32, 3, 5, build_uv=False, reorth=True)["T"]))[:n // 2] / sig[:n // 2]
     assert ro.min() >= 0.5 and ro.max() <= 2.0
     assert lit.min() < 0.1 or lit.max() > 10.0
+
+
+# ---------------------------------------------------------------- NEXT-4: oversampling (reading A28)
+def test_oversample_zero_is_the_literal_scheme():
+    A = np.random.default_rng(3).standard_normal((90, 70))
+    o0, o1 = randutv(A, 16, 1, 9), randutv(A, 16, 1, 9, oversample=0)
+    for key in ("T", "U", "V"):
+        assert np.array_equal(o0[key], o1[key])
+
+
+@pytest.mark.parametrize("m,n,b", [(64, 64, 16), (80, 48, 12), (50, 50, 7)])
+def test_oversample_spanning_sample_reduces_to_svd(m, n, b):
+    """Closed form: when b + p >= s at every step the sample spans the whole
+    trailing row space, the Rayleigh-Ritz selection picks exactly its top-b right
+    singular subspace, and |diag T| = the singular values of A in order (LAPACK)."""
+    A = np.random.default_rng(m + n + b).standard_normal((m, n))
+    o = randutv(A, b, 0, 11, oversample=n)
+    s = np.linalg.svd(A, compute_uv=False)
+    assert np.max(np.abs(np.abs(np.diag(o["T"])) - s)) <= 1e-13 * s[0]
+    assert reconstruction_error(A, o["U"], o["T"], o["V"]) <= 1e-13
+    assert orthogonality_error(o["U"]) <= 1e-13 and orthogonality_error(o["V"]) <= 1e-13
+
+
+def test_oversample_select_is_rayleigh_ritz():
+    """_select returns an orthonormal basis of the b-dimensional subspace of
+    span(Y) on which A_t is largest: ||A_t Y_hat||_F^2 equals the sum of the top
+    b squared singular values of A_t Q_Y (numpy SVD)."""
+    from oracle.randutv import _orth, _select
+    rng = np.random.default_rng(5)
+    At = rng.standard_normal((120, 90)) * (0.9 ** np.arange(90))
+    Y = At.T @ rng.standard_normal((120, 24))
+    Yh = _select(At, Y, 16)
+    assert orthogonality_error(Yh) <= 1e-14
+    sv = np.linalg.svd(At @ _orth(Y), compute_uv=False)
+    assert abs(np.linalg.norm(At @ Yh) ** 2 - np.sum(sv[:16] ** 2)) <= 1e-12 * np.sum(sv[:16] ** 2)
+    # Y_hat lies in span(Y)
+    Q = _orth(Y)
+    assert np.linalg.norm(Yh - Q @ (Q.T @ Yh)) <= 1e-13
+
+
+def test_oversample_improves_range_finder_on_c1():
+    """q = 0 on c1: the rank-64 residual decreases with p and reaches the
+    Eckart-Young optimum sqrt(sum_{j > 64} sigma_j^2) within 1 % at p = b."""
+    A = make_numpy("powspec", 512, 512, cfg_index=1)
+    sig = sigma_powspec(512)
+    opt = math.sqrt(float(np.sum(sig[64:] ** 2)))
+    rhos = [randutv(A, 64, 0, 2001, k=64, thin_u=True, oversample=p)["rho"] for p in (0, 8, 32, 64)]
+    assert all(a >= b for a, b in zip(rhos, rhos[1:]))
+    assert rhos[0] > 1.2 * opt and rhos[-1] <= 1.01 * opt
+
+
+def test_oversample_invariants_ragged_tall():
+    A = np.random.default_rng(8).standard_normal((150, 101))
+    o = randutv(A, 24, 1, 4, oversample=10)
+    assert reconstruction_error(A, o["U"], o["T"], o["V"]) <= 1e-13
+    assert orthogonality_error(o["U"]) <= 1e-13 and orthogonality_error(o["V"]) <= 1e-13
+    assert np.all(np.tril(o["T"], -1) == 0.0)
+    ot = randutv(A, 24, 1, 4, oversample=10, k=48, thin_u=True)
+    assert abs(ot["rho"] - np.linalg.norm(o["T"][48:, 48:])) <= 1e-12 * np.linalg.norm(A)
