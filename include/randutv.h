@@ -116,6 +116,15 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx);
  * converge, which is how the +j status path is tested.  Returns 0, -2 (unknown
  * option) or -3 (value out of range). */
 #define RANDUTV_OPT_JACOBI_SWEEPS 1
+/* RANDUTV_OPT_OVERSAMPLE: p >= 0 (<= 4096) extra sample columns per sampled
+ * step (reading A28): G^(i) has b + p columns
+ * (the first b are the draws of p = 0), Y = (A_t^T A_t)^q A_t^T G, and the b
+ * directions of span(Y) along which A_t is largest are kept (Rayleigh-Ritz:
+ * Q_Y, the Householder QR of A_t Q_Y and the Jacobi SVD of its R) before the
+ * QR that defines V-hat.  p is capped at n - k - b per step.  0 (default) is
+ * the paper's scheme.  Honoured by randutv_factor_ex / _rank / _tol; the
+ * host-streamed and sharded entries return -9 while it is set. */
+#define RANDUTV_OPT_OVERSAMPLE 2
 RANDUTV_API int randutv_set_option(randutv_ctx* ctx, int option, int64_t value);
 
 /* Re-bind the ctx to another stream of the same device. */
@@ -289,6 +298,23 @@ typedef struct randutv_host_report {
 RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b,
                                     int q, uint64_t seed, unsigned flags, size_t device_cache_bytes, double* U_host,
                                     int64_t ldu, double* V_host, int64_t ldv, randutv_host_report* report);
+
+/* Resumable host-streamed randUTV ("resumable per
+ * iteration"): runs sampled steps [step_begin, min(step_end, nsteps)) of the
+ * factorisation whose state lives in the host buffers, and the final step if
+ * step_end > nsteps (nsteps = ceil((n - b) / b) sampled steps).  step_begin =
+ * 0 starts from A (U, V := I); step_begin = j > 0 continues from the host
+ * A_host (= T after step j-1), U_host and V_host a range ending at j left
+ * behind -- with the counter-based G (reading A7) the state (j, T, U, V, seed)
+ * is a complete checkpoint, e.g. saved to disk between calls.  Ranges give
+ * the single call's factorisation to rounding (the deferred U / V transforms
+ * are merged per range).  Arguments as randutv_factor_host plus 15
+ * step_begin (>= 0, <= nsteps), 16 step_end (> step_begin; INT64_MAX = to
+ * the end), 17 report. */
+RANDUTV_API int randutv_factor_host_steps(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda,
+                                          int64_t b, int q, uint64_t seed, unsigned flags, size_t device_cache_bytes,
+                                          double* U_host, int64_t ldu, double* V_host, int64_t ldv,
+                                          int64_t step_begin, int64_t step_end, randutv_host_report* report);
 
 /* ---------------------------------------------------------------------------
  * HQRRP: the paper's other factorisation, the blocked

@@ -811,6 +811,7 @@ int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, dou
   // local checks first; no rank returns before the agreement, so a rank whose
   // arguments or workspace fail never leaves its peers blocked in a collective
   int local = b < 1 ? -6 : dist_check(lay, A, lda, q, flags, U, ldu, V, ldv);
+  if (local == 0 && ctx->oversample > 0) local = -9;  // oversampling is single-GPU only
   const bool uv = !(flags & RANDUTV_NO_UV);
   i64 K = -1;
   if (local == 0 && k != 0) {

@@ -45,6 +45,7 @@ struct randutv_ctx {
   // GEMM tile-scheduler counters: [0..1] main stream, [2..3] side stream (zeroed once)
   int* sched;
   int jacobi_max_sweeps;  // 0 = the default 30 (randutv_set_option)
+  int64_t oversample;     // p extra sample columns (randutv_set_option, reading A28)
   rutv::Launch with_opts(rutv::Launch l) const {
     if (jacobi_max_sweeps > 0) l.jacobi_max_sweeps = jacobi_max_sweeps;
     return l;
@@ -94,6 +95,7 @@ struct Work {
   double* Acat;   // fused S5/S7 update operands: [Z2(k:m) | W_U]  (m x 2b)
   double* Bt;     //                              [W2 | Y^T]       (n x 2b)
   double *Zv, *Zv2, *gemm_ws_v;  // temporaries of the V stream (n x b each; split-K)
+  double *osR, *osU, *osV, *osd, *osjac;  // oversampling: Rayleigh-Ritz SVD (b x b each; b = b + p)
 };
 
 i64 gemm_ws_elems_for(i64 m, i64 n, i64 b);

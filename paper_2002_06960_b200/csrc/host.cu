@@ -409,6 +409,9 @@ int defer_uv(HostRun& R, HostRun::Batch& B, i64 k, const double* W, i64 ldw, con
 // is resident.  Only step 0 needs a separate S2 pass.
 int host_sampled_step(HostRun& R, i64 i) {
   Work& w = R.w;
+  // pass directions depend on the step only (not on the history of the call),
+  // so a run resumed at step i streams -- and sums -- exactly like one call
+  R.dir = (i & 1) == 0;
   const i64 m = R.m, n = R.n, b = R.b, k = i * b, r = m - k, s = n - k;
   const i64 np = R.pc.mats[R.mT].npanels;
   const bool next_sampled = s - b > b;
@@ -507,12 +510,36 @@ using namespace rutv;
 
 extern "C" {
 
+static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b, int q,
+                            uint64_t seed, unsigned flags, size_t device_cache_bytes, double* U_host, int64_t ldu,
+                            double* V_host, int64_t ldv, int64_t step_begin, int64_t step_end,
+                            randutv_host_report* report);
+
 RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b,
                                     int q, uint64_t seed, unsigned flags, size_t device_cache_bytes, double* U_host,
                                     int64_t ldu, double* V_host, int64_t ldv, randutv_host_report* report) {
+  return factor_host_impl(ctx, m, n, A_host, lda, b, q, seed, flags, device_cache_bytes, U_host, ldu, V_host, ldv, 0,
+                          INT64_MAX, report);
+}
+
+RANDUTV_API int randutv_factor_host_steps(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda,
+                                          int64_t b, int q, uint64_t seed, unsigned flags, size_t device_cache_bytes,
+                                          double* U_host, int64_t ldu, double* V_host, int64_t ldv,
+                                          int64_t step_begin, int64_t step_end, randutv_host_report* report) {
+  if (step_begin < 0) return -15;
+  if (step_end <= step_begin) return -16;
+  return factor_host_impl(ctx, m, n, A_host, lda, b, q, seed, flags, device_cache_bytes, U_host, ldu, V_host, ldv,
+                          step_begin, step_end, report);
+}
+
+static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b, int q,
+                            uint64_t seed, unsigned flags, size_t device_cache_bytes, double* U_host, int64_t ldu,
+                            double* V_host, int64_t ldv, int64_t step_begin, int64_t step_end,
+                            randutv_host_report* report) {
   RUTV_TRY(begin_call(ctx));
   const bool uv = !(flags & RANDUTV_NO_UV);
   if (flags & RANDUTV_REORTH) return -9;  // not implemented on the host-streamed path
+  if (ctx->oversample > 0) return -9;      // nor is oversampling (RANDUTV_OPT_OVERSAMPLE)
   if (n < 1) return -3;
   if (m < n) return -2;
   if (!A_host) return -4;
@@ -620,8 +647,11 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
     cudaEventRecord(t0, ctx->stream);
     st = start_status(ctx, R.w);
   }
-  // U := I, V := I panel by panel on the device (no host traffic in)
-  if (st == 0 && uv) {
+  const i64 nsamp = sampled_steps(n, bb);
+  if (st == 0 && step_begin > nsamp) st = -15;  // past the final step
+  // U := I, V := I panel by panel on the device (no host traffic in); a
+  // resumed range (step_begin > 0) continues from the U, V in host memory
+  if (st == 0 && uv && step_begin == 0) {
     for (int mat : {R.mU, R.mV}) {
       const HostMat& M = R.pc.mats[mat];
       for (i64 j = 0; j < M.npanels && st == 0; ++j) {
@@ -649,9 +679,13 @@ RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, doub
     if (st == 0 && flag) st = RANDUTV_ERR_NONFINITE;
   }
   if (st == 0) {
-    const i64 nsamp = sampled_steps(n, bb);
-    for (i64 i = 0; i < nsamp && st == 0; ++i) st = host_sampled_step(R, i);
-    if (st == 0) st = host_final_step(R, nsamp);
+    const i64 last = std::min<i64>(step_end, nsamp);
+    for (i64 i = step_begin; i < last && st == 0; ++i) st = host_sampled_step(R, i);
+    if (st == 0 && step_end > nsamp) st = host_final_step(R, nsamp);
+    // a range that stops before the final step leaves no deferred U / V
+    // transform behind: the host U, V are the state after step last - 1
+    if (st == 0 && step_end <= nsamp) st = flush_uv(R, R.bv);
+    if (st == 0 && step_end <= nsamp) st = flush_uv(R, R.bu);
     if (st == 0) st = R.pc.flush();
     if (st == 0) {
       // the compute stream must not return before the write-backs land

@@ -109,10 +109,15 @@ __device__ __forceinline__ int jacobi_pair(double* xp, double* xq, double* wp, d
   a = warp_sum(a);
   bb = warp_sum(bb);
   g = warp_sum(g);
-  if (!(a > nu2 && bb > nu2 && fabs(g) > tol * sqrt(a * bb))) return 0;
-  const double zeta = (bb - a) / (2.0 * g);
-  const double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-  const double c = 1.0 / sqrt(1.0 + t * t);
+  // |g| > tol sqrt(a bb) without the square root (FP64 sqrt / division are
+  // the long-latency steps of a rotation; a, bb > nu2 keep the product in range)
+  if (!(a > nu2 && bb > nu2 && g * g > (tol * tol) * (a * bb))) return 0;
+  // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (bb - a) / (2 g),
+  // written as 2 g sign(bb - a) / (|bb - a| + sqrt((bb - a)^2 + 4 g^2)): one
+  // square root and one division; c = 1 / sqrt(1 + t^2) by rsqrt
+  const double dba = bb - a;
+  const double t = copysign(1.0, dba) * (2.0 * g) / (fabs(dba) + sqrt(fma(dba, dba, 4.0 * g * g)));
+  const double c = rsqrt(fma(t, t, 1.0));
   const double s = c * t;
   for (int r = lane; r < w; r += 32) {
     const double u = xp[r], v = xq[r];
@@ -472,6 +477,9 @@ __global__ void __launch_bounds__(JCT, 1)
     ++sweeps;
   }
   if (!converged && cta == 0 && tid == 0) atomicMin(status, block_id);
+#ifdef RUTV_JACOBI_PROF
+  if (cta == 0 && tid == 0) printf("jacobi_cluster w=%d P=%d sweeps=%d\n", w, P, sweeps);
+#endif
 
   // ---- column norms, global ranks (stable descending), outputs
   double* Xc = buf[cur];
@@ -546,7 +554,9 @@ int launch_jacobi_svd(const Launch& L, i64 w, const double* B, i64 ldb, double* 
   RUTV_CUDA(cudaMemsetAsync(iflags, 0, sizeof(int) * (MAX_SWEEPS + 2), L.stream));
   const size_t pe = L.pbegin();
   const int msw0 = L.jacobi_max_sweeps < 1 ? 1 : (L.jacobi_max_sweeps > MAX_SWEEPS ? MAX_SWEEPS : L.jacobi_max_sweeps);
-  if (w <= 256 && jacobi_cluster_on()) {
+  // the cluster variant measured faster for w <= 128, the L2-staged kernel
+  // (16 warps per CTA) for w = 256 (tools/leaf_ab.sh)
+  if (w <= 128 && jacobi_cluster_on()) {
     // data-resident cluster variant: nb = 8, P = nc / 16 CTAs (<= 16)
     const int nb = 8, nc = (int)((w + 15) / 16 * 16), P = nc / 16;
     const size_t smem = (size_t)4 * nb * ((size_t)w + nc) * sizeof(double);

@@ -54,38 +54,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Cross-CTA reduction of the PSTRIDE partial sums of column j: every CTA
-// reads all G records (coalesced, all loads in flight), then warp w sums values
-// e = w, w+8, ... with lanes over CTAs + xor butterfly -- the same fixed order
-// in every CTA, so every CTA obtains bitwise identical totals.
-__device__ __forceinline__ void reduce_partials(const double* __restrict__ pj, int G, double* stage, double* tot,
-                                                int tid, int lane, int warp) {
-  // all loads in flight at once (a loop of load -> shared store pairs left the
-  // G x 33 reads ~3 L2 round trips deep; tools/sync_micro.cu: write + grid.sync
-  // + read of 64 records 3.6 us vs grid.sync alone 1.2 us), and past L1: the
-  // same buffer was read two columns ago
-  constexpr int PER = (LEAF_MAX_CTAS * PSTRIDE + LEAF_THREADS - 1) / LEAF_THREADS;
-  double tmp[PER];
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int e = tid + q * LEAF_THREADS;
-    tmp[q] = e < G * PSTRIDE ? __ldcg(pj + e) : 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    const int e = tid + q * LEAF_THREADS;
-    if (e < G * PSTRIDE) stage[e] = tmp[q];
-  }
-  __syncthreads();
-  for (int e = warp; e < PSTRIDE; e += LEAF_THREADS / 32) {
-    double s = 0.0;
-    for (int c = lane; c < G; c += 32) s += stage[c * PSTRIDE + e];
-    s = warp_sum(s);
-    if (lane == 0) tot[e] = s;
-  }
-  __syncthreads();
-}
-
 // P points at the panel's top-left element (row 0, col 0); the leaf is columns
 // [c0, c0+nb), rows [c0, h).  Rows [c0, c0+nb) form the replicated top block;
 // rows [c0+nb, h) are split into contiguous slabs, one per CTA.  R > 0: each
@@ -112,7 +80,6 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
   __shared__ double tot[PSTRIDE];
   __shared__ double wv[NB];
   __shared__ double sc[4];  // tau, scal, beta, flag
-  __shared__ double stage[(CLUSTER ? 16 : LEAF_MAX_CTAS) * PSTRIDE];
   extern __shared__ double slab_s[];  // S * LEAF_THREADS rows x NB columns
   constexpr int SLD = S * LEAF_THREADS;
 
@@ -252,16 +219,17 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
       // next, and cannot write this one again before every CTA has passed the
       // next barrier, i.e. finished reading it
       cl.sync();
-      for (int e = tid; e < G * PSTRIDE; e += LEAF_THREADS) {
-        const double* rr = cl.map_shared_rank(&mine[jj & 1][0], e / PSTRIDE);
-        stage[e] = rr[e % PSTRIDE];
-      }
-      __syncthreads();
-      for (int e = warp; e < PSTRIDE; e += LEAF_THREADS / 32) {
+      // thread e < 33 sums value e over the G records straight from the other
+      // CTAs' shared memory (all G DSMEM loads in flight, then a fixed-order
+      // sum: every CTA obtains bitwise identical totals)
+      if (tid < PSTRIDE) {
+        double vals[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) vals[c] = c < G ? *cl.map_shared_rank(&mine[jj & 1][tid], c) : 0.0;
         double s3 = 0.0;
-        for (int c = lane; c < G; c += 32) s3 += stage[c * PSTRIDE + e];
-        s3 = warp_sum(s3);
-        if (lane == 0) tot[e] = s3;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) s3 += vals[c];
+        tot[tid] = s3;
       }
       __syncthreads();
     } else {
@@ -273,8 +241,21 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
         pj[(size_t)cta * PSTRIDE + tid] = s2;
       }
       cg::this_grid().sync();
-      // ---------------- phase B: every CTA reduces the partials in the same order
-      reduce_partials(pj, G, stage, tot, tid, lane, warp);
+      // ---------------- phase B: every CTA reduces the partials in the same
+      // order: thread e < 33 streams value e of the G records from L2 (16
+      // loads in flight per batch)
+      if (tid < PSTRIDE) {
+        double s3 = 0.0;
+        for (int c0b = 0; c0b < G; c0b += 16) {
+          double vals[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) vals[c] = c0b + c < G ? __ldcg(pj + (size_t)(c0b + c) * PSTRIDE + tid) : 0.0;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) s3 += vals[c];
+        }
+        tot[tid] = s3;
+      }
+      __syncthreads();
     }
     LEAF_T(3);
     if (warp == 0) {
@@ -526,7 +507,14 @@ void leaf_plan(i64 slab_rows, int* G, int* R, int* S) {
   *S = 0;
   if (leaf_cluster_on()) {
     const i64 per_cta_rows = (i64)kLeafClusterMax * LEAF_THREADS;  // rows per (R + S) unit over 16 CTAs
-    for (int units = 1; units <= 5; ++units) {
+    static int maxu = -1;  // RUTV_LEAF_MAXUNITS: cap on (R + S) rows per thread of the cluster leaf (tuning)
+    if (maxu < 0) {
+      const char* e = getenv("RUTV_LEAF_MAXUNITS");
+      // measured (tools/leaf_ab.sh): the cluster leaf wins up to 3 rows per
+      // thread (slab <= 12288); taller slabs are faster on the 64+ CTA grid
+      maxu = e ? atoi(e) : 3;
+    }
+    for (int units = 1; units <= maxu; ++units) {
       if (slab_rows <= per_cta_rows * units) {
         const int r = units >= 2 ? 2 : 1;
         *R = r;

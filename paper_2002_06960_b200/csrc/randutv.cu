@@ -176,6 +176,11 @@ size_t carve(Carver& c, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork) {
   w.qw.partials = c.take<double>(w.qw.partials_elems);
   w.qw.gemm_ws = w.gemm_ws;
   w.qw.gemm_ws_elems = w.gemm_ws_elems;
+  w.osR = c.take<double>(b * b);
+  w.osU = c.take<double>(b * b);
+  w.osV = c.take<double>(b * b);
+  w.osd = c.take<double>(b);
+  w.osjac = c.take<double>(jacobi_scratch_elems(b));
   w.lefts_elems = lefts_K > 0 ? lefts_elems_for(m, b, lefts_K) : 0;
   w.lefts = lefts_K > 0 ? c.take<double>(w.lefts_elems) : nullptr;
   w.Twork = twork ? c.take<double>(m * n) : nullptr;
@@ -447,6 +452,7 @@ struct Problem {
   Launch vl;              // V stream (oneshot GEMMs); vl.stream == nullptr: V on the main stream
   cudaEvent_t eWv, eV;
   bool reorth = false;    // RANDUTV_REORTH: orthonormal Y, Z between power steps (NEXT-4)
+  i64 os = 0;             // oversampling p (reading A28; randutv_set_option)
   // U update on the V stream (after the V update of the same step): it overlaps
   // the next step's sampling, S4 QR and S5; the next S6 (overwrites W_U, T_U),
   // the side stream's U fold and the final step wait for eU
@@ -517,21 +523,43 @@ int orthonormalize(const Launch& L, Work& w, i64 h, i64 b, double* X) {
   return launch_dgemm(L, false, false, h, b, b, -1.0, w.Wu, h, w.qw.S, b, 1.0, X, h, nullptr, 0);
 }
 
+// Reading A28 (oversampling; oracle.randutv._select): the
+// sample Y (s x bp, bp = b + p) is reduced to the b directions of span(Y) on
+// which A_t is largest -- Y := Q_Y (explicit Householder basis), B = A_t Q_Y,
+// R_B from the Householder QR of B, R_B = U_R diag(d) V_R^T (Jacobi), and
+// Y(:, 0:b) := Q_Y V_R(:, 0:b).  Uses the S6 buffers W_U, T_U, tau_U (the
+// caller waited for the previous U update) and the os* Jacobi buffers.
+int select_sample(const Launch& L, Work& w, i64 r, i64 s, i64 b, i64 bp, const double* At, i64 lda, int block_id) {
+  RUTV_TRY(orthonormalize(L, w, s, bp, w.Y));
+  RUTV_TRY(launch_dgemm(L, false, false, r, bp, s, 1.0, At, lda, w.Y, s, 0.0, w.Z, r, w.gemm_ws, w.gemm_ws_elems));
+  RUTV_TRY(panel_qr(L, r, bp, w.Z, r, w.tauU, w.Wu, r, w.TU, bp, w.qw));
+  RUTV_TRY(launch_copy(L, bp, bp, w.Z, r, w.osR, bp));
+  RUTV_TRY(launch_triu(L, bp, bp, w.osR, bp));
+  RUTV_TRY(launch_jacobi_svd(L, bp, w.osR, bp, w.osU, w.osd, w.osV, w.status, block_id, w.osjac,
+                             jacobi_scratch_elems(bp)));
+  RUTV_TRY(launch_dgemm(L, false, false, s, b, bp, 1.0, w.Y, s, w.osV, bp, 0.0, w.Z2, s, nullptr, 0));
+  return launch_copy(L, s, b, w.Z2, s, w.Y, s);
+}
+
 int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   const i64 m = P.m, n = P.n, b = P.b, kk = i * b, r = m - kk, s = n - kk;
   double* At = P.T + kk + kk * P.ldt;
+  // oversampling: b + p sample columns, p capped at s - b (reading A28)
+  const i64 pi = P.os < s - b ? P.os : s - b;
+  const i64 bp = b + (pi > 0 ? pi : 0);
   // S1, S2, S3
-  RUTV_TRY(launch_gaussian(L, P.seed, i, r, b, w.G, r));
-  RUTV_TRY(launch_dgemm(L, true, false, s, b, r, 1.0, At, P.ldt, w.G, r, 0.0, w.Y, s, w.gemm_ws, w.gemm_ws_elems));
-  if (P.reorth && P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));  // W_U, T_U are reused below
+  RUTV_TRY(launch_gaussian(L, P.seed, i, r, bp, w.G, r));
+  RUTV_TRY(launch_dgemm(L, true, false, s, bp, r, 1.0, At, P.ldt, w.G, r, 0.0, w.Y, s, w.gemm_ws, w.gemm_ws_elems));
+  if ((P.reorth || bp > b) && P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));  // W_U, T_U are reused below
   for (int qq = 0; qq < P.q; ++qq) {
-    if (P.reorth) RUTV_TRY(orthonormalize(L, w, s, b, w.Y));
-    RUTV_TRY(launch_dgemm(L, false, false, r, b, s, 1.0, At, P.ldt, w.Y, s, 0.0, w.Z, r, w.gemm_ws,
+    if (P.reorth) RUTV_TRY(orthonormalize(L, w, s, bp, w.Y));
+    RUTV_TRY(launch_dgemm(L, false, false, r, bp, s, 1.0, At, P.ldt, w.Y, s, 0.0, w.Z, r, w.gemm_ws,
                           w.gemm_ws_elems));
-    if (P.reorth) RUTV_TRY(orthonormalize(L, w, r, b, w.Z));
-    RUTV_TRY(launch_dgemm(L, true, false, s, b, r, 1.0, At, P.ldt, w.Z, r, 0.0, w.Y, s, w.gemm_ws,
+    if (P.reorth) RUTV_TRY(orthonormalize(L, w, r, bp, w.Z));
+    RUTV_TRY(launch_dgemm(L, true, false, s, bp, r, 1.0, At, P.ldt, w.Z, r, 0.0, w.Y, s, w.gemm_ws,
                           w.gemm_ws_elems));
   }
+  if (bp > b) RUTV_TRY(select_sample(L, w, r, s, b, bp, At, P.ldt, (int)(i + 1)));
   // S4 (overwrites W_V, T_V: the previous step's V update must have read them)
   if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
   RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
@@ -810,6 +838,11 @@ RANDUTV_API int randutv_set_option(randutv_ctx* ctx, int option, int64_t value) 
     ctx->jacobi_max_sweeps = (int)value;
     return 0;
   }
+  if (option == RANDUTV_OPT_OVERSAMPLE) {
+    if (value < 0 || value > 4096) return -3;
+    ctx->oversample = value;
+    return 0;
+  }
   return -2;
 }
 
@@ -933,7 +966,7 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
   const i64 nrec = econ ? nsamp + 1 : 0;
   Launch L = ctx->launch();
   Work w;
-  RUTV_TRY(prepare(ctx, w, m, n, bb, nrec, false));
+  RUTV_TRY(prepare(ctx, w, m, n, bb + ctx->oversample, nrec, false));
   if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
   RUTV_TRY(start_status(ctx, w));
   if (!alias) RUTV_CUDA(cudaMemcpy2DAsync(T, ldt * 8, A, lda * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream));
@@ -944,6 +977,7 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
   Problem P{m, n, bb, q, seed, T, ldt, (uv && !econ) ? U : nullptr, ldu, uv ? V : nullptr, ldv, econ,
             ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
   P.reorth = (flags & RANDUTV_REORTH) != 0;
+  P.os = ctx->oversample;
   P.ustream = P.U && P.vl.stream && ustream_on();
   P.eWu = ctx->eWu;
   P.eU = ctx->eU;
@@ -1051,13 +1085,13 @@ int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64
     // the main workspace followed by the resid_2 region (fixed k: the
     // trailing block is (m - k) x (n - k))
     Carver dry{nullptr, 0, 0, true};
-    carve(dry, w, m, n, bb, nrec_max, true);
+    carve(dry, w, m, n, bb + ctx->oversample, nrec_max, true);
     carve_spec(dry, sw, m - k, n - k);
     RUTV_TRY(ensure_ws(ctx, dry.off));
     Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
-    carve(real, w, m, n, bb, nrec_max, true);
+    carve(real, w, m, n, bb + ctx->oversample, nrec_max, true);
   } else {
-    RUTV_TRY(prepare(ctx, w, m, n, bb, nrec_max, true));
+    RUTV_TRY(prepare(ctx, w, m, n, bb + ctx->oversample, nrec_max, true));
   }
   if (flags & RANDUTV_CHECK_FINITE) RUTV_TRY(check_finite(ctx, L, w, m, n, A, lda));
   RUTV_TRY(start_status(ctx, w));
@@ -1066,6 +1100,7 @@ int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64
   Problem P{m, n, bb, q, seed, w.Twork, m, nullptr, m, uv ? V : nullptr, ldv, uv,
             ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
   P.reorth = (flags & RANDUTV_REORTH) != 0;
+  P.os = ctx->oversample;
   if (!adaptive) {
     RUTV_TRY(run_loop(L, w, P, K, with_final));
   } else {
@@ -1110,7 +1145,7 @@ int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64
   if (resid_2 && k < n) {
     Carver rc{(char*)ctx->ws, 0, ctx->ws_bytes, false};
     Work wdummy;
-    carve(rc, wdummy, m, n, bb, nrec_max, true);
+    carve(rc, wdummy, m, n, bb + ctx->oversample, nrec_max, true);
     carve_spec(rc, sw, m - k, n - k);
     RUTV_TRY(spectral_norm(L, sw, m - k, n - k, w.Twork + k + k * m, m, seed, &squared));
     RUTV_CUDA(cudaMemcpyAsync(&s2, sw.d, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

@@ -23,6 +23,7 @@ RANDUTV_REORTH = 4
 RANDUTV_ASYNC = 8
 RANDUTV_ECON_U = 16
 RANDUTV_OPT_JACOBI_SWEEPS = 1
+RANDUTV_OPT_OVERSAMPLE = 2
 RANDUTV_ERR_BASE = 0x40000000
 RANDUTV_ERR_CUDA = RANDUTV_ERR_BASE + 0
 RANDUTV_ERR_ALLOC = RANDUTV_ERR_BASE + 1
@@ -87,6 +88,8 @@ SIGNATURES = {
     "randutv_small_svd": (_int, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
     "randutv_factor_host": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint, ctypes.c_size_t, _vp, _i64,
                                    _vp, _i64, ctypes.POINTER(HostReport)]),
+    "randutv_factor_host_steps": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint, ctypes.c_size_t, _vp,
+                                         _i64, _vp, _i64, _i64, _i64, ctypes.POINTER(HostReport)]),
     "randutv_dist_layout": (_int, [_i64, _i64, _i64, _int, _int, ctypes.POINTER(_i64)]),
     "randutv_nccl_unique_id": (_int, [_vp]),
     "randutv_comm_init": (_int, [_vp, _vp, _int, _int]),
@@ -367,6 +370,22 @@ class Context:
                                           _hptr(V), _hld(V) if V is not None else 1, ctypes.byref(rep))
         _check("randutv_factor_host", st)
         return U, V, {k: getattr(rep, k) for k, _ in HostReport._fields_}
+
+    def randutv_factor_host_steps(self, A, U, V, b, q, seed, step_begin, step_end, build_uv=True, cache_bytes=0,
+                                  flags=0):
+        """Steps [step_begin, step_end) of the host-streamed randUTV on the host state
+        (A = T so far, U, V; resumable, see randutv.h); returns the report."""
+        m, n = A.shape
+        if not build_uv:
+            flags |= RANDUTV_NO_UV
+        rep = HostReport()
+        st = self.lib.randutv_factor_host_steps(self.h, m, n, _hptr(A), _hld(A), int(b), int(q),
+                                                int(seed) & (2**64 - 1), flags, int(cache_bytes), _hptr(U),
+                                                _hld(U) if U is not None else 1, _hptr(V),
+                                                _hld(V) if V is not None else 1, int(step_begin),
+                                                min(int(step_end), 2**63 - 1), ctypes.byref(rep))
+        _check("randutv_factor_host_steps", st)
+        return {k: getattr(rep, k) for k, _ in HostReport._fields_}
 
     # ---------------------------------------------------------------- multi-GPU
     def comm_init(self, unique_id, nranks, rank):

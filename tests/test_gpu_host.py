@@ -86,3 +86,46 @@ def test_host_streamed_nonfinite(ctx):
     with pytest.raises(RandUTVError) as e:
         ctx.randutv_factor_host(A, 16, 1, 1, build_uv=False, flags=RANDUTV_CHECK_FINITE, cache_bytes=3 * 64 * 16 * 8)
     assert e.value.status == RANDUTV_ERR_NONFINITE
+
+
+@pytest.mark.parametrize("cuts", [[2], [1, 3, 5], [7]])
+def test_host_streamed_resume(ctx, cuts):
+    """randutv_factor_host_steps (resumable per iteration):
+    the host state (j, T, U, V) after steps [0, j) is a complete checkpoint --
+    a fresh context resumes from copies of it, and the ranges give the single
+    call's factorisation (and the oracle's) to rounding."""
+    from paper_2002_06960_b200.randutv import Context, pinned_colmajor
+    m, n, b, q, seed = 300, 280, 32, 1, 17   # 8 sampled steps + a final block
+    rng = np.random.default_rng(99)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    U1, T1, V1, _ = _run_host(ctx, A, b, q, seed, 4)
+    Ah, Uh, Vh = pinned_colmajor(m, n), pinned_colmajor(m, m), pinned_colmajor(n, n)
+    Ah[:] = A
+    bounds = [0] + cuts + [2 ** 62]
+    for lo, hi in zip(bounds, bounds[1:]):
+        c = Context()   # a new process / context per range: only the host state carries over
+        try:
+            ck = (np.array(Ah), np.array(Uh), np.array(Vh))   # the checkpoint, restored below
+            Ah[:], Uh[:], Vh[:] = ck
+            c.randutv_factor_host_steps(Ah, Uh, Vh, b, q, seed, lo, hi, cache_bytes=4 * max(m, n) * b * 8)
+        finally:
+            c.close()
+    T2, U2, V2 = np.array(Ah), np.array(Uh), np.array(Vh)
+    nA = np.linalg.norm(A)
+    assert np.max(np.abs(T2 - T1)) / nA <= 1e-13
+    assert np.max(np.abs(U2 - U1)) <= 1e-12 and np.max(np.abs(V2 - V1)) <= 1e-12
+    o = oracle_randutv(A, b, q, seed)
+    assert recon_error(A, U2, T2, V2) <= 1e-12
+    assert diag_parity(np.diag(T2), np.diag(o["T"])) <= 1.0
+    assert np.max(np.abs(np.abs(T2) - np.abs(o["T"]))) / nA <= ELEM_TOL
+
+
+def test_host_streamed_resume_arguments(ctx):
+    from paper_2002_06960_b200.randutv import RandUTVError
+    A = np.zeros((64, 64), order="F")
+    with pytest.raises(RandUTVError) as e:
+        ctx.randutv_factor_host_steps(A, None, None, 16, 1, 1, 3, 3, build_uv=False)
+    assert e.value.status == -16
+    with pytest.raises(RandUTVError) as e:
+        ctx.randutv_factor_host_steps(A, None, None, 16, 1, 1, 9, 12, build_uv=False)
+    assert e.value.status == -15
