@@ -307,8 +307,17 @@ def run_ours(args):
             step()
     torch.cuda.synchronize()
     graph_launches = None
-    if args.graph and (sharded or trunc_k is not None):
-        args.graph = False  # graphs are captured for the full single-GPU factorisation only
+    if args.graph and trunc_k is not None:
+        args.graph = False  # graphs are captured for the full factorisation only
+
+    def async_call():
+        # the step as one RANDUTV_ASYNC call (no host synchronisation inside):
+        # single-GPU, or the sharded NCCL path (its collectives are captured too)
+        if sharded:
+            T_loc.copy_(A_loc)
+            ctx.randutv_factor_dist(T_loc, m, n, b, q, seed, U_local=U_loc, V_local=V_loc, flags=8)
+        else:
+            ctx.randutv_factor_ex(A, b, q, seed, U=U, T=T, V=V, flags=fl | 8)  # RANDUTV_ASYNC
     if args.graph:
         # the whole factorisation (main, side and V streams) as one CUDA graph.
         # Two captures of the same call: g without and gp with the per-launch
@@ -321,12 +330,12 @@ def run_ours(args):
             ctx.set_profiling(False)
             ctx.reset_stats()
             with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
-                ctx.randutv_factor_ex(A, b, q, seed, U=U, T=T, V=V, flags=fl | 8)  # RANDUTV_ASYNC
+                async_call()
             graph_launches = ctx.stats()["kernel_launches"]
             if gp is not g:
                 ctx.set_profiling(True)
                 with torch.cuda.graph(gp, stream=stream, capture_error_mode="relaxed"):
-                    ctx.randutv_factor_ex(A, b, q, seed, U=U, T=T, V=V, flags=fl | 8)
+                    async_call()
             with torch.cuda.stream(stream):
                 g.replay()
                 gp.replay()
@@ -341,6 +350,8 @@ def run_ours(args):
             torch.cuda.synchronize()
             ctx.close()
             ctx = Context(dev, stream)
+            if sharded:
+                ctx.comm_init_torch()
             args.graph = False
             graph_launches = None
 

@@ -417,7 +417,15 @@ RANDUTV_API int randutv_comm_init(randutv_ctx* ctx, const void* unique_id, int n
  * V_local (nv x n) receive the rank's rows of U and V (ignored with
  * RANDUTV_NO_UV).  Status: as randutv_factor_ex, identical on every rank (+j
  * Jacobi non-convergence is agreed by an AllReduce-min); RANDUTV_ERR_NOCOMM
- * without randutv_comm_init.  Arguments: 1 ctx, 2 m, 3 n, 4 A_local, 5 lda,
+ * without randutv_comm_init.  Before the first collective every rank's
+ * argument / workspace verdict is agreed (a rank that fails returns its own
+ * code, its peers RANDUTV_ERR_PEER -- nobody is left blocked in a
+ * collective); waits poll ncclCommGetAsyncError and abort the communicators
+ * after RUTV_NCCL_TIMEOUT_S seconds (default 1800) with RANDUTV_ERR_NCCL.
+ * flags & RANDUTV_ASYNC: enqueue only (no host synchronisation, no
+ * agreement: the arguments must be rank-uniform), capturable into a CUDA
+ * graph with its NCCL collectives; randutv_wait gives the status.  Not with
+ * RANDUTV_CHECK_FINITE or the loopback back end (-9).  Arguments: 1 ctx, 2 m, 3 n, 4 A_local, 5 lda,
  * 6 b, 7 q, 8 seed, 9 flags, 10 U_local, 11 ldu, 12 V_local, 13 ldv. */
 RANDUTV_API int randutv_factor_dist(randutv_ctx* ctx, int64_t m, int64_t n, double* A_local, int64_t lda,
                                     int64_t b, int q, uint64_t seed, unsigned flags, double* U_local, int64_t ldu,

@@ -104,9 +104,15 @@ struct Comm {
   virtual int allgather(const double* send, double* recv, i64 count, cudaStream_t s) = 0;
   virtual int bcast(double* buf, i64 count, int root, cudaStream_t s) = 0;
   virtual int allreduce_min_int(int* buf, i64 count, cudaStream_t s) = 0;
+  // row chunks of a pipelined GEMM -> AllReduce (1: no pipelining; the
+  // loopback's collectives synchronise the host, so chunking only adds barriers)
+  virtual int chunks() const { return 1; }
+  // collectives can be captured into a CUDA graph (NCCL: yes; loopback: no)
+  virtual bool capturable() const { return false; }
 };
 
 void comm_free(Comm* c) { delete c; }
+int comm_sync(Comm* c, cudaStream_t s) { return c->sync(s); }
 
 // ---------------------------------------------------------------- NCCL
 
@@ -252,6 +258,8 @@ struct NcclComm : Comm {
     RUTV_NCCL(api->AllReduce(buf, buf, (size_t)count, ncclInt32, ncclMin, comm, s));
     return 0;
   }
+  int chunks() const override { return nranks > 1 ? 4 : 1; }
+  bool capturable() const override { return true; }
 };
 
 // ---------------------------------------------------------------- loopback
@@ -461,6 +469,7 @@ struct DistWork {
   double* colss;   // truncated: per-local-column sums of squares (n_p), then the total
   double* blk;     // truncated: one row block of U_k (b x k) for the U_s application
   double* blkz;    // the pending row block's partial (T W_V) rows (b x b) for its AllReduce
+  double* zc;      // chunked GEMM -> AllReduce: the row chunks, each contiguous (m x b)
 };
 
 size_t carve_dist(Carver& c, DistWork& d, const Layout& lay, i64 K, i64 k) {
@@ -476,6 +485,7 @@ size_t carve_dist(Carver& c, DistWork& d, const Layout& lay, i64 K, i64 k) {
   d.colss = K > 0 ? c.take<double>(lay.ncols(lay.p) + 8) : nullptr;
   d.blk = K > 0 ? c.take<double>(b * k) : nullptr;
   d.blkz = c.take<double>(b * b);
+  d.zc = c.take<double>(m * b);
   return c.off;
 }
 
@@ -493,6 +503,8 @@ struct DistProblem {
   bool uv;      // U and V requested (rank-uniform; U / V above are null on ranks without rows)
 };
 
+constexpr int kMaxChunks = 4;
+
 struct DistRun {
   randutv_ctx* ctx;
   Comm* comm;
@@ -500,7 +512,49 @@ struct DistRun {
   DistWork d;
   DistProblem P;
   Launch L, S;
+  // V stream (one CTA per GEMM tile, as the single-GPU driver): the V update of
+  // step i after QR(Y) and the U update after the (W_U, T_U) broadcast run
+  // there, overlapping the column-block QR, the T updates and the next step's
+  // sampling; events: eWv / eV (W_V ready / V updated), eWu / eU (likewise U)
+  Launch V;
+  bool vs = false;
+  cudaStream_t cs = nullptr;  // comm stream of the chunked main-stream AllReduces
 };
+
+// Z (rows x cols, ld ldz) := produce() then summed over the ranks, in row
+// chunks: chunk c is produced into its own contiguous slice of R.d.zc (ld =
+// its row count), AllReduced on the comm stream while the next chunk's GEMM
+// runs on the main stream, and copied into Z.  `produce(r0, r1, dst, ldd)`
+// enqueues the main-stream work for rows [r0, r1).
+template <class F>
+int gemm_allreduce_rows(DistRun& R, i64 rows, i64 cols, double* Z, i64 ldz, F&& produce) {
+  const Launch& L = R.L;
+  cudaStream_t st = L.stream;
+  int nc = R.comm->chunks();
+  if (nc > kMaxChunks) nc = kMaxChunks;
+  if (rows < 64 * nc) nc = 1;
+  if (nc == 1) {
+    RUTV_TRY(produce(0, rows, Z, ldz));
+    return R.comm->allreduce_sum(Z, rows * cols, st);  // (ldz == rows for the callers)
+  }
+  i64 off[kMaxChunks + 1];
+  for (int c = 0; c <= nc; ++c) off[c] = rows * c / nc;
+  for (int c = 0; c < nc; ++c) {
+    const i64 rc = off[c + 1] - off[c];
+    double* zc = R.d.zc + off[c] * cols;
+    RUTV_TRY(produce(off[c], off[c + 1], zc, rc));
+    RUTV_CUDA(cudaEventRecord(R.ctx->ecomm[c], st));
+    RUTV_CUDA(cudaStreamWaitEvent(R.cs, R.ctx->ecomm[c], 0));
+    RUTV_TRY(R.comm->allreduce_sum(zc, rc * cols, R.cs));
+    RUTV_CUDA(cudaEventRecord(R.ctx->ecomm[kMaxChunks + c], R.cs));
+  }
+  for (int c = 0; c < nc; ++c) {
+    const i64 rc = off[c + 1] - off[c];
+    RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->ecomm[kMaxChunks + c], 0));
+    RUTV_TRY(launch_copy(L, rc, cols, R.d.zc + off[c] * cols, rc, Z + off[c], ldz));
+  }
+  return 0;
+}
 
 // S8 + S9 of a block of width bw whose SVD the owner computes; runs on `Ls`
 // with collectives on `cm`.
@@ -551,9 +605,11 @@ int dist_sampled_step(DistRun& R, i64 i) {
   RUTV_TRY(launch_gaussian(L, R.P.seed, i, r, b, w.G, r));
   RUTV_TRY(launch_dgemm(L, true, false, sl, b, r, 1.0, At, lda, w.G, r, 0.0, R.d.Yl, maxs, w.gemm_ws, w.gemm_ws_elems));
   for (int qq = 0; qq < R.P.q; ++qq) {
-    RUTV_TRY(launch_dgemm(L, false, false, r, b, sl, 1.0, At, lda, R.d.Yl, maxs, 0.0, w.Z, r, w.gemm_ws,
-                          w.gemm_ws_elems));
-    RUTV_TRY(R.comm->allreduce_sum(w.Z, r * b, st));
+    // Z = sum_p A_p Y_p, pipelined in row chunks with its AllReduce
+    RUTV_TRY(gemm_allreduce_rows(R, r, b, w.Z, r, [&](i64 r0, i64 r1, double* dst, i64 ldd) {
+      return launch_dgemm(L, false, false, r1 - r0, b, sl, 1.0, At + r0, lda, R.d.Yl, maxs, 0.0, dst, ldd,
+                          w.gemm_ws, w.gemm_ws_elems);
+    }));
     RUTV_TRY(launch_dgemm(L, true, false, sl, b, r, 1.0, At, lda, w.Z, r, 0.0, R.d.Yl, maxs, w.gemm_ws,
                           w.gemm_ws_elems));
   }
@@ -562,9 +618,25 @@ int dist_sampled_step(DistRun& R, i64 i) {
   cyclic_gather_rows_kernel<<<grid_for(L, s * b), 256, 0, st>>>(s, b, k, b, P, i, R.d.Yall, maxs, maxs * b, w.Y, s);
   L.count();
   RUTV_CHECK_LAUNCH("cyclic_gather_rows_kernel");
+  if (R.vs) RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eV, 0));  // the previous V update read W_V, T_V
   RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
-  // S5 for the V rows first (every rank holds all of W_V; V is not touched by the folds of T)
-  if (R.P.V) RUTV_TRY(apply_right(L, w, R.P.nv, s, b, R.P.V + k * R.P.ldv, R.P.ldv, w.Wv, s, w.TV, b));
+  // S5 for the V rows (every rank holds all of W_V; V is not touched by the
+  // folds of T): on the V stream, overlapping the rest of the step
+  if (R.P.V) {
+    if (R.vs) {
+      RUTV_CUDA(cudaEventRecord(R.ctx->eWv, st));
+      RUTV_CUDA(cudaStreamWaitEvent(R.V.stream, R.ctx->eWv, 0));
+      Work wv = w;
+      wv.Z = w.Zv;
+      wv.Z2 = w.Zv2;
+      wv.gemm_ws = w.gemm_ws_v;
+      wv.gemm_ws_elems = 4 * std::max(lay.m, lay.n) * b;
+      RUTV_TRY(apply_right(R.V, wv, R.P.nv, s, b, R.P.V + k * R.P.ldv, R.P.ldv, w.Wv, s, w.TV, b));
+    } else {
+      RUTV_TRY(apply_right(L, w, R.P.nv, s, b, R.P.V + k * R.P.ldv, R.P.ldv, w.Wv, s, w.TV, b));
+    }
+  }
+  if (R.vs) RUTV_CUDA(cudaEventRecord(R.ctx->eV, R.V.stream));
   const bool fuse = fuse_left();
   // Fused path: the side stream's folds of step i-1 write only row block i-1
   // (rows pk .. k) of the trailing columns, so every other row runs S5-S7
@@ -578,14 +650,22 @@ int dist_sampled_step(DistRun& R, i64 i) {
     L.count();
     RUTV_CHECK_LAUNCH("cyclic_scatter_rows_kernel");
   }
-  // Z = T W_V (AllReduce, m x b; the pending rows are zero here and done later)
-  if (pk > 0)
-    RUTV_TRY(launch_dgemm(L, false, false, pk, b, sl, 1.0, Ap, lda, R.d.Wl, maxs, 0.0, w.Z, m, w.gemm_ws,
-                          w.gemm_ws_elems));
-  if (pb > 0) RUTV_TRY(launch_fill(L, pb, b, 0.0, w.Z + pk, m));
-  RUTV_TRY(launch_dgemm(L, false, false, r, b, sl, 1.0, At, lda, R.d.Wl, maxs, 0.0, w.Z + k, m, w.gemm_ws,
-                        w.gemm_ws_elems));
-  RUTV_TRY(R.comm->allreduce_sum(w.Z, m * b, st));
+  // Z = T W_V (AllReduce, m x b; the pending rows are zero here and done
+  // later), pipelined in row chunks with its AllReduce
+  RUTV_TRY(gemm_allreduce_rows(R, m, b, w.Z, m, [&](i64 r0, i64 r1, double* dst, i64 ldd) {
+    // rows [0, pk): T rows above the pending block; [pk, k): zero; [k, m): A_t
+    const i64 a0 = std::max<i64>(r0, 0), a1 = std::min<i64>(r1, pk);
+    if (a1 > a0)
+      RUTV_TRY(launch_dgemm(L, false, false, a1 - a0, b, sl, 1.0, Ap + a0, lda, R.d.Wl, maxs, 0.0, dst + (a0 - r0),
+                            ldd, w.gemm_ws, w.gemm_ws_elems));
+    const i64 z0 = std::max<i64>(r0, pk), z1 = std::min<i64>(r1, k);
+    if (z1 > z0) RUTV_TRY(launch_fill(L, z1 - z0, b, 0.0, dst + (z0 - r0), ldd));
+    const i64 t0 = std::max<i64>(r0, k), t1 = std::min<i64>(r1, m);
+    if (t1 > t0)
+      RUTV_TRY(launch_dgemm(L, false, false, t1 - t0, b, sl, 1.0, Ap + t0, lda, R.d.Wl, maxs, 0.0, dst + (t0 - r0),
+                            ldd, w.gemm_ws, w.gemm_ws_elems));
+    return 0;
+  }));
   RUTV_TRY(launch_dgemm(L, false, false, m, b, b, 1.0, w.Z, m, w.TV, b, 0.0, w.Z2, m, nullptr, 0));
   // S5 update: unfused -- every trailing column of every row; fused -- column
   // block i (its owner) for the rows outside the pending block
@@ -602,6 +682,7 @@ int dist_sampled_step(DistRun& R, i64 i) {
     RUTV_TRY(launch_triu(L, b, b, At, lda));
     RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, lda));
   }
+  if (R.vs) RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eU, 0));  // the previous U update read W_U, T_U
   RUTV_TRY(R.comm->bcast(R.d.wbuf, r * b + b * b, o, st));
   if (R.P.record) RUTV_CUDA(cudaMemcpyAsync(R.d.lefts + i * (m * b + 2 * b * b), R.d.wbuf, (r * b + b * b) * 8,
                                             cudaMemcpyDeviceToDevice, st));
@@ -612,7 +693,21 @@ int dist_sampled_step(DistRun& R, i64 i) {
                               w.Z2, m, Wu, r, TU, b, pk));
   else
     RUTV_TRY(apply_left_t(L, w, r, lay.ncols(p) - c1, b, R.P.A + k + c1 * lda, lda, Wu, r, TU, b));
-  if (R.P.U) RUTV_TRY(apply_right(L, w, R.P.mu, r, b, R.P.U + k * R.P.ldu, R.P.ldu, Wu, r, TU, b));
+  if (R.P.U) {
+    if (R.vs) {
+      RUTV_CUDA(cudaEventRecord(R.ctx->eWu, st));
+      RUTV_CUDA(cudaStreamWaitEvent(R.V.stream, R.ctx->eWu, 0));
+      Work wu = w;
+      wu.Z = w.Zv;
+      wu.Z2 = w.Zv2;
+      wu.gemm_ws = w.gemm_ws_v;
+      wu.gemm_ws_elems = 4 * std::max(lay.m, lay.n) * b;
+      RUTV_TRY(apply_right(R.V, wu, R.P.mu, r, b, R.P.U + k * R.P.ldu, R.P.ldu, Wu, r, TU, b));
+    } else {
+      RUTV_TRY(apply_right(L, w, R.P.mu, r, b, R.P.U + k * R.P.ldu, R.P.ldu, Wu, r, TU, b));
+    }
+  }
+  if (R.vs) RUTV_CUDA(cudaEventRecord(R.ctx->eU, R.V.stream));
   if (fuse) {
     RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eF, 0));
     if (pb > 0) {
@@ -629,6 +724,7 @@ int dist_sampled_step(DistRun& R, i64 i) {
   // S8, S9 on the side stream / side communicator
   RUTV_CUDA(cudaEventRecord(R.ctx->eR, st));
   RUTV_CUDA(cudaStreamWaitEvent(R.S.stream, R.ctx->eR, 0));
+  if (R.vs) RUTV_CUDA(cudaStreamWaitEvent(R.S.stream, R.ctx->eU, 0));  // U(:, blk), V(:, blk) folds
   RUTV_TRY(dist_svd_and_fold(R, R.S, R.side_comm, i, b, false));
   RUTV_CUDA(cudaEventRecord(R.ctx->eF, R.S.stream));
   return 0;
@@ -643,6 +739,7 @@ int dist_final_step(DistRun& R, i64 i) {
   if (s <= 0) return 0;
   cudaStream_t st = L.stream;
   RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eF, 0));
+  if (R.vs) RUTV_CUDA(cudaStreamWaitEvent(st, R.ctx->eU, 0));  // eU follows eV on the V stream
   const i64 lc = (i / lay.P) * lay.b;
   double* At = R.P.A + k + lc * R.P.lda;
   if (r > s) {
@@ -729,6 +826,23 @@ int agree(Comm* comm, cudaStream_t s, bool ready, int* all_ready) {
   return 0;
 }
 
+int dist_run_loop(DistRun& R, i64 nsamp, bool trunc);
+
+// RANDUTV_ASYNC (full factorisation only): everything enqueued -- the status
+// AllReduce included -- and no host synchronisation, so the call can be
+// captured into a CUDA graph with the NCCL collectives; randutv_wait gives
+// the status through the communicator
+int dist_run_async(DistRun& R) {
+  randutv_ctx* ctx = R.ctx;
+  RUTV_TRY(start_status(ctx, R.d.w));
+  RUTV_TRY(dist_run_loop(R, sampled_steps(R.P.lay.n, R.P.lay.b), false));
+  RUTV_TRY(R.comm->allreduce_min_int(R.d.w.status, 1, R.L.stream));
+  ctx->async_status = R.d.w.status;
+  ctx->async_dist = true;
+  ctx->ws_captured = true;
+  return 0;
+}
+
 // K = -1: full factorisation; K >= 1: truncated after K sampled steps (rank k)
 int dist_run(DistRun& R, i64 K, i64 k, double* resid_fro) {
   const Layout& lay = R.P.lay;
@@ -738,22 +852,8 @@ int dist_run(DistRun& R, i64 K, i64 k, double* resid_fro) {
   const bool trunc = K >= 0;
   const i64 nsamp = trunc ? K : sampled_steps(lay.n, lay.b);
   RUTV_TRY(start_status(ctx, w));
-  if (!trunc && R.P.U && R.P.mu > 0) {
-    RUTV_TRY(launch_set_identity_shift(L, R.P.mu, lay.m, -R.P.u0, R.P.U, R.P.ldu));  // rows u0.. of I
-  }
-  if (R.P.V && R.P.nv > 0) {
-    RUTV_TRY(launch_set_identity_shift(L, R.P.nv, lay.n, -R.P.v0, R.P.V, R.P.ldv));
-  }
-  // the side stream starts after the initialisation
-  RUTV_CUDA(cudaEventRecord(ctx->eF, L.stream));
-  // (truncated: the U updates are replaced by the records; P.U is the U_k output)
-  double* Uk = R.P.U;
-  if (trunc) R.P.U = nullptr;
-  for (i64 i = 0; i < nsamp; ++i) RUTV_TRY(dist_sampled_step(R, i));
-  if (!trunc) RUTV_TRY(dist_final_step(R, nsamp));
-  RUTV_CUDA(cudaStreamWaitEvent(L.stream, ctx->eF, 0));
+  RUTV_TRY(dist_run_loop(R, nsamp, trunc));
   if (trunc) {
-    R.P.U = Uk;
     // rho^2 = sum over ranks of ||T(k:m, local columns >= k)||_F^2
     const i64 nl = lay.ncols(lay.p);
     RUTV_CUDA(cudaMemsetAsync(R.d.colss + nl, 0, sizeof(double), L.stream));
@@ -778,6 +878,41 @@ int dist_run(DistRun& R, i64 K, i64 k, double* resid_fro) {
   // every rank returns the first non-converged block (status word: min)
   RUTV_TRY(R.comm->allreduce_min_int(w.status, 1, L.stream));
   return dist_finish(R);
+}
+
+// U := I, V := I (rows of the rank), the steps, the final step (full only),
+// and every stream joined back into the main one
+int dist_run_loop(DistRun& R, i64 nsamp, bool trunc) {
+  const Layout& lay = R.P.lay;
+  randutv_ctx* ctx = R.ctx;
+  const Launch& L = R.L;
+  if (!trunc && R.P.U && R.P.mu > 0) {
+    RUTV_TRY(launch_set_identity_shift(L, R.P.mu, lay.m, -R.P.u0, R.P.U, R.P.ldu));  // rows u0.. of I
+  }
+  if (R.P.V && R.P.nv > 0) {
+    RUTV_TRY(launch_set_identity_shift(L, R.P.nv, lay.n, -R.P.v0, R.P.V, R.P.ldv));
+  }
+  // the side, V and comm streams start after the initialisation
+  RUTV_CUDA(cudaEventRecord(ctx->eF, L.stream));
+  RUTV_CUDA(cudaStreamWaitEvent(R.cs, ctx->eF, 0));
+  if (R.vs) {
+    RUTV_CUDA(cudaStreamWaitEvent(R.V.stream, ctx->eF, 0));
+    RUTV_CUDA(cudaEventRecord(ctx->eV, R.V.stream));
+    RUTV_CUDA(cudaEventRecord(ctx->eU, R.V.stream));
+  }
+  // (truncated: the U updates are replaced by the records; P.U is the U_k output)
+  double* Uk = R.P.U;
+  if (trunc) R.P.U = nullptr;
+  for (i64 i = 0; i < nsamp; ++i) RUTV_TRY(dist_sampled_step(R, i));
+  if (!trunc) RUTV_TRY(dist_final_step(R, nsamp));
+  R.P.U = Uk;
+  RUTV_CUDA(cudaStreamWaitEvent(L.stream, ctx->eF, 0));
+  if (R.vs) RUTV_CUDA(cudaStreamWaitEvent(L.stream, ctx->eU, 0));
+  // the comm stream's last chunk was already waited for by the main stream
+  // (gemm_allreduce_rows); join it anyway so a captured graph closes over it
+  RUTV_CUDA(cudaEventRecord(ctx->ecomm[2 * kMaxChunks - 1], R.cs));
+  RUTV_CUDA(cudaStreamWaitEvent(L.stream, ctx->ecomm[2 * kMaxChunks - 1], 0));
+  return 0;
 }
 
 // argument checks shared by the NCCL and loopback entries; returns 0 or -i
@@ -825,12 +960,26 @@ int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, dou
   R.side_comm = side_comm;
   R.L = ctx->launch();
   R.S = ctx->side_launch();
+  R.V = ctx->v_launch();
+  const bool async = (flags & RANDUTV_ASYNC) != 0;
+  if (local == 0 && async && (!comm->capturable() || k != 0 || (flags & RANDUTV_CHECK_FINITE))) local = -9;
+  if (local == 0 && !ctx->cstr) {
+    if (cudaStreamCreateWithFlags(&ctx->cstr, cudaStreamNonBlocking) != cudaSuccess) local = RANDUTV_ERR_CUDA;
+    for (int e = 0; e < 2 * kMaxChunks && local == 0; ++e)
+      if (cudaEventCreateWithFlags(&ctx->ecomm[e], cudaEventDisableTiming) != cudaSuccess) local = RANDUTV_ERR_CUDA;
+  }
+  R.cs = ctx->cstr;
   if (local == 0) {
     Carver dry{nullptr, 0, 0, true};
     const size_t need = carve_dist(dry, R.d, lay, K > 0 ? K : 0, k);
     local = ensure_ws(ctx, need);
   }
-  {
+  if (async) {
+    // an ASYNC (graph-capturable) call cannot synchronise the host for the
+    // agreement: the caller guarantees rank-uniform arguments, as NCCL itself
+    // requires
+    if (local != 0) return local;
+  } else {
     int all = 0;
     RUTV_TRY(agree(comm, ctx->stream, local == 0, &all));
     if (local != 0) return local;
@@ -844,6 +993,15 @@ int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, dou
                     uv && K > 0, uv};
   if (R.P.U && R.P.mu == 0) R.P.U = nullptr;
   if (R.P.V && R.P.nv == 0) R.P.V = nullptr;
+  {
+    // RUTV_VSTREAM=0 keeps the U / V updates on the main stream (comparison only)
+    static int v = -1;
+    if (v < 0) {
+      const char* e = getenv("RUTV_VSTREAM");
+      v = e ? atoi(e) : 1;
+    }
+    R.vs = uv && v != 0 && fuse_left();
+  }
   if (flags & RANDUTV_CHECK_FINITE) {
     int bad = 0;
     if (lay.ncols(lay.p) > 0) bad = check_finite(ctx, R.L, R.d.w, m, lay.ncols(lay.p), A, lda);
@@ -852,6 +1010,11 @@ int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, dou
     RUTV_TRY(agree(comm, ctx->stream, bad == 0, &all));
     if (bad != 0 && bad != RANDUTV_ERR_NONFINITE) return bad;
     if (!all) return RANDUTV_ERR_NONFINITE;
+  }
+  if (async) {
+    RUTV_TRY(dist_run_async(R));
+    ctx->stats.factorizations++;
+    return 0;
   }
   const int st = dist_run(R, K, k, resid_fro);
   if (st == 0) ctx->stats.factorizations++;

@@ -42,6 +42,13 @@ struct randutv_ctx {
   cudaStream_t cps;
   // device status word of the last RANDUTV_ASYNC call (randutv_wait)
   int* async_status;
+  // the last RANDUTV_ASYNC call was sharded: randutv_wait waits through the
+  // communicator (asynchronous-error polling, timeout)
+  bool async_dist;
+  // sharded path: the stream its main-stream collectives run on (chunked
+  // AllReduces overlap the GEMMs producing the next chunk)
+  cudaStream_t cstr;
+  cudaEvent_t ecomm[8];
   // GEMM tile-scheduler counters: [0..1] main stream, [2..3] side stream (zeroed once)
   int* sched;
   int jacobi_max_sweeps;  // 0 = the default 30 (randutv_set_option)
@@ -108,6 +115,8 @@ int finish(randutv_ctx* ctx, const Work& w);
 i64 sampled_steps(i64 n, i64 b);
 // dist.cu: release a communicator (NULL is a no-op)
 void comm_free(Comm* c);
+// dist.cu: wait for a stream whose work includes the communicator's collectives
+int comm_sync(Comm* c, cudaStream_t s);
 int start_status(randutv_ctx* ctx, const Work& w);
 int check_finite(randutv_ctx* ctx, const Launch& L, const Work& w, i64 m, i64 n, const double* A, i64 lda);
 

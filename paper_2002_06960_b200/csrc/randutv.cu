@@ -821,6 +821,11 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
     cudaStreamSynchronize(ctx->cps);
     cudaStreamDestroy(ctx->cps);
   }
+  if (ctx->cstr) {
+    cudaStreamSynchronize(ctx->cstr);
+    for (cudaEvent_t e : ctx->ecomm) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->cstr);
+  }
   if (ctx->side) {
     cudaEventDestroy(ctx->eR);
     cudaEventDestroy(ctx->eF);
@@ -999,6 +1004,7 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
   if (flags & RANDUTV_ASYNC) {
     // enqueued only: the status word stays on the device (randutv_wait)
     ctx->async_status = w.status;
+    ctx->async_dist = false;
     ctx->ws_captured = true;
     ctx->stats.factorizations++;
     return 0;
@@ -1011,6 +1017,7 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
 RANDUTV_API int randutv_wait(randutv_ctx* ctx) {
   if (!ctx || ctx->magic != kMagic) return RANDUTV_ERR_CTX;
   RUTV_CUDA(cudaSetDevice(ctx->device));
+  if (ctx->async_dist && ctx->comm) RUTV_TRY(rutv::comm_sync(ctx->comm, ctx->stream));
   RUTV_CUDA(cudaStreamSynchronize(ctx->stream));
   // per-kernel events of the async call (or of the last replay of a graph
   // captured with profiling on)

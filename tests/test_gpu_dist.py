@@ -193,3 +193,56 @@ def test_nccl_single_rank_end_to_end(ctx):
         assert np.max(np.abs(np.abs(to_np(Uk)) - np.abs(to["Uk"]))) <= 1e-9
     finally:
         c.close()
+
+
+def test_nccl_async_graph_capture():
+    """RANDUTV_ASYNC on the sharded NCCL path: no host synchronisation inside the
+    call (the pre-collective agreement is skipped, the status AllReduce is
+    enqueued), so after a warm-up call the whole sharded factorisation -- NCCL
+    collectives, V/U stream and comm stream forks included -- is captured into a
+    CUDA graph; replays give the eager call's bits; randutv_wait returns the
+    status through the communicator.  The loopback communicator (host barriers)
+    rejects the flag."""
+    import ctypes
+    import torch
+    from paper_2002_06960_b200.randutv import RANDUTV_ASYNC, Context, colmajor, nccl_unique_id
+    rng = np.random.default_rng(22)
+    m, n, b, q = 320, 256, 32, 1
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    s = torch.cuda.Stream()
+    c = Context(0, s)
+    try:
+        c.comm_init(nccl_unique_id(), 1, 0)
+        A0 = colmajor(m, n)
+        A0.copy_(torch.from_numpy(np.ascontiguousarray(A)))
+        Al = colmajor(m, n)
+        U, V = colmajor(m, m), colmajor(n, n)
+        Al.copy_(A0)
+        c.randutv_factor_dist(Al, m, n, b, q, 5, U_local=U, V_local=V, nranks=1, rank=0)
+        T_ref, U_ref, V_ref = Al.clone(), U.clone(), V.clone()
+        Al.copy_(A0)
+        with torch.cuda.stream(s):
+            c.randutv_factor_dist(Al, m, n, b, q, 5, U_local=U, V_local=V, nranks=1, rank=0, flags=RANDUTV_ASYNC)
+        assert c.wait() == 0
+        assert torch.equal(Al, T_ref) and torch.equal(U, U_ref) and torch.equal(V, V_ref)
+        g = torch.cuda.CUDAGraph()
+        Al.copy_(A0)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s, capture_error_mode="relaxed"):
+            c.randutv_factor_dist(Al, m, n, b, q, 5, U_local=U, V_local=V, nranks=1, rank=0, flags=RANDUTV_ASYNC)
+        for rep in range(2):
+            Al.copy_(A0)
+            U.zero_()
+            V.zero_()
+            torch.cuda.synchronize()
+            g.replay()
+            assert c.wait() == 0
+            assert torch.equal(Al, T_ref) and torch.equal(U, U_ref) and torch.equal(V, V_ref)
+    finally:
+        c.close()
+    # the loopback back end cannot be captured: -9
+    from paper_2002_06960_b200.randutv import randutv_factor_dist_loopback, RandUTVError
+    Als = [to_dev(A[:, :n // 2]), to_dev(A[:, n // 2:])]
+    with pytest.raises(RandUTVError) as e:
+        randutv_factor_dist_loopback(Als, m, n, n // 2, q, 5, flags=RANDUTV_ASYNC)
+    assert e.value.status == -9

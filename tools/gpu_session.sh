@@ -1,7 +1,8 @@
 #!/bin/bash
 # One gpurun session: tests, bench, ncu launch list, ncu full capture of the top kernel.
-# Usage (from repo root, under gpurun): bash tools/gpu_session.sh [smoke] [tests] [bench] [bench_c2] [kernels]
-#   [bench_variants] [host] [hqrrp] [ncu_launches] [ncu_full]   (ncu_full picks the longest DGEMM of ncu_launches)
+# Usage (from repo root, under gpurun): bash tools/gpu_session.sh [smoke] [tests] [full] [bench] [bench_c2] [kernels]
+#   [bench_variants] [host] [hqrrp] [ncu_launches] [ncu_full] [ncu_gemm] [ncu_leaf] [leaf_ab] [probe_host]
+#   (ncu_full picks the longest DGEMM of ncu_launches)
 set -u
 mkdir -p gpurun_out
 for stage in "$@"; do
@@ -53,6 +54,41 @@ PY
       timeout 900 python bench.py --mode host --steps 1 --warmup 1 --no-uv > gpurun_out/bench_host_c3_tonly.json 2>> gpurun_out/bench_host.err
       timeout 900 python bench.py --algo hqrrp --mode host --steps 1 --warmup 0 > gpurun_out/bench_hqrrp_host_c3.json 2>> gpurun_out/bench_host.err
       echo "host rc=$?"; cut -c1-200 gpurun_out/bench_host_c3*.json gpurun_out/bench_hqrrp_host_c3.json ;;
+    full)
+      # every -m gpu test (with durations), the default bench, c2, the step kernels
+      timeout 3000 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=25 > gpurun_out/pytest_gpu.log 2>&1
+      echo "pytest rc=$?"; tail -40 gpurun_out/pytest_gpu.log
+      timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cut -c1-1500 gpurun_out/bench.json
+      timeout 900 python bench.py --config c2 --no-cpu-baseline > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+      echo "bench c2 rc=$?"; cut -c1-600 gpurun_out/bench_c2.json
+      timeout 300 python tools/bench_kernels.py qr svd > gpurun_out/k2.log 2>&1; cut -c1-200 gpurun_out/k2.log ;;
+    probe_host)
+      # the GPU box's host: cores, memory, numpy DGEMM rate (the oracle's speed)
+      nproc; lscpu | head -20; free -g; df -h /tmp | tail -1
+      python -c "import numpy as np,time;a=np.random.rand(4096,4096);a@a;t=time.time();a@a;print('numpy dgemm GF/s',2*4096**3/(time.time()-t)/1e9)" ;;
+    leaf_ab)
+      # QR leaf plans and Jacobi variants (bench_kernels qr / svd)
+      for v in "RUTV_LEAF_MAXUNITS=5" "RUTV_LEAF_MAXUNITS=3" "RUTV_LEAF_CLUSTER=0"; do
+        echo "== $v" >> gpurun_out/leaf_ab.log; env $v timeout 300 python tools/bench_kernels.py qr >> gpurun_out/leaf_ab.log 2>&1
+      done
+      for v in "RUTV_JACOBI_CLUSTER=1" "RUTV_JACOBI_CLUSTER=0"; do
+        echo "== $v" >> gpurun_out/leaf_ab.log; env $v timeout 300 python tools/bench_kernels.py svd >> gpurun_out/leaf_ab.log 2>&1
+      done
+      cut -c1-200 gpurun_out/leaf_ab.log ;;
+    ncu_leaf)
+      # ncu --set full of the QR leaf kernel at h = 16384 and 4096 (tools/leaf_probe.py)
+      for h in 16384 4096; do
+        timeout 600 ncu --set full --clock-control none --import-source on -k regex:qr_leaf --launch-skip 2 --launch-count 1 \
+          -o gpurun_out/prof_leaf_$h python tools/leaf_probe.py $h > gpurun_out/ncu_leaf_$h.log 2>&1; echo "ncu leaf h=$h rc=$?"
+      done ;;
+    ncu_gemm)
+      # ncu --set full of the skinny S2 product (launch 0) and the rank-b update (launch 18) of bench_kernels gemm
+      CMD="python tools/bench_kernels.py gemm"
+      timeout 300 $CMD > gpurun_out/ncu_gemm_plain.log 2>&1 || { echo "plain run failed"; continue; }
+      for pr in "18 rankb" "0 skinny"; do set -- $pr
+        timeout 900 ncu --set full --clock-control none --import-source on -k regex:dgemm_kernel --launch-skip $1 --launch-count 1 \
+          -o gpurun_out/prof_$2 $CMD > gpurun_out/ncu_$2.log 2>&1; echo "ncu $2 rc=$?"
+      done ;;
     hqrrp)
       timeout 900 python bench.py --algo hqrrp --steps 2 --warmup 1 > gpurun_out/bench_hqrrp_c3.json 2>> gpurun_out/bench_hqrrp.err
       echo "hqrrp rc=$?"; cut -c1-300 gpurun_out/bench_hqrrp_c3.json ;;
