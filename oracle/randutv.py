@@ -44,6 +44,15 @@ from .jacobi import svd_block
 from .philox import gaussian_block
 
 
+def _mm(A, B):
+    """A @ B written in Fortran order (np.matmul into an F-ordered out): the
+    rank-b products below are subtracted from Fortran-ordered views, and a
+    C-ordered temporary would make that subtraction walk memory transposed
+    (50x slower at the full sizes).  Same products, same BLAS call."""
+    out = np.empty((A.shape[0], B.shape[1]), order="F")
+    return np.matmul(A, B, out=out)
+
+
 def sampled_steps(n, b):
     """Number of sampled steps (those with s = n - i b > b)."""
     return max(0, -(-(n - b) // b)) if n > b else 0
@@ -193,10 +202,10 @@ def _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin, record, reorth=False,
     # (X -= ... is X := X - ... elementwise; in place only to hold one m x s
     # temporary at the full sizes)
     X = T[:, kk:]
-    X -= ((X @ WV) @ TV) @ WV.T
+    X -= _mm((X @ WV) @ TV, WV.T)
     if V is not None:
         XV = V[:, kk:]
-        XV -= ((XV @ WV) @ TV) @ WV.T
+        XV -= _mm((XV @ WV) @ TV, WV.T)
     # O6: left QR of the leading column block
     FU, tauU = householder_qr(T[kk:, kk:kk + b])
     WU = unit_lower(FU)
@@ -206,10 +215,10 @@ def _sampled_step(T, U, V, lefts, kk, b, q, seed, i, thin, record, reorth=False,
     T[kk + b:, kk:kk + b] = 0.0
     # O7: left transform of the trailing columns (A3) and U
     Xl = T[kk:, kk + b:]
-    Xl -= WU @ (TU.T @ (WU.T @ Xl))
+    Xl -= _mm(WU, TU.T @ (WU.T @ Xl))
     if U is not None:
         XU = U[:, kk:]
-        XU -= ((XU @ WU) @ TU) @ WU.T
+        XU -= _mm((XU @ WU) @ TU, WU.T)
     # O8, O9
     Us, d, Vs, sweeps = svd_block(R)
     _fold(T, U, V, kk, b, Us, d, Vs)
@@ -234,7 +243,7 @@ def _final_step(T, U, V, lefts, kk, thin, record):
         T[kk + s:, kk:] = 0.0
         if U is not None:
             XU = U[:, kk:]
-            U[:, kk:] = XU - ((XU @ WU) @ TU) @ WU.T
+            U[:, kk:] = XU - _mm((XU @ WU) @ TU, WU.T)
         B = R
     else:
         B = np.array(T[kk:, kk:], order="F", copy=True)   # dense final block (O10)
@@ -270,7 +279,7 @@ def _thin_u(m, c, lefts):
         X[kk:kk + w, :] = Us @ X[kk:kk + w, :]
         if WU is not None:
             Xs = X[kk:, :]
-            X[kk:, :] = Xs - WU @ (TU @ (WU.T @ Xs))
+            X[kk:, :] = Xs - _mm(WU, TU @ (WU.T @ Xs))
     return X
 
 

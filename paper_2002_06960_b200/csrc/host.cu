@@ -56,6 +56,7 @@ struct Slot {
   bool dirty = false;
   int pins = 0;
   uint64_t last = 0;
+  int64_t next_use = 0;  // Belady: position of the panel's next access in the plan
   cudaEvent_t ready = nullptr, idle = nullptr, clean = nullptr;
 };
 
@@ -93,7 +94,14 @@ struct PanelCache {
   uint64_t clock = 0;
   randutv_host_report* rep = nullptr;
   CopyTimer timer;
-
+  // Belady eviction (T-only runs): the driver's panel access sequence of T is
+  // known in advance (build_plan); every get() of T is matched against it and
+  // the victim is the unpinned slot whose next use lies farthest ahead.  A
+  // mismatch (an access the plan does not predict) falls back to LRU.
+  int plan_mat = -1;
+  std::vector<i64> plan, nxt;  // plan[t]: panel of access t; nxt[t]: next access of that panel (or INT64_MAX)
+  i64 cursor = 0;
+  bool use_plan = false;
   int add_mat(double* h, i64 rows, i64 cols, i64 ld) {
     mats.push_back(HostMat{h, rows, cols, ld, (cols + b - 1) / b});
     where.emplace_back((size_t)mats.back().npanels, -1);
@@ -156,7 +164,13 @@ struct PanelCache {
         best = s;
         break;
       }
-      if (best < 0 || slots[s].last < slots[best].last) best = s;
+      if (best < 0) {
+        best = s;
+      } else if (use_plan) {
+        if (slots[s].next_use > slots[best].next_use) best = s;
+      } else if (slots[s].last < slots[best].last) {
+        best = s;
+      }
     }
     if (best < 0) return RANDUTV_ERR_ALLOC;  // every slot pinned: cannot happen with >= 3 slots
     *out = best;
@@ -220,11 +234,20 @@ struct PanelCache {
 
   // pin (mat, panel) for compute on `comp`; returns the device panel (ld = rows)
   int get(int mat, i64 panel, double** d, bool load = true, i64 lo = 0) {
+    int64_t nu = 0;
+    if (use_plan && mat == plan_mat) {
+      if (cursor < (i64)plan.size() && plan[cursor] == panel) {
+        nu = nxt[cursor++];
+      } else {
+        use_plan = false;  // the run left the plan: LRU from here on
+      }
+    }
     int s;
     RUTV_TRY(fetch(mat, panel, load, &s, lo));
     Slot& v = slots[s];
     v.pins++;
     v.last = ++clock;
+    v.next_use = nu;
     RUTV_CUDA(cudaStreamWaitEvent(comp, v.ready, 0));
     *d = v.d;
     return 0;
@@ -239,7 +262,10 @@ struct PanelCache {
   int prefetch(int mat, i64 panel, i64 lo = 0) {
     if (panel < 0 || panel >= mats[mat].npanels) return 0;
     int s;
-    return fetch(mat, panel, true, &s, lo);
+    RUTV_TRY(fetch(mat, panel, true, &s, lo));
+    // the prefetched panel is the plan's next access: never the next victim
+    if (use_plan && mat == plan_mat) slots[s].next_use = cursor;
+    return 0;
   }
   int flush() {
     for (Slot& s : slots)
@@ -247,6 +273,48 @@ struct PanelCache {
     return 0;
   }
 };
+
+// The panel accesses of T the driver makes, in order (host_sampled_step /
+// host_final_step; pass directions as pass() with R.dir = (i & 1) == 0 at each
+// step): [step_begin only: the S2 pass over panels i..], 2q power passes, the
+// T W_V read pass, panel i, the read-write pass over panels i+1..; the final
+// block.  paper_2002_06960_b200/flops.py host_stream_traffic replays the same
+// sequence (the PCIe-byte model).
+void build_plan(i64 n, i64 b, int q, i64 nsamp, i64 step_begin, i64 step_end, std::vector<i64>& plan,
+                std::vector<i64>& nxt) {
+  const i64 np = (n + b - 1) / b;
+  plan.clear();
+  const i64 last = std::min(step_end, nsamp);
+  for (i64 i = step_begin; i < last; ++i) {
+    bool fwd = (i & 1) == 0;
+    auto pass = [&](i64 p0) {
+      for (i64 t = 0; t < np - p0; ++t) plan.push_back(fwd ? p0 + t : np - 1 - t);
+      fwd = !fwd;
+    };
+    if (i == step_begin) pass(i);  // S2 (the previous step's fused pass took it otherwise)
+    for (int qq = 0; qq < 2 * q; ++qq) pass(i);
+    pass(i);                // T W_V
+    plan.push_back(i);      // panel i
+    pass(i + 1);            // S5 + S7 + fold + next S2
+  }
+  if (step_end > nsamp) plan.push_back(nsamp);
+  nxt.assign(plan.size(), INT64_MAX);
+  std::vector<i64> seen((size_t)np, INT64_MAX);
+  for (i64 t = (i64)plan.size() - 1; t >= 0; --t) {
+    nxt[t] = seen[plan[t]];
+    seen[plan[t]] = t;
+  }
+}
+
+// RUTV_HOST_EVICT=lru disables the Belady plan (comparison only)
+bool belady_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_HOST_EVICT");
+    v = (e && strcmp(e, "lru") == 0) ? 0 : 1;
+  }
+  return v != 0;
+}
 
 struct HostRun {
   randutv_ctx* ctx;
@@ -679,6 +747,14 @@ static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_ho
     if (st == 0 && flag) st = RANDUTV_ERR_NONFINITE;
   }
   if (st == 0) {
+    // Belady eviction for T-only runs without the finiteness scan (their T
+    // access sequence is exactly the plan)
+    if (!uv && !(flags & RANDUTV_CHECK_FINITE) && belady_on()) {
+      build_plan(n, bb, q, nsamp, step_begin, step_end, R.pc.plan, R.pc.nxt);
+      R.pc.plan_mat = R.mT;
+      R.pc.cursor = 0;
+      R.pc.use_plan = true;
+    }
     const i64 last = std::min<i64>(step_end, nsamp);
     for (i64 i = step_begin; i < last && st == 0; ++i) st = host_sampled_step(R, i);
     if (st == 0 && step_end > nsamp) st = host_final_step(R, nsamp);

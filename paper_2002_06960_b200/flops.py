@@ -78,3 +78,80 @@ def hqrrp_flops(m, n, b, build_q=True):
         if build_q:
             F += 4.0 * m * r * w
     return F
+
+
+def host_stream_traffic(m, n, b, q, cache_panels, policy="lru"):
+    """PCIe bytes of the host-streamed T-only randUTV (csrc/host.cu, S12) --
+    measurement only: replays the panel access sequence of the driver (per
+    sampled step i, k = i b: [step 0 only: the S2 pass over rows k:m], 2q power
+    passes over rows k:m, the T W_V read pass over all rows, panel i read +
+    written, one read-write pass over panels > i; pass directions alternate,
+    starting forward on even steps; final block read + written) through a
+    cache of `cache_panels` slots and returns (h2d_bytes, d2h_bytes).
+
+    policy "lru" is the driver's (least recently used, one-panel prefetch
+    modelled as an access); "belady" evicts the resident panel whose next use
+    lies farthest ahead (the optimal offline policy, the access sequence being
+    known in advance -- SURVEY.md §8(d) M7).  Also "none": no cache (every
+    access loads, every write-back stores) -- M7's algorithmic floor."""
+    b = min(b, n)
+    np_ = -(-n // b)
+    width = [min(b, n - j * b) for j in range(np_)]
+    seq = []   # (panel, lo, dirty)
+    nsamp = sampled_steps(n, b)
+    for i in range(nsamp):
+        k = i * b
+        fwd = (i % 2 == 0)
+
+        def pass_(p0, lo, dirty):
+            nonlocal fwd
+            order = range(p0, np_) if fwd else range(np_ - 1, p0 - 1, -1)
+            fwd = not fwd
+            for j in order:
+                seq.append((j, lo, dirty))
+        if i == 0:
+            pass_(i, k, False)
+        for _ in range(2 * q):
+            pass_(i, k, False)
+        pass_(i, 0, False)
+        seq.append((i, 0, True))
+        pass_(i + 1, 0, True)
+    seq.append((nsamp, 0, True))
+    if policy == "none":
+        h2d = sum((m - lo) * width[j] * 8 for j, lo, _ in seq)
+        d2h = sum(m * width[j] * 8 for j, _, d in seq if d)
+        return float(h2d), float(d2h)
+    # next-use index per position (Belady)
+    nxt = [0] * len(seq)
+    last = {}
+    for t in range(len(seq) - 1, -1, -1):
+        j = seq[t][0]
+        nxt[t] = last.get(j, 1 << 62)
+        last[j] = t
+    res = {}   # panel -> [lo, dirty, last_use, next_use]
+    h2d = d2h = 0
+    for t, (j, lo, dirty) in enumerate(seq):
+        if j in res:
+            e = res[j]
+            if lo < e[0]:
+                h2d += (e[0] - lo) * width[j] * 8
+                e[0] = lo
+        else:
+            if len(res) >= cache_panels:
+                if policy == "belady":
+                    v = max(res, key=lambda p: res[p][3])
+                else:
+                    v = min(res, key=lambda p: res[p][2])
+                ev = res.pop(v)
+                if ev[1]:
+                    d2h += (m - ev[0]) * width[v] * 8
+            h2d += (m - lo) * width[j] * 8
+            res[j] = [lo, False, t, 0]
+        e = res[j]
+        e[1] = e[1] or dirty
+        e[2] = t
+        e[3] = nxt[t]
+    for j, e in res.items():
+        if e[1]:
+            d2h += (m - e[0]) * width[j] * 8
+    return float(h2d), float(d2h)
