@@ -517,6 +517,18 @@ def run_ours(args):
     return 0
 
 
+def host_model(m, n, b, q, slots):
+    """algorithmic PCIe bytes of the T-only host-streamed
+    run -- the driver's panel access sequence replayed with no cache (the floor
+    without reuse), LRU and Belady eviction (flops.host_stream_traffic)."""
+    from paper_2002_06960_b200.flops import host_stream_traffic
+    out = {}
+    for pol in ("none", "lru", "belady"):
+        h, d = host_stream_traffic(m, n, b, q, slots, pol)
+        out[pol] = {"h2d_bytes": h, "d2h_bytes": d}
+    return out
+
+
 def run_host_streamed(args):
     """S12: randutv_factor_host from pinned host memory through a bounded device
     panel cache, reported like the paper's Table 1: compute time
@@ -586,7 +598,9 @@ def run_host_streamed(args):
                        "real_over_comp": real / comp_ms, "comp_over_io": comp_ms / io if io > 0 else None,
                        "h2d_bytes": r0["h2d_bytes"], "d2h_bytes": r0["d2h_bytes"],
                        "h2d_GBps": r0["h2d_bytes"] / (r0["h2d_ms"] * 1e-3) / 1e9 if r0["h2d_ms"] > 0 else None,
-                       "cache_hits": r0["cache_hits"], "cache_misses": r0["cache_misses"]},
+                       "cache_hits": r0["cache_hits"], "cache_misses": r0["cache_misses"],
+                       "eviction": "lru" if (uv or os.environ.get("RUTV_HOST_EVICT") == "lru") else "belady",
+                       "model": host_model(m, n, b, q, r0["cache_slots"]) if not uv else None},
             "t_over_n3_x1e10": real * 1e-3 / float(n) ** 3 * 1e10}
     print(json.dumps(line), flush=True)
     ctx.close()

@@ -259,12 +259,13 @@ struct PanelCache {
     RUTV_CUDA(cudaEventRecord(v.idle, comp));
     return 0;
   }
-  int prefetch(int mat, i64 panel, i64 lo = 0) {
+  // `ahead` = how many accesses of the plan lie before this panel's use
+  int prefetch(int mat, i64 panel, i64 lo = 0, i64 ahead = 0) {
     if (panel < 0 || panel >= mats[mat].npanels) return 0;
     int s;
     RUTV_TRY(fetch(mat, panel, true, &s, lo));
-    // the prefetched panel is the plan's next access: never the next victim
-    if (use_plan && mat == plan_mat) slots[s].next_use = cursor;
+    // the prefetched panel is (one of) the plan's next accesses: not a victim before its use
+    if (use_plan && mat == plan_mat) slots[s].next_use = cursor + ahead;
     return 0;
   }
   int flush() {
@@ -346,16 +347,30 @@ struct HostRun {
 
 // Visit panels [p0, p1) of `mat` in the current serpentine direction with a
 // one-panel prefetch; f(panel, device ptr) enqueues the work on the compute stream.
+// RUTV_HOST_PREFETCH: panels of a pass fetched ahead of the one computed (default 2)
+i64 prefetch_depth() {
+  static i64 v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_HOST_PREFETCH");
+    v = e ? atoll(e) : 2;
+    if (v < 1) v = 1;
+  }
+  return v;
+}
+
 template <class F>
 int pass(HostRun& R, int mat, i64 p0, i64 p1, bool dirty, F&& f, i64 lo = 0) {
   const bool fwd = R.dir;
   R.dir = !R.dir;
   const i64 cnt = p1 - p0;
+  // never prefetch more than the cache can hold next to the pinned panel
+  const i64 depth = std::min<i64>(prefetch_depth(), (i64)R.pc.slots.size() - 2);
   for (i64 t = 0; t < cnt; ++t) {
     const i64 j = fwd ? p0 + t : p1 - 1 - t;
     double* d;
     RUTV_TRY(R.pc.get(mat, j, &d, true, lo));
-    if (t + 1 < cnt) RUTV_TRY(R.pc.prefetch(mat, fwd ? j + 1 : j - 1, lo));
+    for (i64 a = 1; a <= depth && t + a < cnt; ++a)
+      RUTV_TRY(R.pc.prefetch(mat, fwd ? j + a : j - a, lo, a - 1));
     RUTV_TRY(f(j, d));
     RUTV_TRY(R.pc.put(mat, j, dirty));
   }

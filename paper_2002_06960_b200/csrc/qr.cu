@@ -47,6 +47,7 @@ constexpr int NB = 32;
 constexpr int LEAF_THREADS = 256;
 constexpr int LEAF_MAX_CTAS = 128;
 constexpr int PSTRIDE = NB + 1;  // partial record: [0] = ||x'||^2, [1+l] = x'.P(:,l)
+constexpr int PREC = PSTRIDE + 1;  // its stride in global memory (even: 16-byte copies)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
   __shared__ double wv[NB];
   __shared__ double sc[4];  // tau, scal, beta, flag
   extern __shared__ double slab_s[];  // S * LEAF_THREADS rows x NB columns
+  __shared__ __align__(16) double stage[CLUSTER ? 2 : LEAF_MAX_CTAS * PREC];  // grid leaf: the G partial records
   constexpr int SLD = S * LEAF_THREADS;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -233,26 +235,29 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
       }
       __syncthreads();
     } else {
-      double* pj = partials + (size_t)(jj & 1) * G * PSTRIDE;
+      double* pj = partials + (size_t)(jj & 1) * G * PREC;
       if (tid < PSTRIDE) {
         double s2 = 0.0;
 #pragma unroll
         for (int w = 0; w < LEAF_THREADS / 32; ++w) s2 += wred[w][tid];
-        pj[(size_t)cta * PSTRIDE + tid] = s2;
+        pj[(size_t)cta * PREC + tid] = s2;
       }
       cg::this_grid().sync();
       // ---------------- phase B: every CTA reduces the partials in the same
-      // order: thread e < 33 streams value e of the G records from L2 (16
-      // loads in flight per batch)
+      // order: all threads pull the G x 33 records from L2 into shared memory
+      // at once (cp.async, one L2 round trip, no registers), then thread
+      // e < 33 sums value e over the CTAs in a fixed order
+      // (16-byte cp.async.cg: L2 only -- the records of this parity were
+      // rewritten since the last read, an L1 copy could be stale)
+      for (int e = 2 * tid; e < G * PREC; e += 2 * LEAF_THREADS)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(stage + e)),
+                     "l"(pj + e)
+                     : "memory");
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
       if (tid < PSTRIDE) {
         double s3 = 0.0;
-        for (int c0b = 0; c0b < G; c0b += 16) {
-          double vals[16];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) vals[c] = c0b + c < G ? __ldcg(pj + (size_t)(c0b + c) * PSTRIDE + tid) : 0.0;
-#pragma unroll
-          for (int c = 0; c < 16; ++c) s3 += vals[c];
-        }
+        for (int c = 0; c < G; ++c) s3 += stage[c * PREC + tid];
         tot[tid] = s3;
       }
       __syncthreads();
@@ -580,7 +585,7 @@ int launch_leaf_cluster(const Launch& L, int G, void** args) {
 i64 panel_qr_partials_elems(i64 h, i64 w) {
   (void)h;
   (void)w;
-  return 2 * (i64)LEAF_MAX_CTAS * PSTRIDE;
+  return 2 * (i64)LEAF_MAX_CTAS * PREC;
 }
 
 int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, double* Wx, i64 ldw, double* Tf,

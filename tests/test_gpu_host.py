@@ -129,3 +129,21 @@ def test_host_streamed_resume_arguments(ctx):
     with pytest.raises(RandUTVError) as e:
         ctx.randutv_factor_host_steps(A, None, None, 16, 1, 1, 9, 12, build_uv=False)
     assert e.value.status == -15
+
+
+@pytest.mark.parametrize("m,n,b,q,slots", [(2048, 2048, 128, 1, 5), (3000, 2500, 128, 2, 8), (4096, 4096, 128, 1, 12)])
+def test_host_streamed_traffic_model(ctx, m, n, b, q, slots):
+    """a T-only host-streamed run moves the PCIe bytes of the
+    replay model paper_2002_06960_b200.flops.host_stream_traffic under Belady
+    eviction (within the prefetch's slack: measured 0.3-4 %), and fewer than
+    LRU would on the same access sequence."""
+    from paper_2002_06960_b200.flops import host_stream_traffic
+    from paper_2002_06960_b200.randutv import pinned_colmajor
+    A = pinned_colmajor(m, n)
+    A[:] = np.random.default_rng(m + n).standard_normal((m, n))
+    slot = ((max(m, n) * b + 31) // 32) * 32 * 8
+    _, _, rep = ctx.randutv_factor_host(A, b, q, 3, build_uv=False, cache_bytes=slots * slot)
+    hb, db = host_stream_traffic(m, n, b, q, rep["cache_slots"], "belady")
+    hl, dl = host_stream_traffic(m, n, b, q, rep["cache_slots"], "lru")
+    assert hb <= rep["h2d_bytes"] <= 1.05 * hb and db <= rep["d2h_bytes"] <= 1.06 * db
+    assert rep["h2d_bytes"] < hl
