@@ -452,3 +452,68 @@ def test_oversample_c1_range_finder():
     o = oracle_randutv(A, 64, 0, 2001, k=64, thin_u=True, oversample=64)
     assert abs(rho - o["rho"]) <= 1e-9 * o["rho"]
     assert rho <= 1.01 * opt
+
+
+def test_two_contexts_two_threads():
+    """Thread contract (randutv.h): one host thread per ctx.  Two contexts on the
+    same device driven from two host threads at once (ctypes releases the GIL)
+    give the bits of the sequential calls; the literal entry, which shares one
+    internal ctx per device, serialises concurrent callers."""
+    import threading
+    import torch
+    from paper_2002_06960_b200.randutv import Context, randutv_factor
+    rng = np.random.default_rng(71)
+    As = [np.asfortranarray(rng.standard_normal((400, 360))) for _ in range(2)]
+    ref = []
+    c = Context()
+    try:
+        for A in As:
+            U, T, V, _ = c.randutv_factor_ex(to_dev(A), 32, 1, 9)
+            ref.append((to_np(U), to_np(T), to_np(V)))
+    finally:
+        c.close()
+    out = [None, None]
+    errs = []
+
+    def work(i):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            ci = Context(0, s)
+            try:
+                with torch.cuda.stream(s):
+                    for _ in range(3):
+                        U, T, V, _ = ci.randutv_factor_ex(to_dev(As[i]), 32, 1, 9)
+                s.synchronize()
+                out[i] = (to_np(U), to_np(T), to_np(V))
+            finally:
+                ci.close()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(2):
+        for a, b in zip(out[i], ref[i]):
+            assert np.array_equal(a, b)
+    # the literal entry from two threads at once (host pointers: staged through its internal ctx)
+    lit = [None, None]
+
+    def lit_work(i):
+        m, n = As[i].shape
+        Uh, Th, Vh = np.zeros((m, m), order="F"), np.zeros((m, n), order="F"), np.zeros((n, n), order="F")
+        randutv_factor(m, n, As[i], m, 32, 1, 9, Uh, Th, Vh)
+        lit[i] = (Uh, Th, Vh)
+
+    th = [threading.Thread(target=lit_work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in range(2):
+        for a, b in zip(lit[i], ref[i]):
+            assert np.array_equal(a, b)
