@@ -34,6 +34,7 @@
 //     deterministic run to run.
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -84,6 +85,9 @@ struct Cfg {
 #define RUTV_RASTER_GROUP 64
 #endif
 using CfgSmall = Cfg<64, 64, 2, RUTV_GEMM_STAGES, RUTV_GEMM_MINB, 4>;
+//   Cfg<128, 64,2,3,2,4>: 4 warps (2 x 2) of 64 x 32 -- 32 independent DMMAs per warp and
+//                       k-step instead of 16 (fewer fixed-latency stalls per DMMA), 2 CTAs/SM
+using CfgWide = Cfg<128, 64, 2, 3, 2, 4>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -604,9 +608,25 @@ int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double a
 
 }  // namespace
 
+// RUTV_GEMM_CFG: "wide" = the 128 x 64 tile for every GEMM, "wide_big" = for
+// outputs with both sides >= 1024 only, "wide_skinny" = for skinny long-K
+// products only (A/B tuning; default: 64 x 64 -- measured best on the c3 step,
+// tools/gpu_session.sh cfg_ab: wide 27.3, wide_big 27.8, default 28.1 TFLOP/s)
+static int gemm_cfg_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_GEMM_CFG");
+    v = !e ? 0 : (strcmp(e, "wide") == 0 ? 1 : (strcmp(e, "wide_big") == 0 ? 2 : (strcmp(e, "wide_skinny") == 0 ? 3 : 0)));
+  }
+  return v;
+}
+
 int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                  const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
   if (M <= 0 || N <= 0) return 0;
+  const int mode = gemm_cfg_mode();
+  if (mode == 1 || (mode == 2 && M >= 1024 && N >= 1024) || (mode == 3 && (M <= 512 || N <= 512) && K >= 4096))
+    return launch_with<CfgWide>(L, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_elems);
   return launch_with<CfgSmall>(L, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_elems);
 }
 

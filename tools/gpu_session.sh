@@ -81,6 +81,12 @@ PY
         timeout 600 ncu --set full --clock-control none --import-source on -k regex:qr_leaf --launch-skip 2 --launch-count 1 \
           -o gpurun_out/prof_leaf_$h python tools/leaf_probe.py $h > gpurun_out/ncu_leaf_$h.log 2>&1; echo "ncu leaf h=$h rc=$?"
       done ;;
+    ncu_svd)
+      # ncu --set full of the Jacobi SVD kernels at w = 256 (L2-staged) and 128 (cluster-resident)
+      for w in 256 128; do
+        timeout 600 ncu --set full --clock-control none --import-source on -k regex:jacobi_.*kernel --launch-skip 4 --launch-count 1 \
+          -o gpurun_out/prof_svd_$w python tools/svd_probe.py $w > gpurun_out/ncu_svd_$w.log 2>&1; echo "ncu svd w=$w rc=$?"
+      done ;;
     ncu_gemm)
       # ncu --set full of the skinny S2 product (launch 0) and the rank-b update (launch 18) of bench_kernels gemm
       CMD="python tools/bench_kernels.py gemm"
