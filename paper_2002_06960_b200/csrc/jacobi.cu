@@ -456,9 +456,25 @@ __global__ void __launch_bounds__(JCT, 1)
         double* dst = buf[cur ^ 1];
         const double* s0 = cl.map_shared_rank(buf[cur] + src0_slot * slot, src0_rank);
         const double* s1 = cl.map_shared_rank(buf[cur] + src1_slot * slot, src1_rank);
-        for (int e = tid; e < slot; e += JCT) {
-          dst[e] = s0[e];
-          dst[slot + e] = s1[e];
+        // 16-byte DSMEM loads, four per thread in flight before the stores
+        const double2* a2 = reinterpret_cast<const double2*>(s0);
+        const double2* b2 = reinterpret_cast<const double2*>(s1);
+        double2* d2 = reinterpret_cast<double2*>(dst);
+        const int h2 = slot / 2;
+        for (int e0 = tid; e0 < h2; e0 += 2 * JCT) {
+          const int e1 = e0 + JCT;
+          const double2 x0 = a2[e0], y0 = b2[e0];
+          double2 x1 = make_double2(0.0, 0.0), y1 = x1;
+          if (e1 < h2) {
+            x1 = a2[e1];
+            y1 = b2[e1];
+          }
+          d2[e0] = x0;
+          d2[h2 + e0] = y0;
+          if (e1 < h2) {
+            d2[e1] = x1;
+            d2[h2 + e1] = y1;
+          }
         }
         __syncthreads();
         cur ^= 1;

@@ -23,7 +23,8 @@ for r in rows:
         elif k <= 512 and small > 512:
             key = f"gemm rank-{'b' if k <= 256 else '2b'} update (K={'<=256' if k <= 256 else '<=512'})"
         elif small <= 512:
-            key = "gemm skinny (one side <= 512, long K)"
+            big = max(m, n)
+            key = "gemm skinny (one side <= 512, long K)" + (" big>=8192" if big >= 8192 and k >= 8192 else " smaller")
         else:
             key = "gemm other"
     t = tot[key]
