@@ -35,6 +35,7 @@ struct Profiler {
     double bytes;
     size_t e0, e1;
     int64_t shape[3];  // GEMM M, N, K (for the RUTV_PROF_DUMP per-launch log)
+    cudaStream_t stream;  // for the RUTV_TRACE timeline (one row per stream)
   };
   std::vector<Rec> recs;
   int64_t launches[PK_COUNT] = {0};
@@ -105,6 +106,16 @@ struct Launch {
       if (bit__) once__.fetch_or(bit__, std::memory_order_acq_rel);            \
     }                                                                           \
   } while (0)
+
+// Fault injection for the error-path tests (RUTV_FAULT, read once):
+//   "alloc"          the next workspace growth fails (RANDUTV_ERR_ALLOC)
+//   "alloc:rank=R"   ... only on rank R of a sharded call (the pre-collective
+//                    agreement must then return on every rank, none hangs)
+//   "launch:N"       the N-th DGEMM launch of the process reports a CUDA
+//                    error (RANDUTV_ERR_CUDA mid-factorisation)
+// Tests only; unset in production.
+bool fault_alloc(int rank);
+bool fault_launch();
 
 #define RUTV_TRY(expr)                                          \
   do {                                                          \

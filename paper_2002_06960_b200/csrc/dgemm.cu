@@ -624,6 +624,10 @@ static int gemm_cfg_mode() {
 int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                  const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
   if (M <= 0 || N <= 0) return 0;
+  if (fault_launch()) {
+    set_last_error("dgemm_kernel [RUTV_FAULT injected]", cudaErrorLaunchFailure);
+    return RANDUTV_ERR_CUDA;
+  }
   const int mode = gemm_cfg_mode();
   if (mode == 1 || (mode == 2 && M >= 1024 && N >= 1024) || (mode == 3 && (M <= 512 || N <= 512) && K >= 4096))
     return launch_with<CfgWide>(L, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_elems);

@@ -947,6 +947,10 @@ int dist_factor(randutv_ctx* ctx, Comm* comm, Comm* side_comm, i64 m, i64 n, dou
   // arguments or workspace fail never leaves its peers blocked in a collective
   int local = b < 1 ? -6 : dist_check(lay, A, lda, q, flags, U, ldu, V, ldv);
   if (local == 0 && ctx->oversample > 0) local = -9;  // oversampling is single-GPU only
+  if (local == 0 && fault_alloc(comm->rank)) {
+    set_last_error("cudaMalloc(workspace) [RUTV_FAULT injected]", cudaErrorMemoryAllocation);
+    local = RANDUTV_ERR_ALLOC;
+  }
   const bool uv = !(flags & RANDUTV_NO_UV);
   i64 K = -1;
   if (local == 0 && k != 0) {

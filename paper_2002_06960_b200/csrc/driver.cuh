@@ -34,6 +34,9 @@ struct randutv_ctx {
   cudaEvent_t eWv, eV;
   // U update of step i on the V stream (eWu: W_U ready; eU: U update done)
   cudaEvent_t eWu, eU;
+  // eS: a step reached its QR(Y) (the deferred U update starts); eFuv: the
+  // side stream's U / V folds done
+  cudaEvent_t eS, eFuv, eUf;  // eUf: a deferred U fold read U_s
   // multi-GPU communicators (randutv_comm_init): main-stream and side-stream
   rutv::Comm* comm;
   rutv::Comm* comm_side;

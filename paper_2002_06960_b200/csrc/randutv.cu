@@ -67,7 +67,7 @@ size_t Profiler::begin(cudaStream_t s) {
 void Profiler::end(cudaStream_t s, int kind, double fl, double by, size_t e0, int64_t m, int64_t n, int64_t k) {
   const size_t e1 = begin(s);
   if (!on) return;
-  recs.push_back(Rec{kind, fl, by, e0, e1, {m, n, k}});
+  recs.push_back(Rec{kind, fl, by, e0, e1, {m, n, k}, s});
 }
 
 void Profiler::collect() {
@@ -92,6 +92,36 @@ void Profiler::collect() {
     bytes[r.kind] += r.bytes;
   }
   if (f) fclose(f);
+  // RUTV_TRACE=<file>: the recorded launches as a chrome://tracing / Perfetto
+  // timeline, one row per stream -- the analogue of the paper's Gantt chart of
+  // the task schedule (Fig. 10) without nsys
+  static const char* trace = getenv("RUTV_TRACE");
+  if (trace && !recs.empty()) {
+    FILE* tf = fopen(trace, "w");
+    if (tf) {
+      static const char* names[PK_COUNT] = {"dgemm", "qr_leaf", "jacobi_svd", "gaussian", "fold_wait"};
+      std::vector<cudaStream_t> ids;
+      fprintf(tf, "{\"traceEvents\": [\n");
+      bool first = true;
+      for (const Rec& r : recs) {
+        float t = 0.f, t0 = 0.f;
+        if (cudaEventElapsedTime(&t, pool[r.e0], pool[r.e1]) != cudaSuccess ||
+            cudaEventElapsedTime(&t0, pool[recs[0].e0], pool[r.e0]) != cudaSuccess) {
+          cudaGetLastError();
+          continue;
+        }
+        size_t sid = std::find(ids.begin(), ids.end(), r.stream) - ids.begin();
+        if (sid == ids.size()) ids.push_back(r.stream);
+        fprintf(tf, "%s{\"name\": \"%s %lldx%lldx%lld\", \"ph\": \"X\", \"pid\": 0, \"tid\": %zu, \"ts\": %.3f, "
+                    "\"dur\": %.3f, \"args\": {\"gflop\": %.4f}}",
+                first ? "" : ",\n", names[r.kind], (long long)r.shape[0], (long long)r.shape[1], (long long)r.shape[2],
+                sid, 1e3 * t0, 1e3 * t, r.flops * 1e-9);
+        first = false;
+      }
+      fprintf(tf, "\n]}\n");
+      fclose(tf);
+    }
+  }
   for (int k = 0; k < PK_COUNT; ++k) {
     auto& v = spans[k];
     std::sort(v.begin(), v.end());
@@ -187,8 +217,31 @@ size_t carve(Carver& c, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork) {
   return c.off;
 }
 
+static const char* fault_spec() {
+  static const char* f = getenv("RUTV_FAULT");
+  return f ? f : "";
+}
+
+bool fault_alloc(int rank) {
+  const char* f = fault_spec();
+  if (strncmp(f, "alloc", 5) != 0) return false;
+  const char* r = strstr(f, "rank=");
+  return r ? (rank >= 0 && atoi(r + 5) == rank) : true;
+}
+
+bool fault_launch() {
+  const char* f = fault_spec();
+  if (strncmp(f, "launch:", 7) != 0) return false;
+  static std::atomic<long> count{0};
+  return ++count == atol(f + 7);
+}
+
 int ensure_ws(randutv_ctx* ctx, size_t bytes) {
   if (ctx->ws_bytes >= bytes) return 0;
+  if (fault_alloc(-1)) {
+    set_last_error("cudaMalloc(workspace) [RUTV_FAULT injected]", cudaErrorMemoryAllocation);
+    return RANDUTV_ERR_ALLOC;
+  }
   if (ctx->ws) {
     if (ctx->ws_captured) {
       // an ASYNC call (possibly captured into a CUDA graph) used it: keep it
@@ -395,6 +448,16 @@ int fused_right_left(const Launch& L, Work& w, i64 m, i64 r, i64 b, i64 kk, i64 
   return launch_dgemm(L, false, true, r, c, 2 * b, -1.0, w.Acat, r, w.Bt, c, 1.0, X + kk, ldx, nullptr, 0);
 }
 
+// RUTV_UDEFER=0 enqueues each U update right after its step's S7 (comparison only)
+bool udefer_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_UDEFER");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 // RUTV_USTREAM=0 keeps the U update on the main stream (comparison only)
 bool ustream_on() {
   static int v = -1;
@@ -458,6 +521,17 @@ struct Problem {
   // the side stream's U fold and the final step wait for eU
   bool ustream = false;
   cudaEvent_t eWu = nullptr, eU = nullptr;
+  // Deferred U update (udefer): the U update of step i is enqueued on the V
+  // stream only when step i+1 reaches its QR(Y) (event eS), so it fills the
+  // latency-bound panel QR of step i+1 instead of competing with the
+  // GPU-saturating sampling GEMMs; eFuv = the side stream's U / V folds done
+  // (eF covers only the T folds the main stream waits for)
+  bool udefer = false;
+  cudaEvent_t eS = nullptr, eFuv = nullptr, eUf = nullptr;
+  mutable bool rec_uf = false;
+  mutable bool u_pending = false;
+  mutable i64 u_kk = 0, u_r = 0;
+  mutable bool rec_fuv = false;
   // events recorded during THIS call: waits on the others are skipped (a wait
   // on an event recorded before a CUDA-graph capture began is not capturable)
   mutable bool rec_f = false, rec_v = false, rec_u = false;
@@ -477,15 +551,63 @@ int wait_if(cudaStream_t s, cudaEvent_t e, bool recorded) {
 
 // S8 + S9 for a bw x bw diagonal block at (kk, kk).  `B` is the block to
 // decompose (T11 itself).
-int svd_and_fold(const Launch& L, Work& w, const Problem& P, i64 kk, i64 bw, int block_id) {
+// `side`: the call runs on the side stream behind step i+1 -- the T folds are
+// published by eF (the main stream waits for them), the V and U folds wait for
+// the V / U updates of the step (eV, eU) and are published by eFuv
+int svd_and_fold(const Launch& L, Work& w, const Problem& P, i64 kk, i64 bw, int block_id, bool side = false) {
   double* T11 = P.T + kk + kk * P.ldt;
   RUTV_TRY(launch_jacobi_svd(L, bw, T11, P.ldt, w.Us, w.d, w.Vs, w.status, block_id, w.jac, w.jac_elems));
   RUTV_TRY(launch_set_diag(L, bw, w.d, T11, P.ldt));
   RUTV_TRY(right_mult_inplace(L, w.Zf, kk, bw, P.T + kk * P.ldt, P.ldt, w.Vs, bw));                 // A01 V_s
   RUTV_TRY(left_mult_t_inplace(L, w.Zf, bw, P.n - kk - bw, P.T + kk + (kk + bw) * P.ldt, P.ldt, w.Us, bw));  // U_s^T A12
-  if (P.U) RUTV_TRY(right_mult_inplace(L, w.Zf, P.m, bw, P.U + kk * P.ldu, P.ldu, w.Us, bw));         // U1 U_s
+  if (side) {
+    RUTV_CUDA(cudaEventRecord(P.eF, L.stream));
+    P.rec_f = true;
+    if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
+    if (P.ustream && !P.udefer) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));
+  }
+  // (deferred U updates: the U fold runs on the V stream behind its U update,
+  // enqueue_u_update)
+  if (P.U && !(side && P.udefer))
+    RUTV_TRY(right_mult_inplace(L, w.Zf, P.m, bw, P.U + kk * P.ldu, P.ldu, w.Us, bw));                // U1 U_s
   if (P.V) RUTV_TRY(right_mult_inplace(L, w.Zf, P.n, bw, P.V + kk * P.ldv, P.ldv, w.Vs, bw));         // V1 V_s
+  if (side) {
+    RUTV_CUDA(cudaEventRecord(P.eFuv, L.stream));
+    P.rec_fuv = true;
+  }
   return 0;
+}
+
+// the U update of step kk on the V stream; deferred (Problem::udefer): also
+// the U fold of that step, U(:, blk) U_s, behind it -- after the side stream's
+// SVD (eF) and before the next SVD overwrites U_s (eUf, waited for by the side
+// stream before its next Jacobi)
+int enqueue_u_update(Work& w, const Problem& P, i64 kk, i64 r, bool with_fold) {
+  Work wu = w;
+  wu.Z = w.Zv;
+  wu.Z2 = w.Zv2;
+  wu.gemm_ws = w.gemm_ws_v;
+  wu.gemm_ws_elems = 4 * (P.m > P.n ? P.m : P.n) * P.b;
+  RUTV_TRY(apply_right(P.vl, wu, P.m, r, P.b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, P.b));
+  if (with_fold) {
+    RUTV_TRY(wait_if(P.vl.stream, P.eF, P.rec_f));
+    RUTV_TRY(right_mult_inplace(P.vl, w.Zv, P.m, P.b, P.U + kk * P.ldu, P.ldu, w.Us, P.b));  // U1 U_s
+    RUTV_CUDA(cudaEventRecord(P.eUf, P.vl.stream));
+    P.rec_uf = true;
+  }
+  RUTV_CUDA(cudaEventRecord(P.eU, P.vl.stream));
+  P.rec_u = true;
+  return 0;
+}
+
+// a deferred U update still pending: enqueue it (and its fold) now, behind the
+// main stream's progress so far
+int flush_u_update(const Launch& L, Work& w, const Problem& P) {
+  if (!P.u_pending) return 0;
+  RUTV_CUDA(cudaEventRecord(P.eS, L.stream));
+  RUTV_CUDA(cudaStreamWaitEvent(P.vl.stream, P.eS, 0));
+  P.u_pending = false;
+  return enqueue_u_update(w, P, P.u_kk, P.u_r, true);
 }
 
 double* left_record(Work& w, const Problem& P, int step) { return w.lefts + (i64)step * (P.m * P.b + 2 * P.b * P.b); }
@@ -560,6 +682,8 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
                           w.gemm_ws_elems));
   }
   if (bp > b) RUTV_TRY(select_sample(L, w, r, s, b, bp, At, P.ldt, (int)(i + 1)));
+  // the previous step's deferred U update starts with this step's QR(Y)
+  RUTV_TRY(flush_u_update(L, w, P));
   // S4 (overwrites W_V, T_V: the previous step's V update must have read them)
   if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
   RUTV_TRY(panel_qr(L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
@@ -624,14 +748,13 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
     if (P.U && P.ustream) {
       RUTV_CUDA(cudaEventRecord(P.eWu, L.stream));
       RUTV_CUDA(cudaStreamWaitEvent(P.vl.stream, P.eWu, 0));
-      Work wu = w;
-      wu.Z = w.Zv;
-      wu.Z2 = w.Zv2;
-      wu.gemm_ws = w.gemm_ws_v;
-      wu.gemm_ws_elems = 4 * (m > n ? m : n) * b;
-      RUTV_TRY(apply_right(P.vl, wu, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
-      RUTV_CUDA(cudaEventRecord(P.eU, P.vl.stream));
-      P.rec_u = true;
+      if (P.udefer) {
+        P.u_pending = true;  // enqueued at the next step's QR(Y) (flush_u_update)
+        P.u_kk = kk;
+        P.u_r = r;
+      } else {
+        RUTV_TRY(enqueue_u_update(w, P, kk, r, false));
+      }
     } else if (P.U) {
       RUTV_TRY(apply_right(L, w, m, r, b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, b));
     }
@@ -652,14 +775,17 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   // S8, S9 on the side stream, overlapping S1-S4 of step i+1
   RUTV_CUDA(cudaEventRecord(P.eR, L.stream));
   RUTV_CUDA(cudaStreamWaitEvent(P.side.stream, P.eR, 0));
-  if (P.V && P.vl.stream) RUTV_TRY(wait_if(P.side.stream, P.eV, P.rec_v));
-  if (P.ustream) RUTV_TRY(wait_if(P.side.stream, P.eU, P.rec_u));
-  RUTV_TRY(svd_and_fold(P.side, w, P, kk, b, (int)(i + 1)));
-  if (P.record_lefts) RUTV_TRY(record_left_us(P.side, w, P, (int)i, b));
-  RUTV_CUDA(cudaEventRecord(P.eF, P.side.stream));
-  P.rec_f = true;
+  if (P.udefer) RUTV_TRY(wait_if(P.side.stream, P.eUf, P.rec_uf));  // the previous U fold read U_s
+  RUTV_TRY(svd_and_fold(P.side, w, P, kk, b, (int)(i + 1), true));
+  if (P.record_lefts) {
+    // truncated runs: U_s recorded for the backward U_k accumulation; eFuv
+    // re-recorded behind the copy (the main stream's final join waits for it)
+    RUTV_TRY(record_left_us(P.side, w, P, (int)i, b));
+    RUTV_CUDA(cudaEventRecord(P.eFuv, P.side.stream));
+  }
   if (P.cps) {
-    RUTV_CUDA(cudaStreamWaitEvent(P.cps, P.eF, 0));
+    // block i of T, U, V is final once its U / V folds are done
+    RUTV_CUDA(cudaStreamWaitEvent(P.cps, P.eFuv, 0));
     RUTV_CUDA(cudaMemcpy2DAsync(P.hT + kk * m, m * 8, P.T + kk * P.ldt, P.ldt * 8, m * 8, b, cudaMemcpyDeviceToHost,
                                 P.cps));
     if (P.hU)
@@ -678,9 +804,11 @@ int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
   if (s <= 0) return 0;
   double* At = P.T + kk + kk * P.ldt;
   const bool tall = r > s;
+  RUTV_TRY(flush_u_update(L, w, P));
   {
     const size_t pe = L.pbegin();
     RUTV_TRY(wait_if(L.stream, P.eF, P.rec_f));  // previous step's folds
+    RUTV_TRY(wait_if(L.stream, P.eFuv, P.rec_fuv));
     if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
     if (P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));
     L.pend(PK_OTHER, 0.0, 0.0, pe);
@@ -704,7 +832,9 @@ int final_step(const Launch& L, Work& w, const Problem& P, i64 i) {
 int run_loop(const Launch& L, Work& w, const Problem& P, i64 nsteps, bool with_final) {
   for (i64 i = 0; i < nsteps; ++i) RUTV_TRY(sampled_step(L, w, P, i));
   if (with_final) RUTV_TRY(final_step(L, w, P, nsteps));
+  RUTV_TRY(flush_u_update(L, w, P));
   RUTV_TRY(wait_if(L.stream, P.eF, P.rec_f));
+  RUTV_TRY(wait_if(L.stream, P.eFuv, P.rec_fuv));
   if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
   if (P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));
   return 0;
@@ -728,6 +858,9 @@ int begin_call(randutv_ctx* ctx) {
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eV, cudaEventDisableTiming));
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eWu, cudaEventDisableTiming));
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eU, cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eS, cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eFuv, cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eUf, cudaEventDisableTiming));
   }
   return 0;
 }
@@ -815,6 +948,9 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
     cudaEventDestroy(ctx->eV);
     cudaEventDestroy(ctx->eWu);
     cudaEventDestroy(ctx->eU);
+    cudaEventDestroy(ctx->eS);
+    cudaEventDestroy(ctx->eFuv);
+    cudaEventDestroy(ctx->eUf);
     cudaStreamDestroy(ctx->vstr);
   }
   if (ctx->cps) {
@@ -935,10 +1071,20 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
                           uint64_t seed, unsigned flags, double* U, int64_t ldu, double* T, int64_t ldt, double* V,
                           int64_t ldv, Drain* dr);
 
+// A call that fails after enqueuing work must not return while that work can
+// still write the caller's buffers (the side / V / copy streams included)
+static int drain_on_error(randutv_ctx* ctx, int st) {
+  if (st == 0 || (st > 0 && st < RANDUTV_ERR_BASE) || !ctx || ctx->magic != rutv::kMagic) return st;
+  for (cudaStream_t s : {ctx->stream, ctx->side, ctx->vstr, ctx->cps})
+    if (s) cudaStreamSynchronize(s);
+  cudaGetLastError();
+  return st;
+}
+
 RANDUTV_API int randutv_factor_ex(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b,
                                   int q, uint64_t seed, unsigned flags, double* U, int64_t ldu, double* T,
                                   int64_t ldt, double* V, int64_t ldv) {
-  return factor_ex_impl(ctx, m, n, A, lda, b, q, seed, flags, U, ldu, T, ldt, V, ldv, nullptr);
+  return drain_on_error(ctx, factor_ex_impl(ctx, m, n, A, lda, b, q, seed, flags, U, ldu, T, ldt, V, ldv, nullptr));
 }
 
 static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, int64_t b, int q,
@@ -986,6 +1132,13 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
   P.ustream = P.U && P.vl.stream && ustream_on();
   P.eWu = ctx->eWu;
   P.eU = ctx->eU;
+  P.eS = ctx->eS;
+  P.eFuv = ctx->eFuv;
+  P.eUf = ctx->eUf;
+  // deferral needs W_U, T_U intact until the next QR(Y): the re-orthonormalised
+  // and oversampled power steps reuse them before it; the literal entry's
+  // column-block drain needs each block final at the end of its step
+  P.udefer = P.ustream && udefer_on() && !P.reorth && ctx->oversample == 0 && !dr;
   if (dr && uv) {
     if (!ctx->cps) RUTV_CUDA(cudaStreamCreateWithFlags(&ctx->cps, cudaStreamNonBlocking));
     P.cps = ctx->cps;
@@ -1106,6 +1259,8 @@ int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64
   if (uv) RUTV_TRY(launch_set_identity(L, n, n, V, ldv));
   Problem P{m, n, bb, q, seed, w.Twork, m, nullptr, m, uv ? V : nullptr, ldv, uv,
             ctx->side_launch(), ctx->eR, ctx->eF, vstream_launch(ctx), ctx->eWv, ctx->eV};
+  P.eS = ctx->eS;
+  P.eFuv = ctx->eFuv;
   P.reorth = (flags & RANDUTV_REORTH) != 0;
   P.os = ctx->oversample;
   if (!adaptive) {
@@ -1135,6 +1290,7 @@ int truncated_impl(randutv_ctx* ctx, i64 m, i64 n, const double* A, i64 lda, i64
     with_final = done == nsamp;
     if (with_final) RUTV_TRY(final_step(L, w, P, nsamp));
     RUTV_TRY(wait_if(L.stream, P.eF, P.rec_f));
+    RUTV_TRY(wait_if(L.stream, P.eFuv, P.rec_fuv));
     if (P.V && P.vl.stream) RUTV_TRY(wait_if(L.stream, P.eV, P.rec_v));
     k = with_final ? n : K * bb;
   }
@@ -1194,8 +1350,8 @@ RANDUTV_API int randutv_factor_rank(randutv_ctx* ctx, int64_t m, int64_t n, cons
   if (uv && !V) return -15;
   if (uv && ldv < n) return -16;
   if (!resid_fro) return -17;
-  return truncated_impl(ctx, m, n, A, lda, k, 0.0, b, q, seed, flags, Uk, ldu, Tk, ldt, V, ldv, resid_fro, nullptr,
-                        resid_2);
+  return drain_on_error(ctx, truncated_impl(ctx, m, n, A, lda, k, 0.0, b, q, seed, flags, Uk, ldu, Tk, ldt, V, ldv,
+                                            resid_fro, nullptr, resid_2));
 }
 
 RANDUTV_API int randutv_factor_tol(randutv_ctx* ctx, int64_t m, int64_t n, const double* A, int64_t lda, double tol,
@@ -1219,7 +1375,8 @@ RANDUTV_API int randutv_factor_tol(randutv_ctx* ctx, int64_t m, int64_t n, const
   if (uv && ldv < n) return -16;
   if (!k_out) return -17;
   if (!resid_fro) return -18;
-  return truncated_impl(ctx, m, n, A, lda, 0, tol, b, q, seed, flags, Uk, ldu, Tk, ldt, V, ldv, resid_fro, k_out);
+  return drain_on_error(
+      ctx, truncated_impl(ctx, m, n, A, lda, 0, tol, b, q, seed, flags, Uk, ldu, Tk, ldt, V, ldv, resid_fro, k_out));
 }
 
 // ----------------------------------------------------------------- literal form
