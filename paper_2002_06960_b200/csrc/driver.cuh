@@ -37,6 +37,7 @@ struct randutv_ctx {
   // eS: a step reached its QR(Y) (the deferred U update starts); eFuv: the
   // side stream's U / V folds done
   cudaEvent_t eS, eFuv, eUf;  // eUf: a deferred U fold read U_s
+  cudaEvent_t eUb[2];         // the deferred U update reading (W_U, T_U) buffer j done
   // multi-GPU communicators (randutv_comm_init): main-stream and side-stream
   rutv::Comm* comm;
   rutv::Comm* comm_side;
@@ -105,6 +106,7 @@ struct Work {
   double* Acat;   // fused S5/S7 update operands: [Z2(k:m) | W_U]  (m x 2b)
   double* Bt;     //                              [W2 | Y^T]       (n x 2b)
   double *Zv, *Zv2, *gemm_ws_v;  // temporaries of the V stream (n x b each; split-K)
+  double *Wu2, *TU2;             // second (W_U, T_U) buffer (deferred U update)
   double *osR, *osU, *osV, *osd, *osjac;  // oversampling: Rayleigh-Ritz SVD (b x b each; b = b + p)
 };
 

@@ -185,6 +185,8 @@ size_t carve(Carver& c, Work& w, i64 m, i64 n, i64 b, i64 lefts_K, bool twork) {
   w.Wu = c.take<double>(m * b);
   w.TV = c.take<double>(b * b);
   w.TU = c.take<double>(b * b);
+  w.Wu2 = c.take<double>(m * b);  // second (W_U, T_U) buffer of the deferred U update
+  w.TU2 = c.take<double>(b * b);
   w.tauV = c.take<double>(b);
   w.tauU = c.take<double>(b);
   w.Us = c.take<double>(b * b);
@@ -448,14 +450,18 @@ int fused_right_left(const Launch& L, Work& w, i64 m, i64 r, i64 b, i64 kk, i64 
   return launch_dgemm(L, false, true, r, c, 2 * b, -1.0, w.Acat, r, w.Bt, c, 1.0, X + kk, ldx, nullptr, 0);
 }
 
-// RUTV_UDEFER=0 enqueues each U update right after its step's S7 (comparison only)
-bool udefer_on() {
-  static int v = -1;
-  if (v < 0) {
+// Deferring each U update to the next step's QR(Y) (Problem::udefer), with
+// (W_U, T_U) double-buffered so the next column-block QR does not wait for it,
+// measured c2 (n = 4096) 9.29 -> 9.53 TFLOP/s but c3 (n = 16384) 28.12 ->
+// 28.03: the panel QRs are a large share of a step only for small n, so it is
+// on for n <= 8192.  RUTV_UDEFER=0/1 forces it (comparison only).
+bool udefer_on(i64 n) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("RUTV_UDEFER");
-    v = e ? atoi(e) : 1;
+    v = e ? atoi(e) : -1;
   }
-  return v != 0;
+  return v < 0 ? n <= 8192 : v != 0;
 }
 
 // RUTV_USTREAM=0 keeps the U update on the main stream (comparison only)
@@ -531,6 +537,12 @@ struct Problem {
   mutable bool rec_uf = false;
   mutable bool u_pending = false;
   mutable i64 u_kk = 0, u_r = 0;
+  // (W_U, T_U) double-buffered by step parity when deferring, so the next
+  // column-block QR never waits for the previous U update; eUb[j]: the U
+  // update reading buffer j done
+  mutable int u_buf = 0;
+  cudaEvent_t eUb[2] = {nullptr, nullptr};
+  mutable bool rec_ub[2] = {false, false};
   mutable bool rec_fuv = false;
   // events recorded during THIS call: waits on the others are skipped (a wait
   // on an event recorded before a CUDA-graph capture began is not capturable)
@@ -582,13 +594,17 @@ int svd_and_fold(const Launch& L, Work& w, const Problem& P, i64 kk, i64 bw, int
 // the U fold of that step, U(:, blk) U_s, behind it -- after the side stream's
 // SVD (eF) and before the next SVD overwrites U_s (eUf, waited for by the side
 // stream before its next Jacobi)
-int enqueue_u_update(Work& w, const Problem& P, i64 kk, i64 r, bool with_fold) {
+int enqueue_u_update(Work& w, const Problem& P, i64 kk, i64 r, bool with_fold, int buf = 0) {
   Work wu = w;
   wu.Z = w.Zv;
   wu.Z2 = w.Zv2;
   wu.gemm_ws = w.gemm_ws_v;
   wu.gemm_ws_elems = 4 * (P.m > P.n ? P.m : P.n) * P.b;
-  RUTV_TRY(apply_right(P.vl, wu, P.m, r, P.b, P.U + kk * P.ldu, P.ldu, w.Wu, r, w.TU, P.b));
+  RUTV_TRY(apply_right(P.vl, wu, P.m, r, P.b, P.U + kk * P.ldu, P.ldu, buf ? w.Wu2 : w.Wu, r, buf ? w.TU2 : w.TU, P.b));
+  if (P.udefer) {
+    RUTV_CUDA(cudaEventRecord(P.eUb[buf], P.vl.stream));
+    P.rec_ub[buf] = true;
+  }
   if (with_fold) {
     RUTV_TRY(wait_if(P.vl.stream, P.eF, P.rec_f));
     RUTV_TRY(right_mult_inplace(P.vl, w.Zv, P.m, P.b, P.U + kk * P.ldu, P.ldu, w.Us, P.b));  // U1 U_s
@@ -607,7 +623,7 @@ int flush_u_update(const Launch& L, Work& w, const Problem& P) {
   RUTV_CUDA(cudaEventRecord(P.eS, L.stream));
   RUTV_CUDA(cudaStreamWaitEvent(P.vl.stream, P.eS, 0));
   P.u_pending = false;
-  return enqueue_u_update(w, P, P.u_kk, P.u_r, true);
+  return enqueue_u_update(w, P, P.u_kk, P.u_r, true, P.u_buf);
 }
 
 double* left_record(Work& w, const Problem& P, int step) { return w.lefts + (i64)step * (P.m * P.b + 2 * P.b * P.b); }
@@ -739,12 +755,16 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
     RUTV_TRY(launch_dgemm(L, false, false, r, b, b, 1.0, w.Z + kk, m, w.TV, b, 0.0, w.Z2 + kk, m, nullptr, 0));
     if (pk > 0) RUTV_TRY(launch_dgemm(L, false, true, pk, b, b, -1.0, w.Z2, m, w.Wv, s, 1.0, Tk, P.ldt, nullptr, 0));
     RUTV_TRY(launch_dgemm(L, false, true, r, b, b, -1.0, w.Z2 + kk, m, w.Wv, s, 1.0, Tk + kk, P.ldt, nullptr, 0));
-    if (P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));  // the previous U update read W_U, T_U
-    RUTV_TRY(panel_qr(L, r, b, At, P.ldt, w.tauU, w.Wu, r, w.TU, b, w.qw));
+    const int ub = P.udefer ? (int)(i & 1) : 0;
+    double* WuB = ub ? w.Wu2 : w.Wu;
+    double* TUB = ub ? w.TU2 : w.TU;
+    if (P.udefer) RUTV_TRY(wait_if(L.stream, P.eUb[ub], P.rec_ub[ub]));  // two steps ago: read this buffer
+    else if (P.ustream) RUTV_TRY(wait_if(L.stream, P.eU, P.rec_u));     // the previous U update read W_U, T_U
+    RUTV_TRY(panel_qr(L, r, b, At, P.ldt, w.tauU, WuB, r, TUB, b, w.qw));
     RUTV_TRY(launch_triu(L, b, b, At, P.ldt));
     RUTV_TRY(launch_fill(L, r - b, b, 0.0, At + b, P.ldt));
-    RUTV_TRY(fused_right_left(L, w, m, r, b, kk, s - b, P.T + (kk + b) * P.ldt, P.ldt, w.Wv + b, s, w.Z2, m, w.Wu, r,
-                              w.TU, b, pk));
+    RUTV_TRY(fused_right_left(L, w, m, r, b, kk, s - b, P.T + (kk + b) * P.ldt, P.ldt, w.Wv + b, s, w.Z2, m, WuB, r,
+                              TUB, b, pk));
     if (P.U && P.ustream) {
       RUTV_CUDA(cudaEventRecord(P.eWu, L.stream));
       RUTV_CUDA(cudaStreamWaitEvent(P.vl.stream, P.eWu, 0));
@@ -752,6 +772,7 @@ int sampled_step(const Launch& L, Work& w, const Problem& P, i64 i) {
         P.u_pending = true;  // enqueued at the next step's QR(Y) (flush_u_update)
         P.u_kk = kk;
         P.u_r = r;
+        P.u_buf = ub;
       } else {
         RUTV_TRY(enqueue_u_update(w, P, kk, r, false));
       }
@@ -861,6 +882,8 @@ int begin_call(randutv_ctx* ctx) {
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eS, cudaEventDisableTiming));
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eFuv, cudaEventDisableTiming));
     RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eUf, cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eUb[0], cudaEventDisableTiming));
+    RUTV_CUDA(cudaEventCreateWithFlags(&ctx->eUb[1], cudaEventDisableTiming));
   }
   return 0;
 }
@@ -951,6 +974,8 @@ RANDUTV_API int randutv_destroy(randutv_ctx* ctx) {
     cudaEventDestroy(ctx->eS);
     cudaEventDestroy(ctx->eFuv);
     cudaEventDestroy(ctx->eUf);
+    cudaEventDestroy(ctx->eUb[0]);
+    cudaEventDestroy(ctx->eUb[1]);
     cudaStreamDestroy(ctx->vstr);
   }
   if (ctx->cps) {
@@ -1135,10 +1160,12 @@ static int factor_ex_impl(randutv_ctx* ctx, int64_t m, int64_t n, const double* 
   P.eS = ctx->eS;
   P.eFuv = ctx->eFuv;
   P.eUf = ctx->eUf;
+  P.eUb[0] = ctx->eUb[0];
+  P.eUb[1] = ctx->eUb[1];
   // deferral needs W_U, T_U intact until the next QR(Y): the re-orthonormalised
   // and oversampled power steps reuse them before it; the literal entry's
   // column-block drain needs each block final at the end of its step
-  P.udefer = P.ustream && udefer_on() && !P.reorth && ctx->oversample == 0 && !dr;
+  P.udefer = P.ustream && udefer_on(n) && !P.reorth && ctx->oversample == 0 && !dr;
   if (dr && uv) {
     if (!ctx->cps) RUTV_CUDA(cudaStreamCreateWithFlags(&ctx->cps, cudaStreamNonBlocking));
     P.cps = ctx->cps;
