@@ -570,9 +570,10 @@ int launch_jacobi_svd(const Launch& L, i64 w, const double* B, i64 ldb, double* 
   RUTV_CUDA(cudaMemsetAsync(iflags, 0, sizeof(int) * (MAX_SWEEPS + 2), L.stream));
   const size_t pe = L.pbegin();
   const int msw0 = L.jacobi_max_sweeps < 1 ? 1 : (L.jacobi_max_sweeps > MAX_SWEEPS ? MAX_SWEEPS : L.jacobi_max_sweeps);
-  // the cluster variant measured faster for w <= 128, the L2-staged kernel
-  // (16 warps per CTA) for w = 256 (tools/leaf_ab.sh)
-  if (w <= 128 && jacobi_cluster_on()) {
+  // the cluster variant (16-byte DSMEM exchange) measured at or below the
+  // L2-staged kernel for every w <= 256 (64: 0.56 vs 0.65 ms, 128: 1.48 vs
+  // 1.63, 256: 4.71 vs 4.75; tools/gpu_session.sh leaf_ab)
+  if (w <= 256 && jacobi_cluster_on()) {
     // data-resident cluster variant: nb = 8, P = nc / 16 CTAs (<= 16)
     const int nb = 8, nc = (int)((w + 15) / 16 * 16), P = nc / 16;
     const size_t smem = (size_t)4 * nb * ((size_t)w + nc) * sizeof(double);

@@ -532,10 +532,14 @@ void leaf_plan(i64 slab_rows, int* G, int* R, int* S) {
     }
   }
   const i64 cap1 = (i64)LEAF_MAX_CTAS * LEAF_THREADS;
-  static i64 r2_from = -2;  // RUTV_LEAF_R2_FROM: use 2 rows per thread from this slab height (tuning only)
+  // RUTV_LEAF_R2_FROM: 2 rows per thread from this slab height on (grid
+  // leaves).  Default: every grid leaf (slab > 12288) -- half the CTAs, so half
+  // the partial records per column exchange (16384 rows: 145 -> 141 us; 20000:
+  // 152 -> 144 us, tools/gpu_session.sh leaf_ab)
+  static i64 r2_from = -2;
   if (r2_from == -2) {
     const char* e = getenv("RUTV_LEAF_R2_FROM");
-    r2_from = e ? atoll(e) : -1;
+    r2_from = e ? atoll(e) : 1;
   }
   i64 g;
   if (r2_from > 0 && slab_rows >= r2_from && slab_rows <= 2 * cap1) {

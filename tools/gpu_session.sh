@@ -68,7 +68,7 @@ PY
       python -c "import numpy as np,time;a=np.random.rand(4096,4096);a@a;t=time.time();a@a;print('numpy dgemm GF/s',2*4096**3/(time.time()-t)/1e9)" ;;
     leaf_ab)
       # QR leaf plans and Jacobi variants (bench_kernels qr / svd)
-      for v in "RUTV_LEAF_MAXUNITS=5" "RUTV_LEAF_MAXUNITS=3" "RUTV_LEAF_CLUSTER=0"; do
+      for v in "RUTV_LEAF_MAXUNITS=5" "RUTV_LEAF_MAXUNITS=3" "RUTV_LEAF_R2_FROM=12289" "RUTV_LEAF_CLUSTER=0"; do
         echo "== $v" >> gpurun_out/leaf_ab.log; env $v timeout 300 python tools/bench_kernels.py qr >> gpurun_out/leaf_ab.log 2>&1
       done
       for v in "RUTV_JACOBI_CLUSTER=1" "RUTV_JACOBI_CLUSTER=0"; do
