@@ -120,6 +120,21 @@ def test_host_streamed_resume(ctx, cuts):
     assert np.max(np.abs(np.abs(T2) - np.abs(o["T"]))) / nA <= ELEM_TOL
 
 
+def test_host_streamed_resume_t_only_belady(ctx):
+    """T-only ranges (the Belady plan is rebuilt per range from its first step)
+    give the single call's T to rounding."""
+    from paper_2002_06960_b200.randutv import pinned_colmajor
+    m, n, b, q, seed = 400, 400, 32, 2, 23
+    A = np.asfortranarray(np.random.default_rng(5).standard_normal((m, n)))
+    _, T1, _, _ = _run_host(ctx, A, b, q, seed, 5, build_uv=False)
+    Ah = pinned_colmajor(m, n)
+    Ah[:] = A
+    for lo, hi in [(0, 4), (4, 9), (9, 2 ** 62)]:
+        ctx.randutv_factor_host_steps(Ah, None, None, b, q, seed, lo, hi, build_uv=False,
+                                      cache_bytes=5 * max(m, n) * b * 8)
+    assert np.max(np.abs(np.array(Ah) - T1)) / np.linalg.norm(A) <= 1e-13
+
+
 def test_host_streamed_resume_arguments(ctx):
     from paper_2002_06960_b200.randutv import RandUTVError
     A = np.zeros((64, 64), order="F")
