@@ -460,6 +460,41 @@ RANDUTV_API int randutv_factor_dist_loopback(int device, int nranks, int64_t m, 
                                              double* const* U_locals, int64_t ldu, double* const* V_locals,
                                              int64_t ldv, int64_t k, double* resid_fro);
 
+/* ---------------------------------------------------------------------------
+ * Sharded + host-streamed ("multi-GPU plus host
+ * streaming combined"): the layout of randutv_factor_dist with every rank's
+ * matrices in HOST memory, streamed through the rank's device panel cache as
+ * randutv_factor_host does -- A_local_host (m x n_p, lda >= m) the rank's
+ * block-cyclic columns, overwritten by T; U_local_host (mu x m, ldu >= mu)
+ * and V_local_host (nv x n, ldv >= nv) its rows of U and V (row ranges of
+ * randutv_dist_layout).  Per step: local sample passes with an AllReduce of Z
+ * per power step, the AllGather of Y and the same QR(Y) everywhere, the T W_V
+ * pass + AllReduce, the owner's panel (S5, S6, SVD), ONE broadcast of
+ * [W_U | T_U | U_s | V_s], and one read-write pass over the rank's later
+ * panels; U and V rows stream as in randutv_factor_host (deferred batches).
+ * Results equal randutv_factor_dist's to rounding.  Collective; arguments and
+ * workspace are agreed across the ranks before the first collective.  LRU
+ * eviction (the Belady plan is single-GPU).  flags: RANDUTV_NO_UV only
+ * (CHECK_FINITE / ASYNC / REORTH: -9).  Arguments as randutv_factor_host (the
+ * sharded shapes), report (host, may be NULL) this rank's traffic. */
+RANDUTV_API int randutv_factor_dist_host(randutv_ctx* ctx, int64_t m, int64_t n, double* A_local_host, int64_t lda,
+                                         int64_t b, int q, uint64_t seed, unsigned flags, size_t device_cache_bytes,
+                                         double* U_local_host, int64_t ldu, double* V_local_host, int64_t ldv,
+                                         randutv_host_report* report);
+
+/* randutv_factor_dist_host with `nranks` (<= 16) virtual ranks as host threads on
+ * ONE device (the loopback communicator of randutv_factor_dist_loopback): the
+ * single-GPU test harness.  Host pointer arrays laid out as for
+ * randutv_factor_dist_host (one ld per matrix kind).  Arguments: 1 device,
+ * 2 nranks, 3 m, 4 n, 5 A_locals_host, 6 lda, 7 b, 8 q, 9 seed, 10 flags,
+ * 11 device_cache_bytes (per rank), 12 U_locals_host, 13 ldu, 14 V_locals_host,
+ * 15 ldv. */
+RANDUTV_API int randutv_factor_dist_host_loopback(int device, int nranks, int64_t m, int64_t n,
+                                                  double* const* A_locals_host, int64_t lda, int64_t b, int q,
+                                                  uint64_t seed, unsigned flags, size_t device_cache_bytes,
+                                                  double* const* U_locals_host, int64_t ldu,
+                                                  double* const* V_locals_host, int64_t ldv);
+
 #ifdef __cplusplus
 }
 #endif

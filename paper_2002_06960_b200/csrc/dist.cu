@@ -58,59 +58,6 @@
 
 namespace rutv {
 
-// ============================================================== layout (host)
-
-struct Layout {
-  i64 m, n, b;
-  int P, p;
-  i64 nblocks;
-  i64 width(i64 j) const { return std::min(b, n - j * b); }
-  // local column count of rank q
-  i64 ncols(int q) const {
-    i64 c = 0;
-    for (i64 j = q; j < nblocks; j += P) c += width(j);
-    return c;
-  }
-  // number of rank q's blocks with global index < i
-  i64 lb_before(int q, i64 i) const { return i > q ? (i - q + P - 1) / P : 0; }
-  // local column offset of rank q's first block with global index >= i
-  i64 lcol(int q, i64 i) const { return lb_before(q, i) * b; }
-  i64 trailing_cols(int q, i64 i) const { return ncols(q) - lcol(q, i); }
-  i64 max_trailing(i64 i) const {
-    i64 mx = 0;
-    for (int q = 0; q < P; ++q) mx = std::max(mx, trailing_cols(q, i));
-    return mx;
-  }
-  static i64 row0(i64 rows, int P, int q) { return rows * q / P; }
-};
-
-// ============================================================== communicators
-
-struct Comm {
-  int rank = 0, nranks = 1;
-  int* dflag = nullptr;  // one device int for the pre-collective agreement (agree())
-  virtual ~Comm() {
-    if (dflag) cudaFree(dflag);
-  }
-  // wait for stream `s`, whose work includes this communicator's collectives:
-  // NCCL polls the communicator's asynchronous error state and aborts it on
-  // an error or after the timeout instead of blocking forever on a dead peer
-  virtual int sync(cudaStream_t s) {
-    RUTV_CUDA(cudaStreamSynchronize(s));
-    return 0;
-  }
-  virtual int allreduce_sum(double* buf, i64 count, cudaStream_t s) = 0;
-  // recv holds nranks * count doubles, rank q's block at q * count
-  virtual int allgather(const double* send, double* recv, i64 count, cudaStream_t s) = 0;
-  virtual int bcast(double* buf, i64 count, int root, cudaStream_t s) = 0;
-  virtual int allreduce_min_int(int* buf, i64 count, cudaStream_t s) = 0;
-  // row chunks of a pipelined GEMM -> AllReduce (1: no pipelining; the
-  // loopback's collectives synchronise the host, so chunking only adds barriers)
-  virtual int chunks() const { return 1; }
-  // collectives can be captured into a CUDA graph (NCCL: yes; loopback: no)
-  virtual bool capturable() const { return false; }
-};
-
 void comm_free(Comm* c) { delete c; }
 int comm_sync(Comm* c, cudaStream_t s) { return c->sync(s); }
 
@@ -453,11 +400,35 @@ __global__ void sum_vector_kernel(i64 cnt, const double* __restrict__ v, double*
   if (threadIdx.x == 0) *out = red[0];
 }
 
+// launchers of the layout kernels for the host-streamed sharded driver (host.cu)
+int launch_cyclic_gather_rows(const Launch& L, i64 s, i64 cols, i64 k, i64 b, int P, i64 i, const double* Yall,
+                              i64 ldc, i64 stride, double* Y, i64 ldy);
+int launch_cyclic_scatter_rows(const Launch& L, i64 sl, i64 cols, i64 k, i64 b, int P, int p, i64 lb0,
+                               const double* W, i64 ldw, double* Wl, i64 ldl);
+
 unsigned grid_for(const Launch& L, i64 total) {
   i64 b = (total + 255) / 256;
   const i64 cap = (i64)L.device_sms * 8;
   if (b > cap) b = cap;
   return (unsigned)(b < 1 ? 1 : b);
+}
+
+int launch_cyclic_gather_rows(const Launch& L, i64 s, i64 cols, i64 k, i64 b, int P, i64 i, const double* Yall,
+                              i64 ldc, i64 stride, double* Y, i64 ldy) {
+  if (s <= 0 || cols <= 0) return 0;
+  cyclic_gather_rows_kernel<<<grid_for(L, s * cols), 256, 0, L.stream>>>(s, cols, k, b, P, i, Yall, ldc, stride, Y, ldy);
+  L.count();
+  RUTV_CHECK_LAUNCH("cyclic_gather_rows_kernel");
+  return 0;
+}
+
+int launch_cyclic_scatter_rows(const Launch& L, i64 sl, i64 cols, i64 k, i64 b, int P, int p, i64 lb0,
+                               const double* W, i64 ldw, double* Wl, i64 ldl) {
+  if (sl <= 0 || cols <= 0) return 0;
+  cyclic_scatter_rows_kernel<<<grid_for(L, sl * cols), 256, 0, L.stream>>>(sl, cols, k, b, P, p, lb0, W, ldw, Wl, ldl);
+  L.count();
+  RUTV_CHECK_LAUNCH("cyclic_scatter_rows_kernel");
+  return 0;
 }
 
 // ============================================================== SPMD driver
@@ -1121,6 +1092,50 @@ RANDUTV_API int randutv_factor_dist_rank(randutv_ctx* ctx, int64_t m, int64_t n,
   if (k < 1) return -14;
   return dist_factor(ctx, ctx->comm, ctx->comm_side, m, n, A_local, lda, b, q, seed, flags, Uk_local, ldu, V_local,
                      ldv, k, resid_fro);
+}
+
+RANDUTV_API int randutv_factor_dist_host_loopback(int device, int nranks, int64_t m, int64_t n,
+                                                  double* const* A_locals_host, int64_t lda, int64_t b, int q,
+                                                  uint64_t seed, unsigned flags, size_t device_cache_bytes,
+                                                  double* const* U_locals_host, int64_t ldu,
+                                                  double* const* V_locals_host, int64_t ldv) {
+  if (nranks < 1 || nranks > kMaxLoopRanks) return -2;
+  if (!A_locals_host) return -5;
+  const bool uv = !(flags & RANDUTV_NO_UV);
+  if (uv && (!U_locals_host || !V_locals_host)) return -12;
+  LoopShared sh(nranks);
+  std::vector<int> status(nranks, 0);
+  std::vector<std::thread> th;
+  std::vector<LoopComm*> comms(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    comms[r] = new LoopComm();
+    comms[r]->sh = &sh;
+    comms[r]->rank = r;
+    comms[r]->nranks = nranks;
+  }
+  for (int r = 0; r < nranks; ++r) {
+    th.emplace_back([&, r] {
+      int st = 0;
+      randutv_ctx* ctx = nullptr;
+      cudaStream_t s = nullptr;
+      if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+        st = RANDUTV_ERR_CUDA;
+      if (st == 0) st = randutv_create(&ctx, device, s);
+      if (st == 0) {
+        comms[r]->sms = ctx->sms;
+        st = dist_host_factor(ctx, comms[r], m, n, A_locals_host[r], lda, b, q, seed, flags, device_cache_bytes,
+                              uv ? U_locals_host[r] : nullptr, ldu, uv ? V_locals_host[r] : nullptr, ldv, nullptr);
+      }
+      if (ctx) randutv_destroy(ctx);
+      if (s) cudaStreamDestroy(s);
+      status[r] = st;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (LoopComm* c : comms) delete c;
+  for (int r = 0; r < nranks; ++r)
+    if (status[r] != 0) return status[r];
+  return 0;
 }
 
 RANDUTV_API int randutv_factor_dist_loopback(int device, int nranks, int64_t m, int64_t n, double* const* A_locals,

@@ -4,9 +4,63 @@
 #pragma once
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace rutv {
-struct Comm;  // dist.cu
-}
+
+// 1-D block-cyclic column layout of the sharded paths (dist.cu, host.cu)
+struct Layout {
+  i64 m, n, b;
+  int P, p;
+  i64 nblocks;
+  i64 width(i64 j) const { return std::min(b, n - j * b); }
+  // local column count of rank q
+  i64 ncols(int q) const {
+    i64 c = 0;
+    for (i64 j = q; j < nblocks; j += P) c += width(j);
+    return c;
+  }
+  // number of rank q's blocks with global index < i
+  i64 lb_before(int q, i64 i) const { return i > q ? (i - q + P - 1) / P : 0; }
+  // local column offset of rank q's first block with global index >= i
+  i64 lcol(int q, i64 i) const { return lb_before(q, i) * b; }
+  i64 trailing_cols(int q, i64 i) const { return ncols(q) - lcol(q, i); }
+  i64 max_trailing(i64 i) const {
+    i64 mx = 0;
+    for (int q = 0; q < P; ++q) mx = std::max(mx, trailing_cols(q, i));
+    return mx;
+  }
+  static i64 row0(i64 rows, int P, int q) { return rows * q / P; }
+};
+
+// Collectives of the sharded paths: NCCL or the single-GPU loopback (dist.cu)
+struct Comm {
+  int rank = 0, nranks = 1;
+  int* dflag = nullptr;  // one device int for the pre-collective agreement (agree())
+  virtual ~Comm() {
+    if (dflag) cudaFree(dflag);
+  }
+  // wait for stream `s`, whose work includes this communicator's collectives:
+  // NCCL polls the communicator's asynchronous error state and aborts it on
+  // an error or after the timeout instead of blocking forever on a dead peer
+  virtual int sync(cudaStream_t s) {
+    RUTV_CUDA(cudaStreamSynchronize(s));
+    return 0;
+  }
+  virtual int allreduce_sum(double* buf, i64 count, cudaStream_t s) = 0;
+  // recv holds nranks * count doubles, rank q's block at q * count
+  virtual int allgather(const double* send, double* recv, i64 count, cudaStream_t s) = 0;
+  virtual int bcast(double* buf, i64 count, int root, cudaStream_t s) = 0;
+  virtual int allreduce_min_int(int* buf, i64 count, cudaStream_t s) = 0;
+  // row chunks of a pipelined GEMM -> AllReduce (1: no pipelining; the
+  // loopback's collectives synchronise the host, so chunking only adds barriers)
+  virtual int chunks() const { return 1; }
+  // collectives can be captured into a CUDA graph (NCCL: yes; loopback: no)
+  virtual bool capturable() const { return false; }
+};
+
+
+}  // namespace rutv
 
 struct randutv_ctx {
   int magic;
@@ -120,6 +174,15 @@ int finish(randutv_ctx* ctx, const Work& w);
 i64 sampled_steps(i64 n, i64 b);
 // dist.cu: release a communicator (NULL is a no-op)
 void comm_free(Comm* c);
+// host.cu: the sharded host-streamed factorisation on one rank (NEXT-1)
+int dist_host_factor(randutv_ctx* ctx, Comm* comm, int64_t m, int64_t n, double* A_local, int64_t lda, int64_t b, int q,
+                     uint64_t seed, unsigned flags, size_t cache_bytes, double* U_local, int64_t ldu,
+                     double* V_local, int64_t ldv, randutv_host_report* report);
+// dist.cu: the layout kernels (global trailing order <-> a rank's local order)
+int launch_cyclic_gather_rows(const Launch& L, i64 s, i64 cols, i64 k, i64 b, int P, i64 i, const double* Yall,
+                              i64 ldc, i64 stride, double* Y, i64 ldy);
+int launch_cyclic_scatter_rows(const Launch& L, i64 sl, i64 cols, i64 k, i64 b, int P, int p, i64 lb0,
+                               const double* W, i64 ldw, double* Wl, i64 ldl);
 // dist.cu: wait for a stream whose work includes the communicator's collectives
 int comm_sync(Comm* c, cudaStream_t s);
 int start_status(randutv_ctx* ctx, const Work& w);

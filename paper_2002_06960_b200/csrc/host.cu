@@ -343,6 +343,13 @@ struct HostRun {
   int G = 1;
   Batch bu, bv;
   double *Zb = nullptr, *Zb2 = nullptr;  // max(m, n) x G b temporaries of the merged apply
+  // sharded (randutv_factor_dist_host): the rank's communicator and layout;
+  // Yl / Wl = the rank's rows of Y / W_V (maxs x b), Yall the all-gathered
+  // chunks, wbuf = the owner's broadcast [W_U | T_U | U_s | V_s]
+  Comm* comm = nullptr;
+  Layout lay{};
+  double *Yl = nullptr, *Yall = nullptr, *Wl = nullptr, *wbuf = nullptr;
+  i64 maxs = 0;
 };
 
 // Visit panels [p0, p1) of `mat` in the current serpentine direction with a
@@ -419,14 +426,17 @@ int host_svd_T(HostRun& R, i64 i, i64 bw, double* X) {
 int host_fold_uv(HostRun& R, i64 i, i64 bw) {
   Work& w = R.w;
   double* X;
+  // (panel rows: all of U / V on one GPU, the rank's row range when sharded)
   if (R.mU >= 0) {
+    const i64 rows = R.pc.mats[R.mU].rows;
     RUTV_TRY(R.pc.get(R.mU, i, &X));
-    RUTV_TRY(right_mult_inplace(R.L, w.Zf, R.m, bw, X, R.m, w.Us, bw));
+    RUTV_TRY(right_mult_inplace(R.L, w.Zf, rows, bw, X, rows, w.Us, bw));
     RUTV_TRY(R.pc.put(R.mU, i, true));
   }
   if (R.mV >= 0) {
+    const i64 rows = R.pc.mats[R.mV].rows;
     RUTV_TRY(R.pc.get(R.mV, i, &X));
-    RUTV_TRY(right_mult_inplace(R.L, w.Zf, R.n, bw, X, R.n, w.Vs, bw));
+    RUTV_TRY(right_mult_inplace(R.L, w.Zf, rows, bw, X, rows, w.Vs, bw));
     RUTV_TRY(R.pc.put(R.mV, i, true));
   }
   return 0;
@@ -445,10 +455,11 @@ int flush_uv(HostRun& R, HostRun::Batch& B) {
   const i64 b = R.b, k0 = B.k[0], rows = B.rows, ldc = R.G * b, h = rows - k0;
   double* Wf = B.W + k0;  // rows k0:rows of the batch's W, ld rows
   // D: the folds of the L blocks
+  const i64 prow = R.pc.mats[B.mat].rows;  // panel rows (the rank's row range when sharded)
   for (i64 l = 0; l < L; ++l) {
     double* X;
     RUTV_TRY(R.pc.get(B.mat, B.k[l] / b, &X));
-    RUTV_TRY(right_mult_inplace(R.L, w.Zf, rows, b, X, rows, B.S + l * b * b, b));
+    RUTV_TRY(right_mult_inplace(R.L, w.Zf, prow, b, X, prow, B.S + l * b * b, b));
     RUTV_TRY(R.pc.put(B.mat, B.k[l] / b, true));
   }
   // W^f = D^T W: block row j (rows k_j:k_j+b) of the blocks l <= j
@@ -585,6 +596,141 @@ int host_final_step(HostRun& R, i64 i) {
   return host_fold_uv(R, i, s);
 }
 
+// ---------------------------------------------------------------------------
+// Sharded + host-streamed: the rank's block-cyclic
+// columns of A (dist.cu's layout) live in host memory and stream through the
+// rank's device panel cache; U and V are the rank's row ranges, streamed by
+// column panels.  One step is host_sampled_step's pass structure with dist.cu's
+// collectives: the local sample passes with an AllReduce of Z per power step,
+// the AllGather of Y and the same QR(Y) on every rank, the T W_V read pass +
+// AllReduce, the owner's panel (S5, S6, SVD, T11 = diag d, A01 V_s), ONE
+// broadcast of [W_U | T_U | U_s | V_s], and the read-write pass over the
+// rank's later panels (S5, S7, the U_s^T fold, the next step's local sample).
+
+int hd_sampled_step(HostRun& R, i64 i) {
+  Work& w = R.w;
+  const Layout& lay = R.lay;
+  const int p = lay.p, P = lay.P, o = (int)(i % P);
+  const i64 m = R.m, n = R.n, b = R.b, k = i * b, r = m - k, s = n - k;
+  const i64 np = R.pc.mats[R.mT].npanels;
+  const i64 lp0 = lay.lb_before(p, i), lp1 = lay.lb_before(p, i + 1);
+  const i64 sl = lay.ncols(p) - lp0 * b, maxs = R.maxs;
+  const bool next_sampled = s - b > b;
+  cudaStream_t st = R.L.stream;
+  R.dir = (i & 1) == 0;
+  // S1 + S2 (the first step; afterwards taken by the previous RW pass)
+  if (!R.y_ready) {
+    RUTV_TRY(launch_gaussian(R.L, R.seed, i, r, b, w.G, r));
+    RUTV_TRY(pass(R, R.mT, lp0, np, false, [&](i64 j, double* X) {
+      return launch_dgemm(R.L, true, false, R.pc.width(R.mT, j), b, r, 1.0, X + k, m, w.G, r, 0.0,
+                          R.Yl + (j - lp0) * b, maxs, w.gemm_ws, w.gemm_ws_elems);
+    }, k));
+  }
+  R.y_ready = false;
+  // S3: Z = sum_p A_p Y_p (AllReduce); Y_p = A_p^T Z
+  for (int qq = 0; qq < R.q; ++qq) {
+    RUTV_TRY(launch_fill(R.L, r, b, 0.0, w.Z, r));
+    RUTV_TRY(pass(R, R.mT, lp0, np, false, [&](i64 j, double* X) {
+      return launch_dgemm(R.L, false, false, r, b, R.pc.width(R.mT, j), 1.0, X + k, m, R.Yl + (j - lp0) * b, maxs,
+                          1.0, w.Z, r, nullptr, 0);
+    }, k));
+    RUTV_TRY(R.comm->allreduce_sum(w.Z, r * b, st));
+    RUTV_TRY(pass(R, R.mT, lp0, np, false, [&](i64 j, double* X) {
+      return launch_dgemm(R.L, true, false, R.pc.width(R.mT, j), b, r, 1.0, X + k, m, w.Z, r, 0.0,
+                          R.Yl + (j - lp0) * b, maxs, w.gemm_ws, w.gemm_ws_elems);
+    }, k));
+  }
+  // S4: Y in global order, the same QR on every rank; this rank's rows of W_V
+  RUTV_TRY(R.comm->allgather(R.Yl, R.Yall, maxs * b, st));
+  RUTV_TRY(launch_cyclic_gather_rows(R.L, s, b, k, b, P, i, R.Yall, maxs, maxs * b, w.Y, s));
+  RUTV_TRY(panel_qr(R.L, s, b, w.Y, s, w.tauV, w.Wv, s, w.TV, b, w.qw));
+  RUTV_TRY(launch_cyclic_scatter_rows(R.L, sl, b, k, b, P, p, lp0, w.Wv, s, R.Wl, maxs));
+  // S5 (read): Z = sum_p T_p W_p (all m rows, AllReduce); Z2 = Z T_V
+  RUTV_TRY(launch_fill(R.L, m, b, 0.0, w.Z, m));
+  RUTV_TRY(pass(R, R.mT, lp0, np, false, [&](i64 j, double* X) {
+    return launch_dgemm(R.L, false, false, m, b, R.pc.width(R.mT, j), 1.0, X, m, R.Wl + (j - lp0) * b, maxs, 1.0,
+                        w.Z, m, nullptr, 0);
+  }));
+  RUTV_TRY(R.comm->allreduce_sum(w.Z, m * b, st));
+  RUTV_TRY(launch_dgemm(R.L, false, false, m, b, b, 1.0, w.Z, m, w.TV, b, 0.0, w.Z2, m, nullptr, 0));
+  // the owner's panel i: S5 update, S6, S8, T11 = diag d, A01 V_s
+  double* Wu = R.wbuf;
+  double* TU = Wu + r * b;
+  double* Us = TU + b * b;
+  double* Vs = Us + b * b;
+  if (p == o) {
+    double* X;
+    RUTV_TRY(R.pc.get(R.mT, lp0, &X));
+    RUTV_TRY(launch_dgemm(R.L, false, true, m, b, b, -1.0, w.Z2, m, R.Wl, maxs, 1.0, X, m, nullptr, 0));
+    RUTV_TRY(panel_qr(R.L, r, b, X + k, m, w.tauU, Wu, r, TU, b, w.qw));
+    RUTV_TRY(launch_triu(R.L, b, b, X + k, m));
+    RUTV_TRY(launch_fill(R.L, r - b, b, 0.0, X + k + b, m));
+    RUTV_TRY(launch_jacobi_svd(R.L, b, X + k, m, Us, w.d, Vs, w.status, (int)(i + 1), w.jac, w.jac_elems));
+    RUTV_TRY(launch_set_diag(R.L, b, w.d, X + k, m));
+    RUTV_TRY(right_mult_inplace(R.L, w.Zf, k, b, X, m, Vs, b));  // A01 V_s
+    RUTV_TRY(R.pc.put(R.mT, lp0, true));
+  }
+  RUTV_TRY(R.comm->bcast(R.wbuf, r * b + 3 * b * b, o, st));
+  RUTV_TRY(launch_copy(R.L, b, b, Us, b, w.Us, b));
+  RUTV_TRY(launch_copy(R.L, b, b, Vs, b, w.Vs, b));
+  // the rank's later panels (RW): S5, S7, U_s^T fold, the next step's local sample
+  if (next_sampled) RUTV_TRY(launch_gaussian(R.L, R.seed, i + 1, r - b, b, w.G, r - b));
+  RUTV_TRY(launch_copy(R.L, m, b, w.Z2, m, w.Zf, m));
+  RUTV_TRY(pass(R, R.mT, lp1, np, true, [&](i64 j, double* X) {
+    const i64 wj = R.pc.width(R.mT, j);
+    RUTV_TRY(launch_dgemm(R.L, false, true, m, wj, b, -1.0, w.Zf, m, R.Wl + (j - lp0) * b, maxs, 1.0, X, m, nullptr,
+                          0));
+    RUTV_TRY(apply_left_t(R.L, w, r, wj, b, X + k, m, Wu, r, TU, b));
+    RUTV_TRY(left_mult_t_inplace(R.L, w.Zv, b, wj, X + k, m, w.Us, b));
+    if (!next_sampled) return 0;
+    return launch_dgemm(R.L, true, false, wj, b, r - b, 1.0, X + k + b, m, w.G, r - b, 0.0, R.Yl + (j - lp1) * b,
+                        maxs, w.gemm_ws, w.gemm_ws_elems);
+  }));
+  R.y_ready = next_sampled;
+  if (R.G > 1) {
+    if (R.mV >= 0) RUTV_TRY(defer_uv(R, R.bv, k, w.Wv, s, w.TV, w.Vs));
+    if (R.mU >= 0) RUTV_TRY(defer_uv(R, R.bu, k, Wu, r, TU, w.Us));
+    return 0;
+  }
+  if (R.mV >= 0) RUTV_TRY(stream_apply_right(R, R.mV, i, b, w.Wv, s, w.TV, b));
+  if (R.mU >= 0) RUTV_TRY(stream_apply_right(R, R.mU, i, b, Wu, r, TU, b));
+  return host_fold_uv(R, i, b);
+}
+
+int hd_final_step(HostRun& R, i64 i) {
+  Work& w = R.w;
+  const Layout& lay = R.lay;
+  const int p = lay.p, o = (int)(i % lay.P);
+  const i64 m = R.m, n = R.n, k = i * R.b, r = m - k, s = n - k;
+  RUTV_TRY(flush_uv(R, R.bv));
+  RUTV_TRY(flush_uv(R, R.bu));
+  if (s <= 0) return 0;
+  const bool tall = r > s;
+  double* Wu = R.wbuf;
+  double* TU = Wu + r * s;
+  double* Us = TU + s * s;
+  double* Vs = Us + s * s;
+  if (p == o) {
+    double* X;
+    const i64 lp = lay.lb_before(p, i);
+    RUTV_TRY(R.pc.get(R.mT, lp, &X));
+    if (tall) {
+      RUTV_TRY(panel_qr(R.L, r, s, X + k, m, w.tauU, Wu, r, TU, s, w.qw));
+      RUTV_TRY(launch_triu(R.L, s, s, X + k, m));
+      RUTV_TRY(launch_fill(R.L, r - s, s, 0.0, X + k + s, m));
+    }
+    RUTV_TRY(launch_jacobi_svd(R.L, s, X + k, m, Us, w.d, Vs, w.status, (int)(i + 1), w.jac, w.jac_elems));
+    RUTV_TRY(launch_set_diag(R.L, s, w.d, X + k, m));
+    RUTV_TRY(right_mult_inplace(R.L, w.Zf, k, s, X, m, Vs, s));  // A01 V_s
+    RUTV_TRY(R.pc.put(R.mT, lp, true));
+  }
+  RUTV_TRY(R.comm->bcast(R.wbuf, r * s + 3 * s * s, o, R.L.stream));
+  RUTV_TRY(launch_copy(R.L, s, s, Us, s, w.Us, s));
+  RUTV_TRY(launch_copy(R.L, s, s, Vs, s, w.Vs, s));
+  if (tall && R.mU >= 0) RUTV_TRY(stream_apply_right(R, R.mU, i, s, Wu, r, TU, s));
+  return host_fold_uv(R, i, s);
+}
+
 }  // namespace
 
 }  // namespace rutv
@@ -596,7 +742,32 @@ extern "C" {
 static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b, int q,
                             uint64_t seed, unsigned flags, size_t device_cache_bytes, double* U_host, int64_t ldu,
                             double* V_host, int64_t ldv, int64_t step_begin, int64_t step_end,
-                            randutv_host_report* report);
+                            randutv_host_report* report, Comm* comm = nullptr);
+
+}  // extern "C"
+
+namespace rutv {
+// the sharded host-streamed entry used by randutv_factor_dist_host and its
+// loopback harness (dist.cu): the rank's columns / rows in host memory
+int dist_host_factor(randutv_ctx* ctx, Comm* comm, int64_t m, int64_t n, double* A_local, int64_t lda, int64_t b, int q,
+                     uint64_t seed, unsigned flags, size_t cache_bytes, double* U_local, int64_t ldu,
+                     double* V_local, int64_t ldv, randutv_host_report* report) {
+  return factor_host_impl(ctx, m, n, A_local, lda, b, q, seed, flags, cache_bytes, U_local, ldu, V_local, ldv, 0,
+                          INT64_MAX, report, comm);
+}
+}  // namespace rutv
+
+extern "C" {
+
+RANDUTV_API int randutv_factor_dist_host(randutv_ctx* ctx, int64_t m, int64_t n, double* A_local_host, int64_t lda,
+                                         int64_t b, int q, uint64_t seed, unsigned flags, size_t device_cache_bytes,
+                                         double* U_local_host, int64_t ldu, double* V_local_host, int64_t ldv,
+                                         randutv_host_report* report) {
+  RUTV_TRY(begin_call(ctx));
+  if (!ctx->comm) return RANDUTV_ERR_NOCOMM;
+  return dist_host_factor(ctx, ctx->comm, m, n, A_local_host, lda, b, q, seed, flags, device_cache_bytes,
+                          U_local_host, ldu, V_local_host, ldv, report);
+}
 
 RANDUTV_API int randutv_factor_host(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b,
                                     int q, uint64_t seed, unsigned flags, size_t device_cache_bytes, double* U_host,
@@ -618,22 +789,44 @@ RANDUTV_API int randutv_factor_host_steps(randutv_ctx* ctx, int64_t m, int64_t n
 static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_host, int64_t lda, int64_t b, int q,
                             uint64_t seed, unsigned flags, size_t device_cache_bytes, double* U_host, int64_t ldu,
                             double* V_host, int64_t ldv, int64_t step_begin, int64_t step_end,
-                            randutv_host_report* report) {
+                            randutv_host_report* report, Comm* comm) {
   RUTV_TRY(begin_call(ctx));
   const bool uv = !(flags & RANDUTV_NO_UV);
-  if (flags & RANDUTV_REORTH) return -9;  // not implemented on the host-streamed path
-  if (ctx->oversample > 0) return -9;      // nor is oversampling (RANDUTV_OPT_OVERSAMPLE)
-  if (n < 1) return -3;
-  if (m < n) return -2;
-  if (!A_host) return -4;
-  if (lda < m) return -5;
-  if (b < 1) return -6;
-  if (q < 0) return -7;
-  if (uv && !U_host) return -11;
-  if (uv && ldu < m) return -12;
-  if (uv && !V_host) return -13;
-  if (uv && ldv < n) return -14;
-  const i64 bb = std::min<i64>(b, n);
+  // sharded: the rank's layout (dist.cu) -- its columns of A, rows of U and V
+  const int P = comm ? comm->nranks : 1, prank = comm ? comm->rank : 0;
+  const i64 bb = std::max<i64>(1, std::min<i64>(b, n));
+  Layout lay{m, n, bb, P, prank, (n + bb - 1) / bb};
+  const i64 ncl = lay.ncols(prank);
+  const i64 u0 = Layout::row0(m, P, prank), mu = Layout::row0(m, P, prank + 1) - u0;
+  const i64 v0 = Layout::row0(n, P, prank), nv = Layout::row0(n, P, prank + 1) - v0;
+  int local = 0;
+  if (flags & RANDUTV_REORTH) local = -9;  // not implemented on the host-streamed path
+  else if (ctx->oversample > 0) local = -9;  // nor is oversampling (RANDUTV_OPT_OVERSAMPLE)
+  else if (comm && (flags & (RANDUTV_CHECK_FINITE | RANDUTV_ASYNC))) local = -9;
+  else if (n < 1) local = -3;
+  else if (m < n) local = -2;
+  else if (!A_host && ncl > 0) local = -4;
+  else if (lda < m) local = -5;
+  else if (b < 1) local = -6;
+  else if (q < 0) local = -7;
+  else if (uv && !U_host && mu > 0) local = -11;
+  else if (uv && ldu < std::max<i64>(comm ? mu : m, 1)) local = -12;
+  else if (uv && !V_host && nv > 0) local = -13;
+  else if (uv && ldv < std::max<i64>(comm ? nv : n, 1)) local = -14;
+  // every rank's verdict (arguments here, workspace below) is agreed before
+  // the first collective of a sharded call (dist.cu's agreement)
+  auto agree = [&](int loc) -> int {
+    if (!comm) return loc;
+    if (!comm->dflag && cudaMalloc(&comm->dflag, sizeof(int)) != cudaSuccess) return RANDUTV_ERR_ALLOC;
+    int h = loc == 0 ? 1 : 0;
+    RUTV_CUDA(cudaMemcpyAsync(comm->dflag, &h, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    RUTV_TRY(comm->allreduce_min_int(comm->dflag, 1, ctx->stream));
+    RUTV_CUDA(cudaMemcpyAsync(&h, comm->dflag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    RUTV_TRY(comm->sync(ctx->stream));
+    if (loc != 0) return loc;
+    return h ? 0 : RANDUTV_ERR_PEER;
+  };
+  if (local != 0) return agree(local);
   randutv_host_report rep;
   memset(&rep, 0, sizeof(rep));
 
@@ -648,6 +841,9 @@ static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_ho
   R.pc.b = bb;
   R.pc.rep = &rep;
   R.pc.slot_elems = ((std::max(m, n) * bb + 31) / 32) * 32;
+  R.comm = comm;
+  R.lay = lay;
+  R.maxs = std::max<i64>(lay.max_trailing(0), 1);
   // workspace: the in-HBM driver's buffers + U_s of the deferred fold + the slots
   Carver dry{nullptr, 0, 0, true};
   {
@@ -668,8 +864,16 @@ static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_ho
     R.Zb = c.take<double>(mx * Gb);
     R.Zb2 = c.take<double>(mx * Gb);
   };
+  auto carve_dist = [&](Carver& c) {
+    if (!comm) return;
+    R.Yl = c.take<double>(R.maxs * bb);
+    R.Yall = c.take<double>((i64)P * R.maxs * bb);
+    R.Wl = c.take<double>(R.maxs * bb);
+    R.wbuf = c.take<double>(m * bb + 3 * bb * bb);
+  };
   carve(dry, R.w, m, n, bb, 0, false);
   carve_batch(dry);
+  carve_dist(dry);
   const size_t fixed = dry.off;
   const size_t slot_bytes = (size_t)R.pc.slot_elems * 8;
   size_t budget = device_cache_bytes;
@@ -679,13 +883,18 @@ static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_ho
     budget = fr / 2;
   }
   i64 nslots = (i64)(budget / slot_bytes);
-  const i64 npT = (n + bb - 1) / bb, npU = uv ? (m + bb - 1) / bb : 0, npV = uv ? npT : 0;
+  const i64 npT = (ncl + bb - 1) / bb, npU = uv ? (m + bb - 1) / bb : 0, npV = uv ? (n + bb - 1) / bb : 0;
   nslots = std::min<i64>(nslots, npT + npU + npV);
   if (nslots < 3) nslots = 3;
-  RUTV_TRY(ensure_ws(ctx, fixed + (size_t)nslots * slot_bytes + kAlign));
+  {
+    const int ws_st = fault_alloc(comm ? comm->rank : -1) && comm ? RANDUTV_ERR_ALLOC
+                                                                  : ensure_ws(ctx, fixed + (size_t)nslots * slot_bytes + kAlign);
+    RUTV_TRY(agree(ws_st));
+  }
   Carver real{(char*)ctx->ws, 0, ctx->ws_bytes, false};
   carve(real, R.w, m, n, bb, 0, false);
   carve_batch(real);
+  carve_dist(real);
   double* slots = real.take<double>(nslots * R.pc.slot_elems);
   rep.cache_slots = nslots;
   rep.slot_bytes = (int64_t)slot_bytes;
@@ -700,9 +909,9 @@ static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_ho
     registered.push_back(h);
     return 0;
   };
-  int st = pin(A_host, lda, n);
-  if (st == 0 && uv) st = pin(U_host, ldu, m);
-  if (st == 0 && uv) st = pin(V_host, ldv, n);
+  int st = ncl > 0 ? pin(A_host, lda, ncl) : 0;
+  if (st == 0 && uv && mu > 0) st = pin(U_host, ldu, m);
+  if (st == 0 && uv && nv > 0) st = pin(V_host, ldv, n);
 
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -717,13 +926,18 @@ static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_ho
     R.pc.timer.on = report != nullptr;
     st = R.pc.init(nslots, slots);
   }
+  // sharded: a rank that failed to pin or to set up its streams must not leave
+  // the others waiting in the first collective
+  if (comm) st = agree(st);
   if (st == 0) {
-    R.mT = R.pc.add_mat(A_host, m, n, lda);
-    if (uv) {
-      R.mU = R.pc.add_mat(U_host, m, m, ldu);
-      R.mV = R.pc.add_mat(V_host, n, n, ldv);
+    R.mT = R.pc.add_mat(A_host, m, ncl, lda);  // all of A, or the rank's columns
+    if (uv && mu > 0) {
+      R.mU = R.pc.add_mat(U_host, comm ? mu : m, m, ldu);  // all of U, or the rank's rows
       R.bu.mat = R.mU;
       R.bu.rows = m;
+    }
+    if (uv && nv > 0) {
+      R.mV = R.pc.add_mat(V_host, comm ? nv : n, n, ldv);
       R.bv.mat = R.mV;
       R.bv.rows = n;
     }
@@ -736,11 +950,13 @@ static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_ho
   // resumed range (step_begin > 0) continues from the U, V in host memory
   if (st == 0 && uv && step_begin == 0) {
     for (int mat : {R.mU, R.mV}) {
+      if (mat < 0) continue;
       const HostMat& M = R.pc.mats[mat];
+      const i64 row0 = !comm ? 0 : (mat == R.mU ? u0 : v0);  // global row of the panel's first row
       for (i64 j = 0; j < M.npanels && st == 0; ++j) {
         double* X;
         st = R.pc.get(mat, j, &X, false);
-        if (st == 0) st = launch_set_identity_shift(R.L, M.rows, R.pc.width(mat, j), j * bb, X, M.rows);
+        if (st == 0) st = launch_set_identity_shift(R.L, M.rows, R.pc.width(mat, j), j * bb - row0, X, M.rows);
         if (st == 0) st = R.pc.put(mat, j, true);
       }
     }
@@ -764,15 +980,15 @@ static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_ho
   if (st == 0) {
     // Belady eviction for T-only runs without the finiteness scan (their T
     // access sequence is exactly the plan)
-    if (!uv && !(flags & RANDUTV_CHECK_FINITE) && belady_on()) {
+    if (!comm && !uv && !(flags & RANDUTV_CHECK_FINITE) && belady_on()) {
       build_plan(n, bb, q, nsamp, step_begin, step_end, R.pc.plan, R.pc.nxt);
       R.pc.plan_mat = R.mT;
       R.pc.cursor = 0;
       R.pc.use_plan = true;
     }
     const i64 last = std::min<i64>(step_end, nsamp);
-    for (i64 i = step_begin; i < last && st == 0; ++i) st = host_sampled_step(R, i);
-    if (st == 0 && step_end > nsamp) st = host_final_step(R, nsamp);
+    for (i64 i = step_begin; i < last && st == 0; ++i) st = comm ? hd_sampled_step(R, i) : host_sampled_step(R, i);
+    if (st == 0 && step_end > nsamp) st = comm ? hd_final_step(R, nsamp) : host_final_step(R, nsamp);
     // a range that stops before the final step leaves no deferred U / V
     // transform behind: the host U, V are the state after step last - 1
     if (st == 0 && step_end <= nsamp) st = flush_uv(R, R.bv);
@@ -789,7 +1005,12 @@ static int factor_host_impl(randutv_ctx* ctx, int64_t m, int64_t n, double* A_ho
         cudaEventDestroy(e);
       }
       cudaEventRecord(t1, ctx->stream);
-      st = finish(ctx, R.w);
+      if (comm) {
+        // every rank returns the first non-converged block; waits through the communicator
+        st = comm->allreduce_min_int(R.w.status, 1, ctx->stream);
+        if (st == 0) st = comm->sync(ctx->stream);
+      }
+      if (st == 0) st = finish(ctx, R.w);
     }
   }
   {

@@ -90,6 +90,11 @@ SIGNATURES = {
                                    _vp, _i64, ctypes.POINTER(HostReport)]),
     "randutv_factor_host_steps": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint, ctypes.c_size_t, _vp,
                                          _i64, _vp, _i64, _i64, _i64, ctypes.POINTER(HostReport)]),
+    "randutv_factor_dist_host": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint, ctypes.c_size_t, _vp,
+                                        _i64, _vp, _i64, ctypes.POINTER(HostReport)]),
+    "randutv_factor_dist_host_loopback": (_int, [_int, _int, _i64, _i64, ctypes.POINTER(_vp), _i64, _i64, _int, _u64,
+                                                 _uint, ctypes.c_size_t, ctypes.POINTER(_vp), _i64,
+                                                 ctypes.POINTER(_vp), _i64]),
     "randutv_dist_layout": (_int, [_i64, _i64, _i64, _int, _int, ctypes.POINTER(_i64)]),
     "randutv_nccl_unique_id": (_int, [_vp]),
     "randutv_comm_init": (_int, [_vp, _vp, _int, _int]),
@@ -442,6 +447,29 @@ class Context:
         _check("randutv_factor_dist_rank", st)
         return Uk_local, V_local, rho.value
 
+    def randutv_factor_dist_host(self, A_local, m, n, b, q, seed, build_uv=True, U_local=None, V_local=None,
+                                 cache_bytes=0, flags=0, nranks=None, rank=None):
+        """Sharded + host-streamed randUTV (collective).  A_local (m x n_p,
+        Fortran-ordered float64 host array, pinned ideally) is overwritten by this
+        rank's columns of T; returns (U_local, V_local, report) in host memory."""
+        import torch.distributed as dist
+        if nranks is None:
+            nranks, rank = dist.get_world_size(), dist.get_rank()
+        lay = dist_layout(m, n, b, nranks, rank)
+        if not build_uv:
+            flags |= RANDUTV_NO_UV
+        if build_uv:
+            U_local = pinned_colmajor(lay["u1"] - lay["u0"], m) if U_local is None else U_local
+            V_local = pinned_colmajor(lay["v1"] - lay["v0"], n) if V_local is None else V_local
+        hp = lambda x: x.ctypes.data if x is not None and x.size > 0 else None
+        hld = lambda x, d: max(x.strides[1] // 8, 1) if x is not None and x.ndim == 2 and x.size > 0 else d
+        rep = HostReport()
+        st = self.lib.randutv_factor_dist_host(self.h, m, n, hp(A_local), hld(A_local, m), int(b), int(q),
+                                               int(seed) & (2**64 - 1), flags, int(cache_bytes), hp(U_local),
+                                               hld(U_local, 1), hp(V_local), hld(V_local, 1), ctypes.byref(rep))
+        _check("randutv_factor_dist_host", st)
+        return U_local, V_local, rep
+
     def randutv_small_svd(self, B, allow_nonconvergence=False):
         import torch
         w = B.shape[0]
@@ -569,4 +597,31 @@ def randutv_factor_dist_loopback(A_locals, m, n, b, q, seed, U_locals=None, V_lo
     _check("randutv_factor_dist_loopback", st)
     if k:
         return U_locals, V_locals, rho.value
+    return U_locals, V_locals
+
+
+def randutv_factor_dist_host_loopback(A_locals, m, n, b, q, seed, U_locals=None, V_locals=None, build_uv=True,
+                                      flags=0, cache_bytes=0, device=0):
+    """The sharded host-streamed driver (randutv_factor_dist_host) with
+    len(A_locals) virtual ranks on one GPU.  A_locals: the ranks' block-cyclic
+    columns as Fortran-ordered float64 host arrays (pinned ideally), overwritten
+    by T; U_locals / V_locals (allocated here if None): the ranks' rows of U, V."""
+    lib = load_library()
+    P = len(A_locals)
+    if not build_uv:
+        flags |= RANDUTV_NO_UV
+    lays = [dist_layout(m, n, b, P, p) for p in range(P)]
+    mu = max(l["u1"] - l["u0"] for l in lays)
+    nv = max(l["v1"] - l["v0"] for l in lays)
+    if build_uv:
+        if U_locals is None:
+            U_locals = [pinned_colmajor(mu, m)[:l["u1"] - l["u0"]] for l in lays]
+        if V_locals is None:
+            V_locals = [pinned_colmajor(nv, n)[:l["v1"] - l["v0"]] for l in lays]
+    arr = lambda xs: (_vp * P)(*[x.ctypes.data if x is not None and x.size > 0 else None for x in xs])
+    st = lib.randutv_factor_dist_host_loopback(0 if device is None else int(device), P, int(m), int(n), arr(A_locals),
+                                               int(m), int(b), int(q), int(seed) & (2**64 - 1), flags,
+                                               int(cache_bytes), arr(U_locals) if build_uv else None, max(mu, 1),
+                                               arr(V_locals) if build_uv else None, max(nv, 1))
+    _check("randutv_factor_dist_host_loopback", st)
     return U_locals, V_locals

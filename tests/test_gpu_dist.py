@@ -191,6 +191,14 @@ def test_nccl_single_rank_end_to_end(ctx):
         to = oracle_randutv(A, b, q, 17, k=64, thin_u=True)
         assert abs(rho - to["rho"]) <= 1e-9 * to["rho"]
         assert np.max(np.abs(np.abs(to_np(Uk)) - np.abs(to["Uk"]))) <= 1e-9
+        # sharded + host-streamed entry (NEXT-1) on the same communicator, 3-panel cache
+        from paper_2002_06960_b200.randutv import pinned_colmajor
+        Ah = pinned_colmajor(m, n)
+        Ah[:] = A
+        Uh, Vh, rep = c.randutv_factor_dist_host(Ah, m, n, b, q, 17, cache_bytes=3 * m * b * 8, nranks=1, rank=0)
+        assert rep.h2d_bytes > 0 and rep.cache_slots == 3
+        assert recon_error(A, Uh, Ah, Vh) <= 1e-12
+        assert np.max(np.abs(np.abs(Ah) - np.abs(o["T"]))) / np.linalg.norm(A) <= ELEM_TOL
     finally:
         c.close()
 

@@ -162,3 +162,89 @@ def test_host_streamed_traffic_model(ctx, m, n, b, q, slots):
     hl, dl = host_stream_traffic(m, n, b, q, rep["cache_slots"], "lru")
     assert hb <= rep["h2d_bytes"] <= 1.05 * hb and db <= rep["d2h_bytes"] <= 1.06 * db
     assert rep["h2d_bytes"] < hl
+
+
+def _shard_host_run(A, b, q, seed, P, cache_panels, build_uv=True):
+    """randutv_factor_dist_host (sharded + host-streamed, SURVEY.md §8(f)
+    NEXT-1) with P loopback ranks: every rank's block-cyclic columns and U/V
+    rows live in pinned host memory and stream through a cache_panels-slot
+    device cache per rank."""
+    from paper_2002_06960_b200.randutv import (dist_layout, local_columns, pinned_colmajor,
+                                               randutv_factor_dist_host_loopback)
+    m, n = A.shape
+    bb = min(b, n)
+    locals_ = []
+    for p in range(P):
+        cols = local_columns(n, b, P, p)
+        Al = pinned_colmajor(m, max(len(cols), 1))[:, :len(cols)]
+        Al[:] = A[:, cols]
+        locals_.append(Al)
+    slot = max(m, n) * bb * 8
+    Us, Vs = randutv_factor_dist_host_loopback(locals_, m, n, b, q, seed, build_uv=build_uv,
+                                               cache_bytes=cache_panels * slot)
+    T = np.zeros((m, n), order="F")
+    for p in range(P):
+        cols = local_columns(n, b, P, p)
+        if len(cols):
+            T[:, cols] = locals_[p]
+    if not build_uv:
+        return None, T, None
+    U = np.zeros((m, m), order="F")
+    V = np.zeros((n, n), order="F")
+    for p in range(P):
+        lay = dist_layout(m, n, b, P, p)
+        if lay["u1"] > lay["u0"]:
+            U[lay["u0"]:lay["u1"], :] = Us[p]
+        if lay["v1"] > lay["v0"]:
+            V[lay["v0"]:lay["v1"], :] = Vs[p]
+    return U, T, V
+
+
+@pytest.mark.parametrize("m,n,b,q,P", [
+    (300, 300, 32, 1, 2),
+    (400, 250, 40, 2, 3),     # tall, ragged, 3 ranks
+    (96, 96, 32, 1, 4),       # a rank with no column
+    (129, 129, 128, 0, 2),    # final block of one column
+    (64, 40, 64, 1, 3),       # b >= n: QR + SVD only
+])
+@pytest.mark.parametrize("cache_panels", [3, 1000])
+def test_dist_host_parity(ctx, m, n, b, q, P, cache_panels):
+    rng = np.random.default_rng(5 * m + n + b + 11 * P)
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    U, T, V = _shard_host_run(A, b, q, 23, P, cache_panels)
+    o = oracle_randutv(A, b, q, 23)
+    nA = np.linalg.norm(A)
+    assert recon_error(A, U, T, V) <= 1e-12
+    assert spectral_orth_error(U) <= 1e-12 and spectral_orth_error(V) <= 1e-12
+    assert np.all(np.tril(T, -1) == 0.0)
+    assert diag_parity(np.diag(T), np.diag(o["T"])) <= 1.0
+    assert np.max(np.abs(np.abs(T) - np.abs(o["T"]))) / nA <= ELEM_TOL
+    assert np.max(np.abs(np.abs(U) - np.abs(o["U"]))) <= ELEM_TOL
+    assert np.max(np.abs(np.abs(V) - np.abs(o["V"]))) <= ELEM_TOL
+
+
+def test_dist_host_matches_dist_and_no_uv(ctx):
+    """Same layout, same collectives: the host-streamed sharded T equals the
+    in-HBM sharded T to rounding, is deterministic, and does not depend on U, V."""
+    import torch
+    from paper_2002_06960_b200.randutv import colmajor, local_columns, randutv_factor_dist_loopback
+    rng = np.random.default_rng(77)
+    m, n, b, q, P = 360, 300, 32, 1, 3
+    A = np.asfortranarray(rng.standard_normal((m, n)))
+    r1 = _shard_host_run(A, b, q, 5, P, 3)
+    r2 = _shard_host_run(A, b, q, 5, P, 3)
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
+    _, T3, _ = _shard_host_run(A, b, q, 5, P, 3, build_uv=False)
+    assert np.array_equal(T3, r1[1])
+    locs = []
+    for p in range(P):
+        cols = local_columns(n, b, P, p)
+        Al = colmajor(m, len(cols))
+        Al.copy_(torch.from_numpy(np.ascontiguousarray(A[:, cols])))
+        locs.append(Al)
+    randutv_factor_dist_loopback(locs, m, n, b, q, 5, build_uv=False)
+    Td = np.zeros((m, n), order="F")
+    for p in range(P):
+        Td[:, local_columns(n, b, P, p)] = to_np(locs[p])
+    assert np.max(np.abs(np.abs(Td) - np.abs(r1[1]))) / np.linalg.norm(A) <= ELEM_TOL
