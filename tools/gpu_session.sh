@@ -1,7 +1,8 @@
 #!/bin/bash
 # One gpurun session: tests, bench, ncu launch list, ncu full capture of the top kernel.
 # Usage (from repo root, under gpurun): bash tools/gpu_session.sh [smoke] [tests] [full] [bench] [bench_c2] [kernels]
-#   [bench_variants] [host] [hqrrp] [ncu_launches] [ncu_full] [ncu_gemm] [ncu_leaf] [leaf_ab] [probe_host]
+#   [bench_variants] [host] [host_c5] [hqrrp] [configs] [breakdown] [env_ab] [trace] [gemm_shapes]
+#   [ncu_launches] [ncu_full] [ncu_gemm] [ncu_leaf] [ncu_svd] [leaf_ab] [probe_host]
 #   (ncu_full picks the longest DGEMM of ncu_launches)
 set -u
 mkdir -p gpurun_out
@@ -95,6 +96,42 @@ PY
         timeout 900 ncu --set full --clock-control none --import-source on -k regex:dgemm_kernel --launch-skip $1 --launch-count 1 \
           -o gpurun_out/prof_$2 $CMD > gpurun_out/ncu_$2.log 2>&1; echo "ncu $2 rc=$?"
       done ;;
+    breakdown)
+      # per-launch step breakdown of c3 (V stream concurrent, then serialised) -> profiles/step_breakdown*_rNN.txt
+      RUTV_PROF_DUMP=gpurun_out/prof_dump.txt timeout 900 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-graph > gpurun_out/pd.json 2>&1
+      python tools/gemm_dist.py gpurun_out/prof_dump.txt > gpurun_out/step_breakdown.txt
+      RUTV_VSTREAM=0 RUTV_PROF_DUMP=gpurun_out/prof_dump_serial.txt timeout 900 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-graph > gpurun_out/pd_serial.json 2>&1
+      python tools/gemm_dist.py gpurun_out/prof_dump_serial.txt > gpurun_out/step_breakdown_serial.txt
+      cat gpurun_out/step_breakdown.txt gpurun_out/step_breakdown_serial.txt ;;
+    configs)
+      # c1, c4, c5 and the one-rank sharded NCCL path (bench lines -> profiles/bench_rNN_*.json)
+      timeout 900 python bench.py --config c1 --no-cpu-baseline > gpurun_out/bench_c1.json 2>/dev/null; echo "c1 rc=$?"; cut -c1-400 gpurun_out/bench_c1.json
+      timeout 900 python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c4.json 2>/dev/null; echo "c4 rc=$?"; cut -c1-400 gpurun_out/bench_c4.json
+      timeout 1500 python bench.py --config c5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/bench_c5.json 2>/dev/null; echo "c5 rc=$?"; cut -c1-400 gpurun_out/bench_c5.json
+      timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
+        bench.py --gpus 1 --sharded --no-cpu-baseline > gpurun_out/bench_sharded1.json 2> gpurun_out/bench_sharded1.err
+      echo "sharded rc=$?"; cut -c1-400 gpurun_out/bench_sharded1.json ;;
+    host_c5)
+      # M7's design point: c5 T only from host memory, 16 GiB cache, Belady vs LRU, and the traffic model check
+      python tools/host_model_check.py > gpurun_out/hm.log 2>&1; RUTV_HOST_EVICT=lru python tools/host_model_check.py >> gpurun_out/hm.log 2>&1; cat gpurun_out/hm.log
+      for ev in belady lru; do
+        RUTV_HOST_EVICT=$ev timeout 1500 python bench.py --config c5 --mode host --no-uv --cache-gib 16 --steps 1 --warmup 0 \
+          > gpurun_out/host_c5_16g_$ev.json 2>> gpurun_out/host_c5.err; echo "c5 host $ev rc=$?"; cut -c1-1500 gpurun_out/host_c5_16g_$ev.json
+      done ;;
+    env_ab)
+      # A/B of a runtime knob on c3 and c2: ENV_AB="RUTV_X=1 RUTV_X=0" bash tools/gpu_session.sh env_ab
+      for v in ${ENV_AB:-RUTV_UDEFER=1 RUTV_UDEFER=0}; do
+        for c in c3 c2; do
+          env $v timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "
+import sys, json
+d = json.loads(sys.stdin.read()); print('$v $c', d['value'], d['ms_per_step'], d['roofline']['achieved'])" | tee -a gpurun_out/env_ab.log
+        done
+      done ;;
+    trace)
+      RUTV_TRACE=gpurun_out/trace_c3.json timeout 600 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+      ls -la gpurun_out/trace_c3.json ;;
+    gemm_shapes)
+      timeout 600 python tools/gemm_shapes.py > gpurun_out/gemm_shapes.log 2>&1; echo "gemm_shapes rc=$?"; cat gpurun_out/gemm_shapes.log ;;
     hqrrp)
       timeout 900 python bench.py --algo hqrrp --steps 2 --warmup 1 > gpurun_out/bench_hqrrp_c3.json 2>> gpurun_out/bench_hqrrp.err
       echo "hqrrp rc=$?"; cut -c1-300 gpurun_out/bench_hqrrp_c3.json ;;
