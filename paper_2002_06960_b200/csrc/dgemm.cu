@@ -12,10 +12,12 @@
 // measured chip peak is 37.0 TFLOP/s (profiles/fp64_peak_r01.json), equal to
 // the DFMA peak, and DMMA needs 8x fewer issue slots.  Design (each choice
 // measured on B200, profiles/gemm_tuning_r01.txt):
-//   * CTA tile 64 x 64, BK = 16, 128 threads = 4 warps (2 x 2) of 32 x 32
-//     (4 x 4 DMMA tiles, 32 accumulators/thread), 3 cp.async stages, 3 CTAs
-//     per SM -- the shape of the CUTLASS d884 kernel cuBLAS runs at 98 % of the
-//     DMMA pipe.
+//   * CTA tile 64 x 64, BK = 32, 128 threads = 4 warps (2 x 2) of 32 x 32
+//     (4 x 4 DMMA tiles, 32 accumulators/thread), 2 cp.async stages (36.9 KB
+//     each), 3 CTAs per SM.  Round 2: BK 16 -> 32 with 3 -> 2 stages (the same
+//     32-deep prefetch, half the k-tile barriers per DMMA) took the large c3
+//     shapes from 33.6 to 34.5 TFLOP/s and the c3 step +1.7 %
+//     (profiles/gemm_ab_r02.txt); cuBLAS's d884 kernel: 35.5-35.8.
 //   * Shared layout follows the global contiguous dimension with a 4-double row
 //     pad (conflict-free 64-bit fragment loads); fragments double-buffered in
 //     registers; one wait + barrier per k-tile, placed before the last k-step.
@@ -42,7 +44,10 @@ namespace rutv {
 
 namespace {
 
-constexpr int BK = 16;
+#ifndef RUTV_GEMM_BK  // k-tile depth (A/B tuning override; the default is the measured best)
+#define RUTV_GEMM_BK 32
+#endif
+constexpr int BK = RUTV_GEMM_BK;
 // Shared-memory tile layout.  A tile is Lo rows of Lc doubles (Lc along the
 // operand's contiguous global dimension).  The 8-byte fragment loads of a
 // half-warp hit rows o..o+3 at the same column offsets, so a plain layout has
@@ -70,10 +75,10 @@ struct Cfg {
   static constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_ELEMS * sizeof(double);
 };
-//   Cfg< 64, 64,2,3,3,4>: 4 warps (2 x 2) of 32 x 32, 3 stages, 3 CTAs/SM (the CUTLASS
-//                       d884 64x64 shape cuBLAS picks on B200 at 98 % DMMA-pipe use)
+//   Cfg< 64, 64,2,2,3,4>: 4 warps (2 x 2) of 32 x 32, 2 stages of BK = 32, 3 CTAs/SM (the
+//                       CUTLASS d884 64x64 tile cuBLAS picks on B200, with a deeper k-tile)
 #ifndef RUTV_GEMM_STAGES  // tuning overrides (tools/ab.sh); the defaults are the measured best
-#define RUTV_GEMM_STAGES 3
+#define RUTV_GEMM_STAGES 2
 #endif
 #ifndef RUTV_GEMM_MINB
 #define RUTV_GEMM_MINB 3
@@ -87,7 +92,7 @@ struct Cfg {
 using CfgSmall = Cfg<64, 64, 2, RUTV_GEMM_STAGES, RUTV_GEMM_MINB, 4>;
 //   Cfg<128, 64,2,3,2,4>: 4 warps (2 x 2) of 64 x 32 -- 32 independent DMMAs per warp and
 //                       k-step instead of 16 (fewer fixed-latency stalls per DMMA), 2 CTAs/SM
-using CfgWide = Cfg<128, 64, 2, 3, 2, 4>;
+using CfgWide = Cfg<128, 64, 2, RUTV_GEMM_STAGES, 2, 4>;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -561,7 +566,7 @@ int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double a
   const i64 resident = (i64)CF::MINB * L.device_sms;
   i64 splits = 1;
   if (ws && K > 0) {
-    const i64 maxk = K / (8 * BK);  // at least 128 of K per split
+    const i64 maxk = K / 128;  // at least 128 of K per split
     i64 maxs = ws_elems / (M * N);
     if (maxs > maxk) maxs = maxk;
     if (maxs > 64) maxs = 64;

