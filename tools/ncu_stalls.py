@@ -30,7 +30,12 @@ def main(path):
     h = rows[1]
     isrc, iall = h.index('Source'), h.index('Warp Stall Sampling (All Samples)')
     ix = {k: h.index(k) for k in KS if k in h}
-    data = rows[2:]
+    # multi-kernel reports repeat the header per kernel: keep the first kernel's rows
+    data = []
+    for r in rows[2:]:
+        if len(r) > iall and r[iall] == 'Warp Stall Sampling (All Samples)':
+            break
+        data.append(r)
 
     def g(r, k):
         try:
