@@ -400,6 +400,35 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
     Wx[e % c0 + (c0 + e / c0) * ldw] = 0.0;
 }
 
+// T_LL by recursive doubling (blocks beyond wl stay zero): T = [T1, -T1 S12 T2;
+// 0, T2] merges blocks of 1, 2, 4, 8, 16 reflectors (the compact-WY product
+// rule, exactly the dlarft recurrence in exact arithmetic; 5 parallel levels
+// instead of 32 sequential steps).  Ss = W_L^T W_L, Ts = diag(tau) on entry.
+__device__ __forceinline__ void tll_doubling(double (*Ss)[NB + 1], double (*Ts)[NB + 1], double (*Mm)[NB + 1],
+                                             int tid, int nthr) {
+#pragma unroll
+  for (int sz = 1; sz < NB; sz *= 2) {
+    // Mm = S12 T22 for every pair (rows a.., cols a+sz..) ; T22 upper triangular
+    for (int e = tid; e < (NB / 2) * sz; e += nthr) {
+      const int pair = e / (sz * sz), rem = e % (sz * sz);
+      const int a = pair * 2 * sz, r = a + rem % sz, c = a + sz + rem / sz;
+      double acc = 0.0;
+      for (int l = a + sz; l <= c; ++l) acc = fma(Ss[r][l], Ts[l][c], acc);
+      Mm[r][c] = acc;
+    }
+    __syncthreads();
+    // T12 = -T11 Mm ; T11 upper triangular
+    for (int e = tid; e < (NB / 2) * sz; e += nthr) {
+      const int pair = e / (sz * sz), rem = e % (sz * sz);
+      const int a = pair * 2 * sz, r = a + rem % sz, c = a + sz + rem / sz;
+      double acc = 0.0;
+      for (int l = r; l < a + sz; ++l) acc = fma(Ts[r][l], Mm[l][c], acc);
+      Ts[r][c] = -acc;
+    }
+    __syncthreads();
+  }
+}
+
 // T(c0:c0+w, c0:c0+w) from S = W^T W (same block) and tau: T_jj = tau_j,
 // T(0:j, j) = -tau_j T(0:j,0:j) S(0:j, j)   (dlarft, forward, columnwise).  One warp.
 // The compact-WY factor of one leaf (replaces the larft warp kernel, the two
@@ -428,28 +457,7 @@ __global__ void __launch_bounds__(256) t_block_kernel(const double* __restrict__
     Ts[r][c] = (r == c && r < wl) ? tau[c0 + r] : 0.0;
   }
   __syncthreads();
-  // ---- T_LL by recursive doubling (blocks beyond wl stay zero)
-#pragma unroll
-  for (int sz = 1; sz < NB; sz *= 2) {
-    // Mm = S12 T22 for every pair (rows a.., cols a+sz..) ; T22 upper triangular
-    for (int e = tid; e < (NB / 2) * sz; e += blockDim.x) {
-      const int pair = e / (sz * sz), rem = e % (sz * sz);
-      const int a = pair * 2 * sz, r = a + rem % sz, c = a + sz + rem / sz;
-      double acc = 0.0;
-      for (int l = a + sz; l <= c; ++l) acc = fma(Ss[r][l], Ts[l][c], acc);
-      Mm[r][c] = acc;
-    }
-    __syncthreads();
-    // T12 = -T11 Mm ; T11 upper triangular
-    for (int e = tid; e < (NB / 2) * sz; e += blockDim.x) {
-      const int pair = e / (sz * sz), rem = e % (sz * sz);
-      const int a = pair * 2 * sz, r = a + rem % sz, c = a + sz + rem / sz;
-      double acc = 0.0;
-      for (int l = r; l < a + sz; ++l) acc = fma(Ts[r][l], Mm[l][c], acc);
-      Ts[r][c] = -acc;
-    }
-    __syncthreads();
-  }
+  tll_doubling(Ss, Ts, Mm, tid, blockDim.x);
   // ---- M1(i, :) = S(i, 0:wl) T_LL for every row this CTA's product reads
   const int i0 = blockIdx.x * NB;
   for (int i = i0 + tid; i < c0; i += blockDim.x) {
@@ -489,6 +497,307 @@ __global__ void __launch_bounds__(256) t_block_kernel(const double* __restrict__
     }
 }
 
+
+// ---------------------------------------------------------------- fused leaf update
+// After qr_leaf_kernel has factored leaf L = columns [c0, c0+wl) of the h x w
+// panel, ONE cooperative grid does what the S GEMM (+ split-K reduce),
+// t_block_kernel and the three trailing GEMMs (+ reduce) did in 6-7 launches
+// of ~25 us each (profiles/kernels_qr_r02.txt: 29 GEMM launches = 0.83 ms of a
+// 16384 x 256 panel's 2.1 ms, latency not flops):
+//   phase 1  each CTA c, rows R_c of [c0, h):  Q_c = W_L(R_c)^T X(R_c, 0:w),
+//            X = [W(:, 0:c0+wl) | P(:, c0+wl:w)]   (NB x w partial, DMMA)
+//   phase 2  Q = sum_c Q_c in a fixed order (CTA c reduces a slice)
+//            -> S(0:c0+wl, L) = Q(:, 0:c0+wl)^T,  Z = W_L^T C = Q(:, c0+wl:w)
+//   phase 3  T_LL from S_LL and tau (recursive doubling, every CTA);
+//            T(0:c0, L) = -T(0:c0, 0:c0) S(0:c0, L) T_LL  (CTA c: rows 32c..);
+//            C(R_c, :) -= W_L(R_c) (T_LL^T Z)   (C = P(c0:h, c0+wl:w), DMMA)
+// Every CTA updates only its own rows, so phase 3 needs no further barrier.
+// All sums are fixed-order: the factorisation stays bitwise reproducible for
+// a given (h, w) (G depends on h - c0 and the SM count only).
+constexpr int UPD_THREADS = 256;
+constexpr int UPD_KC = 32;            // rows per staged chunk
+constexpr int UPD_NC = 128;           // X / C columns per pass (8 warps x 16)
+constexpr int UPD_LD = UPD_KC + 4;    // staged chunk: column-major, padded
+constexpr int UPD_ZLD = UPD_NC + 4;   // Z / M2 chunk: row-major (k, col), padded
+constexpr int UPD_MAX_CTAS = 160;
+constexpr int UPD_MIN_ROWS = 64;      // rows per CTA at least
+constexpr size_t UPD_SMEM =
+    sizeof(double) * ((size_t)NB * UPD_LD + (size_t)UPD_NC * UPD_LD + 2 * (size_t)NB * UPD_ZLD + 3 * NB * (NB + 1));
+
+__device__ __forceinline__ void dmma884q(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(UPD_THREADS, 1)
+    panel_update_kernel(double* __restrict__ P, i64 h, i64 ldp, const double* __restrict__ Wx, i64 ldw, i64 w,
+                        i64 c0, int wl, const double* __restrict__ tau, double* __restrict__ T, i64 ldt,
+                        double* __restrict__ rec, double* __restrict__ Qr) {
+  extern __shared__ __align__(16) double usm[];
+  double* Ws = usm;                              // W_L chunk: Ws[j * UPD_LD + kk] = W_L(r0 + kk, j)
+  double* Xs = Ws + NB * UPD_LD;                 // X chunk:   Xs[c * UPD_LD + kk] = X(r0 + kk, n0 + c)
+  double* Zs = Xs + UPD_NC * UPD_LD;             // Z chunk:   Zs[l * UPD_ZLD + c]
+  double* M2 = Zs + NB * UPD_ZLD;                // T_LL^T Z:  M2[k * UPD_ZLD + c]
+  double(*Ts)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(M2 + NB * UPD_ZLD);
+  double(*Ss)[NB + 1] = Ts + NB;
+  double(*Mm)[NB + 1] = Ss + NB;
+
+  cg::grid_group grid = cg::this_grid();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const i64 rows = h - c0;
+  const i64 per = (rows + G - 1) / G;
+  const i64 rb = c0 + (i64)cta * per;
+  const i64 re = rb + per < h ? rb + per : h;  // rb >= re: no rows (zero record)
+  const double* WL = Wx + c0 * ldw;             // column c0 of W, absolute rows
+  const i64 E = (i64)NB * w;                    // entries of Q (NB x w, ld NB)
+
+  // ---------------- phase 1: Q_c = W_L(R_c)^T X(R_c, :)
+  // chunk loads double-buffered in registers: chunk k+1 is in flight while
+  // chunk k's DMMAs run (one L2 round trip per pass, not per chunk)
+  constexpr int XQ = UPD_NC * UPD_KC / UPD_THREADS, WQ = NB * UPD_KC / UPD_THREADS;
+  for (i64 n0 = 0; n0 < w; n0 += UPD_NC) {
+    double acc[4][2][2];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    double xv[XQ], wv[WQ];
+    auto fetch = [&](i64 r0) {
+#pragma unroll
+      for (int q = 0; q < XQ; ++q) {
+        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, c = e / UPD_KC;
+        const i64 r = r0 + kk, col = n0 + c;
+        double x = 0.0;
+        if (r < re && col < w) x = col < c0 + wl ? Wx[r + col * ldw] : P[r + col * ldp];
+        xv[q] = x;
+      }
+#pragma unroll
+      for (int q = 0; q < WQ; ++q) {
+        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, j = e / UPD_KC;
+        const i64 r = r0 + kk;
+        wv[q] = (r < re && j < wl) ? WL[r + (i64)j * ldw] : 0.0;
+      }
+    };
+    if (rb < re) fetch(rb);
+    for (i64 r0 = rb; r0 < re; r0 += UPD_KC) {
+      __syncthreads();  // the previous chunk is consumed
+#pragma unroll
+      for (int q = 0; q < XQ; ++q) {
+        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, c = e / UPD_KC;
+        Xs[c * UPD_LD + kk] = xv[q];
+      }
+#pragma unroll
+      for (int q = 0; q < WQ; ++q) {
+        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, j = e / UPD_KC;
+        Ws[j * UPD_LD + kk] = wv[q];
+      }
+      __syncthreads();
+      if (r0 + UPD_KC < re) fetch(r0 + UPD_KC);
+#pragma unroll
+      for (int kk = 0; kk < UPD_KC; kk += 4) {
+        double a[4], b[2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) a[mi] = Ws[(mi * 8 + g) * UPD_LD + kk + t];
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) b[ni] = Xs[(warp * 16 + ni * 8 + g) * UPD_LD + kk + t];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) dmma884q(acc[mi][ni], a[mi], b[ni]);
+      }
+    }
+    // lane (g, t) holds Q_c(mi*8 + g, n0 + warp*16 + ni*8 + 2t + {0, 1})
+    double* rc = rec + (i64)cta * E;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const i64 col = n0 + warp * 16 + ni * 8 + 2 * t + e;
+          if (col < w) rc[(mi * 8 + g) + col * NB] = acc[mi][ni][e];
+        }
+  }
+  grid.sync();
+
+  // ---------------- phase 2: Q = sum_c Q_c (CTA c: entries [c*epc, (c+1)*epc);
+  // four thread groups each load their <= UPD_MAX_CTAS/4 records at once, sum
+  // them in record order, and the four sums are combined in a fixed order)
+  {
+    const i64 epc = (E + G - 1) / G;
+    const i64 e0 = (i64)cta * epc, e1 = e0 + epc < E ? e0 + epc : E;
+    const int grp = tid >> 6, gl = tid & 63;
+    double* red = Zs;  // scratch
+    for (i64 eb = e0; eb < e1; eb += 64) {
+      const i64 e = eb + gl;
+      double s = 0.0;
+      if (e < e1) {
+        constexpr int RQ = UPD_MAX_CTAS / 4;
+        double x[RQ];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+          const int c = grp + 4 * q;
+          x[q] = c < G ? __ldcg(rec + (i64)c * E + e) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) s += x[q];
+      }
+      __syncthreads();
+      red[tid] = s;
+      __syncthreads();
+      if (grp == 0 && e < e1) Qr[e] = ((red[gl] + red[64 + gl]) + red[128 + gl]) + red[192 + gl];
+    }
+  }
+  grid.sync();
+
+  // ---------------- phase 3a: T_LL (every CTA)
+  for (int e = tid; e < NB * NB; e += UPD_THREADS) {
+    const int r = e % NB, c = e / NB;
+    Ss[r][c] = (r < wl && c < wl) ? __ldcg(Qr + r + (c0 + c) * NB) : 0.0;
+    Ts[r][c] = (r == c && r < wl) ? tau[c0 + r] : 0.0;
+  }
+  __syncthreads();
+  tll_doubling(Ss, Ts, Mm, tid, UPD_THREADS);
+
+  // ---------------- phase 3b: T(0:c0, L) = -T(0:c0, 0:c0) M1, M1 = S(0:c0, L) T_LL
+  // (S(l, j) = Q(j, l)).  Row blocks of 32 from the LAST CTA down (the trailing
+  // CTAs hold the fewest rows); per 32-column chunk l of T: the Q block and the
+  // T block are staged in shared memory, M1's chunk formed there.
+  for (i64 ib = G - 1 - cta; ib * NB < c0; ib += G) {
+    const i64 i0 = ib * NB;
+    double* Qc = Xs;            // Qc[m * NB + ll] = Q(m, lb + ll)   (NB x NB)
+    double* Tc = Xs + NB * NB;  // Tc[ll * NB + ii] = T(i0 + ii, lb + ll)
+    double at[4] = {0.0, 0.0, 0.0, 0.0};
+    const int ii = lane;
+    for (i64 lb = i0; lb < c0; lb += NB) {
+      __syncthreads();
+      for (int e = tid; e < NB * NB; e += UPD_THREADS) {
+        const int m = e % NB, ll = e / NB;  // Q(:, lb + ll) is contiguous
+        const i64 l = lb + ll;
+        Qc[m * NB + ll] = l < c0 ? __ldcg(Qr + m + l * NB) : 0.0;
+        const i64 i = i0 + m;  // here m plays the row ii of the T block
+        Tc[ll * NB + m] = (l < c0 && i < c0 && l >= i) ? T[i + l * ldt] : 0.0;
+      }
+      __syncthreads();
+      for (int e = tid; e < NB * NB; e += UPD_THREADS) {
+        const int ll = e % NB, jj = e / NB;
+        double a = 0.0;
+        for (int m = 0; m <= jj; ++m) a = fma(Qc[m * NB + ll], Ts[m][jj], a);
+        Mm[ll][jj] = a;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int ll = 0; ll < NB; ++ll) {
+        const double til = Tc[ll * NB + ii];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) at[q] = fma(til, Mm[ll][4 * warp + q], at[q]);
+      }
+    }
+    if (i0 + ii < c0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * warp + q < wl) T[i0 + ii + (c0 + 4 * warp + q) * ldt] = -at[q];
+  }
+  // T(L, L) = T_LL, T(L, 0:c0) = 0
+  if (cta == 0)
+    for (i64 e = tid; e < (i64)wl * (c0 + wl); e += UPD_THREADS) {
+      const i64 r = e % wl, c = e / wl;
+      T[c0 + r + c * ldt] = c < c0 ? 0.0 : Ts[r][c - c0];
+    }
+
+  // ---------------- phase 3c: C(R_c, :) -= W_L(R_c) M2,  M2 = T_LL^T Z
+  const i64 cb = c0 + wl, nrest = w - cb;
+  for (i64 n0 = 0; n0 < nrest; n0 += UPD_NC) {
+    __syncthreads();
+    for (int e = tid; e < NB * UPD_NC; e += UPD_THREADS) {
+      const int l = e % NB, c = e / NB;
+      const i64 col = cb + n0 + c;
+      Zs[l * UPD_ZLD + c] = (l < wl && col < w) ? __ldcg(Qr + l + col * NB) : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < NB * UPD_NC; e += UPD_THREADS) {
+      const int c = e % UPD_NC, k = e / UPD_NC;
+      double a = 0.0;
+      for (int l = 0; l <= k; ++l) a = fma(Ts[l][k], Zs[l * UPD_ZLD + c], a);
+      M2[k * UPD_ZLD + c] = a;
+    }
+    double wv[WQ], cv[4][2][2];
+    // W_L rows and this thread's C entries of one chunk (issued together: one
+    // L2 round trip per chunk, the C read of chunk k+1 overlapping chunk k)
+    auto fetch3 = [&](i64 r0) {
+#pragma unroll
+      for (int q = 0; q < WQ; ++q) {
+        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, j = e / UPD_KC;
+        const i64 r = r0 + kk;
+        wv[q] = (r < re && j < wl) ? WL[r + (i64)j * ldw] : 0.0;
+      }
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) {
+        const i64 col = cb + n0 + warp * 16 + ni * 8 + g;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const i64 r = r0 + mi * 8 + 2 * t + e;
+            cv[mi][ni][e] = (col < w && r < re) ? P[r + col * ldp] : 0.0;
+          }
+      }
+    };
+    if (rb < re) fetch3(rb);
+    for (i64 r0 = rb; r0 < re; r0 += UPD_KC) {
+      __syncthreads();  // M2 written / the previous Ws consumed
+#pragma unroll
+      for (int q = 0; q < WQ; ++q) {
+        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, j = e / UPD_KC;
+        Ws[j * UPD_LD + kk] = wv[q];
+      }
+      __syncthreads();
+      double acc[4][2][2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < NB; kk += 4) {
+        double a[4], b[2];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) a[mi] = Ws[(kk + t) * UPD_LD + mi * 8 + g];
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) b[ni] = M2[(kk + t) * UPD_ZLD + warp * 16 + ni * 8 + g];
+        // transposed tile: lane (g, t) gets (W_L M2)(rows 2t, 2t+1 of m-tile mi, column g of n-tile ni)
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) dmma884q(acc[mi][ni], b[ni], a[mi]);
+      }
+      double out[4][2][2];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) out[mi][ni][e] = cv[mi][ni][e] - acc[mi][ni][e];
+      if (r0 + UPD_KC < re) fetch3(r0 + UPD_KC);
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) {
+        const i64 col = cb + n0 + warp * 16 + ni * 8 + g;
+        if (col < w) {
+          double* pc = P + col * ldp;
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const i64 r = r0 + mi * 8 + 2 * t + e;
+              if (r < re) pc[r] = out[mi][ni][e];
+            }
+        }
+      }
+    }
+  }
+}
 
 constexpr int kLeafClusterMax = 16;
 
@@ -586,11 +895,51 @@ int launch_leaf_cluster(const Launch& L, int G, void** args) {
 
 }  // namespace
 
+// leaf records, then the fused update's per-CTA records and the reduced Q
 i64 panel_qr_partials_elems(i64 h, i64 w) {
   (void)h;
-  (void)w;
-  return 2 * (i64)LEAF_MAX_CTAS * PREC;
+  return 2 * (i64)LEAF_MAX_CTAS * PREC + (i64)(UPD_MAX_CTAS + 1) * NB * w;
 }
+
+namespace {
+// RUTV_QR_FUSED=0 keeps the per-leaf S GEMM + t_block + trailing GEMMs (A/B only)
+bool qr_fused_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_QR_FUSED");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
+int launch_panel_update(const Launch& L, i64 h, i64 w, double* P, i64 ldp, const double* Wx, i64 ldw, i64 c0,
+                        int wl, const double* tau, double* Tf, i64 ldtf, const QrWork& qw) {
+  const i64 rows = h - c0;
+  i64 G = (rows + UPD_MIN_ROWS - 1) / UPD_MIN_ROWS;
+  const i64 gmax = L.device_sms < UPD_MAX_CTAS ? L.device_sms : UPD_MAX_CTAS;
+  if (G > gmax) G = gmax;
+  if (G < 1) G = 1;
+  double* rec = qw.partials + 2 * (i64)LEAF_MAX_CTAS * PREC;
+  double* Qr = rec + (i64)UPD_MAX_CTAS * NB * w;
+  RUTV_ONCE_PER_DEVICE(RUTV_CUDA(
+      cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UPD_SMEM)));
+  double* Pp = P;
+  const double* Wp = Wx;
+  const double* tp = tau;
+  double* Tp = Tf;
+  i64 hh = h, lp = ldp, lw = ldw, ww = w, cc = c0, lt = ldtf;
+  int wlv = wl;
+  void* args[] = {&Pp, &hh, &lp, &Wp, &lw, &ww, &cc, &wlv, &tp, &Tp, &lt, &rec, &Qr};
+  const size_t pe = L.pbegin();
+  RUTV_CUDA(cudaLaunchCooperativeKernel((void*)panel_update_kernel, dim3((unsigned)G), dim3(UPD_THREADS), args,
+                                        UPD_SMEM, L.stream));
+  L.count();
+  // algorithmic: Q (2 wl w rows) + the trailing update (2 rows wl nrest)
+  L.pend(PK_DGEMM, 2.0 * (double)rows * wl * (double)(2 * w - c0 - wl), 8.0 * (double)rows * (w + wl + (w - c0 - wl)),
+         pe, wl, w, rows);
+  return 0;
+}
+}  // namespace
 
 int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, double* Wx, i64 ldw, double* Tf,
              i64 ldtf, const QrWork& qw) {
@@ -629,6 +978,10 @@ int panel_qr(const Launch& L, i64 h, i64 w, double* P, i64 ldp, double* tau, dou
       L.pend(PK_QR_LEAF, 4.0 * (double)(h - c0) * wl * wl, 16.0 * (double)(h - c0) * wl, pe);
     }
     // (the leaf kernel wrote the explicit W of this leaf)
+    if (qr_fused_on() && qw.partials_elems >= panel_qr_partials_elems(h, w)) {
+      RUTV_TRY(launch_panel_update(L, h, w, P, ldp, Wx, ldw, c0, wl, tau, Tf, ldtf, qw));
+      continue;
+    }
     // ---- S(0:c0+wl, L) = W(c0:h, 0:c0+wl)^T W(c0:h, L)
     double* SL = qw.S + c0 * w;  // S stored w x w, ld w
     RUTV_TRY(launch_dgemm(L, true, false, c0 + wl, wl, h - c0, 1.0, Wx + c0, ldw, Wx + c0 + c0 * ldw, ldw, 0.0,
