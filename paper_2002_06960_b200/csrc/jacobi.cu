@@ -132,6 +132,69 @@ __device__ __forceinline__ int jacobi_pair(double* xp, double* xq, double* wp, d
   return 1;
 }
 
+// The cluster kernel's rotation on register-resident columns.  Shared memory
+// bandwidth (128 B/clk/SM) bounded the pair above: eight warps each reading and
+// writing two X and two W columns per inner round (~128 KB, ~1000 cycles of a
+// ~2500-cycle round).  Here (u, v) are the X columns in registers (K per lane;
+// the caller keeps the slot-0 column of its warp resident across the cross
+// rounds), and the W columns are not touched: the rotation is accumulated
+// into the CTA's 16 x 16 factor Jm (column-major, J <- J R on columns jp, jq;
+// 16 lanes) and W <- W J is applied once per block round.
+template <int K>
+__device__ __forceinline__ int jacobi_rot_reg(double (&u)[K], double (&v)[K], double tol, double nu2, int lane,
+                                              double* Jm, int jp, int jq) {
+  double a = 0.0, bb = 0.0, g = 0.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    a = fma(u[k], u[k], a);
+    bb = fma(v[k], v[k], bb);
+    g = fma(u[k], v[k], g);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ta = __shfl_xor_sync(0xffffffffu, a, o);
+    const double tb = __shfl_xor_sync(0xffffffffu, bb, o);
+    const double tg = __shfl_xor_sync(0xffffffffu, g, o);
+    a += ta;
+    bb += tb;
+    g += tg;
+  }
+  if (!(a > nu2 && bb > nu2 && g * g > (tol * tol) * (a * bb))) return 0;
+  const double dba = bb - a;
+  const double den = fabs(dba) + sqrt(fma(dba, dba, 4.0 * g * g));
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(den));
+  y = fma(y, fma(-den, y, 1.0), y);
+  y = fma(y, fma(-den, y, 1.0), y);
+  const double t = copysign(1.0, dba) * (2.0 * g) * y;
+  const double c = rsqrt(fma(t, t, 1.0));
+  const double s = c * t;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const double x = u[k], z = v[k];
+    u[k] = c * x - s * z;
+    v[k] = s * x + c * z;
+  }
+  if (lane < 16) {
+    const double x = Jm[jp * 16 + lane], z = Jm[jq * 16 + lane];
+    Jm[jp * 16 + lane] = c * x - s * z;
+    Jm[jq * 16 + lane] = s * x + c * z;
+  }
+  return 1;
+}
+
+template <int K>
+__device__ __forceinline__ void col_load(double (&u)[K], const double* x, int w, int lane) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) u[k] = lane + 32 * k < w ? x[lane + 32 * k] : 0.0;
+}
+template <int K>
+__device__ __forceinline__ void col_store(const double (&u)[K], double* x, int w, int lane) {
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    if (lane + 32 * k < w) x[lane + 32 * k] = u[k];
+}
+
 // Xg: w x nc (X = B^T, zero padded columns), Wg: nc x nc, both column-major in
 // global memory (L2 resident).  red: >= 2 P + nc doubles; flags: MAX_SWEEPS+1 ints (zeroed).
 __global__ void __launch_bounds__(JT)
@@ -368,6 +431,7 @@ __global__ void __launch_bounds__(JCT, 1)
   __shared__ double dn[2 * 8];  // this CTA's column norms (2 nb <= 16)
   __shared__ double dall[256];  // every column norm (global column order)
   __shared__ int srot;
+  __shared__ double Jm[256];    // the block round's W rotation (16 x 16, column-major)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = JCT / 32;
   const int cta = (int)cl.block_rank(), P = (int)cl.num_blocks();
   const int nblk = 2 * P;
@@ -427,29 +491,71 @@ __global__ void __launch_bounds__(JCT, 1)
       double* X1 = Xs + slot;
       double* W0 = X0 + sx;
       double* W1 = X1 + sx;
+      // J := I (the block round's accumulated W rotation, 16 x 16)
+      for (int e = tid; e < 256; e += JCT) Jm[e] = (e % 17 == 0) ? 1.0 : 0.0;
+      __syncthreads();
       if (r == 0) {
-        // intra-block pairs of both blocks: nb-1 inner rounds, nb/2 pairs per block
+        // intra-block pairs of both blocks: nb-1 inner rounds, nb/2 pairs per block (warp = pair)
         for (int t = 0; t < nb - 1; ++t) {
-          for (int pi = warp; pi < nb; pi += nwarps) {
-            const int blk = pi / (nb / 2), k = pi % (nb / 2);
-            const int p = rr(k, t, nb), q = rr(nb - 1 - k, t, nb);
-            double* Xb = blk == 0 ? X0 : X1;
-            double* Wb = blk == 0 ? W0 : W1;
-            rotated |= jacobi_pair(Xb + (size_t)p * w, Xb + (size_t)q * w, Wb + (size_t)p * nc, Wb + (size_t)q * nc,
-                                   w, nc, tol, nu2, lane);
+          const int blk = warp / (nb / 2), k = warp % (nb / 2);
+          const int p = rr(k, t, nb), q = rr(nb - 1 - k, t, nb);
+          double* Xb = blk == 0 ? X0 : X1;
+          double u[8], v[8];
+          col_load<8>(u, Xb + (size_t)p * w, w, lane);
+          col_load<8>(v, Xb + (size_t)q * w, w, lane);
+          if (jacobi_rot_reg<8>(u, v, tol, nu2, lane, Jm, blk * nb + p, blk * nb + q)) {
+            rotated = 1;
+            col_store<8>(u, Xb + (size_t)p * w, w, lane);
+            col_store<8>(v, Xb + (size_t)q * w, w, lane);
           }
           __syncthreads();
         }
       }
-      // cross pairs (a in slot 0, (a + t) mod nb in slot 1): nb inner rounds of nb disjoint pairs
-      for (int t = 0; t < nb; ++t) {
-        for (int a = warp; a < nb; a += nwarps) {
+      // cross pairs (a in slot 0, (a + t) mod nb in slot 1): nb inner rounds of
+      // nb disjoint pairs; warp a keeps slot-0 column a in registers throughout
+      {
+        const int a = warp;
+        double u[8];
+        col_load<8>(u, X0 + (size_t)a * w, w, lane);
+        for (int t = 0; t < nb; ++t) {
           const int q = (a + t) % nb;
-          rotated |= jacobi_pair(X0 + (size_t)a * w, X1 + (size_t)q * w, W0 + (size_t)a * nc, W1 + (size_t)q * nc, w,
-                                 nc, tol, nu2, lane);
+          double v[8];
+          col_load<8>(v, X1 + (size_t)q * w, w, lane);
+          if (jacobi_rot_reg<8>(u, v, tol, nu2, lane, Jm, a, nb + q)) {
+            rotated = 1;
+            col_store<8>(v, X1 + (size_t)q * w, w, lane);
+          }
+          __syncthreads();
         }
-        __syncthreads();
+        col_store<8>(u, X0 + (size_t)a * w, w, lane);
       }
+      // W <- W J over the 16 columns [W0 | W1]: DMMA m8n8k4, warp per 8-row
+      // block (both 8-column halves), fragments straight from shared memory;
+      // a warp reads all 16 columns of its rows before the mma writes them
+      for (int rb8 = warp; rb8 * 8 < nc; rb8 += nwarps) {
+        const int row = rb8 * 8 + (lane >> 2), t4 = lane & 3;
+        double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int k = kk * 4 + t4;  // column of [W0 | W1]
+          const double av = k < nb ? W0[(size_t)k * nc + row] : W1[(size_t)(k - nb) * nc + row];
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni) {
+            const double bv = Jm[(ni * 8 + (lane >> 2)) * 16 + k];
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(acc[ni][0]), "+d"(acc[ni][1])
+                         : "d"(av), "d"(bv));
+          }
+        }
+        // lane (g, t4) holds rows rb8*8 + g, columns ni*8 + 2 t4 + {0, 1}: W0 for ni = 0, W1 for ni = 1
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          double* Wd = ni == 0 ? W0 : W1;
+          Wd[(size_t)(2 * t4) * nc + row] = acc[ni][0];
+          Wd[(size_t)(2 * t4 + 1) * nc + row] = acc[ni][1];
+        }
+      }
+      __syncthreads();
       if (nblk > 2) {
         // rotate the tournament: fetch the two incoming blocks into the other buffer
         cl.sync();

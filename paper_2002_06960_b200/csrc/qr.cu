@@ -265,12 +265,14 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
     LEAF_T(3);
     if (warp == 0) {
       // dlarfg (every lane, identical) and the w entries in one warp: one barrier
+      // beta = -sign(alpha) hypot(alpha, ||x'||) as one square root of
+      // alpha^2 + ||x'||^2 (the exchange already carries ||x'||^2; equal to
+      // dlarfg's up to rounding, without sqrt -> hypot on the critical path)
       const double alpha = TB[jj][jj];
-      const double xi = sqrt(tot[0]);
       double t0 = 0.0, s0 = 0.0, b0 = alpha;
-      const bool act = xi != 0.0;
+      const bool act = tot[0] != 0.0;
       if (act) {
-        b0 = -copysign(hypot(alpha, xi), alpha);
+        b0 = -copysign(sqrt(fma(alpha, alpha, tot[0])), alpha);
         t0 = (b0 - alpha) / b0;
         s0 = 1.0 / (alpha - b0);
       }
@@ -515,12 +517,13 @@ __global__ void __launch_bounds__(256) t_block_kernel(const double* __restrict__
 // All sums are fixed-order: the factorisation stays bitwise reproducible for
 // a given (h, w) (G depends on h - c0 and the SM count only).
 constexpr int UPD_THREADS = 256;
-constexpr int UPD_KC = 32;            // rows per staged chunk
+constexpr int UPD_KC = 32;            // rows per staged chunk (= lanes: thread (lane, warp) stages row lane)
 constexpr int UPD_NC = 128;           // X / C columns per pass (8 warps x 16)
 constexpr int UPD_LD = UPD_KC + 4;    // staged chunk: column-major, padded
 constexpr int UPD_ZLD = UPD_NC + 4;   // Z / M2 chunk: row-major (k, col), padded
 constexpr int UPD_MAX_CTAS = 160;
 constexpr int UPD_MIN_ROWS = 64;      // rows per CTA at least
+static_assert(UPD_KC == 32 && UPD_NC == 128 && UPD_THREADS == 256, "panel_update_kernel's staging map");
 constexpr size_t UPD_SMEM =
     sizeof(double) * ((size_t)NB * UPD_LD + (size_t)UPD_NC * UPD_LD + 2 * (size_t)NB * UPD_ZLD + 3 * NB * (NB + 1));
 
@@ -564,36 +567,33 @@ __global__ void __launch_bounds__(UPD_THREADS, 1)
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    // thread (lane, warp) stages row r0 + lane of columns warp + 8q: per-pass
+    // column pointers, so a chunk load is one predicated load per element
+    const double* xp[XQ];
+#pragma unroll
+    for (int q = 0; q < XQ; ++q) {
+      const i64 col = n0 + warp + 8 * q;
+      xp[q] = col >= w ? nullptr : (col < c0 + wl ? Wx + col * ldw : P + col * ldp);
+    }
+    const double* wp[WQ];
+#pragma unroll
+    for (int q = 0; q < WQ; ++q) wp[q] = warp + 8 * q < wl ? WL + (i64)(warp + 8 * q) * ldw : nullptr;
     double xv[XQ], wv[WQ];
     auto fetch = [&](i64 r0) {
+      const i64 r = r0 + lane;
+      const bool rin = r < re;
 #pragma unroll
-      for (int q = 0; q < XQ; ++q) {
-        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, c = e / UPD_KC;
-        const i64 r = r0 + kk, col = n0 + c;
-        double x = 0.0;
-        if (r < re && col < w) x = col < c0 + wl ? Wx[r + col * ldw] : P[r + col * ldp];
-        xv[q] = x;
-      }
+      for (int q = 0; q < XQ; ++q) xv[q] = (rin && xp[q]) ? xp[q][r] : 0.0;
 #pragma unroll
-      for (int q = 0; q < WQ; ++q) {
-        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, j = e / UPD_KC;
-        const i64 r = r0 + kk;
-        wv[q] = (r < re && j < wl) ? WL[r + (i64)j * ldw] : 0.0;
-      }
+      for (int q = 0; q < WQ; ++q) wv[q] = (rin && wp[q]) ? wp[q][r] : 0.0;
     };
     if (rb < re) fetch(rb);
     for (i64 r0 = rb; r0 < re; r0 += UPD_KC) {
       __syncthreads();  // the previous chunk is consumed
 #pragma unroll
-      for (int q = 0; q < XQ; ++q) {
-        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, c = e / UPD_KC;
-        Xs[c * UPD_LD + kk] = xv[q];
-      }
+      for (int q = 0; q < XQ; ++q) Xs[(warp + 8 * q) * UPD_LD + lane] = xv[q];
 #pragma unroll
-      for (int q = 0; q < WQ; ++q) {
-        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, j = e / UPD_KC;
-        Ws[j * UPD_LD + kk] = wv[q];
-      }
+      for (int q = 0; q < WQ; ++q) Ws[(warp + 8 * q) * UPD_LD + lane] = wv[q];
       __syncthreads();
       if (r0 + UPD_KC < re) fetch(r0 + UPD_KC);
 #pragma unroll
@@ -725,35 +725,36 @@ __global__ void __launch_bounds__(UPD_THREADS, 1)
       M2[k * UPD_ZLD + c] = a;
     }
     double wv[WQ], cv[4][2][2];
+    const double* wp[WQ];
+#pragma unroll
+    for (int q = 0; q < WQ; ++q) wp[q] = warp + 8 * q < wl ? WL + (i64)(warp + 8 * q) * ldw : nullptr;
+    double* cp[2];
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const i64 col = cb + n0 + warp * 16 + ni * 8 + g;
+      cp[ni] = col < w ? P + col * ldp : nullptr;
+    }
     // W_L rows and this thread's C entries of one chunk (issued together: one
     // L2 round trip per chunk, the C read of chunk k+1 overlapping chunk k)
     auto fetch3 = [&](i64 r0) {
+      const i64 r = r0 + lane;
 #pragma unroll
-      for (int q = 0; q < WQ; ++q) {
-        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, j = e / UPD_KC;
-        const i64 r = r0 + kk;
-        wv[q] = (r < re && j < wl) ? WL[r + (i64)j * ldw] : 0.0;
-      }
+      for (int q = 0; q < WQ; ++q) wv[q] = (r < re && wp[q]) ? wp[q][r] : 0.0;
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni) {
-        const i64 col = cb + n0 + warp * 16 + ni * 8 + g;
+      for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const i64 r = r0 + mi * 8 + 2 * t + e;
-            cv[mi][ni][e] = (col < w && r < re) ? P[r + col * ldp] : 0.0;
+            const i64 rr = r0 + mi * 8 + 2 * t + e;
+            cv[mi][ni][e] = (cp[ni] && rr < re) ? cp[ni][rr] : 0.0;
           }
-      }
     };
     if (rb < re) fetch3(rb);
     for (i64 r0 = rb; r0 < re; r0 += UPD_KC) {
       __syncthreads();  // M2 written / the previous Ws consumed
 #pragma unroll
-      for (int q = 0; q < WQ; ++q) {
-        const int e = tid + q * UPD_THREADS, kk = e % UPD_KC, j = e / UPD_KC;
-        Ws[j * UPD_LD + kk] = wv[q];
-      }
+      for (int q = 0; q < WQ; ++q) Ws[(warp + 8 * q) * UPD_LD + lane] = wv[q];
       __syncthreads();
       double acc[4][2][2];
 #pragma unroll
@@ -783,9 +784,8 @@ __global__ void __launch_bounds__(UPD_THREADS, 1)
       if (r0 + UPD_KC < re) fetch3(r0 + UPD_KC);
 #pragma unroll
       for (int ni = 0; ni < 2; ++ni) {
-        const i64 col = cb + n0 + warp * 16 + ni * 8 + g;
-        if (col < w) {
-          double* pc = P + col * ldp;
+        if (cp[ni]) {
+          double* pc = cp[ni];
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
