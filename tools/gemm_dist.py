@@ -35,3 +35,17 @@ T = sum(v[1] for v in tot.values())
 print(f"{'class':42s} {'launches':>8s} {'ms':>9s} {'share':>6s} {'TF/s':>7s}")
 for key, (c, ms, fl) in sorted(tot.items(), key=lambda x: -x[1][1]):
     print(f"{key:42s} {c:8d} {ms:9.1f} {ms / T:6.1%} {fl / (ms * 1e-3) / 1e12 if ms else 0:7.2f}")
+
+# the heaviest individual shapes (M, N, K) by summed time, with their rate
+if len(sys.argv) > 2:
+    shp = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for r in rows:
+        if int(r[0]) != 0:
+            continue
+        key = (int(r[1]), int(r[2]), int(r[3]))
+        shp[key][0] += 1
+        shp[key][1] += float(r[4])
+        shp[key][2] += float(r[5])
+    print(f"\n{'M':>7s} {'N':>7s} {'K':>7s} {'launches':>8s} {'ms':>8s} {'TF/s':>7s}")
+    for (m, n, k), (c, ms, fl) in sorted(shp.items(), key=lambda x: -x[1][1])[:int(sys.argv[2])]:
+        print(f"{m:7d} {n:7d} {k:7d} {c:8d} {ms:8.2f} {fl / (ms * 1e-3) / 1e12 if ms else 0:7.2f}")
