@@ -48,11 +48,43 @@ constexpr int LEAF_THREADS = 256;
 constexpr int LEAF_MAX_CTAS = 128;
 constexpr int PSTRIDE = NB + 1;  // partial record: [0] = ||x'||^2, [1+l] = x'.P(:,l)
 constexpr int PREC = PSTRIDE + 1;  // its stride in global memory (even: 16-byte copies)
+// leaf record area: 2 parities x 128 CTAs x PREC (grid leaf)
+constexpr long long LEAF_REC_ELEMS = 2LL * LEAF_MAX_CTAS * PREC;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// DSMEM push exchange (cluster leaf, PUSH): each CTA stores its partial
+// record straight into every CTA's inbox with st.async, which completes bytes
+// on the receiver's mbarrier; the receiver waits on its own barrier -- one
+// remote-store latency per column instead of a cluster barrier + DSMEM loads.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
 }
 
 // P points at the panel's top-left element (row 0, col 0); the leaf is columns
@@ -71,11 +103,14 @@ __device__ __forceinline__ double warp_sum(double v) {
 // 16 * 256 * (R + S) rows and the per-column exchange stays a cluster barrier
 // + DSMEM instead of a grid barrier + L2 round trips (c3's 16384-row panels:
 // R = 2, S = 2).
-template <int R, bool CLUSTER, int S = 0>
+template <int R, bool CLUSTER, int S = 0, bool PUSH = false>
 __global__ void __launch_bounds__(LEAF_THREADS, 1)
     qr_leaf_kernel(double* __restrict__ P, i64 h, i64 ldp, i64 c0, int nb, double* __restrict__ tau,
                    double* __restrict__ partials, double* __restrict__ Wx, i64 ldw) {
   __shared__ double mine[2][PSTRIDE];  // CLUSTER: this CTA's record, by column parity
+  // PUSH: inbox[parity][source CTA][value] and one mbarrier per parity
+  __shared__ __align__(16) double inbox[PUSH ? 2 : 1][PUSH ? 16 : 1][PSTRIDE];
+  __shared__ __align__(8) uint64_t ibar[2];
   __shared__ double TB[NB][NB + 1];  // TB[r][c]: top-block row r, leaf column c
   __shared__ double wred[LEAF_THREADS / 32][PSTRIDE];
   __shared__ double tot[PSTRIDE];
@@ -116,9 +151,16 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
     const int r = e % NB, c = e / NB;
     TB[r][c] = (r < nb && c < nb) ? L0[r + (i64)c * ldp] : 0.0;
   }
+  if constexpr (PUSH) {
+    if (tid == 0) {
+      mbar_init(smem_addr(&ibar[0]), 1);
+      mbar_init(smem_addr(&ibar[1]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cg::this_cluster().sync();  // every CTA's barriers exist before the first push
+  }
   __syncthreads();
 
-#pragma unroll 1
 #ifdef RUTV_LEAF_PROF
   long long tp[8];
 #define LEAF_T(i) tp[i] = clock64()
@@ -209,9 +251,37 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
     LEAF_T(1);
     __syncthreads();
     LEAF_T(2);
-    if constexpr (CLUSTER) {
+    if constexpr (PUSH) {
+      // the record of this CTA into every CTA's inbox (slot cta), completing
+      // 8 bytes per value on the receiver's barrier of this column's parity;
+      // thread 0 arms its own barrier for the G x 33 values it will receive.
+      // A CTA cannot push column jj+2 into a parity another CTA still reads:
+      // it needs that CTA's column jj+1 record first, sent after the read.
+      const int par = jj & 1;
+      const uint32_t bar = smem_addr(&ibar[par]);
+      if (tid == 0) mbar_expect_tx(bar, (uint32_t)(G * PSTRIDE * 8));
+      if (tid < PSTRIDE) {
+        double s2 = 0.0;
+#pragma unroll
+        for (int w = 0; w < LEAF_THREADS / 32; ++w) s2 += wred[w][tid];
+        const uint32_t dst = smem_addr(&inbox[par][cta][tid]);
+        for (int c = 0; c < G; ++c) st_async_f64(mapa_rank(dst, c), s2, mapa_rank(bar, c));
+      }
+      mbar_wait_cluster(bar, (uint32_t)((jj >> 1) & 1));
+      if (tid < PSTRIDE) {
+        double vals[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) vals[c] = c < G ? inbox[par][c][tid] : 0.0;
+        double s3 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) s3 += vals[c];
+        tot[tid] = s3;
+      }
+      __syncthreads();
+    } else if constexpr (CLUSTER) {
       cg::cluster_group cl = cg::this_cluster();
       if (tid < PSTRIDE) {
+
         double s2 = 0.0;
 #pragma unroll
         for (int w = 0; w < LEAF_THREADS / 32; ++w) s2 += wred[w][tid];
@@ -869,9 +939,19 @@ void leaf_plan(i64 slab_rows, int* G, int* R, int* S) {
   *G = (int)g;
 }
 
+// RUTV_LEAF_PUSH=0: the cluster-barrier + DSMEM-load exchange (A/B only)
+bool leaf_push_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_LEAF_PUSH");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
+
 template <int R, int S>
 int launch_leaf_cluster(const Launch& L, int G, void** args) {
-  void* fn = (void*)qr_leaf_kernel<R, true, S>;
+  void* fn = leaf_push_on() ? (void*)qr_leaf_kernel<R, true, S, true> : (void*)qr_leaf_kernel<R, true, S>;
   const size_t smem = (size_t)S * LEAF_THREADS * NB * sizeof(double);
   RUTV_ONCE_PER_DEVICE({
     RUTV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -898,7 +978,7 @@ int launch_leaf_cluster(const Launch& L, int G, void** args) {
 // leaf records, then the fused update's per-CTA records and the reduced Q
 i64 panel_qr_partials_elems(i64 h, i64 w) {
   (void)h;
-  return 2 * (i64)LEAF_MAX_CTAS * PREC + (i64)(UPD_MAX_CTAS + 1) * NB * w;
+  return LEAF_REC_ELEMS + (i64)(UPD_MAX_CTAS + 1) * NB * w;
 }
 
 namespace {
@@ -919,7 +999,7 @@ int launch_panel_update(const Launch& L, i64 h, i64 w, double* P, i64 ldp, const
   const i64 gmax = L.device_sms < UPD_MAX_CTAS ? L.device_sms : UPD_MAX_CTAS;
   if (G > gmax) G = gmax;
   if (G < 1) G = 1;
-  double* rec = qw.partials + 2 * (i64)LEAF_MAX_CTAS * PREC;
+  double* rec = qw.partials + LEAF_REC_ELEMS;
   double* Qr = rec + (i64)UPD_MAX_CTAS * NB * w;
   RUTV_ONCE_PER_DEVICE(RUTV_CUDA(
       cudaFuncSetAttribute(panel_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UPD_SMEM)));
