@@ -395,25 +395,35 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
             if (l > jj) slab_s[sr + l * SLD] = fma(-tv, wv[l], slab_s[sr + l * SLD]);
         }
       }
-      // replicated top block, element-parallel over (row r >= j, column l > j):
-      // the pivot row j has the implicit unit reflector entry; column j itself
-      // (read here) is scaled after the barrier
-      for (int e = tid; e < NB * NB; e += LEAF_THREADS) {
-        const int r = e / NB, l = e % NB;
-        if (r >= jj && r < nb && l > jj && l < nb) {
-          const double vv = (r == jj) ? 1.0 : TB[r][jj] * scal;
-          TB[r][l] = fma(-t * vv, wv[l], TB[r][l]);
+    }
+    {
+      // replicated top block: thread (row r = tid/8, columns 4(tid%8) .. +4),
+      // the 8 threads of a row in one warp (was element-parallel with a
+      // division per element and a separate barrier for the column scaling:
+      // ~12 % of the leaf's stall samples, ncu source profile).  The pivot row
+      // j has the implicit unit reflector entry; column j is scaled in place
+      // once the row's 8 threads have read it (__syncwarp)
+      const int r = tid >> 3, cq = (tid & 7) * 4;
+      const bool row_on = active && r >= jj && r < nb;
+      double vv = 0.0;
+      if (row_on) {
+        vv = (r == jj) ? 1.0 : TB[r][jj] * scal;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int l = cq + q;
+          if (l > jj && l < nb) TB[r][l] = fma(-t * vv, wv[l], TB[r][l]);
         }
       }
+      __syncwarp();
+      if (row_on && cq == 0 && r > jj) TB[r][jj] = vv;
     }
-    __syncthreads();
-    LEAF_T(4);
-    if (active && tid > jj && tid < nb) TB[tid][jj] *= scal;
     if (tid == 0) {
+      // read again only after the loop (the next column touches rows > jj)
       TB[jj][jj] = sc[2];
       if (cta == 0) tau[c0 + jj] = t;
     }
     __syncthreads();
+    LEAF_T(4);
     LEAF_T(5);
 #ifdef RUTV_LEAF_PROF
     if (tid == 0 && cta == 0 && jj == 8 && c0 == 0)
@@ -421,6 +431,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1)
              (long long)h, tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[5] - tp[0]);
 #endif
   }
+  __syncthreads();  // the last column's TB writes before the write-back
   if constexpr (CLUSTER) cg::this_cluster().sync();  // no CTA exits while its record may still be read
   // the factored leaf into P and its explicit reflectors W (unit diagonal,
   // zeros above) into Wx(0:h, c0:c0+nb): the slab rows are the same values
