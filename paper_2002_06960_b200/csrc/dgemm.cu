@@ -158,9 +158,10 @@ __device__ __forceinline__ const double* chunk0(const double* g, i64 ld, i64 c0,
   return g + (c0 + (tid % CPR) * VEC) + (o0 + tid / CPR) * ld;
 }
 
-// Persistent tile loop.  The work items are w = 0 .. tiles*splits-1 (tile
-// w % tiles = (t % gm, t / gm), K-split w / tiles; consecutive items share the
-// B panel in L2).  With `sched` (two device ints, zero between launches) the
+// Persistent tile loop over the work items (whole tiles, then the k-ranges of
+// the split tail tiles: see dgemm_kernel; consecutive items share a panel in
+// L2, tile_origin).  Items differ in length (k-tiles), so the long ones come
+// first.  With `sched` (two device ints, zero between launches) the
 // CTAs claim items dynamically with atomicAdd -- CTAs that become resident late
 // (e.g. while the side stream's Jacobi SVD holds SMs) simply take fewer items,
 // so the grid never waits on a straggler; the last CTA to finish re-zeroes the
@@ -171,11 +172,47 @@ __device__ __forceinline__ const double* chunk0(const double* g, i64 ld, i64 c0,
 constexpr int RING = 8;           // in-flight item ids (>= STAGES + 1)
 constexpr int RASTER_GROUP = RUTV_RASTER_GROUP;  // tile rows per raster group
 
+// Origin (in tiles) of output tile `tile` of a gm x gn tile grid.
+__device__ __forceinline__ void tile_origin(int tile, int gm, int gn, int& tm, int& tn) {
+  if (gn <= RASTER_GROUP / 2 || gm <= RASTER_GROUP / 2) {
+    // skinny output: raster along the short side, so the few tiles sharing a
+    // panel of the long operand run together (skinny A_t^T G: the 4 N-tiles of
+    // an A_t panel read it from DRAM once instead of four times)
+    if (gn <= gm) {
+      tm = tile / gn;
+      tn = tile % gn;
+    } else {
+      tm = tile % gm;
+      tn = tile / gm;
+    }
+  } else {
+    // grouped raster: groups of RASTER_GROUP tile rows walked column by
+    // column, so the resident items share a few B panels and the group's A
+    // panels stay in L2 while C streams through (a plain row-major raster
+    // re-read the B operand of the c3 rank-2b update ~38x from DRAM: ncu,
+    // 1.58x the compulsory bytes)
+    const int g = tile / (RASTER_GROUP * gn), loc = tile % (RASTER_GROUP * gn);
+    const int gr = (gm - g * RASTER_GROUP) < RASTER_GROUP ? gm - g * RASTER_GROUP : RASTER_GROUP;
+    tm = g * RASTER_GROUP + loc % gr;
+    tn = loc / gr;
+  }
+}
+
+// Work items (tail-split schedule).  Items 0 .. full-1 are whole tiles
+// 0 .. full-1 over all of K, written straight to C.  The remaining
+// tail = tiles - full tiles are split into `tsplits` k-ranges of `kchunk`
+// (item full + z*tail + tt: tile full + tt, k-range z); their partial tiles go
+// to `part` in a compact layout (BM x BN column-major per (z, tt), at
+// (z*tail + tt)*BM*BN) and tail_reduce_kernel sums them in the fixed order
+// z = 0 .. tsplits-1.  full = tiles is the unsplit GEMM, full = 0 is plain
+// split-K over every tile; a tail of the last partial wave split across the
+// whole chip is the data-parallel + stream-K hybrid (the full waves run at
+// full efficiency, only the ragged last wave is split).
 template <class CF, bool TA, bool TB, int VA, int VB, bool CPF>
 __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     dgemm_kernel(i64 M, i64 N, i64 K, double alpha, const double* __restrict__ A, i64 lda,
                  const double* __restrict__ B, i64 ldb, double beta, double* __restrict__ C, i64 ldc,
-                 i64 kchunk, int splits, double* __restrict__ part, int* __restrict__ sched) {
+                 i64 kchunk, int full, int tsplits, double* __restrict__ part, int* __restrict__ sched) {
   constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, MI = CF::MI, NI = CF::NI;
   constexpr int A_ELEMS = CF::A_ELEMS, STAGE_ELEMS = CF::STAGE_ELEMS;
   extern __shared__ __align__(16) double smem[];
@@ -184,8 +221,8 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % CF::WM, wn = warp / CF::WM;
   const int gm = (int)((M + BM - 1) / BM), gn = (int)((N + BN - 1) / BN);
-  const int tiles = gm * gn, items = tiles * splits;
-  const int ktiles = (int)((kchunk + BK - 1) / BK);  // every split has kchunk (last: ragged, masked)
+  const int tiles = gm * gn, tail = tiles - full, items = full + tail * tsplits;
+  const int ktiles_full = (int)((K + BK - 1) / BK);
 
   // item id of sequence number `seq` of this CTA (thread 0 only)
   auto claim = [&](int seq) -> int {
@@ -194,39 +231,34 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   };
   struct TileP {
     i64 m0, n0, kb, ke;
-    int split;
+    int slot;  // -1: whole tile, written to C; else partial slot z*tail + tt
+    int nkt;
   };
   // per-item constants (the only integer divisions: once per item, 32-bit)
   auto params = [&](int item) {
-    const int tile = item % tiles, split = item / tiles;
     TileP tp;
-    if (gn <= RASTER_GROUP / 2 || gm <= RASTER_GROUP / 2) {
-      // skinny output: raster along the short side, so the few tiles sharing a
-      // panel of the long operand run together (skinny A_t^T G: the 4 N-tiles of
-      // an A_t panel read it from DRAM once instead of four times)
-      if (gn <= gm) {
-        tp.m0 = (i64)(tile / gn) * BM;
-        tp.n0 = (i64)(tile % gn) * BN;
-      } else {
-        tp.m0 = (i64)(tile % gm) * BM;
-        tp.n0 = (i64)(tile / gm) * BN;
-      }
+    int tile;
+    if (CPF || item < full) {  // the CPF instantiation runs unsplit GEMMs only
+      tile = item;
+      tp.slot = -1;
+      tp.kb = 0;
+      tp.ke = K;
+      tp.nkt = ktiles_full;
     } else {
-      // grouped raster: groups of RASTER_GROUP tile rows walked column by
-      // column, so the resident items share a few B panels and the group's A
-      // panels stay in L2 while C streams through (a plain row-major raster
-      // re-read the B operand of the c3 rank-2b update ~38x from DRAM: ncu,
-      // 1.58x the compulsory bytes)
-      const int g = tile / (RASTER_GROUP * gn), loc = tile % (RASTER_GROUP * gn);
-      const int gr = (gm - g * RASTER_GROUP) < RASTER_GROUP ? gm - g * RASTER_GROUP : RASTER_GROUP;
-      tp.m0 = (i64)(g * RASTER_GROUP + loc % gr) * BM;
-      tp.n0 = (i64)(loc / gr) * BN;
+      const int j = item - full, z = j / tail;
+      tile = full + (j - z * tail);
+      tp.slot = j;
+      tp.kb = (i64)z * kchunk;
+      tp.ke = (tp.kb + kchunk < K) ? tp.kb + kchunk : K;
+      tp.nkt = (int)((tp.ke - tp.kb + BK - 1) / BK);
     }
-    tp.kb = (i64)split * kchunk;
-    tp.ke = (tp.kb + kchunk < K) ? tp.kb + kchunk : K;
-    tp.split = split;
+    int tm, tn;
+    tile_origin(tile, gm, gn, tm, tn);
+    tp.m0 = (i64)tm * BM;
+    tp.n0 = (i64)tn * BN;
     return tp;
   };
+  auto nkt_of = [&](const TileP& tp) { return CPF ? ktiles_full : tp.nkt; };
   // producer-side per-item constants of the fast path: the thread's first chunk
   // at k-tile 0 of each operand, and whether the tile is interior in M / N
   constexpr int THR = CF::THREADS;
@@ -268,9 +300,24 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   // N-side fragment is fed as the mma's A operand), so lane (g, t) holds
   // C[rows 2t, 2t+1][col g]: two consecutive rows of one column, i.e. one
   // 16-byte load/store in column-major C (half the epilogue instructions).
-  const bool cvec = part ? ((M & 1) == 0) : ((((uintptr_t)C & 15) == 0) && ((ldc & 1) == 0));
+  const bool cvec = (((uintptr_t)C & 15) == 0) && ((ldc & 1) == 0);
   auto epilogue = [&](const TileP& tp) {
-    if (!part && cvec && tp.m0 + BM <= M && tp.n0 + BN <= N) {
+    if (!CPF && tp.slot >= 0) {
+      // partial tile of a k-range: compact BM x BN column-major slot, always
+      // whole (the reduction reads only the in-range elements)
+      double* pb = part + (i64)tp.slot * (BM * BN) + (wm * (MI * 8) + 2 * t) +
+                   (wn * (NI * 8) + g) * BM;
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi) {
+          *reinterpret_cast<double2*>(pb + mi * 8 + ni * 8 * BM) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+          acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        }
+      }
+      return;
+    }
+    if (cvec && tp.m0 + BM <= M && tp.n0 + BN <= N) {
       // interior tile: no bounds checks, one base pointer, 16-byte accesses
       double* cb = C + (tp.m0 + wm * (MI * 8) + 2 * t) + (tp.n0 + wn * (NI * 8) + g) * ldc;
 #pragma unroll
@@ -299,14 +346,11 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) {
         const i64 col = tp.n0 + wn * (NI * 8) + ni * 8 + g;
-        double* cp = part ? part + (i64)tp.split * M * N + row + col * M : C + row + col * ldc;
+        double* cp = C + row + col * ldc;
         if (col < N) {
           if (cvec && row + 1 < M) {
             double2 v;
-            if (part) {
-              v.x = acc[mi][ni][0];
-              v.y = acc[mi][ni][1];
-            } else if (beta == 0.0) {
+            if (beta == 0.0) {
               v.x = alpha * acc[mi][ni][0];
               v.y = alpha * acc[mi][ni][1];
             } else {
@@ -319,8 +363,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               if (row + e < M) {
-                if (part) cp[e] = acc[mi][ni][e];
-                else cp[e] = (beta == 0.0) ? alpha * acc[mi][ni][e] : alpha * acc[mi][ni][e] + beta * cp[e];
+                cp[e] = (beta == 0.0) ? alpha * acc[mi][ni][e] : alpha * acc[mi][ni][e] + beta * cp[e];
               }
             }
           }
@@ -330,13 +373,19 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     }
   };
 
-  if (ktiles == 0) {  // K == 0: C = beta C
+  if (ktiles_full == 0) {  // K == 0: C = beta C (the host passes full = tiles)
     for (int w = blockIdx.x; w < items; w += gridDim.x) epilogue(params(w));
     return;
   }
 
-  // ---- prologue: claim the items of the first STAGES-1 loads
-  const int pre = (STAGES - 1) / ktiles + 1;
+  // ---- prologue: claim the items of the first STAGES-1 loads (no more: a
+  // claimed item waits for this CTA even when others are idle)
+  int min_nkt = full > 0 ? ktiles_full : (1 << 30);
+  if (tail > 0) {
+    const int c0 = (int)((kchunk + BK - 1) / BK), cl = (int)((K - (i64)(tsplits - 1) * kchunk + BK - 1) / BK);
+    min_nkt = min(min_nkt, min(c0, cl));
+  }
+  const int pre = (STAGES - 1) / min_nkt + 1;
   if (tid == 0)
     for (int q = 0; q < pre; ++q) ring[q % RING] = claim(q);
   int claimed = pre;
@@ -351,7 +400,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     if (p_item < items) load_stage(p_stage, ptp, p_kt);
     cp_async_commit();
     p_stage = p_stage + 1 == STAGES ? 0 : p_stage + 1;
-    if (++p_kt == ktiles) {
+    if (++p_kt == nkt_of(ptp)) {
       p_kt = 0;
       ++p_seq;
       p_item = ring[p_seq % RING];
@@ -362,7 +411,6 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     }
   }
 
-  const int pf_kt = ktiles > 3 ? ktiles - 3 : 0;  // k-tile at which the C tile is prefetched
   // fragments of one k-step (4 of K), double-buffered in registers: the loads
   // for step kk+1 are issued before the DMMAs of step kk, and the per-k-tile
   // wait + barrier sits before the LAST step's DMMAs (whose fragments are
@@ -404,7 +452,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
       if (p_item < items) load_stage(p_stage, ptp, p_kt);
       cp_async_commit();
       p_stage = p_stage + 1 == STAGES ? 0 : p_stage + 1;
-      if (++p_kt == ktiles) {
+      if (++p_kt == nkt_of(ptp)) {
         p_kt = 0;
         ++p_seq;
         p_need = true;
@@ -433,7 +481,8 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
     // the epilogue's C read is latency-bound (ncu: its DFMAs carried ~25 % of the
     // stall samples): pull the item's C tile into L2 a few k-tiles ahead
     // (a separate instantiation: the branch alone costs the long-K products ~15 %)
-    if constexpr (CPF) if (c_kt == pf_kt) {
+    // (k-tile nkt - 3 of a whole tile: its C is read by the epilogue)
+    if constexpr (CPF) if (c_kt == (ktiles_full > 3 ? ktiles_full - 3 : 0)) {
 #pragma unroll
       for (int h = 0; h < (BM / 16) * BN / CF::THREADS; ++h) {
         const int line = tid + h * CF::THREADS;           // 128-byte lines: BM/16 per column
@@ -442,7 +491,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
         if (row < M && col < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + row + col * ldc));
       }
     }
-    if (++c_kt == ktiles) {
+    if (++c_kt == nkt_of(ctp)) {
       epilogue(ctp);
       c_kt = 0;
       ++c_seq;
@@ -465,13 +514,22 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MINB)
   }
 }
 
-__global__ void splitk_reduce_kernel(i64 M, i64 N, int splits, double alpha, const double* __restrict__ part,
-                                     double beta, double* __restrict__ C, i64 ldc) {
-  const i64 total = M * N;
+// C(tail tiles) = alpha * sum_z part(z, tt) + beta C, z = 0 .. tsplits-1 in
+// order (bitwise deterministic).  Consecutive threads walk a tile's column
+// (coalesced in column-major C and in the compact partial slots).
+template <int BM, int BN>
+__global__ void tail_reduce_kernel(i64 M, i64 N, int full, int tail, int tsplits, int gm, int gn, double alpha,
+                                   const double* __restrict__ part, double beta, double* __restrict__ C, i64 ldc) {
+  constexpr i64 TE = (i64)BM * BN;
+  const i64 total = (i64)tail * TE;
   for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
+    const int tt = (int)(idx / TE), loc = (int)(idx % TE);
+    int tm, tn;
+    tile_origin(full + tt, gm, gn, tm, tn);
+    const i64 row = (i64)tm * BM + loc % BM, col = (i64)tn * BN + loc / BM;
+    if (row >= M || col >= N) continue;
     double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += part[(i64)z * total + idx];
-    const i64 row = idx % M, col = idx / M;
+    for (int z = 0; z < tsplits; ++z) s += part[((i64)z * tail + tt) * TE + loc];
     double* cp = C + row + col * ldc;
     const double v = alpha * s;
     *cp = (beta == 0.0) ? v : v + beta * (*cp);
@@ -490,12 +548,11 @@ bool use_sched(const Launch& L) {
 
 template <class CF, bool TA, bool TB, int VA, int VB, bool CPF>
 int launch_t(const Launch& L, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
-             i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
-  const int splits = (int)((K + kchunk - 1) / (kchunk > 0 ? kchunk : 1));
+             i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, int full, int tsplits, double* part) {
   RUTV_ONCE_PER_DEVICE(RUTV_CUDA(cudaFuncSetAttribute(
       dgemm_kernel<CF, TA, TB, VA, VB, CPF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM_BYTES)));
   dgemm_kernel<CF, TA, TB, VA, VB, CPF><<<grid, CF::THREADS, CF::SMEM_BYTES, L.stream>>>(M, N, K, alpha, A, lda, B, ldb,
-                                                                               beta, C, ldc, kchunk, splits < 1 ? 1 : splits, part,
+                                                                               beta, C, ldc, kchunk, full, tsplits, part,
                                                                                use_sched(L) ? L.sched : nullptr);
   L.count();
   RUTV_CHECK_LAUNCH("dgemm_kernel");
@@ -504,33 +561,44 @@ int launch_t(const Launch& L, i64 M, i64 N, i64 K, double alpha, const double* A
 
 template <class CF, bool TA, bool TB, bool CPF>
 int launch_v(const Launch& L, int va, int vb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
-             const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
+             const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, int full, int tsplits, double* part) {
   if (va == 2 && vb == 2)
-    return launch_t<CF, TA, TB, 2, 2, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+    return launch_t<CF, TA, TB, 2, 2, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
   if (va == 2)
-    return launch_t<CF, TA, TB, 2, 1, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+    return launch_t<CF, TA, TB, 2, 1, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
   if (vb == 2)
-    return launch_t<CF, TA, TB, 1, 2, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  return launch_t<CF, TA, TB, 1, 1, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+    return launch_t<CF, TA, TB, 1, 2, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
+  return launch_t<CF, TA, TB, 1, 1, CPF>(L, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
 }
 
 template <class CF, bool TA, bool TB>
 int launch_p(const Launch& L, int va, int vb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
-             const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, double* part) {
-  // C prefetch instantiation for read-modify-write epilogues (beta != 0, no split-K)
-  if (beta != 0.0 && part == nullptr)
-    return launch_v<CF, TA, TB, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  return launch_v<CF, TA, TB, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+             const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid, i64 kchunk, int full, int tsplits, double* part) {
+  // C prefetch instantiation for unsplit read-modify-write epilogues
+  // (beta != 0, every item a whole tile)
+  if (beta != 0.0 && tsplits == 1)
+    return launch_v<CF, TA, TB, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
+  return launch_v<CF, TA, TB, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
 }
 
 template <class CF>
 int launch_cfg(const Launch& L, bool ta, bool tb, int va, int vb, i64 M, i64 N, i64 K, double alpha,
                const double* A, i64 lda, const double* B, i64 ldb, double beta, double* C, i64 ldc, dim3 grid,
-               i64 kchunk, double* part) {
-  if (!ta && !tb) return launch_p<CF, false, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  if (ta && !tb) return launch_p<CF, true, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  if (!ta && tb) return launch_p<CF, false, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
-  return launch_p<CF, true, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part);
+               i64 kchunk, int full, int tsplits, double* part) {
+  if (!ta && !tb) return launch_p<CF, false, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
+  if (ta && !tb) return launch_p<CF, true, false>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
+  if (!ta && tb) return launch_p<CF, false, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
+  return launch_p<CF, true, true>(L, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, full, tsplits, part);
+}
+
+// RUTV_GEMM_TAIL=0: no tail-split schedules (unsplit or plain split-K only; A/B)
+bool tail_split_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RUTV_GEMM_TAIL");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
 }
 
 // RUTV_GEMM_PERSIST=0 launches one CTA per tile (tuning comparison only)
@@ -557,53 +625,70 @@ int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double a
   const i64 gm = (M + CF::BM - 1) / CF::BM, gn = (N + CF::BN - 1) / CF::BN;
   const i64 tiles = gm * gn;
   if (tiles > (i64)1 << 30) return -5;
-  // resident CTAs.  All items cost the same, so the grid runs in waves of
-  // `resident` items and a partial last wave idles the rest of the chip
-  // (skinny A_t^T G: 512 tiles on 296 slots = 1.73 waves).  Choose the K split
-  // minimising a time model: waves x k-tiles per item x (one k-tile of one
-  // item at peak share) + the split-K reduction (partials written + read at
-  // HBM speed, plus a launch).
+  // resident CTAs.  Whole-tile items all cost the same, so the grid runs in
+  // waves of `resident` items and a partial last wave idles the rest of the
+  // chip (skinny X W_V at step 48 of c3: 1024 tiles on 444 slots = 2.3 waves).
+  // Choose the schedule minimising a time model: waves x k-tiles per item x
+  // (one k-tile of one item at peak share) + the reduction of the split
+  // tiles (partials written + read at HBM speed, plus a launch).  Candidates:
+  // unsplit; the last partial wave (or the last 1.x waves) split into k-ranges
+  // that fill the chip (the data-parallel + stream-K hybrid); every tile split
+  // (plain split-K).  RUTV_GEMM_TAIL=0 restricts to unsplit / plain split-K.
+  // Measured (tools/gemm_shapes.py, profiles/gemm_tail_r02d.txt): the tail
+  // split wins on the M = 16384, N = b products with K <= 6144 (c3 step 48
+  // X W_V 31.8 -> 34.4 TFLOP/s) but loses ~2 % on long-K ones (step 32
+  // A_t^T G: its whole-tile items of 256 k-tiles straggle when residency is
+  // uneven), and the c3 step was 0.3 % slower with it unrestricted -- so it is
+  // taken only for K <= 6144 and a modelled gain of at least 3 %.
   const i64 resident = (i64)CF::MINB * L.device_sms;
-  i64 splits = 1;
+  const i64 kt = (K + BK - 1) / BK;
+  const i64 TE = (i64)CF::BM * CF::BN;
+  const double t_kt = 2.0 * CF::BM * CF::BN * BK / (37e12 / (double)resident);  // s per k-tile per item
+  i64 full = tiles, tsplits = 1, kchunk = K;
   if (ws && K > 0) {
-    const i64 maxk = K / 128;  // at least 128 of K per split
-    i64 maxs = ws_elems / (M * N);
-    if (maxs > maxk) maxs = maxk;
-    if (maxs > 64) maxs = 64;
-    const double t_kt = 2.0 * CF::BM * CF::BN * BK / (37e12 / (double)resident);  // s per k-tile per item
-    double best = 1e30;
-    for (i64 sp = 1; sp <= (maxs > 1 ? maxs : 1); ++sp) {
-      const i64 kch = ((K + sp - 1) / sp + BK - 1) / BK;
-      const double waves = std::ceil((double)(tiles * sp) / (double)resident);
-      double t = waves * (double)kch * t_kt;
-      if (sp > 1) t += (double)(sp + 2) * (double)M * (double)N * 8.0 / 5e12 + RUTV_SPLIT_FIXED_US * 1e-6;
-      if (t < best * (1.0 - 1e-6)) {
-        best = t;
-        splits = sp;
+    double best = std::ceil((double)tiles / (double)resident) * (double)kt * t_kt;
+    const i64 rem = tiles % resident;
+    const i64 cand[3] = {tiles, tail_split_on() ? rem : 0, tail_split_on() ? rem + resident : 0};
+    for (int ci = 0; ci < 3; ++ci) {
+      const i64 T = cand[ci];
+      if (T <= 0 || T > tiles || (ci > 0 && T == tiles)) continue;
+      const i64 F = tiles - T;  // a multiple of resident (or 0)
+      i64 maxs = ws_elems / (T * TE);
+      if (maxs > kt / 4) maxs = kt / 4;  // at least 4 k-tiles (128 of K) per k-range
+      if (maxs > 64) maxs = 64;
+      for (i64 sp = 2; sp <= maxs; ++sp) {
+        const i64 kch = (kt + sp - 1) / sp;
+        const double t = (double)(F / resident) * (double)kt * t_kt +
+                         std::ceil((double)(T * sp) / (double)resident) * (double)kch * t_kt +
+                         (double)(sp + 2) * (double)T * (double)TE * 8.0 / 5e12 + RUTV_SPLIT_FIXED_US * 1e-6;
+        const bool ok = ci == 0 || (kt <= 192 && t < best * 0.97);
+        if (ok && t < best * (1.0 - 1e-6)) {
+          best = t;
+          full = F;
+          kchunk = kch * BK;
+          tsplits = (K + kchunk - 1) / kchunk;
+        }
       }
     }
   }
-  i64 kchunk = K;
-  if (splits > 1) {
-    kchunk = ((K + splits - 1) / splits + BK - 1) / BK * BK;
-    splits = (K + kchunk - 1) / kchunk;
-  }
   if (kchunk <= 0) kchunk = 1;
+  const i64 tail = tiles - full;
   const int va = vec_of(A, lda), vb = vec_of(B, ldb);
   const size_t pe = L.pbegin();
-  // persistent grid: at most one wave of resident CTAs over all tiles x splits
-  i64 ctas = tiles * splits;
+  // persistent grid: at most one wave of resident CTAs over all items
+  i64 ctas = full + tail * tsplits;
   if (persistent_on() && !L.oneshot && ctas > resident) ctas = resident;
   dim3 grid((unsigned)ctas, 1, 1);
-  double* part = splits > 1 ? ws : nullptr;
-  RUTV_TRY(launch_cfg<CF>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, part));
-  if (splits > 1) {
-    const i64 total = M * N;
-    i64 blocks = (total + 255) / 256;
+  double* part = tail > 0 ? ws : nullptr;
+  RUTV_TRY(launch_cfg<CF>(L, ta, tb, va, vb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, grid, kchunk, (int)full,
+                          (int)tsplits, part));
+  if (tail > 0) {
+    i64 blocks = (tail * TE + 255) / 256;
     if (blocks > (i64)L.device_sms * 8) blocks = (i64)L.device_sms * 8;
-    splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, L.stream>>>(M, N, (int)splits, alpha, ws, beta, C, ldc);
+    tail_reduce_kernel<CF::BM, CF::BN><<<(unsigned)blocks, 256, 0, L.stream>>>(
+        M, N, (int)full, (int)tail, (int)tsplits, (int)gm, (int)gn, alpha, ws, beta, C, ldc);
     L.count();
-    RUTV_CHECK_LAUNCH("splitk_reduce_kernel");
+    RUTV_CHECK_LAUNCH("tail_reduce_kernel");
   }
   // algorithmic: 2MNK flops; compulsory bytes: read A, B (and C if beta != 0), write C
   L.pend(PK_DGEMM, 2.0 * (double)M * (double)N * (double)K,

@@ -39,6 +39,9 @@ GEMM_CASES = [
     (0, 0, 300, 200, 100), (1, 0, 257, 129, 1000), (0, 1, 128, 128, 64), (1, 1, 65, 191, 33),
     (1, 0, 64, 48, 20000),   # split-K path
     (0, 0, 5000, 64, 4096), (0, 1, 1000, 1000, 256), (1, 0, 3, 1, 7), (0, 0, 1, 1, 1),
+    # tail-split schedule (whole tiles for the full waves of 444 slots, the
+    # last partial wave split into k-ranges + tail_reduce_kernel), ragged edges
+    (0, 0, 8000, 250, 2100), (1, 0, 7001, 300, 3001), (0, 1, 8192, 256, 2048),
 ]
 
 

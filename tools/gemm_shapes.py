@@ -34,7 +34,8 @@ for i in steps:
     r = s = n - b * i
     cases = [("S2 TN A^T G", 1, 0, s, b, r, 0.0), ("S3 NN A Y", 0, 0, r, b, s, 0.0),
              ("S5 NN X W", 0, 0, n, b, s, 0.0), ("S7 TN X^T W", 1, 0, s - b, b, r, 0.0),
-             ("rank-b NT", 0, 1, n, s, b, 1.0), ("rank-2b NT", 0, 1, r, s - b, 2 * b, 1.0)]
+             ("rank-b NT", 0, 1, n, s, b, 1.0), ("rank-2b NT", 0, 1, r, s - b, 2 * b, 1.0),
+             ("m x b x b NN (Z T_V)", 0, 0, r, b, b, 0.0)]
     for label, ta, tb, M, N, K, beta in cases:
         if M <= 0 or N <= 0 or K <= 0:
             continue
