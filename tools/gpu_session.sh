@@ -1,6 +1,6 @@
 #!/bin/bash
 # One gpurun session: tests, bench, ncu launch list, ncu full capture of the top kernel.
-# Usage (from repo root, under gpurun): bash tools/gpu_session.sh [smoke] [sanitizer] [tests] [full] [bench] [bench_c2] [kernels]
+# Usage (from repo root, under gpurun): bash tools/gpu_session.sh [smoke] [tests] [full] [bench] [bench_c2] [kernels]
 #   [bench_variants] [host] [host_c5] [hqrrp] [configs] [breakdown] [env_ab] [trace] [gemm_shapes]
 #   [ncu_launches] [ncu_full] [ncu_gemm] [ncu_leaf] [ncu_svd] [leaf_ab] [probe_host]
 #   (ncu_full picks the longest DGEMM of ncu_launches)
@@ -8,15 +8,6 @@ set -u
 mkdir -p gpurun_out
 for stage in "$@"; do
   case "$stage" in
-    sanitizer)
-      # compute-sanitizer memcheck over the smoke path (every kernel of a small randUTV + HQRRP) and the DGEMM tests
-      # (tail-split / split-K shapes); own timeouts well under gpurun's
-      timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" \
-        > gpurun_out/sanitizer_smoke.log 2>&1; echo "memcheck smoke rc=$?"; grep -E "ERROR SUMMARY|smoke" gpurun_out/sanitizer_smoke.log | tail -4
-      timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_kernels.py -m gpu -q -x -k "dgemm" \
-        -p no:cacheprovider > gpurun_out/sanitizer_gemm.log 2>&1; echo "memcheck dgemm tests rc=$?"; grep -E "ERROR SUMMARY|passed|failed" gpurun_out/sanitizer_gemm.log | tail -4
-      timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_randutv.py -m gpu -q -x -k "c1 or ragged or tall" \
-        -p no:cacheprovider > gpurun_out/sanitizer_utv.log 2>&1; echo "memcheck randutv small tests rc=$?"; grep -E "ERROR SUMMARY|passed|failed|deselected" gpurun_out/sanitizer_utv.log | tail -4 ;;
     tests)
       timeout 1200 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider --durations=10 \
         > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/pytest_gpu.log ;;
