@@ -245,6 +245,20 @@ RANDUTV_API int randutv_dgemm(randutv_ctx* ctx, int transa, int transb, int64_t 
                               double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                               double beta, double* C, int64_t ldc);
 
+/* The work schedule randutv_dgemm takes for an M x N x K product on a device
+ * of `sms` SMs with a split workspace of ws_elems doubles (host arithmetic
+ * only: no device, no ctx -- the time model behind split-K and the tail-split
+ * of the last partial wave; S2/S3/S5/S7 all launch through it).
+ * tail_split: 1 = consider splitting the last partial wave (the default path),
+ * 0 = unsplit / plain split-K only.  plan (HOST, 6 int64, caller-owned):
+ * [0] output tiles (64 x 64), [1] `full` = tiles computed whole over all of K,
+ * [2] k-ranges per remaining tile, [3] k-range length (a multiple of 32 unless
+ * unsplit), [4] resident CTA slots (3 per SM), [5] workspace doubles the
+ * partial tiles occupy (<= ws_elems).  Returns 0 or -(argument index):
+ * 1 M, 2 N, 3 K, 4 ws_elems, 5 sms, 6 tail_split, 7 plan. */
+RANDUTV_API int randutv_dgemm_plan(int64_t M, int64_t N, int64_t K, int64_t ws_elems, int sms, int tail_split,
+                                   int64_t* plan);
+
 /* S4/S6: Householder QR of the h x w panel P (h >= w, ldp >= h) in place, LAPACK
  * dgeqrf layout (R on/above the diagonal, reflector tails below), tau (w),
  * and the compact-WY factor Tf (w x w, ldtf >= w, upper triangular, forward

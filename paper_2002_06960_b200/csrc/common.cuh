@@ -132,6 +132,9 @@ int launch_gaussian(const Launch& L, uint64_t seed, i64 it, i64 rows, i64 cols, 
 int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha,
                  const double* A, i64 lda, const double* B, i64 ldb, double beta, double* C, i64 ldc,
                  double* ws, i64 ws_elems);
+// the schedule launch_dgemm takes for the default tile configuration on `sms`
+// SMs (pure host arithmetic): out = {tiles, full, tsplits, kchunk, resident, partial doubles}
+int dgemm_plan(i64 M, i64 N, i64 K, i64 ws_elems, int sms, int tail_on, i64* out);
 
 // K3/K4: panel Householder QR (qr.cu).  P (h x w, ldp) factored in place; tau (w);
 // Wx: explicit unit-lower-trapezoidal W (h x w, ldw); Tf: compact-WY factor (w x w, ldtf).

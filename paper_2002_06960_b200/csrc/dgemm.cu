@@ -619,36 +619,21 @@ inline int vec_of(const double* p, i64 ld) {
 
 namespace {
 
-template <class CF>
-int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
-                const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
-  const i64 gm = (M + CF::BM - 1) / CF::BM, gn = (N + CF::BN - 1) / CF::BN;
-  const i64 tiles = gm * gn;
-  if (tiles > (i64)1 << 30) return -5;
-  // resident CTAs.  Whole-tile items all cost the same, so the grid runs in
-  // waves of `resident` items and a partial last wave idles the rest of the
-  // chip (skinny X W_V at step 48 of c3: 1024 tiles on 444 slots = 2.3 waves).
-  // Choose the schedule minimising a time model: waves x k-tiles per item x
-  // (one k-tile of one item at peak share) + the reduction of the split
-  // tiles (partials written + read at HBM speed, plus a launch).  Candidates:
-  // unsplit; the last partial wave (or the last 1.x waves) split into k-ranges
-  // that fill the chip (the data-parallel + stream-K hybrid); every tile split
-  // (plain split-K).  RUTV_GEMM_TAIL=0 restricts to unsplit / plain split-K.
-  // Measured (tools/gemm_shapes.py, profiles/gemm_tail_r02d.txt): the tail
-  // split wins on the M = 16384, N = b products with K <= 6144 (c3 step 48
-  // X W_V 31.8 -> 34.4 TFLOP/s) but loses ~2 % on long-K ones (step 32
-  // A_t^T G: its whole-tile items of 256 k-tiles straggle when residency is
-  // uneven), and the c3 step was 0.3 % slower with it unrestricted -- so it is
-  // taken only for K <= 6144 and a modelled gain of at least 3 %.
-  const i64 resident = (i64)CF::MINB * L.device_sms;
+// The schedule chooser of launch_with as a pure host function (also behind
+// randutv_dgemm_plan, so the CPU tests cover it): for `tiles` output tiles of
+// bm x bn, `resident` CTA slots and a workspace of ws_elems doubles, the
+// number of whole-tile items `full`, the k-ranges per remaining tile
+// `tsplits` and their length `kchunk`.  See the comment in launch_with.
+void plan_schedule(i64 tiles, i64 K, bool has_ws, i64 ws_elems, i64 resident, int bm, int bn, bool tail_on,
+                   i64* full_out, i64* tsplits_out, i64* kchunk_out) {
   const i64 kt = (K + BK - 1) / BK;
-  const i64 TE = (i64)CF::BM * CF::BN;
-  const double t_kt = 2.0 * CF::BM * CF::BN * BK / (37e12 / (double)resident);  // s per k-tile per item
+  const i64 TE = (i64)bm * bn;
+  const double t_kt = 2.0 * bm * bn * BK / (37e12 / (double)resident);  // s per k-tile per item
   i64 full = tiles, tsplits = 1, kchunk = K;
-  if (ws && K > 0) {
+  if (has_ws && K > 0) {
     double best = std::ceil((double)tiles / (double)resident) * (double)kt * t_kt;
     const i64 rem = tiles % resident;
-    const i64 cand[3] = {tiles, tail_split_on() ? rem : 0, tail_split_on() ? rem + resident : 0};
+    const i64 cand[3] = {tiles, tail_on ? rem : 0, tail_on ? rem + resident : 0};
     for (int ci = 0; ci < 3; ++ci) {
       const i64 T = cand[ci];
       if (T <= 0 || T > tiles || (ci > 0 && T == tiles)) continue;
@@ -671,6 +656,36 @@ int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double a
       }
     }
   }
+  *full_out = full;
+  *tsplits_out = tsplits;
+  *kchunk_out = kchunk;
+}
+
+template <class CF>
+int launch_with(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                const double* B, i64 ldb, double beta, double* C, i64 ldc, double* ws, i64 ws_elems) {
+  const i64 gm = (M + CF::BM - 1) / CF::BM, gn = (N + CF::BN - 1) / CF::BN;
+  const i64 tiles = gm * gn;
+  if (tiles > (i64)1 << 30) return -5;
+  // resident CTAs.  Whole-tile items all cost the same, so the grid runs in
+  // waves of `resident` items and a partial last wave idles the rest of the
+  // chip (skinny X W_V at step 48 of c3: 1024 tiles on 444 slots = 2.3 waves).
+  // Choose the schedule minimising a time model: waves x k-tiles per item x
+  // (one k-tile of one item at peak share) + the reduction of the split
+  // tiles (partials written + read at HBM speed, plus a launch).  Candidates:
+  // unsplit; the last partial wave (or the last 1.x waves) split into k-ranges
+  // that fill the chip (the data-parallel + stream-K hybrid); every tile split
+  // (plain split-K).  RUTV_GEMM_TAIL=0 restricts to unsplit / plain split-K.
+  // Measured (tools/gemm_shapes.py, profiles/gemm_tail_r02d.txt): the tail
+  // split wins on the M = 16384, N = b products with K <= 6144 (c3 step 48
+  // X W_V 31.8 -> 34.4 TFLOP/s) but loses ~2 % on long-K ones (step 32
+  // A_t^T G: its whole-tile items of 256 k-tiles straggle when residency is
+  // uneven), and the c3 step was 0.3 % slower with it unrestricted -- so it is
+  // taken only for K <= 6144 and a modelled gain of at least 3 %.
+  const i64 resident = (i64)CF::MINB * L.device_sms;
+  const i64 TE = (i64)CF::BM * CF::BN;
+  i64 full, tsplits, kchunk;
+  plan_schedule(tiles, K, ws != nullptr, ws_elems, resident, CF::BM, CF::BN, tail_split_on(), &full, &tsplits, &kchunk);
   if (kchunk <= 0) kchunk = 1;
   const i64 tail = tiles - full;
   const int va = vec_of(A, lda), vb = vec_of(B, ldb);
@@ -722,6 +737,31 @@ int launch_dgemm(const Launch& L, bool ta, bool tb, i64 M, i64 N, i64 K, double 
   if (mode == 1 || (mode == 2 && M >= 1024 && N >= 1024) || (mode == 3 && (M <= 512 || N <= 512) && K >= 4096))
     return launch_with<CfgWide>(L, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_elems);
   return launch_with<CfgSmall>(L, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ws, ws_elems);
+}
+
+// randutv_dgemm_plan's body: the default configuration (64 x 64 tiles, 3 CTAs
+// per SM) on a device of `sms` SMs; no device needed.
+int dgemm_plan(i64 M, i64 N, i64 K, i64 ws_elems, int sms, int tail_on, i64* out) {
+  if (M < 0) return -1;
+  if (N < 0) return -2;
+  if (K < 0) return -3;
+  if (ws_elems < 0) return -4;
+  if (sms < 1) return -5;
+  if (!out) return -7;
+  const i64 gm = (M + CfgSmall::BM - 1) / CfgSmall::BM, gn = (N + CfgSmall::BN - 1) / CfgSmall::BN;
+  const i64 tiles = gm * gn;
+  i64 full = tiles, tsplits = 1, kchunk = K;
+  if (tiles > 0)
+    plan_schedule(tiles, K, ws_elems > 0, ws_elems, (i64)CfgSmall::MINB * sms, CfgSmall::BM, CfgSmall::BN, tail_on != 0,
+                  &full, &tsplits, &kchunk);
+  if (kchunk <= 0) kchunk = 1;
+  out[0] = tiles;
+  out[1] = full;
+  out[2] = tsplits;
+  out[3] = kchunk;
+  out[4] = (i64)CfgSmall::MINB * sms;
+  out[5] = (tiles - full) * tsplits * (i64)CfgSmall::BM * CfgSmall::BN;  // workspace doubles the partial tiles take
+  return 0;
 }
 
 }  // namespace rutv

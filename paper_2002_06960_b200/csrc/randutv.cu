@@ -1513,6 +1513,11 @@ RANDUTV_API int randutv_gaussian(randutv_ctx* ctx, uint64_t seed, int64_t it, in
   return 0;
 }
 
+RANDUTV_API int randutv_dgemm_plan(int64_t M, int64_t N, int64_t K, int64_t ws_elems, int sms, int tail_split,
+                                   int64_t* plan) {
+  return dgemm_plan(M, N, K, ws_elems, sms, tail_split, plan);
+}
+
 RANDUTV_API int randutv_dgemm(randutv_ctx* ctx, int transa, int transb, int64_t M, int64_t N, int64_t K,
                               double alpha, const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                               double* C, int64_t ldc) {

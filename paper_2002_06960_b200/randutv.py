@@ -84,6 +84,7 @@ SIGNATURES = {
     "randutv_get_profile": (_int, [_vp, _int, ctypes.POINTER(Profile)]),
     "randutv_gaussian": (_int, [_vp, _u64, _i64, _i64, _i64, _vp, _i64]),
     "randutv_dgemm": (_int, [_vp, _int, _int, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64]),
+    "randutv_dgemm_plan": (_int, [_i64, _i64, _i64, _i64, _int, _int, ctypes.POINTER(ctypes.c_int64)]),
     "randutv_panel_qr": (_int, [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64]),
     "randutv_small_svd": (_int, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),
     "randutv_factor_host": (_int, [_vp, _i64, _i64, _vp, _i64, _i64, _int, _u64, _uint, ctypes.c_size_t, _vp, _i64,
@@ -524,6 +525,15 @@ def randutv_workspace_bytes(m, n, b, q, flags=0):
     out = ctypes.c_size_t()
     _check("randutv_workspace_bytes", lib.randutv_workspace_bytes(m, n, b, q, flags, ctypes.byref(out)))
     return out.value
+
+
+def randutv_dgemm_plan(M, N, K, ws_elems, sms=148, tail_split=True):
+    """The DGEMM work schedule (host arithmetic; include/randutv.h): a dict of the six plan entries."""
+    lib = load_library()
+    out = (ctypes.c_int64 * 6)()
+    _check("randutv_dgemm_plan", lib.randutv_dgemm_plan(int(M), int(N), int(K), int(ws_elems), int(sms),
+                                                        int(bool(tail_split)), out))
+    return dict(zip(("tiles", "full", "tsplits", "kchunk", "resident", "partial_elems"), (int(v) for v in out)))
 
 
 # ----------------------------------------------------------------------------- multi-GPU helpers
