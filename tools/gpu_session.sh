@@ -1,7 +1,7 @@
 #!/bin/bash
 # One gpurun session: tests, bench, ncu launch list, ncu full capture of the top kernel.
 # Usage (from repo root, under gpurun): bash tools/gpu_session.sh [smoke] [tests] [full] [bench] [bench_c2] [kernels]
-#   [bench_variants] [host] [host_c5] [hqrrp] [configs] [breakdown] [env_ab] [trace] [gemm_shapes]
+#   [bench_variants] [host] [host_c5] [hqrrp] [configs] [breakdown] [env_ab] [trace] [gemm_shapes] [gemm_tail]
 #   [ncu_launches] [ncu_full] [ncu_gemm] [ncu_leaf] [ncu_svd] [leaf_ab] [probe_host]
 #   (ncu_full picks the longest DGEMM of ncu_launches)
 set -u
@@ -130,6 +130,19 @@ d = json.loads(sys.stdin.read()); print('$v $c', d['value'], d['ms_per_step'], d
     trace)
       RUTV_TRACE=gpurun_out/trace_c3.json timeout 600 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
       ls -la gpurun_out/trace_c3.json ;;
+    gemm_tail)
+      # tail-split DGEMM schedule A/B (round 2d): GEMM tests, c3 shape sweep, c3/c2 benches with RUTV_GEMM_TAIL=1/0
+      timeout 600 python -m pytest tests/test_gpu_kernels.py -m gpu -q -k "dgemm" -p no:cacheprovider > gpurun_out/pt_gemm.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pt_gemm.log
+      STEPS=${STEPS:-0,16,32,40,44,48,52,56,60} timeout 400 python tools/gemm_shapes.py > gpurun_out/shapes_tail1.log 2>&1
+      RUTV_GEMM_TAIL=0 STEPS=${STEPS:-0,16,32,40,44,48,52,56,60} timeout 400 python tools/gemm_shapes.py > gpurun_out/shapes_tail0.log 2>&1
+      for t in 1 0 1 0; do
+        RUTV_GEMM_TAIL=$t timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_t$t.json 2>gpurun_out/bench_t$t.err
+        python -c "import json;d=json.load(open('gpurun_out/bench_t$t.json'));print('c3 TAIL=$t', d['value'], d['ms_per_step'], d['roofline']['achieved'], d['roofline']['frac'])"
+      done
+      for t in 1 0; do
+        RUTV_GEMM_TAIL=$t timeout 600 python bench.py --config c2 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_c2_t$t.json 2>gpurun_out/bench_c2.err
+        python -c "import json;d=json.load(open('gpurun_out/bench_c2_t$t.json'));print('c2 TAIL=$t', d['value'], d['ms_per_step'], d['roofline']['achieved'], d['roofline']['frac'])"
+      done ;;
     gemm_shapes)
       timeout 600 python tools/gemm_shapes.py > gpurun_out/gemm_shapes.log 2>&1; echo "gemm_shapes rc=$?"; cat gpurun_out/gemm_shapes.log ;;
     hqrrp)
